@@ -1,0 +1,183 @@
+"""ctypes loader for the plain-C CPU oracle (oracle/oracle.c).
+
+TEST INFRASTRUCTURE ONLY: tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / --impl reference legs may import this; the product package
+(paper_0707_3548_b200) never does.  Shares no code with the CUDA path.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+_d = ctypes.c_double
+_i64 = ctypes.c_int64
+_i = ctypes.c_int
+_pd = ctypes.POINTER(ctypes.c_double)
+
+
+def build() -> str:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+    return _LIB
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        src = os.path.join(_HERE, "oracle.c")
+        if not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(src):
+            build()
+        L = ctypes.CDLL(_LIB)
+        L.oracle_house.argtypes = [_d, _pd, _i64, _pd, _pd, _pd]
+        L.oracle_house.restype = None
+        for name in ("oracle_geqrt",):
+            getattr(L, name).argtypes = [_i, _i, _pd, _pd]
+        L.oracle_tsqrt.argtypes = [_i, _i, _pd, _pd, _pd]
+        L.oracle_larfb.argtypes = [_i, _i, _pd, _pd, _pd, _i]
+        L.oracle_ssrfb.argtypes = [_i, _i, _pd, _pd, _pd, _pd, _i]
+        L.oracle_pack.argtypes = [_i64, _i64, _i, _pd, _i64, _pd]
+        L.oracle_unpack.argtypes = [_i64, _i64, _i, _pd, _pd, _i64]
+        L.oracle_get_r.argtypes = [_i64, _i64, _i, _pd, _pd, _i64]
+        L.oracle_geqrf_tiles.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _i]
+        L.oracle_ormqr_tiles.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _i, _i64, _pd, _i]
+        L.oracle_flops_standard.argtypes = [_i64, _i64]
+        L.oracle_flops_standard.restype = _d
+        L.oracle_kernel_flops.argtypes = [_i, _d]
+        L.oracle_kernel_flops.restype = _d
+        L.oracle_flops_eq4.argtypes = [_i64, _i64, _d]
+        L.oracle_flops_eq4.restype = _d
+        L.oracle_last_task_counts.argtypes = [ctypes.POINTER(_i64)]
+        L.oracle_last_task_counts.restype = None
+        _lib = L
+    return _lib
+
+
+def _p(a: np.ndarray):
+    assert a.dtype == np.float64 and (a.flags.f_contiguous or a.flags.c_contiguous)
+    return a.ctypes.data_as(_pd)
+
+
+def _chk(rc: int, what: str):
+    if rc != 0:
+        raise ValueError(f"{what}: invalid argument {-rc}")
+
+
+# ---- thin wrappers (numpy in / out; column-major tiles) -------------------------------
+
+def house(x):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    beta, tau = _d(), _d()
+    v = np.zeros(max(len(x) - 1, 1))
+    rest = np.ascontiguousarray(x[1:]) if len(x) > 1 else np.zeros(1)
+    lib().oracle_house(float(x[0]), _p(rest), len(x) - 1, ctypes.byref(beta), ctypes.byref(tau), _p(v))
+    return beta.value, tau.value, np.concatenate([[1.0], v[:len(x) - 1]])
+
+
+def tile(a):
+    """numpy (b, b) -> column-major contiguous copy."""
+    return np.asfortranarray(np.array(a, dtype=np.float64))
+
+
+def geqrt(A, s):
+    A = tile(A); b = A.shape[0]
+    T = np.zeros((s, b), order="F")
+    _chk(lib().oracle_geqrt(b, s, _p(A), _p(T)), "geqrt")
+    return A, T
+
+
+def tsqrt(R, B, s):
+    R = tile(R); B = tile(B); b = R.shape[0]
+    T = np.zeros((s, b), order="F")
+    _chk(lib().oracle_tsqrt(b, s, _p(R), _p(B), _p(T)), "tsqrt")
+    return R, B, T
+
+
+def larfb(V, T, C, trans=1):
+    V = tile(V); T = tile(T); C = tile(C); b = V.shape[0]; s = T.shape[0]
+    _chk(lib().oracle_larfb(b, s, _p(V), _p(T), _p(C), trans), "larfb")
+    return C
+
+
+def ssrfb(V, T, C1, C2, trans=1):
+    V = tile(V); T = tile(T); C1 = tile(C1); C2 = tile(C2); b = V.shape[0]; s = T.shape[0]
+    _chk(lib().oracle_ssrfb(b, s, _p(V), _p(T), _p(C1), _p(C2), trans), "ssrfb")
+    return C1, C2
+
+
+def dims(m, n, b):
+    return -(-m // b), -(-n // b)
+
+
+def pack(A, b):
+    A = np.asfortranarray(A, dtype=np.float64); m, n = A.shape
+    p, q = dims(m, n, b)
+    At = np.zeros(p * q * b * b)
+    _chk(lib().oracle_pack(m, n, b, _p(A), m, _p(At)), "pack")
+    return At
+
+
+def unpack(At, m, n, b):
+    A = np.zeros((m, n), order="F")
+    _chk(lib().oracle_unpack(m, n, b, _p(np.ascontiguousarray(At)), _p(A), m), "unpack")
+    return A
+
+
+def geqrf(A, b, s, nthreads=1):
+    """Factor column-major A; returns (At tiles after factorization, T slots)."""
+    A = np.asfortranarray(A, dtype=np.float64); m, n = A.shape
+    p, q = dims(m, n, b)
+    At = pack(A, b)
+    T = np.zeros(p * q * s * b)
+    _chk(lib().oracle_geqrf_tiles(m, n, b, s, _p(At), _p(T), nthreads), "geqrf")
+    return At, T
+
+
+def geqrf_tiles_inplace(m, n, b, s, At, T, nthreads=1):
+    _chk(lib().oracle_geqrf_tiles(m, n, b, s, _p(At), _p(T), nthreads), "geqrf")
+
+
+def get_r(At, m, n, b):
+    k = min(m, n)
+    R = np.zeros((k, n), order="F")
+    _chk(lib().oracle_get_r(m, n, b, _p(np.ascontiguousarray(At)), _p(R), k), "get_r")
+    return R
+
+
+def ormqr(At, T, m, n, b, s, B, trans, nthreads=1):
+    """Apply Q^T (trans=1) or Q (trans=0) to column-major m x nrhs B; returns new B."""
+    B = np.asfortranarray(B, dtype=np.float64); nrhs = B.shape[1]
+    Bt = pack(B, b)
+    _chk(lib().oracle_ormqr_tiles(m, n, b, s, _p(np.ascontiguousarray(At)), _p(np.ascontiguousarray(T)),
+                                  trans, nrhs, _p(Bt), nthreads), "ormqr")
+    return unpack(Bt, m, nrhs, b)
+
+
+def orgqr(At, T, m, n, b, s, k=None, nthreads=1):
+    k = n if k is None else k
+    E = np.zeros((m, k), order="F")
+    E[np.arange(min(m, k)), np.arange(min(m, k))] = 1.0
+    return ormqr(At, T, m, n, b, s, E, 0, nthreads)
+
+
+def task_counts():
+    c = (_i64 * 4)()
+    lib().oracle_last_task_counts(c)
+    return dict(G=c[0], L=c[1], T=c[2], S=c[3])
+
+
+def flops_standard(m, n):
+    return lib().oracle_flops_standard(m, n)
+
+
+def kernel_flops(kind, b):
+    return lib().oracle_kernel_flops({"GEQT2": 0, "LARFB": 1, "TSQT2": 2, "SSRFB": 3}[kind], float(b))
+
+
+def flops_eq4(p, q, b):
+    return lib().oracle_flops_eq4(p, q, float(b))

@@ -1,0 +1,622 @@
+/*
+ * oracle.c -- plain CPU oracle for tiled QR (arXiv 0707.3548).
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.h): loaded by tests/, smoke() and the
+ * cpu_baseline / --impl reference legs of bench.py, never by the product path.
+ *
+ * Every routine is a literal, loop-by-loop transcription of the step it cites;
+ * there is no blocking, fusion or reordering beyond what the cited text or the
+ * DESIGN.md reading states.  Compiled with -O2 -ffp-contract=off (no FMA
+ * contraction, no reassociation).
+ */
+#include "oracle.h"
+#include <math.h>
+#include <pthread.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define TILE(At, i, j, p, b) ((At) + ((int64_t)(i) + (int64_t)(j) * (p)) * (int64_t)(b) * (b))
+#define TSLOT(T, i, k, p, s, b) ((T) + ((int64_t)(i) + (int64_t)(k) * (p)) * (int64_t)(s) * (b))
+
+/* ---------------------------------------------------------------------------
+ * Householder generator.  PAPER.md:141-149 ("applying min(m,n) Householder
+ * reflections"); the generator itself is unstated, DESIGN.md
+ * readings R2-R4:
+ *   sigma = sum_{r} x_r^2 (ascending r)
+ *   sigma == 0      : tau = 0, beta = alpha, v = 0            (R3, dlarfg)
+ *   otherwise       : nu = sqrt(alpha^2 + sigma);
+ *                     beta = -nu if alpha >= 0 (incl. -0.0), else +nu  (R2)
+ *                     tau = (beta - alpha)/beta;  v = x / (alpha - beta)
+ *   H = I - tau u u^T, u = (1, v), H (alpha, x)^T = (beta, 0)^T.
+ * No overflow/underflow rescaling (R4).  v may alias x.
+ * ------------------------------------------------------------------------- */
+void oracle_house(double alpha, const double* x, int64_t L, double* beta, double* tau, double* v) {
+  double sigma = 0.0;
+  for (int64_t r = 0; r < L; ++r) sigma += x[r] * x[r];
+  if (sigma == 0.0) {
+    *tau = 0.0;
+    *beta = alpha;
+    for (int64_t r = 0; r < L; ++r) v[r] = 0.0;
+    return;
+  }
+  double nu = sqrt(alpha * alpha + sigma);
+  double bt = (alpha >= 0.0) ? -nu : nu;
+  double denom = alpha - bt;
+  *beta = bt;
+  *tau = (bt - alpha) / bt;
+  for (int64_t r = 0; r < L; ++r) v[r] = x[r] / denom;
+}
+
+/* T_l column j (forward, column-wise DLARFT; PAPER.md:153-157, 213-219;
+ * DESIGN.md R6):  T_l[j][j] = tau;  T_l[0:j, j] = -tau * T_l[0:j, 0:j] * z. */
+static void larft_column(double* Tl, int s, int j, double tau, const double* z) {
+  Tl[(int64_t)j * s + j] = tau;
+  for (int t = 0; t < j; ++t) {
+    double acc = 0.0;
+    for (int tp = t; tp < j; ++tp) acc += Tl[(int64_t)tp * s + t] * z[tp];
+    Tl[(int64_t)j * s + t] = -tau * acc;
+  }
+}
+
+/* W <- T_l^T W (trans=1) or W <- T_l W (trans=0), W of length s, T_l upper. */
+static void apply_tl(const double* Tl, int s, double* W, double* W2, int trans) {
+  for (int a = 0; a < s; ++a) {
+    double acc = 0.0;
+    if (trans) {
+      for (int ap = 0; ap <= a; ++ap) acc += Tl[(int64_t)a * s + ap] * W[ap];
+    } else {
+      for (int ap = a; ap < s; ++ap) acc += Tl[(int64_t)ap * s + a] * W[ap];
+    }
+    W2[a] = acc;
+  }
+}
+
+static int check_bs(int b, int s) {
+  if (b < 1) return -1;
+  if (s < 1 || s > b || b % s != 0) return -2;
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * GEQRT / DGEQT2: A_kk <- V_kk, R_kk ; T_kk.
+ * With inner blocking s (R5): for each block l of s
+ * columns, an unblocked (rank-1 per column, R7) QR of the s columns, the T_l
+ * column recurrence, then the level-3 update C -= U_l T_l^T U_l^T C of the
+ * columns right of the block.  s == b is the paper's unblocked kernel.
+ * ------------------------------------------------------------------------- */
+int oracle_geqrt(int b, int s, double* A, double* T) {
+  int rc = check_bs(b, s);
+  if (rc) return rc;
+  double* z = (double*)malloc(sizeof(double) * s);
+  double* W = (double*)malloc(sizeof(double) * s);
+  double* W2 = (double*)malloc(sizeof(double) * s);
+#define Ak(r, c) A[(int64_t)(r) + (int64_t)(c) * b]
+  for (int l = 0; l < b / s; ++l) {
+    int c0 = l * s;
+    double* Tl = T + (int64_t)l * s * s;
+    for (int64_t e = 0; e < (int64_t)s * s; ++e) Tl[e] = 0.0;
+    for (int c = c0; c < c0 + s; ++c) {
+      double beta, tau;
+      oracle_house(Ak(c, c), &Ak(c + 1, c), b - c - 1, &beta, &tau, &Ak(c + 1, c));
+      Ak(c, c) = beta;
+      for (int cp = c + 1; cp < c0 + s; ++cp) {
+        double w = Ak(c, cp);
+        for (int r = c + 1; r < b; ++r) w += Ak(r, c) * Ak(r, cp);
+        Ak(c, cp) -= tau * w;
+        for (int r = c + 1; r < b; ++r) Ak(r, cp) -= tau * w * Ak(r, c);
+      }
+      int j = c - c0;
+      for (int t = 0; t < j; ++t) {
+        /* z_t = u_{c0+t}^T u_c : u_c has 1 at row c, v below; u_{c0+t}[c] = A[c, c0+t]. */
+        double acc = Ak(c, c0 + t);
+        for (int r = c + 1; r < b; ++r) acc += Ak(r, c0 + t) * Ak(r, c);
+        z[t] = acc;
+      }
+      larft_column(Tl, s, j, tau, z);
+    }
+    /* trailing columns t in [c0+s, b): W = U_l^T C; W <- T_l^T W; C -= U_l W. */
+    for (int t = c0 + s; t < b; ++t) {
+      for (int a = 0; a < s; ++a) {
+        int ca = c0 + a;
+        double acc = Ak(ca, t); /* unit diagonal of U_l */
+        for (int r = ca + 1; r < b; ++r) acc += Ak(r, ca) * Ak(r, t);
+        W[a] = acc;
+      }
+      apply_tl(Tl, s, W, W2, 1);
+      for (int r = c0; r < b; ++r) {
+        double acc = 0.0;
+        for (int a = 0; a < s; ++a) {
+          int ca = c0 + a;
+          double u = (r == ca) ? 1.0 : (r > ca ? Ak(r, ca) : 0.0);
+          acc += u * W2[a];
+        }
+        Ak(r, t) -= acc;
+      }
+    }
+  }
+#undef Ak
+  free(z); free(W); free(W2);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * TSQRT / DTSQT2: QR of [R_kk; A_ik]; reflectors [I; V_ik].
+ * R = upper triangle (incl. diagonal) of the diagonal tile; the strict lower
+ * part (V_kk) is never read or written.  SURVEY 8(c) c-4.
+ * ------------------------------------------------------------------------- */
+int oracle_tsqrt(int b, int s, double* R, double* B, double* T) {
+  int rc = check_bs(b, s);
+  if (rc) return rc;
+  double* z = (double*)malloc(sizeof(double) * s);
+  double* W = (double*)malloc(sizeof(double) * s);
+  double* W2 = (double*)malloc(sizeof(double) * s);
+#define Rk(r, c) R[(int64_t)(r) + (int64_t)(c) * b]
+#define Bk(r, c) B[(int64_t)(r) + (int64_t)(c) * b]
+  for (int l = 0; l < b / s; ++l) {
+    int c0 = l * s;
+    double* Tl = T + (int64_t)l * s * s;
+    for (int64_t e = 0; e < (int64_t)s * s; ++e) Tl[e] = 0.0;
+    for (int c = c0; c < c0 + s; ++c) {
+      double beta, tau;
+      oracle_house(Rk(c, c), &Bk(0, c), b, &beta, &tau, &Bk(0, c));
+      Rk(c, c) = beta;
+      for (int cp = c + 1; cp < c0 + s; ++cp) {
+        double w = Rk(c, cp);
+        for (int r = 0; r < b; ++r) w += Bk(r, c) * Bk(r, cp);
+        Rk(c, cp) -= tau * w;
+        for (int r = 0; r < b; ++r) Bk(r, cp) -= tau * w * Bk(r, c);
+      }
+      int j = c - c0;
+      for (int t = 0; t < j; ++t) {
+        /* identity tops are orthogonal (e_{c0+t} . e_c = 0) */
+        double acc = 0.0;
+        for (int r = 0; r < b; ++r) acc += Bk(r, c0 + t) * Bk(r, c);
+        z[t] = acc;
+      }
+      larft_column(Tl, s, j, tau, z);
+    }
+    for (int t = c0 + s; t < b; ++t) {
+      for (int a = 0; a < s; ++a) {
+        double acc = Rk(c0 + a, t);
+        for (int r = 0; r < b; ++r) acc += Bk(r, c0 + a) * Bk(r, t);
+        W[a] = acc;
+      }
+      apply_tl(Tl, s, W, W2, 1);
+      for (int a = 0; a < s; ++a) Rk(c0 + a, t) -= W2[a];
+      for (int r = 0; r < b; ++r) {
+        double acc = 0.0;
+        for (int a = 0; a < s; ++a) acc += Bk(r, c0 + a) * W2[a];
+        Bk(r, t) -= acc;
+      }
+    }
+  }
+#undef Rk
+#undef Bk
+  free(z); free(W); free(W2);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * LARFB / DLARFB: A_kj <- Q_kk^T A_kj (trans=1, R1)
+ * or Q_kk A_kj (trans=0).  Reads only the strict lower part of V (unit lower
+ * U_l).
+ * ------------------------------------------------------------------------- */
+int oracle_larfb(int b, int s, const double* V, const double* T, double* C, int trans) {
+  int rc = check_bs(b, s);
+  if (rc) return rc;
+  double* W = (double*)malloc(sizeof(double) * s);
+  double* W2 = (double*)malloc(sizeof(double) * s);
+  int nl = b / s;
+  for (int li = 0; li < nl; ++li) {
+    int l = trans ? li : nl - 1 - li;
+    int c0 = l * s;
+    const double* Tl = T + (int64_t)l * s * s;
+    for (int t = 0; t < b; ++t) {
+      double* Ct = C + (int64_t)t * b;
+      for (int a = 0; a < s; ++a) {
+        int ca = c0 + a;
+        double acc = Ct[ca];
+        for (int r = ca + 1; r < b; ++r) acc += V[r + (int64_t)ca * b] * Ct[r];
+        W[a] = acc;
+      }
+      apply_tl(Tl, s, W, W2, trans);
+      for (int r = c0; r < b; ++r) {
+        double acc = 0.0;
+        for (int a = 0; a < s; ++a) {
+          int ca = c0 + a;
+          double u = (r == ca) ? 1.0 : (r > ca ? V[r + (int64_t)ca * b] : 0.0);
+          acc += u * W2[a];
+        }
+        Ct[r] -= acc;
+      }
+    }
+  }
+  free(W); free(W2);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * SSRFB / DSSRFB:
+ * [A_kj; A_ij] <- (I - [I;V] T^T [I;V]^T) [A_kj; A_ij] per inner block l
+ * (trans=1), or the Q form with T_l, l descending (trans=0).  SURVEY 8(c) c-6.
+ * ------------------------------------------------------------------------- */
+int oracle_ssrfb(int b, int s, const double* V, const double* T, double* C1, double* C2, int trans) {
+  int rc = check_bs(b, s);
+  if (rc) return rc;
+  double* W = (double*)malloc(sizeof(double) * s);
+  double* W2 = (double*)malloc(sizeof(double) * s);
+  int nl = b / s;
+  for (int li = 0; li < nl; ++li) {
+    int l = trans ? li : nl - 1 - li;
+    int c0 = l * s;
+    const double* Tl = T + (int64_t)l * s * s;
+    for (int t = 0; t < b; ++t) {
+      double* C1t = C1 + (int64_t)t * b;
+      double* C2t = C2 + (int64_t)t * b;
+      for (int a = 0; a < s; ++a) {
+        double acc = C1t[c0 + a];
+        const double* Va = V + (int64_t)(c0 + a) * b;
+        for (int r = 0; r < b; ++r) acc += Va[r] * C2t[r];
+        W[a] = acc;
+      }
+      apply_tl(Tl, s, W, W2, trans);
+      for (int a = 0; a < s; ++a) C1t[c0 + a] -= W2[a];
+      for (int r = 0; r < b; ++r) {
+        double acc = 0.0;
+        for (int a = 0; a < s; ++a) acc += V[r + (int64_t)(c0 + a) * b] * W2[a];
+        C2t[r] -= acc;
+      }
+    }
+  }
+  free(W); free(W2);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Block Data Layout with zero padding to tile multiples
+ * (R9).
+ * ------------------------------------------------------------------------- */
+int oracle_pack(int64_t m, int64_t n, int b, const double* A, int64_t lda, double* At) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (b < 1) return -3;
+  if (lda < m) return -5;
+  int64_t p = (m + b - 1) / b, q = (n + b - 1) / b;
+  for (int64_t j = 0; j < q; ++j)
+    for (int64_t i = 0; i < p; ++i) {
+      double* t = TILE(At, i, j, p, b);
+      for (int64_t c = 0; c < b; ++c)
+        for (int64_t r = 0; r < b; ++r) {
+          int64_t gr = i * b + r, gc = j * b + c;
+          t[r + c * b] = (gr < m && gc < n) ? A[gr + gc * lda] : 0.0;
+        }
+    }
+  return 0;
+}
+
+int oracle_unpack(int64_t m, int64_t n, int b, const double* At, double* A, int64_t lda) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  if (b < 1) return -3;
+  if (lda < m) return -5;
+  int64_t p = (m + b - 1) / b;
+  for (int64_t gc = 0; gc < n; ++gc)
+    for (int64_t gr = 0; gr < m; ++gr)
+      A[gr + gc * lda] = TILE(At, gr / b, gc / b, p, b)[(gr % b) + (gc % b) * b];
+  return 0;
+}
+
+int oracle_get_r(int64_t m, int64_t n, int b, const double* At, double* R, int64_t ldr) {
+  int64_t k = m < n ? m : n;
+  if (ldr < k) return -5;
+  int64_t p = (m + b - 1) / b;
+  for (int64_t gc = 0; gc < n; ++gc)
+    for (int64_t gr = 0; gr < k; ++gr)
+      R[gr + gc * ldr] = (gr <= gc) ? TILE(At, gr / b, gc / b, p, b)[(gr % b) + (gc % b) * b] : 0.0;
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Algorithm 1, flat tree, 0-based:
+ *   for k < min(p,q): GEQRT(k); LARFB(k,j) j>k; for i>k: TSQRT(k,i); SSRFB(k,i,j) j>k
+ * ------------------------------------------------------------------------- */
+enum { KG = 0, KT = 1, KL = 2, KS = 3 }; /* priority classes */
+
+typedef struct {
+  int64_t m, n, p, q;
+  int b, s;
+  double* At;
+  double* T;
+} qr_ctx;
+
+static int64_t g_counts[4];
+
+static void run_task(const qr_ctx* X, int kind, int64_t k, int64_t i, int64_t j) {
+  int64_t p = X->p;
+  int b = X->b, s = X->s;
+  switch (kind) {
+    case KG: oracle_geqrt(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b)); break;
+    case KL: oracle_larfb(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b), TILE(X->At, k, j, p, b), 1); break;
+    case KT: oracle_tsqrt(b, s, TILE(X->At, k, k, p, b), TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b)); break;
+    case KS:
+      oracle_ssrfb(b, s, TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b), TILE(X->At, k, j, p, b),
+                   TILE(X->At, i, j, p, b), 1);
+      break;
+  }
+}
+
+/* ---- DAG form: tasks, edges, 4-level priority ------------
+ * Edges derived from each kernel's read/write sets (SPEC dag module):
+ *   G(k)     <- S(k-1,k,k)
+ *   L(k,j)   <- G(k), S(k-1,k,j)
+ *   T(k,i)   <- G(k) if i == k+1 else T(k,i-1); S(k-1,i,k)
+ *   S(k,i,j) <- T(k,i); L(k,j) if i == k+1 else S(k,i-1,j); S(k-1,i,j)
+ * Priority G > T > L > S, ties by smaller k, then i, then j (R10).   */
+typedef struct {
+  int kind;
+  int64_t k, i, j;
+  int npred;        /* remaining predecessors */
+} dag_task;
+
+typedef struct {
+  qr_ctx X;
+  dag_task* tasks;
+  int64_t ntasks, ndone;
+  int64_t* heap;
+  int64_t heap_n;
+  int64_t* idG; int64_t* idL; int64_t* idT; int64_t* idS;  /* index maps */
+  int64_t* efrom; int64_t* eto; int64_t nedge;             /* edge list */
+  int64_t* soff; int64_t* succ;                            /* CSR successors */
+  pthread_mutex_t mu;
+  pthread_cond_t cv;
+} dag_ctx;
+
+static int task_less(const dag_task* a, const dag_task* b) {
+  if (a->kind != b->kind) return a->kind < b->kind;
+  if (a->k != b->k) return a->k < b->k;
+  if (a->i != b->i) return a->i < b->i;
+  return a->j < b->j;
+}
+static void heap_push(dag_ctx* D, int64_t id) {
+  int64_t x = D->heap_n++;
+  D->heap[x] = id;
+  while (x > 0) {
+    int64_t par = (x - 1) / 2;
+    if (!task_less(&D->tasks[D->heap[x]], &D->tasks[D->heap[par]])) break;
+    int64_t t = D->heap[x]; D->heap[x] = D->heap[par]; D->heap[par] = t;
+    x = par;
+  }
+}
+static int64_t heap_pop(dag_ctx* D) {
+  int64_t top = D->heap[0];
+  D->heap[0] = D->heap[--D->heap_n];
+  int64_t x = 0;
+  for (;;) {
+    int64_t l = 2 * x + 1, r = l + 1, m = x;
+    if (l < D->heap_n && task_less(&D->tasks[D->heap[l]], &D->tasks[D->heap[m]])) m = l;
+    if (r < D->heap_n && task_less(&D->tasks[D->heap[r]], &D->tasks[D->heap[m]])) m = r;
+    if (m == x) break;
+    int64_t t = D->heap[x]; D->heap[x] = D->heap[m]; D->heap[m] = t;
+    x = m;
+  }
+  return top;
+}
+
+static void add_edge(dag_ctx* D, int64_t from, int64_t to) {
+  D->efrom[D->nedge] = from;
+  D->eto[D->nedge] = to;
+  D->nedge++;
+  D->tasks[to].npred++;
+}
+
+static void* dag_worker(void* arg) {
+  dag_ctx* D = (dag_ctx*)arg;
+  for (;;) {
+    pthread_mutex_lock(&D->mu);
+    while (D->heap_n == 0 && D->ndone < D->ntasks) pthread_cond_wait(&D->cv, &D->mu);
+    if (D->heap_n == 0) { pthread_mutex_unlock(&D->mu); return NULL; }
+    int64_t id = heap_pop(D);
+    pthread_mutex_unlock(&D->mu);
+    dag_task* t = &D->tasks[id];
+    run_task(&D->X, t->kind, t->k, t->i, t->j);
+    pthread_mutex_lock(&D->mu);
+    g_counts[t->kind]++;
+    D->ndone++;
+    for (int64_t e = D->soff[id]; e < D->soff[id + 1]; ++e) {
+      dag_task* u = &D->tasks[D->succ[e]];
+      if (--u->npred == 0) heap_push(D, D->succ[e]);
+    }
+    pthread_cond_broadcast(&D->cv);
+    pthread_mutex_unlock(&D->mu);
+  }
+}
+
+static int geqrf_dag(const qr_ctx* X, int nthreads) {
+  int64_t p = X->p, q = X->q, K = p < q ? p : q;
+  dag_ctx D;
+  memset(&D, 0, sizeof(D));
+  D.X = *X;
+  int64_t nt = 0;
+  for (int64_t k = 0; k < K; ++k) nt += 1 + (q - k - 1) + (p - k - 1) + (p - k - 1) * (q - k - 1);
+  D.ntasks = nt;
+  D.tasks = (dag_task*)calloc(nt, sizeof(dag_task));
+  D.heap = (int64_t*)malloc(sizeof(int64_t) * nt);
+  D.idG = (int64_t*)malloc(sizeof(int64_t) * K);
+  D.idL = (int64_t*)malloc(sizeof(int64_t) * K * q);
+  D.idT = (int64_t*)malloc(sizeof(int64_t) * K * p);
+  D.idS = (int64_t*)malloc(sizeof(int64_t) * K * p * q);
+  D.efrom = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
+  D.eto = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
+#define IDL(k, j) D.idL[(k) * q + (j)]
+#define IDT(k, i) D.idT[(k) * p + (i)]
+#define IDS(k, i, j) D.idS[((k) * p + (i)) * q + (j)]
+  int64_t id = 0;
+  for (int64_t k = 0; k < K; ++k) {
+    D.tasks[id] = (dag_task){KG, k, k, k, 0}; D.idG[k] = id++;
+    for (int64_t j = k + 1; j < q; ++j) { D.tasks[id] = (dag_task){KL, k, k, j, 0}; IDL(k, j) = id++; }
+    for (int64_t i = k + 1; i < p; ++i) {
+      D.tasks[id] = (dag_task){KT, k, i, k, 0}; IDT(k, i) = id++;
+      for (int64_t j = k + 1; j < q; ++j) { D.tasks[id] = (dag_task){KS, k, i, j, 0}; IDS(k, i, j) = id++; }
+    }
+  }
+  for (int64_t k = 0; k < K; ++k) {
+    if (k > 0) add_edge(&D, IDS(k - 1, k, k), D.idG[k]);
+    for (int64_t j = k + 1; j < q; ++j) {
+      add_edge(&D, D.idG[k], IDL(k, j));
+      if (k > 0) add_edge(&D, IDS(k - 1, k, j), IDL(k, j));
+    }
+    for (int64_t i = k + 1; i < p; ++i) {
+      add_edge(&D, i == k + 1 ? D.idG[k] : IDT(k, i - 1), IDT(k, i));
+      if (k > 0) add_edge(&D, IDS(k - 1, i, k), IDT(k, i));
+      for (int64_t j = k + 1; j < q; ++j) {
+        add_edge(&D, IDT(k, i), IDS(k, i, j));
+        add_edge(&D, i == k + 1 ? IDL(k, j) : IDS(k, i - 1, j), IDS(k, i, j));
+        if (k > 0) add_edge(&D, IDS(k - 1, i, j), IDS(k, i, j));
+      }
+    }
+  }
+#undef IDL
+#undef IDT
+#undef IDS
+  D.soff = (int64_t*)calloc(nt + 1, sizeof(int64_t));
+  D.succ = (int64_t*)malloc(sizeof(int64_t) * (D.nedge + 1));
+  for (int64_t e = 0; e < D.nedge; ++e) D.soff[D.efrom[e] + 1]++;
+  for (int64_t t = 0; t < nt; ++t) D.soff[t + 1] += D.soff[t];
+  {
+    int64_t* fill = (int64_t*)malloc(sizeof(int64_t) * (nt + 1));
+    memcpy(fill, D.soff, sizeof(int64_t) * (nt + 1));
+    for (int64_t e = 0; e < D.nedge; ++e) D.succ[fill[D.efrom[e]]++] = D.eto[e];
+    free(fill);
+  }
+  for (int64_t t = 0; t < nt; ++t)
+    if (D.tasks[t].npred == 0) heap_push(&D, t);
+  pthread_mutex_init(&D.mu, NULL);
+  pthread_cond_init(&D.cv, NULL);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+  for (int w = 0; w < nthreads; ++w) pthread_create(&th[w], NULL, dag_worker, &D);
+  for (int w = 0; w < nthreads; ++w) pthread_join(th[w], NULL);
+  pthread_mutex_destroy(&D.mu);
+  pthread_cond_destroy(&D.cv);
+  int ok = (D.ndone == nt);
+  free(th); free(D.tasks); free(D.heap); free(D.idG); free(D.idL); free(D.idT); free(D.idS);
+  free(D.efrom); free(D.eto); free(D.soff); free(D.succ);
+  return ok ? 0 : -99;
+}
+
+int oracle_geqrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double* T, int nthreads) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  int rc = check_bs(b, s);
+  if (rc) return rc - 2;
+  if (nthreads < 1) return -7;
+  qr_ctx X = {m, n, (m + b - 1) / b, (n + b - 1) / b, b, s, At, T};
+  int64_t p = X.p, q = X.q, K = p < q ? p : q;
+  memset(g_counts, 0, sizeof(g_counts));
+  for (int64_t e = 0; e < p * q * (int64_t)s * b; ++e) T[e] = 0.0;
+  if (nthreads > 1) return geqrf_dag(&X, nthreads);
+  for (int64_t k = 0; k < K; ++k) {
+    run_task(&X, KG, k, k, k); g_counts[KG]++;
+    for (int64_t j = k + 1; j < q; ++j) { run_task(&X, KL, k, k, j); g_counts[KL]++; }
+    for (int64_t i = k + 1; i < p; ++i) {
+      run_task(&X, KT, k, i, k); g_counts[KT]++;
+      for (int64_t j = k + 1; j < q; ++j) { run_task(&X, KS, k, i, j); g_counts[KS]++; }
+    }
+  }
+  return 0;
+}
+
+void oracle_last_task_counts(int64_t counts[4]) {
+  counts[0] = g_counts[KG]; counts[1] = g_counts[KL]; counts[2] = g_counts[KT]; counts[3] = g_counts[KS];
+}
+
+/* ---------------------------------------------------------------------------
+ * Apply Q^T / Q to a tile-major B (R8).
+ * Q = product of all reflectors in creation order (GEQRT(k), TSQRT(k,k+1..p-1),
+ * k ascending).  Q^T B replays the factorization's LARFB/SSRFB on B's tiles;
+ * Q B runs the reverse order with T_l un-transposed.  Tile columns of B are
+ * independent, so nthreads > 1 splits them across threads.
+ * ------------------------------------------------------------------------- */
+typedef struct {
+  int64_t m, n, p, q, qb, j0, j1;
+  int b, s, trans;
+  const double* At; const double* T; double* Bt;
+} orm_ctx;
+
+static void orm_columns(const orm_ctx* X) {
+  int64_t p = X->p, K = X->p < X->q ? X->p : X->q;
+  int b = X->b, s = X->s;
+  for (int64_t j = X->j0; j < X->j1; ++j) {
+    if (X->trans) {
+      for (int64_t k = 0; k < K; ++k) {
+        oracle_larfb(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b), TILE(X->Bt, k, j, p, b), 1);
+        for (int64_t i = k + 1; i < p; ++i)
+          oracle_ssrfb(b, s, TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b), TILE(X->Bt, k, j, p, b),
+                       TILE(X->Bt, i, j, p, b), 1);
+      }
+    } else {
+      for (int64_t k = K - 1; k >= 0; --k) {
+        for (int64_t i = p - 1; i > k; --i)
+          oracle_ssrfb(b, s, TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b), TILE(X->Bt, k, j, p, b),
+                       TILE(X->Bt, i, j, p, b), 0);
+        oracle_larfb(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b), TILE(X->Bt, k, j, p, b), 0);
+      }
+    }
+  }
+}
+static void* orm_worker(void* a) { orm_columns((const orm_ctx*)a); return NULL; }
+
+int oracle_ormqr_tiles(int64_t m, int64_t n, int b, int s, const double* At, const double* T,
+                       int trans, int64_t nrhs, double* Bt, int nthreads) {
+  if (m < 1) return -1;
+  if (n < 1) return -2;
+  int rc = check_bs(b, s);
+  if (rc) return rc - 2;
+  if (trans != 0 && trans != 1) return -7;
+  if (nrhs < 1) return -8;
+  if (nthreads < 1) return -10;
+  int64_t p = (m + b - 1) / b, q = (n + b - 1) / b, qb = (nrhs + b - 1) / b;
+  if (nthreads > qb) nthreads = (int)qb;
+  orm_ctx* X = (orm_ctx*)malloc(sizeof(orm_ctx) * nthreads);
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
+  for (int w = 0; w < nthreads; ++w) {
+    X[w] = (orm_ctx){m, n, p, q, qb, qb * w / nthreads, qb * (w + 1) / nthreads, b, s, trans, At, T, Bt};
+    if (nthreads == 1) orm_columns(&X[w]);
+    else pthread_create(&th[w], NULL, orm_worker, &X[w]);
+  }
+  if (nthreads > 1)
+    for (int w = 0; w < nthreads; ++w) pthread_join(th[w], NULL);
+  free(X); free(th);
+  return 0;
+}
+
+/* ---------------------------------------------------------------------------
+ * Flop models.
+ * ------------------------------------------------------------------------- */
+double oracle_flops_standard(int64_t m, int64_t n) {
+  /* QR requires 2n^2(m - n/3) (m >= n); by symmetry
+   * 2m^2(n - m/3) when m < n. */
+  double M = (double)m, N = (double)n;
+  if (m >= n) return 2.0 * N * N * (M - N / 3.0);
+  return 2.0 * M * M * (N - M / 3.0);
+}
+
+double oracle_kernel_flops(int kind, double b) {
+  double b3 = b * b * b;
+  switch (kind) {
+    case 0: return 2.0 * b3;          /* DGEQT2 */
+    case 1: return 3.0 * b3;          /* DLARFB */
+    case 2: return 10.0 / 3.0 * b3;   /* DTSQT2 */
+    case 3: return 5.0 * b3;          /* DSSRFB */
+  }
+  return -1.0;
+}
+
+double oracle_flops_eq4(int64_t p, int64_t q, double b) {
+  /* Eq. (4), exact sum over k = 1..min(p,q). */
+  double tot = 0.0;
+  int64_t K = p < q ? p : q;
+  for (int64_t k = 1; k <= K; ++k)
+    tot += oracle_kernel_flops(0, b) + (double)(q - k) * oracle_kernel_flops(1, b) +
+           (double)(p - k) * oracle_kernel_flops(2, b) + (double)(p - k) * (double)(q - k) * oracle_kernel_flops(3, b);
+  return tot;
+}
