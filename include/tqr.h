@@ -1,0 +1,139 @@
+/*
+ * tqr.h -- C ABI of the B200-native (sm_100a) fp64 tiled QR library.
+ *
+ * Method: the tiled QR factorization of arXiv 0707.3548 (PAPER.md, "Tiled
+ * algorithms" / "A Fine-Grain Algorithm for QR Factorization"),
+ * executed out of order under its DAG by a persistent
+ * device-side executor.  Storage is the paper's Block Data Layout
+ * (PAPER.md:642-666): b x b tiles, column-major inside a tile, tiles
+ * column-major in the p x q grid; tile (i,j) starts at (i + j*p)*b*b.
+ *
+ * Conventions shared by every call
+ *   - All data pointers are DEVICE pointers owned by the caller (e.g. torch
+ *     tensors); the library never frees or reallocates caller memory.  They must
+ *     be 16-byte aligned.  The library allocates only inside tqr_plan_create and
+ *     frees that in tqr_plan_destroy.
+ *   - Every call is asynchronous on the plan's CUDA stream (tqr_params.stream);
+ *     it returns after enqueueing.  Device faults surface at tqr_sync or at the
+ *     next call.
+ *   - Errors are return codes; nothing throws or aborts across the ABI.  After
+ *     TQR_ERR_INVALID_ARG, tqr_last_bad_arg() gives the LAPACK-style 1-based
+ *     index of the offending argument of the failing call.
+ *   - T factors: slot (i,k) (i >= k) holds s x b doubles at (i + k*p)*s*b of the
+ *     T array; inside a slot, T_l (s x s upper triangular, zeros below) occupies
+ *     columns [l*s, l*s+s).  Slot (k,k) comes from GEQRT(k), slot (i,k), i>k,
+ *     from TSQRT(k,i).  (Inner blocking s is DESIGN.md reading R5; s == b is the
+ *     paper's kernel.)
+ *   - Q^T = H_N ... H_1 is applied as I - V T^T V^T per inner block (DESIGN.md
+ *     reading R1: the paper prints (I - V T V^T), which is
+ *     the forward product H_1 ... H_b; the factorization applies its transpose).
+ */
+#ifndef TQR_H
+#define TQR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TQR_OK = 0,
+  TQR_ERR_INVALID_ARG = 1, /* see tqr_last_bad_arg() */
+  TQR_ERR_CUDA = 2,        /* a CUDA runtime call failed (message: tqr_last_error()) */
+  TQR_ERR_NCCL = 3,        /* multi-GPU transport failure */
+  TQR_ERR_OOM = 4,         /* device allocation inside tqr_plan_create failed */
+  TQR_ERR_UNSUPPORTED = 5  /* valid but not built (e.g. (b,s) without a kernel instance) */
+} tqr_status;
+
+typedef struct tqr_plan tqr_plan;
+
+typedef struct {
+  int64_t m;       /* rows of A, >= 1 */
+  int64_t n;       /* columns of A, >= 1 */
+  int32_t b;       /* tile size, >= 1 (built instances: see tqr_supported) */
+  int32_t s;       /* inner block size: 1 <= s <= b, s divides b */
+  int32_t device;  /* CUDA device ordinal */
+  void* stream;    /* cudaStream_t to enqueue on; NULL = legacy default stream */
+  int32_t nranks;  /* 1 (single GPU).  >1 reserved for the 1D block-cyclic multi-GPU layout */
+  int32_t rank;    /* 0 <= rank < nranks */
+  uint32_t flags;  /* TQR_FLAG_* */
+} tqr_params;
+
+#define TQR_FLAG_TRACE 1u /* record per-task (sm, start, end) %globaltimer stamps */
+
+/* ---- plan -------------------------------------------------------------------------- */
+/* Validates p (argument 2's fields: m=1, n=2, b=3, s=4, device=5, nranks=7, rank=8 are
+ * reported as bad-arg indices), builds the DAG task tables and
+ * allocates device-side task tables and progress counters. */
+tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p);
+tqr_status tqr_plan_destroy(tqr_plan* plan);
+
+/* Sizes of the caller-owned tile arrays, in doubles: At = p*q*b*b, T = p*q*s*b
+ * (m rounded up to p = ceil(m/b) tiles, n to q = ceil(n/b)). */
+tqr_status tqr_tiles_size(const tqr_plan* plan, size_t* a_doubles, size_t* t_doubles);
+/* Extra device workspace the caller must pass as `work` (bytes; may be 0). */
+tqr_status tqr_workspace_size(const tqr_plan* plan, size_t* bytes);
+
+/* ---- layout ------------------------------------------------------ */
+/* Column-major m x n A (lda >= m) -> tile-major At, zero padding beyond m, n. */
+tqr_status tqr_pack(tqr_plan* plan, const double* A, int64_t lda, double* At);
+/* Tile-major At -> column-major m x n A (lda >= m); padding is dropped. */
+tqr_status tqr_unpack(tqr_plan* plan, const double* At, double* A, int64_t ldr);
+
+/* ---- factorization (Algorithm 1) ---------------------------------- */
+/* In: At = packed A.  Out: At holds R in its upper trapezoid and the Householder
+ * vectors V below it (V_kk strictly lower in diagonal tiles, V_ik full in tiles
+ * below the diagonal); T receives every T slot.
+ * GEQRT, TSQRT, LARFB and SSRFB tasks run out of order on the device in a
+ * topological order of the DAG with the paper's G > T > L > S priorities. */
+tqr_status tqr_geqrf(tqr_plan* plan, double* At, double* T, void* work);
+
+/* R = upper trapezoid of the factored tiles, min(m,n) x n column-major (ldr >= min(m,n)),
+ * zeros below the diagonal. */
+tqr_status tqr_get_r(tqr_plan* plan, const double* At, double* R, int64_t ldr);
+
+/* Apply Q^T (trans = 'T') or Q (trans = 'N') from the factors (At, T) to a tile-major
+ * m x nrhs matrix Bt laid out like At (p row tiles, ceil(nrhs/b) tile columns),
+ * in place.  (DORMQR analogue; reading R8.) */
+tqr_status tqr_ormqr(tqr_plan* plan, char trans, const double* At, const double* T,
+                     double* Bt, int64_t nrhs, void* work);
+
+/* Form the first k columns of Q explicitly (Q [I_k; 0]) into tile-major Qt
+ * (p row tiles, ceil(k/b) tile columns); 1 <= k <= m.  (DORGQR analogue.) */
+tqr_status tqr_orgqr(tqr_plan* plan, const double* At, const double* T, int64_t k,
+                     double* Qt, void* work);
+
+/* ---- flop models -------------------------------------------------------------------- */
+/* Standard count 2n^2(m - n/3) for m >= n, 2m^2(n - m/3) otherwise. */
+double tqr_flops_standard(int64_t m, int64_t n);
+/* Executed count of the tiled algorithm with inner blocking s:
+ * per task GEQRT 4/3 b^3 + 2/3 s b^2, LARFB 2b^3 + s b^2, TSQRT 2b^3 + 4/3 s b^2,
+ * SSRFB 4b^3 + s b^2 -- at s == b the paper's 2, 3, 10/3, 5 b^3. */
+double tqr_flops_tiled(int64_t m, int64_t n, int32_t b, int32_t s);
+
+/* ---- misc --------------------------------------------------------------------------- */
+tqr_status tqr_sync(tqr_plan* plan);              /* cudaStreamSynchronize + error check */
+const char* tqr_status_string(tqr_status st);
+const char* tqr_last_error(void);                 /* thread-local detail of the last failure */
+int32_t tqr_last_bad_arg(void);                   /* thread-local; 0 if none */
+int32_t tqr_supported(int32_t b, int32_t s);      /* 1 if a kernel instance exists for (b, s) */
+
+/* Introspection of the host-built schedule (pure host, usable without a GPU):
+ * number of tasks of each kind {G, T, L, S} in the plan-independent DAG for a
+ * p x q tile grid with `nslice` column slices per tile, and a topological check of
+ * the dispatch order the library would use with `workers` concurrent CTAs.
+ * Returns TQR_OK when the order is a valid topological order of the DAG. */
+tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
+                                int64_t counts[4], int64_t* n_edges);
+
+/* Trace of the last tqr_geqrf with TQR_FLAG_TRACE: up to `cap` records of
+ * {kind, k, i, j, slice, sm, start_ns, end_ns} as 8 int64 each (host memory);
+ * returns the number of records written in *n. */
+tqr_status tqr_trace_fetch(tqr_plan* plan, int64_t* rec, int64_t cap, int64_t* n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TQR_H */

@@ -1,0 +1,359 @@
+// tqr_device.cuh -- sm_100a device building blocks of the tiled QR executor.
+//
+// fp64 on B200: tcgen05 has no f64 kind, so the fp64 tensor-core instruction is the
+// warp-level DMMA.8x8x4 (`mma.sync.m8n8k4.f64`).  The M0 probe measured it at
+// 37.14 TFLOP/s over 148 SMs (= 64 FMA/clk/SM at 1965 MHz), vs ~34 TFLOP/s for DFMA,
+// sharing one pipe (profiles/r01_m0_fp64_probe.txt).  All level-3 work below is DMMA.
+//
+// Register-resident column groups.  Every update (LARFB, SSRFB, the trailing updates
+// inside GEQRT/TSQRT, and apply-Q) is "apply a block reflector (Y_l, T_l) to a set of
+// columns".  Each warp owns a group of 8 columns of the target tile and keeps the
+// whole b x 8 group in DMMA accumulator registers, transposed: the group is C^T
+// (8 x b), accumulator tile t covers tile rows [8t, 8t+8).  With the column mapping
+// phi(n) below, an accumulator fragment is ALSO a valid A-operand fragment for the
+// k-step over the same rows, so W^T = C^T Y (GEMM1), W^T <- W^T T_l (T multiply) and
+// C^T -= W^T Y^T (GEMM2) chain through registers with no shuffles and no shared
+// memory round trip.  Shared memory only holds the reflector panel Y_l (b x s) and
+// T_l (s x s) in the bank-conflict-free 8x8-block swizzle swz<R>().
+//
+// DMMA m8n8k4 fragment layouts (PTX ISA, mma.m8n8k4 .f64):
+//   A 8x4 : a0 = A[lane>>2][lane&3]          B 4x8 : b0 = B[lane&3][lane>>2]
+//   C 8x8 : c0,c1 = C[lane>>2][2*(lane&3) + {0,1}]
+// Accumulator column n (0..7) of an 8-wide block maps to block-local index phi(n):
+//   phi(2j+h) = 4h + j  -> fragment element h of lane (j = lane&3) holds index 4h+j,
+// which is exactly the k index (lane&3) of a k-step over indices {4h .. 4h+3}.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tqr {
+
+// Per-(b, s) CTA shape.  A column group (8 columns) is held by RS warps, each owning
+// RW <= 128 consecutive rows (64 accumulator registers at most, so 16 warps fit the
+// 64K-register file); for b >= 256 the W partials of a group are summed through shared
+// memory under a named barrier.  A CTA holds GPS groups = SLICE columns.
+template <int B, int S>
+struct Cfg {
+  static constexpr int RW = B < 128 ? B : 128;
+  static constexpr int RS = B / RW;
+  static constexpr int NWARP = B >= 128 ? 16 : 8;
+  static constexpr int NT = NWARP * 32;
+  static constexpr int GPS = NWARP / RS;
+  static constexpr int SLICE = 8 * GPS;
+  static constexpr int XW = (S / 8) * 2 * 32;  // doubles per warp for a W fragment set
+  static_assert(GPS >= 1 && (RS == 1 || GPS <= 15), "named barriers 1..15");
+};
+
+__device__ __forceinline__ int phi(int n) { return ((n & 1) << 2) | (n >> 1); }
+
+// 8x8-block swizzled layout of an R x C operand (R, C multiples of 8): element (r, c) at
+// block (r/8, c/8) (blocks column-major), inside the block column-major with the row
+// index XOR-ed by (c & 6).  Conflict-free (one wavefront per half warp) for both the
+// GEMM1 pattern (rows 4h+j, cols phi(n)) and the GEMM2 pattern (rows phi(n), cols
+// 4h+j); row pairs (2m, 2m+1) stay adjacent, so 16-byte cp.async fills work.
+template <int R>
+__device__ __forceinline__ int swz(int r, int c) {
+  return ((((c >> 3) * (R >> 3)) + (r >> 3)) << 6) + ((c & 7) << 3) + ((r & 7) ^ (c & 6));
+}
+
+__device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d[0]), "+d"(d[1])
+      : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.s32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned smid() {
+  unsigned r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// ---------------------------------------------------------------------------------------
+// Column-group register I/O.  acc[t][h] <-> C[8t + 4h + (lane&3)][col0 + (lane>>2)] of a
+// column-major tile with leading dimension B.  Global tile data is always read with .cg
+// (L2, never L1): tiles are rewritten by other CTAs during the persistent launch.
+// ---------------------------------------------------------------------------------------
+// acc covers rows [8*t0, 8*t0 + RW) of the tile; row blocks below tlo are skipped.
+template <int B, int RW>
+__device__ __forceinline__ void load_cols(double (&acc)[RW / 8][2], const double* tile, int col0, int t0, int tlo) {
+  const int lane = threadIdx.x & 31;
+  const double* col = tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + (lane & 3);
+#pragma unroll
+  for (int t = 0; t < RW / 8; ++t) {
+    if (t0 + t < tlo) { acc[t][0] = 0.0; acc[t][1] = 0.0; continue; }
+    acc[t][0] = __ldcg(col + 8 * t);
+    acc[t][1] = __ldcg(col + 8 * t + 4);
+  }
+}
+template <int B, int RW>
+__device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], double* tile, int col0, int t0, int tlo) {
+  const int lane = threadIdx.x & 31;
+  double* col = tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + (lane & 3);
+#pragma unroll
+  for (int t = 0; t < RW / 8; ++t) {
+    if (t0 + t < tlo) continue;
+    __stcg(col + 8 * t, acc[t][0]);
+    __stcg(col + 8 * t + 4, acc[t][1]);
+  }
+}
+template <int S>
+__device__ __forceinline__ void negate(double (&wn)[S / 8][2]) {
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) { wn[u][0] = -wn[u][0]; wn[u][1] = -wn[u][1]; }
+}
+// w[u][h] <-> C1[row0 + 8u + 4h + (lane&3)][col0 + (lane>>2)]  (s rows of the "top" tile)
+template <int B, int S>
+__device__ __forceinline__ void load_top(double (&w)[S / 8][2], const double* tile, int row0, int col0) {
+  const int lane = threadIdx.x & 31;
+  const double* col = tile + (size_t)(col0 + (lane >> 2)) * B + row0 + (lane & 3);
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) {
+    w[u][0] = __ldcg(col + 8 * u);
+    w[u][1] = __ldcg(col + 8 * u + 4);
+  }
+}
+// per-warp shared-memory copy of a W-shaped fragment set (lane-interleaved: conflict-free)
+template <int S>
+__device__ __forceinline__ void frag_put(double* st, const double (&w)[S / 8][2]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) { st[(2 * u) * 32 + lane] = w[u][0]; st[(2 * u + 1) * 32 + lane] = w[u][1]; }
+}
+// C1 <- C1 - W with C1 from the stash
+template <int B, int S>
+__device__ __forceinline__ void store_top_minus(const double* st, const double (&wn)[S / 8][2], double* tile,
+                                                int row0, int col0) {
+  const int lane = threadIdx.x & 31;
+  double* col = tile + (size_t)(col0 + (lane >> 2)) * B + row0 + (lane & 3);
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) {
+    __stcg(col + 8 * u, st[(2 * u) * 32 + lane] - wn[u][0]);
+    __stcg(col + 8 * u + 4, st[(2 * u + 1) * 32 + lane] - wn[u][1]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Block-reflector apply on one warp's column group (PAPER.md:395-402 DLARFB and
+// PAPER.md:430-466 DSSRFB, per inner block l; readings R1, R5):
+//   W   = C1 + Y_l^T C            (w holds C1, or 0, on entry; GEMM1)
+//   W  <- T_l^T W  (QT)  or  T_l W (!QT)
+//   C  -= Y_l W                   (GEMM2)
+// apply_cg_w computes wn = W (after the T multiply); the caller consumes it (C1 -= W),
+// negates it in place and calls apply_cg_c for GEMM2.  Rows of Y below 8*tlo are zero
+// and skipped.  All three products are DMMA.8x8x4 chains through registers.
+// ---------------------------------------------------------------------------------------
+template <int B, int S, int RW, bool QT>
+__device__ __forceinline__ void apply_cg_w(const double (&acc)[RW / 8][2], double (&w)[S / 8][2],
+                                           double (&wn)[S / 8][2], const double* __restrict__ Ys,
+                                           const double* __restrict__ Ts, int t0, int tlo) {
+  const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
+  // GEMM1: W^T[8 x S] += C^T[8 x RW] * Y[RW x S]   (this warp's rows)
+#pragma unroll
+  for (int t = 0; t < RW / 8; ++t) {
+    if (t0 + t < tlo) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u = 0; u < S / 8; ++u) dmma(w[u], acc[t][h], Ys[swz<B>(8 * (t0 + t) + 4 * h + j, 8 * u + pn)]);
+  }
+}
+
+// Sum the RS row-part partials of W of one column group (fixed order: bitwise identical
+// in every warp of the group), through xbuf and the group's named barrier.
+template <int RS, int S>
+__device__ __forceinline__ void group_reduce(double (&w)[S / 8][2], double* xbuf_group, int rpart, int gi) {
+  if (RS == 1) return;
+  const int lane = threadIdx.x & 31;
+  constexpr int XW = (S / 8) * 2 * 32;
+  frag_put<S>(xbuf_group + rpart * XW, w);
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(32 * RS) : "memory");
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      double x = xbuf_group[(2 * u + h) * 32 + lane];
+#pragma unroll
+      for (int r = 1; r < RS; ++r) x += xbuf_group[r * XW + (2 * u + h) * 32 + lane];
+      w[u][h] = x;
+    }
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(32 * RS) : "memory");
+}
+
+// T multiply: wn = W^T T_l (QT: W <- T_l^T W) or W^T T_l^T (!QT: W <- T_l W)
+template <int S, bool QT>
+__device__ __forceinline__ void t_multiply(const double (&w)[S / 8][2], double (&wn)[S / 8][2],
+                                           const double* __restrict__ Ts) {
+  const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) { wn[u][0] = 0.0; wn[u][1] = 0.0; }
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int u2 = 0; u2 < S / 8; ++u2) {
+        if (QT ? (u2 < u) : (u2 > u)) continue;  // T_l upper triangular
+        const double tv = QT ? Ts[swz<S>(8 * u + 4 * h + j, 8 * u2 + pn)] : Ts[swz<S>(8 * u2 + pn, 8 * u + 4 * h + j)];
+        dmma(wn[u2], w[u][h], tv);
+      }
+}
+
+// GEMM2: C^T[8 x RW] += nwn^T[8 x S] * Y^T[S x RW], nwn = -W
+template <int B, int S, int RW>
+__device__ __forceinline__ void apply_cg_c(double (&acc)[RW / 8][2], const double (&nwn)[S / 8][2],
+                                           const double* __restrict__ Ys, int t0, int tlo) {
+  const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
+#pragma unroll
+  for (int t = 0; t < RW / 8; ++t) {
+    if (t0 + t < tlo) continue;
+#pragma unroll
+    for (int u = 0; u < S / 8; ++u)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) dmma(acc[t], nwn[u][h], Ys[swz<B>(8 * (t0 + t) + pn, 8 * u + 4 * h + j)]);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Panel factorization of one inner block (s columns) in shared memory: dgeqr2-style,
+// rank-1 per column (R7), warp-shuffle norms and dot products.
+//
+//   TS = true  (TSQRT): P = B[:, c0:c0+S] (all B rows), the column's
+//              "top" lives in Rb (the s x s diagonal block of R, upper triangle); the
+//              reflector is [e_c; v], identity tops are mutually orthogonal.
+//   TS = false (GEQRT): P holds rows [c0, B) of A_kk[:, c0:c0+S];
+//              column jj's alpha is P[jj][jj], its x is P[jj+1 :][jj].
+// Column jj belongs to warp jj % NW (NW = warps in the CTA).  One __syncthreads per column: the owner of column
+// jj+1 updates it first and immediately generates the next reflector, overlapping the
+// other warps' updates.  Householder generator = DESIGN.md R2-R4 (oracle_house).
+// Outputs: P holds V_l, Rb / P's upper part holds the new R entries, tau[S], and
+// Z[t + jj*S] = u_t^T u_jj for t < jj (the DLARFT dot products).
+// ---------------------------------------------------------------------------------------
+template <int B, int S, int NW, bool TS>
+__device__ void panel_factor(double* P, int nrows, double* Rb, double* tau, double* Z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NR = (B + 31) / 32;  // rows per lane
+  auto top = [&](int r, int c) -> double& { return TS ? Rb[r + c * S] : P[r + c * B]; };
+
+  // generate reflector for column jj (called by its owner warp, all lanes); sigma known
+  auto house = [&](int jj, double sigma) {
+    const double alpha = top(jj, jj);
+    double beta, tv, scale;
+    if (sigma == 0.0) {
+      beta = alpha; tv = 0.0; scale = 0.0;
+    } else {
+      const double nu = sqrt(alpha * alpha + sigma);
+      beta = (alpha >= 0.0) ? -nu : nu;
+      tv = (beta - alpha) / beta;
+      scale = alpha - beta;
+    }
+    const int lo = TS ? 0 : jj + 1;
+    for (int r = lo + lane; r < nrows; r += 32) P[r + jj * B] = (scale == 0.0) ? 0.0 : P[r + jj * B] / scale;
+    if (lane == 0) { top(jj, jj) = beta; tau[jj] = tv; }
+  };
+  auto colsq = [&](int jj) {
+    const int lo = TS ? 0 : jj + 1;
+    double sg = 0.0;
+    for (int r = lo + lane; r < nrows; r += 32) { const double x = P[r + jj * B]; sg += x * x; }
+    return warp_sum(sg);
+  };
+
+  if (warp == 0) house(0, colsq(0));
+  for (int jj = 0; jj < S; ++jj) {
+    __syncthreads();  // v_jj, tau_jj visible
+    const double tj = tau[jj];
+    const int lo = TS ? 0 : jj + 1;
+    // my columns, jj+1 first (it feeds the next reflector)
+    const int first = (jj + 1 < S && (jj + 1) % NW == warp) ? jj + 1 : -1;
+    for (int pass = 0; pass < 1 + (S + NW - 1) / NW; ++pass) {
+      int c;
+      if (pass == 0) { c = first; if (c < 0) continue; }
+      else { c = warp + (pass - 1) * NW; if (c >= S || c == jj || c == first) continue; }
+      double vr[NR], xr[NR];
+      double d = 0.0;
+#pragma unroll
+      for (int x = 0; x < NR; ++x) {
+        const int r = lane + 32 * x;
+        const bool ok = (r >= lo) && (r < nrows);
+        vr[x] = ok ? P[r + jj * B] : 0.0;
+        xr[x] = ok ? P[r + c * B] : 0.0;
+        d += vr[x] * xr[x];
+      }
+      d = warp_sum(d);
+      if (c > jj) {
+        const double w = top(jj, c) + d;
+        const double tw = tj * w;
+        double sg = 0.0;
+#pragma unroll
+        for (int x = 0; x < NR; ++x) {
+          const int r = lane + 32 * x;
+          if (r >= lo && r < nrows) {
+            const double nv = xr[x] - tw * vr[x];
+            P[r + c * B] = nv;
+            if (!TS && r == jj + 1) continue;  // GEQRT: row jj+1 is the next alpha, not in x
+            sg += nv * nv;
+          }
+        }
+        if (lane == 0) top(jj, c) -= tw;
+        if (c == jj + 1) {
+          sg = warp_sum(sg);
+          __syncwarp();
+          house(c, sg);
+        }
+      } else {
+        // DLARFT dot: u_c^T u_jj (c < jj); GEQRT's u_c has A[jj][c] at row jj
+        if (lane == 0) Z[c + jj * S] = (TS ? 0.0 : P[jj + c * B]) + d;
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// T_l from tau and the dot products Z (forward column-wise DLARFT, PAPER.md:153-157;
+// same recurrence and summation order as the oracle's larft_column):
+//   T[j][j] = tau_j ;  T[t][j] = -tau_j * sum_{t'=t}^{j-1} T[t][t'] Z[t'][j]
+// Tp: S x S plain column-major.  Executed by one warp.
+template <int S>
+__device__ void build_t(double* Tp, const double* tau, const double* Z) {
+  const int lane = threadIdx.x & 31;
+  for (int e = lane; e < S * S; e += 32) Tp[e] = 0.0;
+  __syncwarp();
+  for (int jj = 0; jj < S; ++jj) {
+    const double tj = tau[jj];
+    for (int t = lane; t < jj; t += 32) {
+      double acc = 0.0;
+      for (int tp = t; tp < jj; ++tp) acc += Tp[t + tp * S] * Z[tp + jj * S];
+      Tp[t + jj * S] = -tj * acc;
+    }
+    if (lane == 0) Tp[jj + jj * S] = tj;
+    __syncwarp();
+  }
+}
+
+}  // namespace tqr

@@ -1,0 +1,199 @@
+"""Thin ctypes binding over libtqr.so (include/tqr.h).  Argument marshalling only:
+every step of the factorization runs in the library's CUDA kernels.  PyTorch supplies
+device memory and the stream.  There is no fallback: a missing or failing library
+raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtqr.so")
+
+TQR_OK = 0
+TQR_FLAG_TRACE = 1
+_STATUS = {0: "TQR_OK", 1: "TQR_ERR_INVALID_ARG", 2: "TQR_ERR_CUDA", 3: "TQR_ERR_NCCL", 4: "TQR_ERR_OOM",
+           5: "TQR_ERR_UNSUPPORTED"}
+
+
+class TqrError(RuntimeError):
+    def __init__(self, status: int, detail: str, bad_arg: int):
+        self.status, self.detail, self.bad_arg = status, detail, bad_arg
+        super().__init__(f"{_STATUS.get(status, status)}: {detail}" + (f" (argument {bad_arg})" if bad_arg else ""))
+
+
+class _Params(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_int64), ("n", ctypes.c_int64), ("b", ctypes.c_int32), ("s", ctypes.c_int32),
+                ("device", ctypes.c_int32), ("stream", ctypes.c_void_p), ("nranks", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("flags", ctypes.c_uint32)]
+
+
+_lib = None
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+
+
+def lib():
+    """Load libtqr.so (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run paper_0707_3548_b200/build.py (or __graft_entry__.build())")
+        L = ctypes.CDLL(LIB_PATH)
+        L.tqr_plan_create.argtypes = [ctypes.POINTER(_vp), ctypes.POINTER(_Params)]
+        L.tqr_plan_destroy.argtypes = [_vp]
+        L.tqr_tiles_size.argtypes = [_vp, ctypes.POINTER(ctypes.c_size_t), ctypes.POINTER(ctypes.c_size_t)]
+        L.tqr_workspace_size.argtypes = [_vp, ctypes.POINTER(ctypes.c_size_t)]
+        L.tqr_pack.argtypes = [_vp, _vp, _i64, _vp]
+        L.tqr_unpack.argtypes = [_vp, _vp, _vp, _i64]
+        L.tqr_geqrf.argtypes = [_vp, _vp, _vp, _vp]
+        L.tqr_get_r.argtypes = [_vp, _vp, _vp, _i64]
+        L.tqr_ormqr.argtypes = [_vp, ctypes.c_char, _vp, _vp, _vp, _i64, _vp]
+        L.tqr_orgqr.argtypes = [_vp, _vp, _vp, _i64, _vp, _vp]
+        L.tqr_flops_standard.argtypes = [_i64, _i64]
+        L.tqr_flops_standard.restype = ctypes.c_double
+        L.tqr_flops_tiled.argtypes = [_i64, _i64, _i32, _i32]
+        L.tqr_flops_tiled.restype = ctypes.c_double
+        L.tqr_sync.argtypes = [_vp]
+        L.tqr_status_string.argtypes = [ctypes.c_int]
+        L.tqr_status_string.restype = ctypes.c_char_p
+        L.tqr_last_error.restype = ctypes.c_char_p
+        L.tqr_last_bad_arg.restype = _i32
+        L.tqr_supported.argtypes = [_i32, _i32]
+        L.tqr_supported.restype = _i32
+        L.tqr_schedule_inspect.argtypes = [_i64, _i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
+        L.tqr_trace_fetch.argtypes = [_vp, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)]
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != TQR_OK:
+        L = lib()
+        raise TqrError(st, L.tqr_last_error().decode(), L.tqr_last_bad_arg())
+
+
+def _ptr(t) -> int:
+    if t is None:
+        return 0
+    if t.dtype.__repr__() != "torch.float64":
+        raise TypeError("tqr works on float64 tensors")
+    if not t.is_cuda:
+        raise TypeError("tqr needs device (CUDA) tensors")
+    if not t.is_contiguous():
+        raise TypeError("tensor must be contiguous")
+    return t.data_ptr()
+
+
+# ---- pure functions (no GPU needed) ------------------------------------------------------
+
+def flops_standard(m: int, n: int) -> float:
+    return lib().tqr_flops_standard(m, n)
+
+
+def flops_tiled(m: int, n: int, b: int, s: int) -> float:
+    return lib().tqr_flops_tiled(m, n, b, s)
+
+
+def supported(b: int, s: int) -> bool:
+    return bool(lib().tqr_supported(b, s))
+
+
+def schedule_inspect(p: int, q: int, nslice: int, workers: int):
+    """Task counts {G,T,L,S} and edge count of the DAG; raises if the dispatch order is
+    not topological."""
+    c = (_i64 * 4)()
+    ne = _i64()
+    _check(lib().tqr_schedule_inspect(p, q, nslice, workers, c, ctypes.byref(ne)))
+    return dict(G=c[0], T=c[1], L=c[2], S=c[3]), ne.value
+
+
+# ---- plan ----------------------------------------------------------------------------------
+
+class Plan:
+    """One factorization shape (m, n, b, s) on one device and stream.
+
+    Arrays are torch float64 CUDA tensors owned by the caller; tile-major arrays are flat
+    (see tiles_size()).  All calls enqueue on the stream given at creation (default: the
+    current torch stream).
+    """
+
+    def __init__(self, m: int, n: int, b: int, s: int, device: int = 0, stream=None, trace: bool = False):
+        import torch
+        self.m, self.n, self.b, self.s = m, n, b, s
+        self.p, self.q = -(-m // b), -(-n // b)
+        if stream is None:
+            stream = torch.cuda.current_stream(device)
+        self.stream = stream
+        prm = _Params(m, n, b, s, device, ctypes.c_void_p(stream.cuda_stream), 1, 0,
+                      TQR_FLAG_TRACE if trace else 0)
+        h = _vp()
+        _check(lib().tqr_plan_create(ctypes.byref(h), ctypes.byref(prm)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().tqr_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def tiles_size(self):
+        a, t = ctypes.c_size_t(), ctypes.c_size_t()
+        _check(lib().tqr_tiles_size(self._h, ctypes.byref(a), ctypes.byref(t)))
+        return a.value, t.value
+
+    def alloc(self):
+        import torch
+        a, t = self.tiles_size()
+        dev = self.stream.device
+        return torch.empty(a, dtype=torch.float64, device=dev), torch.empty(t, dtype=torch.float64, device=dev)
+
+    def pack(self, A, At):
+        """A: (n, m) row-major view of a column-major m x n matrix, i.e. A.T contiguous
+        (use `A_colmajor = X.t().contiguous()` of an m x n tensor X) or any tensor whose
+        storage is column-major with leading dimension lda = m."""
+        _check(lib().tqr_pack(self._h, _ptr(A), self.m, _ptr(At)))
+
+    def unpack(self, At, A):
+        _check(lib().tqr_unpack(self._h, _ptr(At), _ptr(A), self.m))
+
+    def geqrf(self, At, T):
+        _check(lib().tqr_geqrf(self._h, _ptr(At), _ptr(T), None))
+
+    def get_r(self, At, R):
+        _check(lib().tqr_get_r(self._h, _ptr(At), _ptr(R), min(self.m, self.n)))
+
+    def ormqr(self, trans: str, At, T, Bt, nrhs: int):
+        _check(lib().tqr_ormqr(self._h, trans.encode(), _ptr(At), _ptr(T), _ptr(Bt), nrhs, None))
+
+    def orgqr(self, At, T, k: int, Qt):
+        _check(lib().tqr_orgqr(self._h, _ptr(At), _ptr(T), k, _ptr(Qt), None))
+
+    def sync(self):
+        _check(lib().tqr_sync(self._h))
+
+    def trace(self, cap: int = 1 << 22):
+        import numpy as np
+        rec = np.zeros((cap, 8), dtype=np.int64)
+        n = _i64()
+        _check(lib().tqr_trace_fetch(self._h, rec.ctypes.data_as(ctypes.POINTER(_i64)), cap, ctypes.byref(n)))
+        return rec[: n.value]
+
+
+# ---- convenience (column-major torch <-> tiles) ---------------------------------------------
+
+def colmajor(X):
+    """m x n tensor -> its column-major storage as a contiguous (n, m) tensor."""
+    return X.t().contiguous()
+
+
+def from_colmajor(Xc):
+    """(n, m) contiguous column-major storage -> m x n tensor view."""
+    return Xc.t()

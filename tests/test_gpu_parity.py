@@ -1,0 +1,104 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded
+inputs.  Tolerances (BASELINE.json north_star): R elementwise within 1e-10 * ||A||_F of the
+oracle's R; backward error and orthogonality of the GPU's own factors below 10 * n * eps.
+"""
+import numpy as np
+import pytest
+
+import oracle
+import tqr_inputs
+from gpu_util import run_factor
+
+pytestmark = pytest.mark.gpu
+EPS = np.finfo(np.float64).eps
+
+
+def _cases():
+    # (m, n, b, s, dist): several tiles and a ragged tail for each built (b, s)
+    return [
+        (256, 256, 64, 16, "uniform"),   # C1
+        (67, 41, 16, 8, "uniform"),      # padding case
+        (41, 67, 16, 16, "uniform"),     # m < n, s == b
+        (100, 90, 32, 8, "uniform"),
+        (96, 96, 32, 32, "uniform"),     # s == b (the paper's unblocked kernels)
+        (300, 200, 64, 64, "uniform"),
+        (520, 300, 128, 32, "uniform"),
+        (700, 600, 256, 32, "uniform"),  # C3 tiling, ragged
+        (1280, 300, 256, 32, "normal"),  # C4-shaped tall-skinny
+    ]
+
+
+@pytest.mark.parametrize("m,n,b,s,dist", _cases())
+def test_factor_parity(m, n, b, s, dist):
+    A = tqr_inputs.make(m, n, dist, 4242 + m + n + b)
+    g = run_factor(A, b, s)
+    At_o, T_o = oracle.geqrf(A, b, s, nthreads=4)
+    R_o = oracle.get_r(At_o, m, n, b)
+    nA = np.linalg.norm(A)
+    err = np.max(np.abs(np.triu(g["R"]) - np.triu(R_o)))
+    assert err <= 1e-10 * nA, f"R mismatch {err:.3e} > {1e-10 * nA:.3e}"
+    assert np.array_equal(np.tril(g["R"], -1), np.zeros_like(g["R"]) * 0) or np.all(np.tril(g["R"], -1) == 0)
+    # V and T (diagnostic, same tolerance scale)
+    assert np.max(np.abs(g["At"] - At_o)) <= 1e-9 * max(1.0, nA)
+    assert np.max(np.abs(g["T"] - T_o)) <= 1e-9 * max(1.0, nA)
+    # backward error / orthogonality of the GPU factors, Q formed by the oracle's apply-Q
+    k = min(m, n)
+    Q = oracle.orgqr(g["At"], g["T"], m, n, b, s, k=k, nthreads=4)
+    assert np.linalg.norm(A - Q @ g["R"]) / (nA * n * EPS) < 10
+    assert np.linalg.norm(np.eye(k) - Q.T @ Q) / (n * EPS) < 10
+
+
+def test_factor_deterministic():
+    A = tqr_inputs.uniform(700, 600, 5)
+    g1 = run_factor(A, 256, 32)
+    g2 = run_factor(A, 256, 32)
+    assert np.array_equal(g1["At"], g2["At"]) and np.array_equal(g1["T"], g2["T"])
+
+
+@pytest.mark.parametrize("m,n,b,s,nrhs", [(256, 256, 64, 16, 100), (700, 600, 256, 32, 300), (67, 41, 16, 8, 20),
+                                           (520, 300, 128, 32, 128)])
+@pytest.mark.parametrize("trans", ["T", "N"])
+def test_ormqr_parity(m, n, b, s, nrhs, trans):
+    import torch
+    from paper_0707_3548_b200 import Plan
+    A = tqr_inputs.uniform(m, n, 17 + m)
+    g = run_factor(A, b, s)
+    plan = g["plan"]
+    Bm = tqr_inputs.uniform(m, nrhs, 99)
+    Bt = torch.from_numpy(oracle.pack(Bm, b)).cuda()
+    plan.ormqr(trans, g["At_dev"], g["T_dev"], Bt, nrhs)
+    plan.sync()
+    got = oracle.unpack(Bt.cpu().numpy(), m, nrhs, b)
+    want = oracle.ormqr(g["At"], g["T"], m, n, b, s, Bm, 1 if trans == "T" else 0, nthreads=4)
+    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.linalg.norm(Bm)) * m
+
+
+@pytest.mark.parametrize("m,n,b,s", [(256, 256, 64, 16), (700, 600, 256, 32), (520, 300, 128, 32)])
+def test_orgqr_and_backward_error_on_gpu(m, n, b, s):
+    import torch
+    A = tqr_inputs.uniform(m, n, 23 + m)
+    g = run_factor(A, b, s)
+    plan = g["plan"]
+    k = n
+    qb = -(-k // b)
+    Qt = torch.empty(plan.p * qb * b * b, dtype=torch.float64, device="cuda")
+    plan.orgqr(g["At_dev"], g["T_dev"], k, Qt)
+    plan.sync()
+    Q = oracle.unpack(Qt.cpu().numpy(), m, k, b)
+    Q_o = oracle.orgqr(g["At"], g["T"], m, n, b, s, k=k, nthreads=4)
+    assert np.max(np.abs(Q - Q_o)) <= 1e-12 * m
+    nA = np.linalg.norm(A)
+    assert np.linalg.norm(A - Q @ g["R"]) / (nA * n * EPS) < 10
+    assert np.linalg.norm(np.eye(k) - Q.T @ Q) / (n * EPS) < 10
+
+
+def test_identity_and_zero_columns():
+    for m, n, b, s in ((128, 128, 32, 8), (256, 192, 64, 16)):
+        g = run_factor(np.eye(m, n), b, s)
+        np.testing.assert_array_equal(g["R"], np.eye(min(m, n), n))
+        assert np.all(g["T"] == 0.0)
+    A = tqr_inputs.uniform(200, 150, 3)
+    A[:, 10:20] = 0.0   # rank-deficient: tau = 0 reflectors, not an error
+    g = run_factor(A, 64, 16)
+    At_o, T_o = oracle.geqrf(A, 64, 16)
+    assert np.max(np.abs(g["R"] - oracle.get_r(At_o, 200, 150, 64))) <= 1e-10 * np.linalg.norm(A)
