@@ -1,0 +1,305 @@
+#!/usr/bin/env python3
+"""bench.py -- fp64 tiled-QR throughput on B200 (BASELINE.json metric).
+
+One step = the whole hot path on one matrix already resident
+in HBM: pack A into tiles (a1), the DAG-executed factorization GEQRT/TSQRT/LARFB/SSRFB
+(a2-a6, one persistent launch), and R extraction (a7).  value = standard flops
+2mn^2 - 2n^3/3 per step / step time, summed over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl tqr|reference]
+
+N > 1 (torchrun): every rank factors its own matrix (independent replicas, weak scaling;
+DESIGN.md "Multi-GPU").  Timing: CUDA events on the plan's stream, barrier +
+synchronize on both sides, max over ranks.  Inputs (2 GiB at C3) exceed L2 (126 MB), so
+no flush is needed between steps.
+
+--impl reference times the CPU oracle (oracle/, the deliberately plain C implementation
+of the same algorithm) as it stands on the host cores, on a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import tqr_inputs  # noqa: E402
+
+METRIC = "fp64 tiled-QR GFLOP/s (2mn²−2n³/3) and % of fp64 peak at 1/2/4/8 B200"
+# fp64 DMMA.8x8x4 peak measured on this pool's B200 (tools/probe_fp64.cu, profiles/r01_m0_fp64_probe.txt):
+# 37.14 TFLOP/s = 148 SM x 64 FMA/clk x 2 x 1.965 GHz (99.8% of nominal).  MEASURED_PEAKS.json has no
+# fp64 entry; this is our own measurement of the same pipe.
+FP64_PEAK_TFLOPS = 37.14
+FP64_NOMINAL_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C3", choices=sorted(tqr_inputs.CONFIGS))
+    ap.add_argument("--impl", default="tqr", choices=["tqr", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--trace", default="", help="write a per-task execution trace (JSON) of one extra step")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu: int):
+        self.gpu, self.samples, self.stop = gpu, [], threading.Event()
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 4 + i and s[4 + i] == "Active"})
+        pw = [float(s[2]) for s in self.samples if s[2].replace(".", "").isdigit()]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.samples)}
+
+
+def cpu_baseline_sample(cfg, threads):
+    """The oracle as it stands, on a bounded sample of the workload: a smaller square matrix
+    with the same tiling (b, s), same distribution and seed recipe, factored by the oracle's
+    DAG executor on `threads` host threads.  Returns (GFLOP/s standard count, seconds, desc)."""
+    import oracle
+    b, s = cfg["b"], cfg["s"]
+    m = n = min(cfg["m"], cfg["n"], max(8 * b, 6144 // b * b))
+    if cfg["m"] > 4 * cfg["n"]:  # tall-skinny: keep the aspect ratio class
+        n = min(cfg["n"], 4 * b)
+        m = min(cfg["m"], 32 * n)
+    A = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"])
+    t0 = time.perf_counter()
+    oracle.geqrf(A, b, s, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return oracle.flops_standard(m, n) / dt / 1e9, dt, f"oracle_geqrf_tiles {m}x{n} b={b} s={s} ({cfg['dist']}), " \
+                                                       f"{threads} threads, one factorization"
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return 0
+    threads = len(os.sched_getaffinity(0))
+    vals = []
+    desc = ""
+    for it in range(args.warmup + args.steps):
+        v, dt, desc = cpu_baseline_sample(cfg, threads)
+        if it >= args.warmup:
+            vals.append(v)
+    value = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "b": cfg["b"], "s": cfg["s"],
+                       "sample": desc},
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    cfg = dict(tqr_inputs.CONFIGS[args.config])
+    cfg["name"] = {"C1": "C1 square QR m=n=256 b=64 s=16 U[-0.5,0.5)",
+                   "C2": "C2 square QR m=n=4096 b=128 s=32 U[-0.5,0.5)",
+                   "C3": "C3 square QR m=n=16384 b=256 s=32 U[-0.5,0.5)",
+                   "C4": "C4 tall-skinny QR m=131072 n=2048 b=256 s=32 N(0,1)",
+                   "C5": "C5 square QR m=n=65536 b=512 s=64 U[-0.5,0.5)"}[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank)
+
+    import torch
+    import torch.distributed as dist
+    import paper_0707_3548_b200 as tqr
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    m, n, b, s = cfg["m"], cfg["n"], cfg["b"], cfg["s"]
+    stream = torch.cuda.Stream()
+    plan = tqr.Plan(m, n, b, s, device=local, stream=stream)
+    A_host = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"] + 1000 * rank)   # replicas: one matrix per rank
+    A_pin = torch.from_numpy(np.ascontiguousarray(A_host.T)).pin_memory()       # column-major storage, pinned
+    del A_host
+    with torch.cuda.stream(stream):
+        A_dev = A_pin.to(f"cuda:{local}", non_blocking=True)
+        At, T = plan.alloc()
+        R = torch.empty((n, min(m, n)), dtype=torch.float64, device=f"cuda:{local}")
+    stream.synchronize()
+
+    def step():
+        plan.pack(A_dev, At)
+        plan.geqrf(At, T)
+        plan.get_r(At, R)
+
+    flops = tqr.flops_standard(m, n)
+    flops_exec = tqr.flops_tiled(m, n, b, s)
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+
+    # ---- timed region: K steps, per-step events around the executor launch too ----
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        e0.record(stream)
+        for kk in range(args.steps):
+            plan.pack(A_dev, At)
+            ev[kk][0].record(stream)
+            plan.geqrf(At, T)
+            ev[kk][1].record(stream)
+            plan.get_r(At, R)
+        e1.record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    kern_ms = statistics.mean(a.elapsed_time(b_) for a, b_ in ev)
+    if world > 1:
+        t = torch.tensor([ms, kern_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms, kern_ms = t.tolist()
+    value = world * flops / (ms * 1e-3) / 1e9
+
+    # ---- e2e: host buffers through the public API (H2D A, pack, factor, R, D2H R) ----
+    e2e = None
+    if not args.no_e2e:
+        R_pin = torch.empty((n, min(m, n)), dtype=torch.float64).pin_memory()
+        with torch.cuda.stream(stream):
+            for _ in range(1):
+                A_dev.copy_(A_pin, non_blocking=True); step(); R_pin.copy_(R, non_blocking=True)
+        stream.synchronize()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            f0.record(stream)
+            for _ in range(args.steps):
+                A_dev.copy_(A_pin, non_blocking=True)
+                step()
+                R_pin.copy_(R, non_blocking=True)
+            f1.record(stream)
+        stream.synchronize()
+        barrier()
+        ems = f0.elapsed_time(f1) / args.steps
+        if world > 1:
+            t = torch.tensor([ems], device=f"cuda:{local}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = t.item()
+        e2e = {"value": world * flops / (ems * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": A_pin.numel() * 8, "d2h_bytes_per_step": R_pin.numel() * 8,
+               "ms_per_step": ems}
+
+    # ---- optional trace of one extra step ----
+    if args.trace and rank == 0:
+        tplan = tqr.Plan(m, n, b, s, device=local, stream=stream, trace=True)
+        tplan.pack(A_dev, At)
+        tplan.geqrf(At, T)
+        tplan.sync()
+        rec = tplan.trace()
+        t0 = int(rec[:, 6].min())
+        with open(args.trace, "w") as f:
+            json.dump({"fields": ["kind", "k", "i", "j", "slice", "sm", "start_ns", "end_ns"],
+                       "t0": t0, "records": rec.tolist()}, f)
+        tplan.close()
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = len(os.sched_getaffinity(0))
+        v, dt, desc = cpu_baseline_sample(cfg, threads)
+        cpu = {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc, "seconds": dt}
+
+    achieved = flops / (kern_ms * 1e-3) / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg["name"], "m": m, "n": n, "b": b, "s": s, "dist": cfg["dist"],
+                   "seed": cfg["seed"], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "l2": "inputs 2 GiB > 126 MB L2; no flush between steps" if m * n * 8 > (1 << 28)
+                   else "inputs smaller than L2 (not flushed)",
+                   "step": "pack + geqrf (persistent DAG executor) + get_r"},
+        "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
+        "executed_gflops": world * flops_exec / (ms * 1e-3) / 1e9,
+        "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "kernel": f"exec_kernel<{b},{s}> (tqr_geqrf)", "kernel_ms": kern_ms,
+                     "flops_per_launch": flops,
+                     "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt); "
+                                    "MEASURED_PEAKS.json has no fp64 entry"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": 3 * args.steps,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
