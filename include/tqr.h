@@ -73,7 +73,10 @@ tqr_status tqr_plan_destroy(tqr_plan* plan);
 /* Sizes of the caller-owned tile arrays, in doubles: At = p*q*b*b, T = p*q*s*b
  * (m rounded up to p = ceil(m/b) tiles, n to q = ceil(n/b)). */
 tqr_status tqr_tiles_size(const tqr_plan* plan, size_t* a_doubles, size_t* t_doubles);
-/* Extra device workspace the caller must pass as `work` (bytes; may be 0). */
+/* Device workspace the caller must pass as `work` to geqrf/ormqr/orgqr (bytes):
+ * (p*q*b*b + p*q*s*b) doubles holding packed (shared-memory-layout) copies of every
+ * reflector panel and T block, written once by the panel tasks and streamed by TMA bulk
+ * copies into every update task.  Not needed after the call returns. */
 tqr_status tqr_workspace_size(const tqr_plan* plan, size_t* bytes);
 
 /* ---- layout ------------------------------------------------------ */
@@ -88,7 +91,7 @@ tqr_status tqr_unpack(tqr_plan* plan, const double* At, double* A, int64_t ldr);
  * below the diagonal); T receives every T slot.
  * GEQRT, TSQRT, LARFB and SSRFB tasks run out of order on the device in a
  * topological order of the DAG with the paper's G > T > L > S priorities. */
-tqr_status tqr_geqrf(tqr_plan* plan, double* At, double* T, void* work);
+tqr_status tqr_geqrf(tqr_plan* plan, double* At, double* T, void* work);  /* work: see tqr_workspace_size */
 
 /* R = upper trapezoid of the factored tiles, min(m,n) x n column-major (ldr >= min(m,n)),
  * zeros below the diagonal. */
@@ -132,6 +135,19 @@ tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t wo
  * {kind, k, i, j, slice, sm, start_ns, end_ns} as 8 int64 each (host memory);
  * returns the number of records written in *n. */
 tqr_status tqr_trace_fetch(tqr_plan* plan, int64_t* rec, int64_t cap, int64_t* n);
+
+/* Profiling aid: run `count` mutually independent tasks of one kind (0 = GEQRT, 1 = TSQRT,
+ * 2 = LARFB slice, 3 = SSRFB slice) through the same persistent executor on the plan's
+ * tiles, with no DAG dependencies.  Results in At/T are meaningless afterwards (tasks race
+ * on shared tiles); only the timing is.  Used to profile one kernel body in isolation with
+ * ncu.  Requires p >= 2 and q >= 2. */
+tqr_status tqr_profile_tasks(tqr_plan* plan, int32_t kind, int64_t count, double* At, double* T, void* work);
+
+/* Profiling builds only (libtqr_phases.so, compiled with -DTQR_PROFILE_PHASES): attach a
+ * caller-owned device array of 8 int64 per-phase clock64 totals (warp 0 of every CTA adds
+ * its cycles in: 0 prologue, 1 cp.async wait, 2 barrier, 3 staging issue, 4 apply,
+ * 5 epilogue, 6 dispatch + dependency wait).  NULL detaches.  No-op in product builds. */
+tqr_status tqr_phase_counters(tqr_plan* plan, long long* d_counters);
 
 #ifdef __cplusplus
 }

@@ -7,12 +7,13 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-LIB = os.path.join(HERE, "libtqr.so")
+PHASES = os.environ.get("TQR_PHASES", "0") == "1"   # profiling variant with phase timers
+LIB = os.path.join(HERE, "libtqr_phases.so" if PHASES else "libtqr.so")
 SOURCES = ["tqr_exec.cu", "tqr_host.cpp"]
 HEADERS = ["tqr_device.cuh", "tqr_internal.h", os.path.join("..", "..", "include", "tqr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"]
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"] + (["-DTQR_PROFILE_PHASES"] if PHASES else [])
 
 
 def _stale() -> bool:
@@ -29,7 +30,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + ".o")
+        obj = os.path.join(CSRC, src + (".ph" if PHASES else "") + ".o")
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -29,18 +29,21 @@
 namespace tqr {
 
 // Per-(b, s) CTA shape.  A column group (8 columns) is held by RS warps, each owning
-// RW <= 128 consecutive rows (64 accumulator registers at most, so 16 warps fit the
-// 64K-register file); for b >= 256 the W partials of a group are summed through shared
-// memory under a named barrier.  A CTA holds GPS groups = SLICE columns.
+// RW <= 128 consecutive rows (64 accumulator registers at most); for b >= 256 the W
+// partials of a group are summed through shared memory under a named barrier.  A CTA has
+// 8 warps (up to 255 registers per thread: the executor contains device-function calls,
+// and ptxas spilled the accumulators of the inlined update path at a 128-register cap)
+// and holds GPS groups = SLICE columns.
 template <int B, int S>
 struct Cfg {
   static constexpr int RW = B < 128 ? B : 128;
   static constexpr int RS = B / RW;
-  static constexpr int NWARP = B >= 128 ? 16 : 8;
+  static constexpr int NWARP = 8;  // 255-register budget: no spills in the DMMA paths
   static constexpr int NT = NWARP * 32;
   static constexpr int GPS = NWARP / RS;
   static constexpr int SLICE = 8 * GPS;
   static constexpr int XW = (S / 8) * 2 * 32;  // doubles per warp for a W fragment set
+  static constexpr int C1W = 8 * (S + 4);      // doubles per group for a staged C1 block
   static_assert(GPS >= 1 && (RS == 1 || GPS <= 15), "named barriers 1..15");
 };
 
@@ -69,6 +72,33 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// ---- TMA bulk copies (cp.async.bulk -> SASS UBLKCP) completing on an mbarrier ----------
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (bytes % 16 == 0, both addresses 16-byte aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+// order this thread's generic-proxy accesses before subsequent async-proxy (TMA) accesses
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -100,25 +130,23 @@ __device__ __forceinline__ double warp_sum(double x) {
 // column-major tile with leading dimension B.  Global tile data is always read with .cg
 // (L2, never L1): tiles are rewritten by other CTAs during the persistent launch.
 // ---------------------------------------------------------------------------------------
-// acc covers rows [8*t0, 8*t0 + RW) of the tile; row blocks below tlo are skipped.
+// acc covers rows [8*t0, 8*t0 + RW) of the tile.
 template <int B, int RW>
-__device__ __forceinline__ void load_cols(double (&acc)[RW / 8][2], const double* tile, int col0, int t0, int tlo) {
+__device__ __forceinline__ void load_cols(double (&acc)[RW / 8][2], const double* tile, int col0, int t0) {
   const int lane = threadIdx.x & 31;
   const double* col = tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + (lane & 3);
 #pragma unroll
   for (int t = 0; t < RW / 8; ++t) {
-    if (t0 + t < tlo) { acc[t][0] = 0.0; acc[t][1] = 0.0; continue; }
     acc[t][0] = __ldcg(col + 8 * t);
     acc[t][1] = __ldcg(col + 8 * t + 4);
   }
 }
 template <int B, int RW>
-__device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], double* tile, int col0, int t0, int tlo) {
+__device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], double* tile, int col0, int t0) {
   const int lane = threadIdx.x & 31;
   double* col = tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + (lane & 3);
 #pragma unroll
   for (int t = 0; t < RW / 8; ++t) {
-    if (t0 + t < tlo) continue;
     __stcg(col + 8 * t, acc[t][0]);
     __stcg(col + 8 * t + 4, acc[t][1]);
   }
@@ -140,22 +168,35 @@ __device__ __forceinline__ void load_top(double (&w)[S / 8][2], const double* ti
   }
 }
 // per-warp shared-memory copy of a W-shaped fragment set (lane-interleaved: conflict-free)
+// C1 block of one column group in shared memory: column n (0..7) at n*(S+4), rows
+// contiguous (one 16-byte-aligned bulk copy per column); fragment (u, h) of lane reads
+// element (row 8u+4h+j, column n) -> conflict-free (stride S+4 = 4 mod 16 doubles).
+template <int S>
+__device__ __forceinline__ int c1_idx(int u, int h, int lane) {
+  return (lane >> 2) * (S + 4) + 8 * u + 4 * h + (lane & 3);
+}
+template <int S>
+__device__ __forceinline__ void c1_put(double* c1s, const double (&w)[S / 8][2]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) { c1s[c1_idx<S>(u, 0, lane)] = w[u][0]; c1s[c1_idx<S>(u, 1, lane)] = w[u][1]; }
+}
 template <int S>
 __device__ __forceinline__ void frag_put(double* st, const double (&w)[S / 8][2]) {
   const int lane = threadIdx.x & 31;
 #pragma unroll
   for (int u = 0; u < S / 8; ++u) { st[(2 * u) * 32 + lane] = w[u][0]; st[(2 * u + 1) * 32 + lane] = w[u][1]; }
 }
-// C1 <- C1 - W with C1 from the stash
+// C1 <- C1 - W with C1 from its shared-memory stage (c1_idx layout)
 template <int B, int S>
-__device__ __forceinline__ void store_top_minus(const double* st, const double (&wn)[S / 8][2], double* tile,
+__device__ __forceinline__ void store_top_minus(const double* c1s, const double (&wn)[S / 8][2], double* tile,
                                                 int row0, int col0) {
   const int lane = threadIdx.x & 31;
   double* col = tile + (size_t)(col0 + (lane >> 2)) * B + row0 + (lane & 3);
 #pragma unroll
   for (int u = 0; u < S / 8; ++u) {
-    __stcg(col + 8 * u, st[(2 * u) * 32 + lane] - wn[u][0]);
-    __stcg(col + 8 * u + 4, st[(2 * u + 1) * 32 + lane] - wn[u][1]);
+    __stcg(col + 8 * u, c1s[c1_idx<S>(u, 0, lane)] - wn[u][0]);
+    __stcg(col + 8 * u + 4, c1s[c1_idx<S>(u, 1, lane)] - wn[u][1]);
   }
 }
 
@@ -165,45 +206,20 @@ __device__ __forceinline__ void store_top_minus(const double* st, const double (
 //   W   = C1 + Y_l^T C            (w holds C1, or 0, on entry; GEMM1)
 //   W  <- T_l^T W  (QT)  or  T_l W (!QT)
 //   C  -= Y_l W                   (GEMM2)
-// apply_cg_w computes wn = W (after the T multiply); the caller consumes it (C1 -= W),
-// negates it in place and calls apply_cg_c for GEMM2.  Rows of Y below 8*tlo are zero
-// and skipped.  All three products are DMMA.8x8x4 chains through registers.
+// Rows of Y outside the reflector block are explicit zeros in shared memory (no branches in
+// the unrolled DMMA loops).  All three products are DMMA.8x8x4 chains through registers.
 // ---------------------------------------------------------------------------------------
-template <int B, int S, int RW, bool QT>
-__device__ __forceinline__ void apply_cg_w(const double (&acc)[RW / 8][2], double (&w)[S / 8][2],
-                                           double (&wn)[S / 8][2], const double* __restrict__ Ys,
-                                           const double* __restrict__ Ts, int t0, int tlo) {
+template <int B, int S, int RW>
+__device__ __forceinline__ void gemm1(const double (&acc)[RW / 8][2], double (&w)[S / 8][2],
+                                      const double* __restrict__ Ys, int t0) {
   const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
-  // GEMM1: W^T[8 x S] += C^T[8 x RW] * Y[RW x S]   (this warp's rows)
+  // W^T[8 x S] += C^T[8 x RW] * Y[RW x S]   (this warp's rows; 4 independent chains)
 #pragma unroll
-  for (int t = 0; t < RW / 8; ++t) {
-    if (t0 + t < tlo) continue;
+  for (int t = 0; t < RW / 8; ++t)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int u = 0; u < S / 8; ++u) dmma(w[u], acc[t][h], Ys[swz<B>(8 * (t0 + t) + 4 * h + j, 8 * u + pn)]);
-  }
-}
-
-// Sum the RS row-part partials of W of one column group (fixed order: bitwise identical
-// in every warp of the group), through xbuf and the group's named barrier.
-template <int RS, int S>
-__device__ __forceinline__ void group_reduce(double (&w)[S / 8][2], double* xbuf_group, int rpart, int gi) {
-  if (RS == 1) return;
-  const int lane = threadIdx.x & 31;
-  constexpr int XW = (S / 8) * 2 * 32;
-  frag_put<S>(xbuf_group + rpart * XW, w);
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(32 * RS) : "memory");
-#pragma unroll
-  for (int u = 0; u < S / 8; ++u)
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      double x = xbuf_group[(2 * u + h) * 32 + lane];
-#pragma unroll
-      for (int r = 1; r < RS; ++r) x += xbuf_group[r * XW + (2 * u + h) * 32 + lane];
-      w[u][h] = x;
-    }
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + gi), "r"(32 * RS) : "memory");
 }
 
 // T multiply: wn = W^T T_l (QT: W <- T_l^T W) or W^T T_l^T (!QT: W <- T_l W)
@@ -225,19 +241,87 @@ __device__ __forceinline__ void t_multiply(const double (&w)[S / 8][2], double (
       }
 }
 
-// GEMM2: C^T[8 x RW] += nwn^T[8 x S] * Y^T[S x RW], nwn = -W
+// GEMM2: C^T[8 x RW] += nwn^T[8 x S] * Y^T[S x RW], nwn = -W.  Loop order (u, h) outer so
+// consecutive DMMAs hit different accumulators (dependency distance RW/8).
 template <int B, int S, int RW>
-__device__ __forceinline__ void apply_cg_c(double (&acc)[RW / 8][2], const double (&nwn)[S / 8][2],
-                                           const double* __restrict__ Ys, int t0, int tlo) {
+__device__ __forceinline__ void gemm2(double (&acc)[RW / 8][2], const double (&nwn)[S / 8][2],
+                                      const double* __restrict__ Ys, int t0) {
   const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
 #pragma unroll
-  for (int t = 0; t < RW / 8; ++t) {
-    if (t0 + t < tlo) continue;
+  for (int u = 0; u < S / 8; ++u)
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int t = 0; t < RW / 8; ++t) dmma(acc[t], nwn[u][h], Ys[swz<B>(8 * (t0 + t) + pn, 8 * u + 4 * h + j)]);
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// C1 <- C1 - W with C1 held in registers (fragment layout of w)
+template <int B, int S>
+__device__ __forceinline__ void store_top_minus_r(const double (&c1)[S / 8][2], const double (&wn)[S / 8][2],
+                                                  double* tile, int row0, int col0) {
+  const int lane = threadIdx.x & 31;
+  double* col = tile + (size_t)(col0 + (lane >> 2)) * B + row0 + (lane & 3);
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) {
+    __stcg(col + 8 * u, c1[u][0] - wn[u][0]);
+    __stcg(col + 8 * u + 4, c1[u][1] - wn[u][1]);
+  }
+}
+
+// One column group's block-reflector apply (all RS warps of group gi call it together):
+//   W = [C1] + Y^T C (row partials summed in a fixed order);  W <- T^{T|1} W;
+//   [C1 -= W to global];  C -= Y W.
+// c1: the group's C1 block in registers (fragment layout of w; used by rpart 0 only);
+// top/row0: where C1 - W is stored.  xg: the group's RS partial buffers.  BAR2 protects
+// xg when the caller reuses it before all warps of the group have read it.
+template <int B, int S, int RW, int RS, bool QT, bool BAR2, bool HAS_C1>
+__device__ __forceinline__ void group_apply(double (&acc)[RW / 8][2], const double* __restrict__ Ys,
+                                            const double* __restrict__ Ts, const double* c1s, double* top,
+                                            int row0, int col0, int t0, int gi, int rpart, double* xg) {
+  const int lane = threadIdx.x & 31;
+  constexpr int XW = (S / 8) * 2 * 32;
+  double w[S / 8][2], wn[S / 8][2];
+#pragma unroll
+  for (int u = 0; u < S / 8; ++u) {
+    w[u][0] = (HAS_C1 && rpart == 0) ? c1s[c1_idx<S>(u, 0, lane)] : 0.0;
+    w[u][1] = (HAS_C1 && rpart == 0) ? c1s[c1_idx<S>(u, 1, lane)] : 0.0;
+  }
+  gemm1<B, S, RW>(acc, w, Ys, t0);
+  if (RS > 1) {
+    frag_put<S>(xg + rpart * XW, w);
+    named_bar(1 + gi, 32 * RS);
 #pragma unroll
     for (int u = 0; u < S / 8; ++u)
 #pragma unroll
-      for (int h = 0; h < 2; ++h) dmma(acc[t], nwn[u][h], Ys[swz<B>(8 * (t0 + t) + pn, 8 * u + 4 * h + j)]);
+      for (int h = 0; h < 2; ++h) {
+        double x = xg[(2 * u + h) * 32 + lane];
+#pragma unroll
+        for (int r = 1; r < RS; ++r) x += xg[r * XW + (2 * u + h) * 32 + lane];
+        w[u][h] = x;
+      }
+    if (BAR2) named_bar(1 + gi, 32 * RS);
   }
+  t_multiply<S, QT>(w, wn, Ts);
+  if (HAS_C1 && rpart == 0) store_top_minus<B, S>(c1s, wn, top, row0, col0);
+  negate<S>(wn);
+  gemm2<B, S, RW>(acc, wn, Ys, t0);
+}
+
+// Warp-local cp.async of one group's C1 block (rows [row0, row0+S), 8 columns from col0)
+// into c1s (c1_idx layout: column n at n*(S+4)); 16-byte chunks, S/2 per column.
+template <int B, int S>
+__device__ __forceinline__ void c1_fetch(double* c1s, const double* tile, int row0, int col0) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int q = lane; q < 8 * (S / 2); q += 32) {
+    const int n = q / (S / 2), r2 = 2 * (q % (S / 2));
+    cp_async16(c1s + n * (S + 4) + r2, tile + (size_t)(col0 + n) * B + row0 + r2);
+  }
+  cp_async_commit();
 }
 
 // ---------------------------------------------------------------------------------------

@@ -13,21 +13,51 @@
 
 namespace tqr {
 
+// Optional phase timing (build with -DTQR_PROFILE_PHASES): warp 0 of every CTA accumulates
+// clock64 deltas per phase; totals are added to ExecArgs::phases at kernel exit.
+#ifdef TQR_PROFILE_PHASES
+#define PH_DECL __shared__ long long s_ph[8]
+#define PH_T0 long long ph_t = clock64()
+#define PH_MARK(idx)                                         \
+  do {                                                       \
+    if (threadIdx.x == 0) {                                  \
+      long long ph_n = clock64();                            \
+      s_ph[idx] += ph_n - ph_t;                              \
+      ph_t = ph_n;                                           \
+    }                                                        \
+  } while (0)
+#else
+#define PH_DECL
+#define PH_T0
+#define PH_MARK(idx) do {} while (0)
+#endif
+
 template <int B, int S>
 struct Layout {
   using C = Cfg<B, S>;
-  static constexpr int YSZ = B * S;          // one Y buffer
+  static constexpr int YSZ = B * S;          // one Y buffer (swizzled panel)
   static constexpr int TSZ = S * S;
-  static constexpr int Y0 = 0, Y1 = YSZ;     // Y[2]
+  static constexpr int Y0 = 0, Y1 = YSZ;
   static constexpr int T0 = 2 * YSZ, T1 = 2 * YSZ + TSZ;
-  static constexpr int RB = 2 * YSZ + 2 * TSZ;
-  static constexpr int ZZ = RB + TSZ;
-  static constexpr int TAU = ZZ + TSZ;
-  static constexpr int STASH = TAU + S;                       // C1 block, one per group
-  static constexpr int XBUF = STASH + C::GPS * C::XW;         // W partials, one per warp
-  static constexpr int TOTAL = XBUF + (C::RS > 1 ? C::NWARP * C::XW : 0);
+  static constexpr int XBUF = 2 * YSZ + 2 * TSZ;  // W partials, one per warp (RS > 1)
+  static constexpr int XSZ = C::RS > 1 ? C::NWARP * C::XW : 0;
+  static constexpr int C1S = XBUF + XSZ;          // C1 blocks, 2 buffers x GPS groups
+  static constexpr int C1SZ = C::GPS * C::C1W;
+  // panel-only scratch, aliased onto the partial / C1 buffers (dead in panels until the
+  // trailing update, which starts after Rb/Z/tau are consumed)
+  static constexpr int RB = XBUF, ZZ = RB + TSZ, TAU = ZZ + TSZ;
+  static constexpr int PANEL_END = TAU + S;
+  static constexpr int UPD_END = C1S + 2 * C1SZ;
+  // 2 "full" mbarriers (8 B each) + 2 int32 "done" counters
+  static constexpr int MBAR = (PANEL_END > UPD_END ? PANEL_END : UPD_END);
+  static constexpr int TOTAL = MBAR + 3;  // doubles
+#ifdef TQR_PROFILE_PHASES
+  static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double) + 64;
+#else
   static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double);
+#endif
   static_assert(BYTES <= 232448, "shared memory budget");
+  static_assert((T0 % 2) == 0 && (Y1 % 2) == 0 && (MBAR % 1) == 0, "16-byte aligned TMA destinations");
 };
 
 __device__ __forceinline__ double* tile_ptr(double* base, int i, int j, int p, int B) {
@@ -36,39 +66,18 @@ __device__ __forceinline__ double* tile_ptr(double* base, int i, int j, int p, i
 __device__ __forceinline__ double* tslot_ptr(double* base, int i, int k, int p, int B, int S) {
   return base + ((size_t)i + (size_t)k * p) * (size_t)S * B;
 }
-
-// One column group's block-reflector apply for the warps of group gi (rows part rpart):
-//   W = [C1 +] Y^T C  (partials summed over the group);  W <- T^{T|1} W;  [C1 -= W];  C -= Y W
-// HAS_TOP: SSRFB/TSQRT-type (C1 = rows [row0, row0+S) of `top`, col0.. of the group).
-template <int B, int S, bool QT, bool HAS_TOP>
-__device__ __forceinline__ void group_apply(double* sm, double (&acc)[Cfg<B, S>::RW / 8][2], const double* Ys,
-                                            const double* Ts, double* top, int row0, int col0, int t0, int tlo,
-                                            int gi, int rpart) {
-  using C = Cfg<B, S>;
-  using L = Layout<B, S>;
-  double w[S / 8][2], wn[S / 8][2];
-  double* st = sm + L::STASH + gi * C::XW;
-  if (HAS_TOP && rpart == 0) {
-    load_top<B, S>(w, top, row0, col0);
-    frag_put<S>(st, w);
-  } else {
-#pragma unroll
-    for (int u = 0; u < S / 8; ++u) { w[u][0] = 0.0; w[u][1] = 0.0; }
-  }
-  apply_cg_w<B, S, C::RW, QT>(acc, w, wn, Ys, Ts, t0, tlo);
-  group_reduce<C::RS, S>(w, sm + L::XBUF + gi * C::RS * C::XW, rpart, gi);
-  t_multiply<S, QT>(w, wn, Ts);
-  if (HAS_TOP && rpart == 0) store_top_minus<B, S>(st, wn, top, row0, col0);
-  negate<S>(wn);
-  apply_cg_c<B, S, C::RW>(acc, wn, Ys, t0, tlo);
-}
+// Workspace: packed copies of every reflector panel, written once by the panel
+// task that creates it, read by every update task through TMA bulk copies.
+//   Yp tile (i,k), panel l: B*S doubles at tile_ptr(Yp, i, k) + l*B*S, swz<B> layout;
+//     diagonal tiles hold U_l (0 above the block, unit-lower top block, V below).
+//   Tp slot (i,k), block l: S*S doubles at tslot_ptr(Tp, i, k) + l*S*S, swz<S> layout.
 
 // ---------------------------------------------------------------------------------------
 // GEQRT(k): per inner block l, panel of rows [c0,B) x cols [c0,c0+S),
-// T_l, then the LARFB-type update of columns [c0+S, B) (rows >= c0).
+// T_l, then the LARFB-type update of columns [c0+S, B) (Y rows < c0 are zero).
 // ---------------------------------------------------------------------------------------
 template <int B, int S>
-__device__ __noinline__ void task_geqrt(double* sm, double* Akk, double* Tk) {
+__device__ __forceinline__ void task_geqrt(double* sm, double* Akk, double* Tk, double* Ypk, double* Tpk) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -89,11 +98,15 @@ __device__ __noinline__ void task_geqrt(double* sm, double* Akk, double* Tk) {
     panel_factor<B, S, C::NWARP, false>(P, nrows, nullptr, tau, Z);
     if (warp == 0) build_t<S>(Tp, tau, Z);
     __syncthreads();
-    for (int e = tid; e < nrows * S; e += C::NT) {
-      const int r = e % nrows, c = e / nrows;
-      const double v = P[r + c * B];
-      __stcg(Akk + (size_t)(c0 + c) * B + c0 + r, v);
-      Ys[swz<B>(c0 + r, c)] = (r == c) ? 1.0 : (r > c ? v : 0.0);
+    for (int e = tid; e < B * S; e += C::NT) {
+      const int r = e % B, c = e / B;
+      double y = 0.0;
+      if (r >= c0) {
+        const double v = P[(r - c0) + c * B];
+        __stcg(Akk + (size_t)(c0 + c) * B + r, v);
+        y = (r - c0 == c) ? 1.0 : (r - c0 > c ? v : 0.0);
+      }
+      Ys[swz<B>(r, c)] = y;
     }
     for (int e = tid; e < S * S; e += C::NT) {
       const double v = Tp[e];
@@ -101,11 +114,14 @@ __device__ __noinline__ void task_geqrt(double* sm, double* Akk, double* Tk) {
       Ts[swz<S>(e % S, e / S)] = v;
     }
     __syncthreads();
+    for (int e = tid; e < B * S; e += C::NT) __stcg(Ypk + (size_t)l * B * S + e, Ys[e]);
+    for (int e = tid; e < S * S; e += C::NT) __stcg(Tpk + (size_t)l * S * S + e, Ts[e]);
     for (int g = (c0 + S) / 8 + gi; g < B / 8; g += C::GPS) {
       double acc[C::RW / 8][2];
-      load_cols<B, C::RW>(acc, Akk, 8 * g, t0, c0 / 8);
-      group_apply<B, S, true, false>(sm, acc, Ys, Ts, nullptr, 0, 8 * g, t0, c0 / 8, gi, rpart);
-      store_cols<B, C::RW>(acc, Akk, 8 * g, t0, c0 / 8);
+      load_cols<B, C::RW>(acc, Akk, 8 * g, t0);
+      group_apply<B, S, C::RW, C::RS, true, true, false>(acc, Ys, Ts, nullptr, nullptr, 0, 8 * g, t0, gi, rpart,
+                                                         sm + L::XBUF + gi * C::RS * C::XW);
+      store_cols<B, C::RW>(acc, Akk, 8 * g, t0);
     }
     __syncthreads();
   }
@@ -117,7 +133,7 @@ __device__ __noinline__ void task_geqrt(double* sm, double* Akk, double* Tk) {
 // B[:, c0+S:B].  Only the upper triangle of A(k,k) is read or written.
 // ---------------------------------------------------------------------------------------
 template <int B, int S>
-__device__ __noinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, double* Tik) {
+__device__ __forceinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, double* Tik, double* Ypi, double* Tpi) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -129,6 +145,10 @@ __device__ __noinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, do
   double* Rb = sm + L::RB;
   double* Z = sm + L::ZZ;
   double* tau = sm + L::TAU;
+#ifdef TQR_PROFILE_PHASES
+  long long* s_ph = (long long*)(sm + Layout<B, S>::TOTAL);
+#endif
+  PH_T0;
   for (int l = 0; l < B / S; ++l) {
     const int c0 = l * S;
     const double* src = Aik + (size_t)c0 * B;
@@ -138,9 +158,12 @@ __device__ __noinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, do
       Rb[e] = (r <= c) ? __ldcg(Akk + (size_t)(c0 + c) * B + c0 + r) : 0.0;
     }
     __syncthreads();
+    PH_MARK(0);
     panel_factor<B, S, C::NWARP, true>(P, B, Rb, tau, Z);
+    PH_MARK(1);
     if (warp == 0) build_t<S>(Tp, tau, Z);
     __syncthreads();
+    PH_MARK(2);
     double* dst = Aik + (size_t)c0 * B;
     for (int e = tid; e < B * S; e += C::NT) {
       const double v = P[e];
@@ -154,14 +177,25 @@ __device__ __noinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, do
       __stcg(Tik + (size_t)l * S * S + e, v);
       Ts[swz<S>(r, c)] = v;
     }
-    __syncthreads();
+    __syncthreads();  // Rb/Z/tau dead from here: their space is reused by c1s / xbuf
+    for (int e = tid; e < B * S; e += C::NT) __stcg(Ypi + (size_t)l * B * S + e, Ys[e]);
+    for (int e = tid; e < S * S; e += C::NT) __stcg(Tpi + (size_t)l * S * S + e, Ts[e]);
+    PH_MARK(3);
+    double* c1s = sm + L::C1S + gi * C::C1W;
     for (int g = (c0 + S) / 8 + gi; g < B / 8; g += C::GPS) {
       double acc[C::RW / 8][2];
-      load_cols<B, C::RW>(acc, Aik, 8 * g, t0, 0);
-      group_apply<B, S, true, true>(sm, acc, Ys, Ts, Akk, c0, 8 * g, t0, 0, gi, rpart);
-      store_cols<B, C::RW>(acc, Aik, 8 * g, t0, 0);
+      load_cols<B, C::RW>(acc, Aik, 8 * g, t0);
+      if (rpart == 0) {
+        c1_fetch<B, S>(c1s, Akk, c0, 8 * g);
+        cp_async_wait<0>();
+        __syncwarp();
+      }
+      group_apply<B, S, C::RW, C::RS, true, true, true>(acc, Ys, Ts, c1s, Akk, c0, 8 * g, t0, gi, rpart,
+                                                        sm + L::XBUF + gi * C::RS * C::XW);
+      store_cols<B, C::RW>(acc, Aik, 8 * g, t0);
     }
     __syncthreads();
+    PH_MARK(4);
   }
 }
 
@@ -170,86 +204,125 @@ __device__ __noinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, do
 //   SS = false: C <- (I - U_l T_l^{T or 1} U_l^T) C for each l (U_l unit lower of V)
 //   SS = true : [C1; C] <- (I - [E_l; V_l] T_l^{T or 1} [E_l; V_l]^T) [C1; C]
 // QT = true: Q^T direction (l ascending, T_l^T); false: Q direction (l descending, T_l).
-// Y_l / T_l are double-buffered in shared memory by cp.async; the slice stays in
-// registers for the whole task.
+// Y_l, T_l and (SS) the slice's C1 block are staged by cp.async into double buffers; the
+// slice stays in registers for the whole task; one __syncthreads per inner block.
 // ---------------------------------------------------------------------------------------
-template <int B, int S, bool SS>
-__device__ __forceinline__ void issue_panel(double* Ys, double* Ts, const double* V, const double* Tsl, int l) {
-  using C = Cfg<B, S>;
-  const int tid = threadIdx.x;
-  const int c0 = l * S;
-  if (SS) {
-    for (int qd = tid; qd < B * S / 2; qd += C::NT) {
-      const int c = qd / (B / 2), r = 2 * (qd % (B / 2));
-      cp_async16(Ys + swz<B>(r, c), V + (size_t)(c0 + c) * B + r);
-    }
-  } else {
-    const int nr = B - c0 - S;  // rows below the s x s top block
-    for (int qd = tid; qd < nr * S / 2; qd += C::NT) {
-      const int c = qd / (nr / 2), r = c0 + S + 2 * (qd % (nr / 2));
-      cp_async16(Ys + swz<B>(r, c), V + (size_t)(c0 + c) * B + r);
-    }
-    // unit-lower top block: 1 on the diagonal, V_kk strictly below, 0 above (R is not read)
-    for (int e = tid; e < S * S; e += C::NT) {
-      const int r = e % S, c = e / S;
-      Ys[swz<B>(c0 + r, c)] = (r == c) ? 1.0 : (r > c ? __ldcg(V + (size_t)(c0 + c) * B + c0 + r) : 0.0);
-    }
-  }
-  for (int qd = tid; qd < S * S / 2; qd += C::NT) {
-    const int c = qd / (S / 2), r = 2 * (qd % (S / 2));
-    cp_async16(Ts + swz<S>(r, c), Tsl + (size_t)l * S * S + (size_t)c * S + r);
-  }
-  cp_async_commit();
+// Stage panel l (Y_l: B*S doubles, T_l: S*S) from the packed workspace into buffer `buf`
+// with two TMA bulk copies completing on mbarrier full[buf].  One thread.
+template <int B, int S>
+__device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const double* Tp, int l, int buf) {
+  using L = Layout<B, S>;
+  constexpr unsigned YB = B * S * 8, TB = S * S * 8;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
+  fence_proxy_async();
+  mbar_expect_tx(full + buf, YB + TB);
+  bulk_g2s(sm + (buf ? L::Y1 : L::Y0), Yp + (size_t)l * B * S, YB, full + buf);
+  bulk_g2s(sm + (buf ? L::T1 : L::T0), Tp + (size_t)l * S * S, TB, full + buf);
 }
 
+// Pipeline: two buffers; panels l0, l1 are issued at task start; the LAST warp to finish
+// with a buffer (shared-memory counter) issues its refill two panels ahead, so no
+// __syncthreads is needed inside the panel loop and the refill overlaps a whole panel of
+// math.  C1 (SS) is prefetched into registers one panel ahead by the group's rpart-0 warp.
 template <int B, int S, bool SS, bool QT>
-__device__ __noinline__ void task_update(double* sm, const double* V, const double* Tsl, double* C1, double* Ct,
-                                         int slice) {
+__device__ __forceinline__ void task_update(double* sm, const double* Yp, const double* Tp, double* C1, double* Ct,
+                                            int slice) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   constexpr int NL = B / S;
-  const int warp = threadIdx.x >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
   const int cg0 = slice * C::SLICE + gi * 8;
   const bool active = cg0 < B;
+  const bool top_owner = SS && active && rpart == 0;
+  double* c1s0 = sm + L::C1S + gi * C::C1W;           // C1 buffer for even li
+  double* c1s1 = sm + L::C1S + L::C1SZ + gi * C::C1W;  // C1 buffer for odd li
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
+  int* done = reinterpret_cast<int*>(full + 2);
+#ifdef TQR_PROFILE_PHASES
+  long long* s_ph = (long long*)(sm + Layout<B, S>::TOTAL);
+#endif
+  PH_T0;
   double acc[C::RW / 8][2];
-  if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0, 0);
-  issue_panel<B, S, SS>(sm + L::Y0, sm + L::T0, V, Tsl, QT ? 0 : NL - 1);
+  if (top_owner) c1_fetch<B, S>(c1s0, C1, (QT ? 0 : NL - 1) * S, cg0);
+  if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
+  if (threadIdx.x == 0) {
+    mbar_init(full, 1);
+    mbar_init(full + 1, 1);
+    done[0] = 0;
+    done[1] = 0;
+    fence_mbar_init();
+    issue_panel<B, S>(sm, Yp, Tp, QT ? 0 : NL - 1, 0);
+    if (NL > 1) issue_panel<B, S>(sm, Yp, Tp, QT ? 1 : NL - 2, 1);
+  }
+  __syncthreads();
+  PH_MARK(0);
   for (int li = 0; li < NL; ++li) {
     const int l = QT ? li : NL - 1 - li;
     const int buf = li & 1;
-    if (li + 1 < NL) {
-      const int ln = QT ? li + 1 : NL - 2 - li;
-      issue_panel<B, S, SS>(sm + (buf ? L::Y0 : L::Y1), sm + (buf ? L::T0 : L::T1), V, Tsl, ln);
-      cp_async_wait<1>();
-    } else {
-      cp_async_wait<0>();
+    if (top_owner) {
+      cp_async_wait<0>();  // this panel's C1 block
+      __syncwarp();
+      if (li + 1 < NL) c1_fetch<B, S>(buf ? c1s0 : c1s1, C1, (QT ? li + 1 : NL - 2 - li) * S, cg0);
     }
-    __syncthreads();
+    mbar_wait(full + buf, (li >> 1) & 1);
+    PH_MARK(1);
     if (active) {
-      const double* Yb = sm + (buf ? L::Y1 : L::Y0);
-      const double* Tb = sm + (buf ? L::T1 : L::T0);
-      group_apply<B, S, QT, SS>(sm, acc, Yb, Tb, C1, l * S, cg0, t0, SS ? 0 : (l * S) / 8, gi, rpart);
+      group_apply<B, S, C::RW, C::RS, QT, true, SS>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
+                                                     buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
+                                                     sm + L::XBUF + gi * C::RS * C::XW);
     }
-    __syncthreads();
+    PH_MARK(4);
+    __syncwarp();
+    if (lane == 0 && li + 2 < NL) {
+      if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
+        done[buf] = 0;
+        issue_panel<B, S>(sm, Yp, Tp, QT ? li + 2 : NL - 3 - li, buf);
+      }
+    }
+    PH_MARK(3);
   }
-  if (active) store_cols<B, C::RW>(acc, Ct, cg0, t0, 0);
+  if (active) store_cols<B, C::RW>(acc, Ct, cg0, t0);
+  __syncthreads();  // all reads of the staging buffers done before the next task reuses them
+  PH_MARK(5);
+}
+
+// LARFB body.  Every task body is inlined into the executor: with device-function calls
+// present, ptxas spilled the accumulators of the update path (call ABI register limits).
+template <int B, int S>
+__device__ __forceinline__ void task_larfb(double* sm, const double* Yp, const double* Tp, double* Ct, int slice) {
+  task_update<B, S, false, true>(sm, Yp, Tp, nullptr, Ct, slice);
 }
 
 // ---------------------------------------------------------------------------------------
 // Persistent executor.
 // ---------------------------------------------------------------------------------------
-template <int B, int S>
+// MODE 0: factorization (GEQRT/TSQRT out of line, LARFB/SSRFB inlined); MODE 1: apply Q^T;
+// MODE 2: apply Q.  Separate instances keep device-function calls out of the update paths.
+template <int B, int S, int MODE>
 __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_task[TASK_INTS];
   __shared__ int s_ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef TQR_PROFILE_PHASES
+  long long* s_ph = (long long*)(sm + Layout<B, S>::TOTAL);
+  if (tid < 8) s_ph[tid] = 0;
+  __syncthreads();
+#endif
   for (;;) {
+    PH_T0;
     if (tid == 0) s_ticket = atomicAdd(a.ticket, 1);
     __syncthreads();
     const int tk = s_ticket;
+#ifdef TQR_PROFILE_PHASES
+    if (tk >= a.ntasks) {
+      if (tid < 8 && a.phases) atomicAdd((unsigned long long*)&a.phases[tid], (unsigned long long)s_ph[tid]);
+      return;
+    }
+#else
     if (tk >= a.ntasks) return;
+#endif
     if (tid < TASK_INTS) s_task[tid] = a.tasks[(size_t)tk * TASK_INTS + tid];
     __syncthreads();
     unsigned long long t_grab = 0, t_start = 0;
@@ -270,48 +343,47 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
         }
       }
       __syncwarp();
+      fence_proxy_async();  // producer data (generic-proxy stores) -> our TMA reads
     }
     __syncthreads();
+    PH_MARK(6);
     if (a.trace && tid == 0) t_start = globaltimer();
     const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
     const int p = a.p;
-    switch (kind) {
-      case K_G:
-        task_geqrt<B, S>(sm, tile_ptr(a.A, k, k, p, B), tslot_ptr(a.T, k, k, p, B, S));
-        break;
-      case K_T:
-        task_tsqrt<B, S>(sm, tile_ptr(a.A, k, k, p, B), tile_ptr(a.A, i, k, p, B), tslot_ptr(a.T, i, k, p, B, S));
-        break;
-      case K_L:
-        task_update<B, S, false, true>(sm, tile_ptr(a.A, k, k, p, B), tslot_ptr(a.T, k, k, p, B, S), nullptr,
-                                       tile_ptr(a.A, k, j, p, B), sl);
-        break;
-      case K_S:
-        task_update<B, S, true, true>(sm, tile_ptr(a.A, i, k, p, B), tslot_ptr(a.T, i, k, p, B, S),
-                                      tile_ptr(a.A, k, j, p, B), tile_ptr(a.A, i, j, p, B), sl);
-        break;
-      case K_LQT:
-        task_update<B, S, false, true>(sm, tile_ptr(a.A, k, k, p, B), tslot_ptr(a.T, k, k, p, B, S), nullptr,
-                                       tile_ptr(a.Bt, k, j, p, B), sl);
-        break;
-      case K_SQT:
-        task_update<B, S, true, true>(sm, tile_ptr(a.A, i, k, p, B), tslot_ptr(a.T, i, k, p, B, S),
-                                      tile_ptr(a.Bt, k, j, p, B), tile_ptr(a.Bt, i, j, p, B), sl);
-        break;
-      case K_LQ:
-        task_update<B, S, false, false>(sm, tile_ptr(a.A, k, k, p, B), tslot_ptr(a.T, k, k, p, B, S), nullptr,
-                                        tile_ptr(a.Bt, k, j, p, B), sl);
-        break;
-      case K_SQ:
-        task_update<B, S, true, false>(sm, tile_ptr(a.A, i, k, p, B), tslot_ptr(a.T, i, k, p, B, S),
-                                       tile_ptr(a.Bt, k, j, p, B), tile_ptr(a.Bt, i, j, p, B), sl);
-        break;
-      default:
-        break;
+    if (MODE == 0) {
+      switch (kind) {
+        case K_G:
+          task_geqrt<B, S>(sm, tile_ptr(a.A, k, k, p, B), tslot_ptr(a.T, k, k, p, B, S), tile_ptr(a.Yp, k, k, p, B),
+                           tslot_ptr(a.Tp, k, k, p, B, S));
+          break;
+        case K_T:
+          task_tsqrt<B, S>(sm, tile_ptr(a.A, k, k, p, B), tile_ptr(a.A, i, k, p, B), tslot_ptr(a.T, i, k, p, B, S),
+                           tile_ptr(a.Yp, i, k, p, B), tslot_ptr(a.Tp, i, k, p, B, S));
+          break;
+        case K_L:
+          task_larfb<B, S>(sm, tile_ptr(a.Yp, k, k, p, B), tslot_ptr(a.Tp, k, k, p, B, S), tile_ptr(a.A, k, j, p, B),
+                           sl);
+          break;
+        case K_S:
+          task_update<B, S, true, true>(sm, tile_ptr(a.Yp, i, k, p, B), tslot_ptr(a.Tp, i, k, p, B, S),
+                                        tile_ptr(a.A, k, j, p, B), tile_ptr(a.A, i, j, p, B), sl);
+          break;
+        default:
+          break;
+      }
+    } else {
+      constexpr bool QT = MODE == 1;
+      if (kind == K_LQT || kind == K_LQ)
+        task_update<B, S, false, QT>(sm, tile_ptr(a.Yp, k, k, p, B), tslot_ptr(a.Tp, k, k, p, B, S), nullptr,
+                                     tile_ptr(a.Bt, k, j, p, B), sl);
+      else
+        task_update<B, S, true, QT>(sm, tile_ptr(a.Yp, i, k, p, B), tslot_ptr(a.Tp, i, k, p, B, S),
+                                    tile_ptr(a.Bt, k, j, p, B), tile_ptr(a.Bt, i, j, p, B), sl);
     }
     __syncthreads();
     if (tid == 0) {
       __threadfence();
+      fence_proxy_async();
       st_release(a.ctr + s_task[5], s_task[6]);
       if (a.trace) {
         unsigned long long* tr = a.trace + (size_t)tk * 4;
@@ -331,28 +403,40 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
 #define TQR_INSTANCES(X) \
   X(16, 8) X(16, 16) X(32, 8) X(32, 32) X(64, 16) X(64, 64) X(128, 32) X(256, 32)
 
-template <int B, int S>
-static cudaError_t launch_one(const ExecArgs& a, int grid, cudaStream_t st) {
+template <int B, int S, int MODE>
+static cudaError_t launch_mode(const ExecArgs& a, int grid, cudaStream_t st) {
   using L = Layout<B, S>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(exec_kernel<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaError_t e =
+        cudaFuncSetAttribute(exec_kernel<B, S, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   ExecArgs args = a;
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((const void*)exec_kernel<B, S>, dim3(grid), dim3(Cfg<B, S>::NT), params, L::BYTES,
-                                     st);
+  return cudaLaunchCooperativeKernel((const void*)exec_kernel<B, S, MODE>, dim3(grid), dim3(Cfg<B, S>::NT), params,
+                                     L::BYTES, st);
+}
+template <int B, int S>
+static cudaError_t launch_one(const ExecArgs& a, int mode, int grid, cudaStream_t st) {
+  if (mode == 1) return launch_mode<B, S, 1>(a, grid, st);
+  if (mode == 2) return launch_mode<B, S, 2>(a, grid, st);
+  return launch_mode<B, S, 0>(a, grid, st);
 }
 
 template <int B, int S>
 static int max_ctas_one(int device) {
   using L = Layout<B, S>;
-  cudaFuncSetAttribute(exec_kernel<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-  int per_sm = 0, sms = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exec_kernel<B, S>, Cfg<B, S>::NT, L::BYTES) != cudaSuccess)
-    return 0;
+  int per_sm = 0, sms = 0, worst = 1 << 30;
+  const void* fns[3] = {(const void*)exec_kernel<B, S, 0>, (const void*)exec_kernel<B, S, 1>,
+                        (const void*)exec_kernel<B, S, 2>};
+  for (const void* f : fns) {
+    cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, Cfg<B, S>::NT, L::BYTES) != cudaSuccess) return 0;
+    worst = per_sm < worst ? per_sm : worst;
+  }
+  per_sm = worst;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   return per_sm * sms;
 }
@@ -364,8 +448,8 @@ bool exec_supported(int b, int s) {
   return false;
 }
 
-cudaError_t launch_exec(int b, int s, const ExecArgs& a, int grid, cudaStream_t st) {
-#define X(BB, SS) if (b == BB && s == SS) return launch_one<BB, SS>(a, grid, st);
+cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cudaStream_t st) {
+#define X(BB, SS) if (b == BB && s == SS) return launch_one<BB, SS>(a, mode, grid, st);
   TQR_INSTANCES(X)
 #undef X
   return cudaErrorInvalidValue;
@@ -429,6 +513,43 @@ __global__ void eye_tiles_kernel(double* __restrict__ Qt, int64_t m, int64_t k, 
   }
 }
 
+// Packed reflector panels for apply-Q from the boundary factors (At, T): the same Yp/Tp
+// contents the factorization writes, one thread per element of the lower tile triangle.
+template <int B, int S>
+__global__ void pack_factors_kernel(const double* __restrict__ A, const double* __restrict__ T, double* __restrict__ Yp,
+                                    double* __restrict__ Tp, int p, int K) {
+  const int64_t bb = (int64_t)B * B;
+  const int64_t total = (int64_t)p * K * bb;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tile = e / bb;
+    const int in = (int)(e % bb);
+    const int i = (int)(tile % p), k = (int)(tile / p);
+    if (i < k) continue;
+    // element `in` of the packed tile: panel l, swizzled position -> (r, c) of the panel
+    const int l = in / (B * S), q = in % (B * S);
+    const int blk = q >> 6, w = q & 63;
+    const int cb = blk / (B / 8), rb = blk % (B / 8);
+    const int cc = w >> 3;
+    const int c = cb * 8 + cc, r = rb * 8 + ((w & 7) ^ (c & 6));
+    const double* At = A + tile * bb;
+    const int gc = l * S + c;  // column inside the tile
+    double y;
+    if (i > k) {
+      y = At[(size_t)gc * B + r];
+    } else {
+      y = r < gc ? 0.0 : (r == gc ? 1.0 : At[(size_t)gc * B + r]);
+    }
+    Yp[tile * bb + in] = y;
+    if (q < S * S) {  // T block l of slot (i, k) in swz<S>
+      const int tb = q >> 6, tw = q & 63;
+      const int tcb = tb / (S / 8), trb = tb % (S / 8);
+      const int tc = tcb * 8 + (tw >> 3), tr = trb * 8 + ((tw & 7) ^ (tc & 6));
+      const int64_t slot = tile * (int64_t)S * B;
+      Tp[slot + (int64_t)l * S * S + q] = T[slot + (int64_t)l * S * S + (int64_t)tc * S + tr];
+    }
+  }
+}
+
 static int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
@@ -453,6 +574,16 @@ cudaError_t launch_get_r(const double* At, double* R, int64_t ldr, int64_t m, in
   get_r_kernel<<<grid_for(k * n), 256, 0, st>>>(At, R, ldr, m, n, b, p);
   return cudaGetLastError();
 }
+cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, double* Tp, int b, int s, int64_t p,
+                                int64_t K, cudaStream_t st) {
+  const int64_t total = p * K * (int64_t)b * b;
+#define X(BB, SS) \
+  if (b == BB && s == SS) { pack_factors_kernel<BB, SS><<<grid_for(total), 256, 0, st>>>(A, T, Yp, Tp, (int)p, (int)K); return cudaGetLastError(); }
+  TQR_INSTANCES(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qb, cudaStream_t st) {
   const int64_t total = p * qb * (int64_t)b * b;
   eye_tiles_kernel<<<grid_for(total), 256, 0, st>>>(Qt, m, k, b, p, total);

@@ -165,15 +165,16 @@ static bool list_schedule(TaskGen& G, int workers, int nctr, Sched& out) {
 }
 
 // Rough per-task durations (ns) for the list schedule only (never affect results):
-// fp64 DMMA peak per SM ~251 GFLOP/s (M0 probe), assumed efficiencies per kind.
+// fp64 DMMA peak per SM ~251 GFLOP/s (M0 probe), efficiencies per kind as measured by
+// tools/prof_tasks.py (r01: GEQRT ~9%, TSQRT ~14%, LARFB ~34%, SSRFB ~60% of the SM peak).
 struct DurModel {
   double g, t, l, s;
   DurModel(int b, int s_, int w) {
     const double B = b, Sv = s_, W = w, sm = 251.0;  // GFLOP/s per SM == flop/ns
-    g = 3000 + (4.0 / 3 * B * B * B + 2.0 / 3 * Sv * B * B) / (0.15 * sm);
-    t = 3000 + (2.0 * B * B * B + 4.0 / 3 * Sv * B * B) / (0.30 * sm);
-    l = 1500 + (2.0 * B * B * W + Sv * B * W) / (0.6 * sm);
-    s = 1500 + (4.0 * B * B * W + Sv * B * W) / (0.8 * sm);
+    g = 3000 + (4.0 / 3 * B * B * B + 2.0 / 3 * Sv * B * B) / (0.09 * sm);
+    t = 3000 + (2.0 * B * B * B + 4.0 / 3 * Sv * B * B) / (0.14 * sm);
+    l = 1500 + (2.0 * B * B * W + Sv * B * W) / (0.34 * sm);
+    s = 1500 + (4.0 * B * B * W + Sv * B * W) / (0.6 * sm);
   }
 };
 
@@ -191,7 +192,8 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, int 
     out.counts[0]++;
     for (int j = k + 1; j < q; ++j)
       for (int sl = 0; sl < nsl; ++sl) {
-        id = G.add(K_L, k, k, j, sl, COL(k, j, sl), 1, dm.l, 2);
+        // lookahead (R10): updates of column k+1 feed panel k+1 -> critical path
+        id = G.add(K_L, k, k, j, sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
         G.dep(id, PANEL(k), 1, 1);
         if (k > 0) G.dep(id, COL(k - 1, j, sl), 1, 2);
         out.counts[2]++;
@@ -203,7 +205,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, int 
       out.counts[1]++;
       for (int j = k + 1; j < q; ++j)
         for (int sl = 0; sl < nsl; ++sl) {
-          id = G.add(K_S, k, i, j, sl, COL(k, j, sl), i - k + 1, dm.s, 3);
+          id = G.add(K_S, k, i, j, sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
           G.dep(id, PANEL(k), 1, i - k + 1);
           G.dep(id, COL(k, j, sl), 1, i - k);
           if (k > 0) G.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
@@ -261,6 +263,7 @@ struct DevSched {
   int* d_tasks = nullptr;
   int ntasks = 0;
   int nctr = 0;
+  int mode = 0;  // executor instance: 0 factorization, 1 apply Q^T, 2 apply Q
 };
 
 }  // namespace
@@ -276,6 +279,7 @@ struct tqr_plan {
   int nctr_cap = 0;
   int* d_ticket = nullptr;
   unsigned long long* d_trace = nullptr;
+  long long* d_phases = nullptr;  // set by tqr_phase_counters (profiling builds)
   int trace_cap = 0;
   int trace_n = 0;
 };
@@ -284,7 +288,7 @@ static tqr_status upload(tqr_plan* P, const Sched& s, DevSched& d) {
   CU(cudaMalloc(&d.d_tasks, s.rec.size() * sizeof(int) + 16));
   CU(cudaMemcpy(d.d_tasks, s.rec.data(), s.rec.size() * sizeof(int), cudaMemcpyHostToDevice));
   d.ntasks = s.ntasks;
-  d.nctr = s.nctr;
+  d.nctr = s.nctr;  // (mode is set by the caller)
   if (s.nctr > P->nctr_cap) {
     if (P->d_ctr) cudaFree(P->d_ctr);
     CU(cudaMalloc(&P->d_ctr, sizeof(int) * (size_t)std::max(1, s.nctr)));
@@ -293,18 +297,21 @@ static tqr_status upload(tqr_plan* P, const Sched& s, DevSched& d) {
   return TQR_OK;
 }
 
-static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, double* Bt, bool trace) {
+static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, double* Bt, void* work, bool trace) {
   if (d.ntasks == 0) return TQR_OK;
   CU(cudaMemsetAsync(P->d_ctr, 0, sizeof(int) * (size_t)std::max(1, d.nctr), P->st));
   CU(cudaMemsetAsync(P->d_ticket, 0, sizeof(int), P->st));
   ExecArgs a;
   a.A = A; a.T = T; a.Bt = Bt;
+  a.Yp = reinterpret_cast<double*>(work);
+  a.Tp = a.Yp + (size_t)P->p * P->q * P->prm.b * P->prm.b;
   a.tasks = d.d_tasks;
   a.ntasks = d.ntasks;
   a.p = (int)P->p;
   a.ticket = P->d_ticket;
   a.ctr = P->d_ctr;
   a.trace = nullptr;
+  a.phases = P->d_phases;
   if (trace) {
     if (P->trace_cap < d.ntasks) {
       if (P->d_trace) cudaFree(P->d_trace);
@@ -315,7 +322,7 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
     P->trace_n = d.ntasks;
   }
   const int grid = std::min(P->workers, std::max(1, d.ntasks));
-  CU(launch_exec(P->prm.b, P->prm.s, a, grid, P->st));
+  CU(launch_exec(P->prm.b, P->prm.s, d.mode, a, grid, P->st));
   return TQR_OK;
 }
 
@@ -425,9 +432,13 @@ tqr_status tqr_tiles_size(const tqr_plan* P, size_t* a, size_t* t) {
   if (t) *t = (size_t)P->p * P->q * s * b;
   return TQR_OK;
 }
+static size_t work_bytes(const tqr_plan* P) {
+  const size_t b = (size_t)P->prm.b, s = (size_t)P->prm.s;
+  return ((size_t)P->p * P->q * b * b + (size_t)P->p * P->q * s * b) * sizeof(double);
+}
 tqr_status tqr_workspace_size(const tqr_plan* P, size_t* bytes) {
   if (!P) return bad_arg(1, "plan is NULL");
-  if (bytes) *bytes = 0;
+  if (bytes) *bytes = work_bytes(P);
   return TQR_OK;
 }
 
@@ -460,9 +471,10 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   if (!P) return bad_arg(1, "plan is NULL");
   if (!At) return bad_arg(2, "At is NULL");
   if (!T) return bad_arg(3, "T is NULL");
+  if (!work) return bad_arg(4, "work is NULL (tqr_workspace_size bytes required)");
   const size_t tsz = (size_t)P->p * P->q * P->prm.s * P->prm.b;
   CU(cudaMemsetAsync(T, 0, tsz * sizeof(double), P->st));
-  return run(P, P->fact, At, T, nullptr, (P->prm.flags & TQR_FLAG_TRACE) != 0);
+  return run(P, P->fact, At, T, nullptr, work, (P->prm.flags & TQR_FLAG_TRACE) != 0);
 }
 
 static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** out) {
@@ -481,6 +493,7 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
       return TQR_ERR_UNSUPPORTED;
     }
     DevSched d;
+    d.mode = trans ? 1 : 2;
     tqr_status st = upload(P, s, d);
     if (st != TQR_OK) return st;
     it = P->orm.emplace(key, d).first;
@@ -497,10 +510,14 @@ tqr_status tqr_ormqr(tqr_plan* P, char trans, const double* At, const double* T,
   if (!T) return bad_arg(4, "T is NULL");
   if (!Bt) return bad_arg(5, "Bt is NULL");
   if (nrhs < 1) return bad_arg(6, "nrhs < 1");
+  if (!work) return bad_arg(7, "work is NULL (tqr_workspace_size bytes required)");
   DevSched* d = nullptr;
   tqr_status st = orm_sched(P, trans == 'T' || trans == 't', nrhs, &d);
   if (st != TQR_OK) return st;
-  return run(P, *d, const_cast<double*>(At), const_cast<double*>(T), Bt, false);
+  double* Yp = reinterpret_cast<double*>(work);
+  double* Tp = Yp + (size_t)P->p * P->q * P->prm.b * P->prm.b;
+  CU(launch_pack_factors(At, T, Yp, Tp, P->prm.b, P->prm.s, P->p, P->K, P->st));
+  return run(P, *d, const_cast<double*>(At), const_cast<double*>(T), Bt, work, false);
 }
 
 tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, double* Qt, void* work) {
@@ -509,6 +526,7 @@ tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, 
   if (!T) return bad_arg(3, "T is NULL");
   if (k < 1 || k > P->prm.m) return bad_arg(4, "k outside [1, m]");
   if (!Qt) return bad_arg(5, "Qt is NULL");
+  if (!work) return bad_arg(6, "work is NULL (tqr_workspace_size bytes required)");
   const int64_t qb = (k + P->prm.b - 1) / P->prm.b;
   CU(launch_eye_tiles(Qt, P->prm.m, k, P->prm.b, P->p, qb, P->st));
   return tqr_ormqr(P, 'N', At, T, Qt, k, work);
@@ -561,6 +579,52 @@ tqr_status tqr_trace_fetch(tqr_plan* P, int64_t* rec, int64_t cap, int64_t* n) {
     o[7] = (int64_t)raw[r * 4 + 3];
   }
   *n = cnt;
+  return TQR_OK;
+}
+
+tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* At, double* T, void* work) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (kind < 0 || kind > 7) return bad_arg(2, "kind outside [0, 7]");
+  if (count < 1 || count > (1 << 24)) return bad_arg(3, "count outside [1, 2^24]");
+  if (!At) return bad_arg(4, "At is NULL");
+  if (!T) return bad_arg(5, "T is NULL");
+  if (P->p < 2 || P->q < 2) {
+    g_err = "profiling needs p >= 2 and q >= 2";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  Sched s;
+  s.rec.assign((size_t)count * TASK_INTS, 0);
+  for (int64_t t = 0; t < count; ++t) {
+    int* q = &s.rec[(size_t)t * TASK_INTS];
+    const int i = 1 + (int)(t % (P->p - 1));
+    const int j = 1 + (int)((t / (P->p - 1)) % (P->q - 1));
+    q[0] = kind;
+    q[1] = kind == 0 ? (int)(t % P->K) : 0;
+    const bool lkind = kind == 2 || kind == 4 || kind == 6;
+    q[2] = (kind == 0 || lkind) ? q[1] : i;
+    q[3] = (kind == 0 || kind == 1) ? q[1] : j;
+    q[4] = (int)(t % P->nsl);
+    q[5] = 0;
+    q[6] = 1;
+  }
+  s.ntasks = (int)count;
+  s.nctr = 1;
+  DevSched d;
+  d.mode = kind >= 6 ? 2 : (kind >= 4 ? 1 : 0);
+  tqr_status st = upload(P, s, d);
+  if (st != TQR_OK) return st;
+  if (!work) return bad_arg(6, "work is NULL");
+  st = run(P, d, At, T, At, work, false);
+  cudaStreamSynchronize(P->st);
+  cudaFree(d.d_tasks);
+  return st;
+}
+
+// Profiling builds (-DTQR_PROFILE_PHASES): attach a device array of 8 int64 phase-cycle
+// totals (NULL detaches).  Not declared in tqr.h: development aid only.
+tqr_status tqr_phase_counters(tqr_plan* P, long long* d_counters) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  P->d_phases = d_counters;
   return TQR_OK;
 }
 

@@ -29,17 +29,21 @@ struct ExecArgs {
   double* A;          // tile-major factors (p x q tiles)
   double* T;          // T slots (p x q slots of s*b)
   double* Bt;         // apply-Q target, tile-major with p row tiles
+  double* Yp;         // workspace: packed reflector panels (p x q tiles of b*b)
+  double* Tp;         // workspace: packed T blocks (p x q slots of s*b)
   const int* tasks;   // TASK_INTS per task, dispatch order
   int ntasks;
   int p;              // row tiles (same for A and Bt)
   int* ticket;        // next ticket (reset to 0 before the launch)
   int* ctr;           // monotone progress counters (reset to 0)
   unsigned long long* trace;  // 4 per task or nullptr
+  long long* phases;          // TQR_PROFILE_PHASES builds: 8 phase-cycle totals, or nullptr
 };
 
 // Launch the persistent executor for tile size b, inner block s.  Returns cudaSuccess or
 // the launch error; *grid_out receives the co-resident grid used.
-cudaError_t launch_exec(int b, int s, const ExecArgs& a, int grid, cudaStream_t st);
+// mode: 0 factorization, 1 apply Q^T, 2 apply Q.
+cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cudaStream_t st);
 // Max co-resident CTAs for (b, s) on this device (0 if no instance).
 int exec_max_ctas(int b, int s, int device);
 bool exec_supported(int b, int s);
@@ -52,6 +56,8 @@ cudaError_t launch_unpack(const double* At, double* A, int64_t lda, int64_t m, i
                           cudaStream_t st);
 cudaError_t launch_get_r(const double* At, double* R, int64_t ldr, int64_t m, int64_t n, int b, int64_t p,
                          cudaStream_t st);
+cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, double* Tp, int b, int s, int64_t p,
+                                int64_t K, cudaStream_t st);
 cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qb, cudaStream_t st);
 
 }  // namespace tqr

@@ -9,7 +9,8 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtqr.so")
+# TQR_LIB selects a profiling build (libtqr_phases.so); default is the product library.
+LIB_PATH = os.environ.get("TQR_LIB") or os.path.join(HERE, "libtqr.so")
 
 TQR_OK = 0
 TQR_FLAG_TRACE = 1
@@ -65,6 +66,8 @@ def lib():
         L.tqr_supported.restype = _i32
         L.tqr_schedule_inspect.argtypes = [_i64, _i64, _i32, _i32, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]
         L.tqr_trace_fetch.argtypes = [_vp, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)]
+        L.tqr_profile_tasks.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp]
+        L.tqr_phase_counters.argtypes = [_vp, _vp]
         _lib = L
     return _lib
 
@@ -149,11 +152,24 @@ class Plan:
         _check(lib().tqr_tiles_size(self._h, ctypes.byref(a), ctypes.byref(t)))
         return a.value, t.value
 
+    def workspace_size(self) -> int:
+        w = ctypes.c_size_t()
+        _check(lib().tqr_workspace_size(self._h, ctypes.byref(w)))
+        return w.value
+
     def alloc(self):
+        """Tile array At and T slots (caller-owned; the plan's workspace is allocated lazily)."""
         import torch
         a, t = self.tiles_size()
         dev = self.stream.device
         return torch.empty(a, dtype=torch.float64, device=dev), torch.empty(t, dtype=torch.float64, device=dev)
+
+    def work(self):
+        """The plan's device workspace (tqr_workspace_size bytes), allocated on first use."""
+        import torch
+        if getattr(self, "_work", None) is None:
+            self._work = torch.empty(max(1, self.workspace_size()), dtype=torch.uint8, device=self.stream.device)
+        return self._work
 
     def pack(self, A, At):
         """A: (n, m) row-major view of a column-major m x n matrix, i.e. A.T contiguous
@@ -164,20 +180,31 @@ class Plan:
     def unpack(self, At, A):
         _check(lib().tqr_unpack(self._h, _ptr(At), _ptr(A), self.m))
 
-    def geqrf(self, At, T):
-        _check(lib().tqr_geqrf(self._h, _ptr(At), _ptr(T), None))
+    def geqrf(self, At, T, work=None):
+        w = self.work() if work is None else work
+        _check(lib().tqr_geqrf(self._h, _ptr(At), _ptr(T), w.data_ptr()))
 
     def get_r(self, At, R):
         _check(lib().tqr_get_r(self._h, _ptr(At), _ptr(R), min(self.m, self.n)))
 
-    def ormqr(self, trans: str, At, T, Bt, nrhs: int):
-        _check(lib().tqr_ormqr(self._h, trans.encode(), _ptr(At), _ptr(T), _ptr(Bt), nrhs, None))
+    def ormqr(self, trans: str, At, T, Bt, nrhs: int, work=None):
+        w = self.work() if work is None else work
+        _check(lib().tqr_ormqr(self._h, trans.encode(), _ptr(At), _ptr(T), _ptr(Bt), nrhs, w.data_ptr()))
 
-    def orgqr(self, At, T, k: int, Qt):
-        _check(lib().tqr_orgqr(self._h, _ptr(At), _ptr(T), k, _ptr(Qt), None))
+    def orgqr(self, At, T, k: int, Qt, work=None):
+        w = self.work() if work is None else work
+        _check(lib().tqr_orgqr(self._h, _ptr(At), _ptr(T), k, _ptr(Qt), w.data_ptr()))
 
     def sync(self):
         _check(lib().tqr_sync(self._h))
+
+    def profile_tasks(self, kind: int, count: int, At, T):
+        """Run `count` independent tasks of one kind (0 G, 1 T, 2 L, 3 S); timing only."""
+        _check(lib().tqr_profile_tasks(self._h, kind, count, _ptr(At), _ptr(T), self.work().data_ptr()))
+
+    def phase_counters(self, d_counters):
+        """Attach an int64 CUDA tensor of 8 phase-cycle totals (profiling builds only)."""
+        _check(lib().tqr_phase_counters(self._h, None if d_counters is None else d_counters.data_ptr()))
 
     def trace(self, cap: int = 1 << 22):
         import numpy as np

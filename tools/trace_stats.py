@@ -1,0 +1,37 @@
+"""Summarise a bench.py --trace JSON: per-kind durations, SM utilisation over time, panel
+critical-path timing.  Development aid."""
+import json
+import sys
+
+import numpy as np
+
+d = json.load(open(sys.argv[1]))
+r = np.array(d["records"], dtype=np.int64)
+kind, k, i, j, sl, sm, st, en = r.T
+t0 = st.min()
+st = (st - t0) / 1e3
+en = (en - t0) / 1e3
+dur = en - st
+T = en.max()
+nsm = len(set(sm.tolist()))
+print(f"makespan {T / 1e3:.1f} ms, tasks {len(r)}, SMs {nsm}")
+for kd, name in enumerate("GTLS"):
+    m = kind == kd
+    if m.any():
+        print(f"  {name}: n={m.sum():6d} median {np.median(dur[m]):8.1f} us  total {dur[m].sum() / 1e3:9.1f} SM-ms "
+              f"({100 * dur[m].sum() / (nsm * T):.1f}% of SM-time)")
+print(f"  busy fraction {dur.sum() / (nsm * T):.3f}")
+g = np.where(kind == 0)[0]
+gs = st[g][np.argsort(k[g])]
+print("  G(k) start (ms) every 8th:", np.round(gs[::8] / 1e3, 1))
+# panel chain: T tasks of step k: time from first to last
+for kk in [0, 1, 8, 32, 48, 60]:
+    m = (kind == 1) & (k == kk)
+    if m.any():
+        print(f"  step {kk}: T chain {st[m].min() / 1e3:.1f} -> {en[m].max() / 1e3:.1f} ms ({m.sum()} TSQRTs, "
+              f"median {np.median(dur[m]):.0f} us)")
+bins = np.linspace(0, T, 11)
+u = []
+for a, b in zip(bins[:-1], bins[1:]):
+    u.append(np.clip(np.minimum(en, b) - np.maximum(st, a), 0, None).sum() / (nsm * (b - a)))
+print("  utilisation by decile:", " ".join(f"{x:.2f}" for x in u))
