@@ -278,11 +278,12 @@ __device__ __forceinline__ void store_top_minus_r(const double (&c1)[S / 8][2], 
 // c1: the group's C1 block in registers (fragment layout of w; used by rpart 0 only);
 // top/row0: where C1 - W is stored.  xg: the group's RS partial buffers.  BAR2 protects
 // xg when the caller reuses it before all warps of the group have read it.
-template <int B, int S, int RW, int RS, bool QT, bool BAR2, bool HAS_C1>
+template <int B, int S, int RW, int RS, bool QT, bool BAR2>
 __device__ __forceinline__ void group_apply(double (&acc)[RW / 8][2], const double* __restrict__ Ys,
                                             const double* __restrict__ Ts, const double* c1s, double* top,
                                             int row0, int col0, int t0, int gi, int rpart, double* xg) {
   const int lane = threadIdx.x & 31;
+  const bool HAS_C1 = top != nullptr;  // SSRFB / TSQRT type: C1 block staged in c1s
   constexpr int XW = (S / 8) * 2 * 32;
   double w[S / 8][2], wn[S / 8][2];
 #pragma unroll
@@ -328,24 +329,24 @@ __device__ __forceinline__ void c1_fetch(double* c1s, const double* tile, int ro
 // Panel factorization of one inner block (s columns) in shared memory: dgeqr2-style,
 // rank-1 per column (R7), warp-shuffle norms and dot products.
 //
-//   TS = true  (TSQRT): P = B[:, c0:c0+S] (all B rows), the column's
+//   TS = true  (TSQRT): P rows [0, B) of the block's columns; the column's
 //              "top" lives in Rb (the s x s diagonal block of R, upper triangle); the
 //              reflector is [e_c; v], identity tops are mutually orthogonal.
-//   TS = false (GEQRT): P holds rows [c0, B) of A_kk[:, c0:c0+S];
-//              column jj's alpha is P[jj][jj], its x is P[jj+1 :][jj].
-// Column jj belongs to warp jj % NW (NW = warps in the CTA).  One __syncthreads per column: the owner of column
-// jj+1 updates it first and immediately generates the next reflector, overlapping the
-// other warps' updates.  Householder generator = DESIGN.md R2-R4 (oracle_house).
-// Outputs: P holds V_l, Rb / P's upper part holds the new R entries, tau[S], and
-// Z[t + jj*S] = u_t^T u_jj for t < jj (the DLARFT dot products).
+//   TS = false (GEQRT): P holds the tile rows, block columns; column jj's
+//              alpha is P[c0+jj][jj], its x is P[c0+jj+1 :][jj].
+// P column c at P + c*LDP.  Column jj belongs to warp jj % NW.  One __syncthreads per
+// column: the owner of column jj+1 updates it first and immediately generates the next
+// reflector, overlapping the other warps' updates.  Householder generator = DESIGN.md
+// R2-R4 (the oracle's), with v = x * (1/(alpha-beta)).  Outputs: P holds V_l (below the
+// diagonal for GEQRT), Rb / P's upper part the new R entries, tau[S].
 // ---------------------------------------------------------------------------------------
-template <int B, int S, int NW, bool TS>
-__device__ void panel_factor(double* P, int nrows, double* Rb, double* tau, double* Z) {
+template <int B, int S, int NW, int LDP>
+__device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, double* tau, const bool TS) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NR = (B + 31) / 32;  // rows per lane
-  auto top = [&](int r, int c) -> double& { return TS ? Rb[r + c * S] : P[r + c * B]; };
+  auto top = [&](int r, int c) -> double& { return TS ? Rb[r + c * S] : P[c0 + r + c * LDP]; };
+  auto lo_of = [&](int jj) { return TS ? 0 : c0 + jj + 1; };
 
-  // generate reflector for column jj (called by its owner warp, all lanes); sigma known
   auto house = [&](int jj, double sigma) {
     const double alpha = top(jj, jj);
     double beta, tv, scale;
@@ -355,72 +356,105 @@ __device__ void panel_factor(double* P, int nrows, double* Rb, double* tau, doub
       const double nu = sqrt(alpha * alpha + sigma);
       beta = (alpha >= 0.0) ? -nu : nu;
       tv = (beta - alpha) / beta;
-      scale = alpha - beta;
+      scale = 1.0 / (alpha - beta);
     }
-    const int lo = TS ? 0 : jj + 1;
-    for (int r = lo + lane; r < nrows; r += 32) P[r + jj * B] = (scale == 0.0) ? 0.0 : P[r + jj * B] / scale;
+    const int lo = lo_of(jj);
+#pragma unroll
+    for (int x = 0; x < NR; ++x) {
+      const int r = lane + 32 * x;
+      if (r >= lo && r < B) P[r + jj * LDP] *= scale;
+    }
     if (lane == 0) { top(jj, jj) = beta; tau[jj] = tv; }
   };
   auto colsq = [&](int jj) {
-    const int lo = TS ? 0 : jj + 1;
-    double sg = 0.0;
-    for (int r = lo + lane; r < nrows; r += 32) { const double x = P[r + jj * B]; sg += x * x; }
-    return warp_sum(sg);
+    const int lo = lo_of(jj);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int x = 0; x < NR; ++x) {
+      const int r = lane + 32 * x;
+      const double v = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
+      if (x & 1) s1 += v * v; else s0 += v * v;
+    }
+    return warp_sum(s0 + s1);
   };
 
   if (warp == 0) house(0, colsq(0));
   for (int jj = 0; jj < S; ++jj) {
     __syncthreads();  // v_jj, tau_jj visible
     const double tj = tau[jj];
-    const int lo = TS ? 0 : jj + 1;
-    // my columns, jj+1 first (it feeds the next reflector)
+    const int lo = lo_of(jj);
+    double vr[NR];
+#pragma unroll
+    for (int x = 0; x < NR; ++x) {
+      const int r = lane + 32 * x;
+      vr[x] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
+    }
+    // my columns c > jj: jj+1 first (it feeds the next reflector)
     const int first = (jj + 1 < S && (jj + 1) % NW == warp) ? jj + 1 : -1;
     for (int pass = 0; pass < 1 + (S + NW - 1) / NW; ++pass) {
       int c;
       if (pass == 0) { c = first; if (c < 0) continue; }
-      else { c = warp + (pass - 1) * NW; if (c >= S || c == jj || c == first) continue; }
-      double vr[NR], xr[NR];
-      double d = 0.0;
+      else { c = warp + (pass - 1) * NW; if (c <= jj || c == first || c >= S) continue; }
+      double xr[NR];
+      double d0 = 0.0, d1 = 0.0;
 #pragma unroll
       for (int x = 0; x < NR; ++x) {
         const int r = lane + 32 * x;
-        const bool ok = (r >= lo) && (r < nrows);
-        vr[x] = ok ? P[r + jj * B] : 0.0;
-        xr[x] = ok ? P[r + c * B] : 0.0;
-        d += vr[x] * xr[x];
+        xr[x] = (r >= lo && r < B) ? P[r + c * LDP] : 0.0;
+        if (x & 1) d1 += vr[x] * xr[x]; else d0 += vr[x] * xr[x];
       }
-      d = warp_sum(d);
-      if (c > jj) {
-        const double w = top(jj, c) + d;
-        const double tw = tj * w;
-        double sg = 0.0;
+      const double d = warp_sum(d0 + d1);
+      const double tw = tj * (top(jj, c) + d);
+      const int nlo = TS ? 0 : c0 + jj + 2;  // rows of the next column's x (GEQRT: below its alpha)
+      double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-        for (int x = 0; x < NR; ++x) {
-          const int r = lane + 32 * x;
-          if (r >= lo && r < nrows) {
-            const double nv = xr[x] - tw * vr[x];
-            P[r + c * B] = nv;
-            if (!TS && r == jj + 1) continue;  // GEQRT: row jj+1 is the next alpha, not in x
-            sg += nv * nv;
-          }
+      for (int x = 0; x < NR; ++x) {
+        const int r = lane + 32 * x;
+        if (r >= lo && r < B) {
+          const double nv = xr[x] - tw * vr[x];
+          P[r + c * LDP] = nv;
+          if (r >= nlo) { if (x & 1) s1 += nv * nv; else s0 += nv * nv; }
         }
-        if (lane == 0) top(jj, c) -= tw;
-        if (c == jj + 1) {
-          sg = warp_sum(sg);
-          __syncwarp();
-          house(c, sg);
-        }
-      } else {
-        // DLARFT dot: u_c^T u_jj (c < jj); GEQRT's u_c has A[jj][c] at row jj
-        if (lane == 0) Z[c + jj * S] = (TS ? 0.0 : P[jj + c * B]) + d;
+      }
+      if (lane == 0) top(jj, c) -= tw;
+      if (c == jj + 1) {
+        const double sg = warp_sum(s0 + s1);
+        __syncwarp();
+        house(c, sg);
       }
     }
   }
   __syncthreads();
 }
 
-// T_l from tau and the dot products Z (forward column-wise DLARFT, PAPER.md:153-157;
-// same recurrence and summation order as the oracle's larft_column):
+// Gram matrix of the staged panel (DLARFT dot products): Z[a + b*S] = Y[:, a]^T Y[:, b]
+// for the upper block triangle, by DMMA on the swizzled Ys (GEQRT: Y = U_l with its unit
+// diagonal and zeros above; TSQRT: Y = V_l, identity tops orthogonal).
+template <int B, int S, int NW>
+__device__ void gram_upper(const double* __restrict__ Ys, double* Z) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
+  constexpr int NU = S / 8, NTILE = NU * (NU + 1) / 2;
+  for (int tile = warp; tile < NTILE; tile += NW) {
+    int u1 = 0, rem = tile;
+    while (rem >= NU - u1) { rem -= NU - u1; ++u1; }
+    const int u2 = u1 + rem;
+    double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+#pragma unroll 4
+    for (int t = 0; t < B / 8; ++t)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const double a = Ys[swz<B>(8 * t + 4 * h + j, 8 * u1 + pn)];
+        const double bb = Ys[swz<B>(8 * t + 4 * h + j, 8 * u2 + pn)];
+        if (t & 1) dmma(g1, a, bb); else dmma(g0, a, bb);
+      }
+    // element (m = lane>>2, n = 2j+h): Z[8u1 + phi(m)][8u2 + phi(2j+h)], phi(2j+h) = 4h+j
+#pragma unroll
+    for (int h = 0; h < 2; ++h) Z[(8 * u1 + pn) + (8 * u2 + 4 * h + j) * S] = g0[h] + g1[h];
+  }
+}
+
+// T_l from tau and the Gram matrix Z (forward column-wise DLARFT, PAPER.md:153-157;
+// same recurrence as the oracle's larft_column, inner sums split in 4 for latency):
 //   T[j][j] = tau_j ;  T[t][j] = -tau_j * sum_{t'=t}^{j-1} T[t][t'] Z[t'][j]
 // Tp: S x S plain column-major.  Executed by one warp.
 template <int S>
@@ -431,9 +465,16 @@ __device__ void build_t(double* Tp, const double* tau, const double* Z) {
   for (int jj = 0; jj < S; ++jj) {
     const double tj = tau[jj];
     for (int t = lane; t < jj; t += 32) {
-      double acc = 0.0;
-      for (int tp = t; tp < jj; ++tp) acc += Tp[t + tp * S] * Z[tp + jj * S];
-      Tp[t + jj * S] = -tj * acc;
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int tp = t;
+      for (; tp + 3 < jj; tp += 4) {
+        a0 += Tp[t + tp * S] * Z[tp + jj * S];
+        a1 += Tp[t + (tp + 1) * S] * Z[tp + 1 + jj * S];
+        a2 += Tp[t + (tp + 2) * S] * Z[tp + 2 + jj * S];
+        a3 += Tp[t + (tp + 3) * S] * Z[tp + 3 + jj * S];
+      }
+      for (; tp < jj; ++tp) a0 += Tp[t + tp * S] * Z[tp + jj * S];
+      Tp[t + jj * S] = -tj * ((a0 + a1) + (a2 + a3));
     }
     if (lane == 0) Tp[jj + jj * S] = tj;
     __syncwarp();

@@ -37,14 +37,16 @@ struct Layout {
   using C = Cfg<B, S>;
   static constexpr int YSZ = B * S;          // one Y buffer (swizzled panel)
   static constexpr int TSZ = S * S;
-  static constexpr int Y0 = 0, Y1 = YSZ;
-  static constexpr int T0 = 2 * YSZ, T1 = 2 * YSZ + TSZ;
+  // Y0 T0 | Y1 T1: the panel tasks overlay P (ld B+4) on the contiguous (Y1, T1) region
+  static constexpr int Y0 = 0, T0 = YSZ, Y1 = YSZ + TSZ, T1 = 2 * YSZ + TSZ;
+  static constexpr int LDP = B + 4;
+  static_assert(LDP * S <= YSZ + TSZ, "P overlay");
   static constexpr int XBUF = 2 * YSZ + 2 * TSZ;  // W partials, one per warp (RS > 1)
   static constexpr int XSZ = C::RS > 1 ? C::NWARP * C::XW : 0;
   static constexpr int C1S = XBUF + XSZ;          // C1 blocks, 2 buffers x GPS groups
   static constexpr int C1SZ = C::GPS * C::C1W;
-  // panel-only scratch, aliased onto the partial / C1 buffers (dead in panels until the
-  // trailing update, which starts after Rb/Z/tau are consumed)
+  // panel-only scratch (Rb, Z, tau; Rb reused for the plain T_l), aliased onto the partial /
+  // C1 buffers, which the panel task uses only in its left-looking phase
   static constexpr int RB = XBUF, ZZ = RB + TSZ, TAU = ZZ + TSZ;
   static constexpr int PANEL_END = TAU + S;
   static constexpr int UPD_END = C1S + 2 * C1SZ;
@@ -72,141 +74,6 @@ __device__ __forceinline__ double* tslot_ptr(double* base, int i, int k, int p, 
 //     diagonal tiles hold U_l (0 above the block, unit-lower top block, V below).
 //   Tp slot (i,k), block l: S*S doubles at tslot_ptr(Tp, i, k) + l*S*S, swz<S> layout.
 
-// ---------------------------------------------------------------------------------------
-// GEQRT(k): per inner block l, panel of rows [c0,B) x cols [c0,c0+S),
-// T_l, then the LARFB-type update of columns [c0+S, B) (Y rows < c0 are zero).
-// ---------------------------------------------------------------------------------------
-template <int B, int S>
-__device__ __forceinline__ void task_geqrt(double* sm, double* Akk, double* Tk, double* Ypk, double* Tpk) {
-  using C = Cfg<B, S>;
-  using L = Layout<B, S>;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
-  double* P = sm + L::Y1;
-  double* Ys = sm + L::Y0;
-  double* Tp = sm + L::T1;
-  double* Ts = sm + L::T0;
-  double* Z = sm + L::ZZ;
-  double* tau = sm + L::TAU;
-  for (int l = 0; l < B / S; ++l) {
-    const int c0 = l * S, nrows = B - c0;
-    for (int e = tid; e < nrows * S; e += C::NT) {
-      const int r = e % nrows, c = e / nrows;
-      P[r + c * B] = __ldcg(Akk + (size_t)(c0 + c) * B + c0 + r);
-    }
-    __syncthreads();
-    panel_factor<B, S, C::NWARP, false>(P, nrows, nullptr, tau, Z);
-    if (warp == 0) build_t<S>(Tp, tau, Z);
-    __syncthreads();
-    for (int e = tid; e < B * S; e += C::NT) {
-      const int r = e % B, c = e / B;
-      double y = 0.0;
-      if (r >= c0) {
-        const double v = P[(r - c0) + c * B];
-        __stcg(Akk + (size_t)(c0 + c) * B + r, v);
-        y = (r - c0 == c) ? 1.0 : (r - c0 > c ? v : 0.0);
-      }
-      Ys[swz<B>(r, c)] = y;
-    }
-    for (int e = tid; e < S * S; e += C::NT) {
-      const double v = Tp[e];
-      __stcg(Tk + (size_t)l * S * S + e, v);
-      Ts[swz<S>(e % S, e / S)] = v;
-    }
-    __syncthreads();
-    for (int e = tid; e < B * S; e += C::NT) __stcg(Ypk + (size_t)l * B * S + e, Ys[e]);
-    for (int e = tid; e < S * S; e += C::NT) __stcg(Tpk + (size_t)l * S * S + e, Ts[e]);
-    for (int g = (c0 + S) / 8 + gi; g < B / 8; g += C::GPS) {
-      double acc[C::RW / 8][2];
-      load_cols<B, C::RW>(acc, Akk, 8 * g, t0);
-      group_apply<B, S, C::RW, C::RS, true, true, false>(acc, Ys, Ts, nullptr, nullptr, 0, 8 * g, t0, gi, rpart,
-                                                         sm + L::XBUF + gi * C::RS * C::XW);
-      store_cols<B, C::RW>(acc, Akk, 8 * g, t0);
-    }
-    __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// TSQRT(k,i): per inner block l, panel of B[:, c0:c0+S] against the
-// s x s diagonal block of R, T_l, then the SSRFB-type update of R[c0:c0+S, c0+S:B] and
-// B[:, c0+S:B].  Only the upper triangle of A(k,k) is read or written.
-// ---------------------------------------------------------------------------------------
-template <int B, int S>
-__device__ __forceinline__ void task_tsqrt(double* sm, double* Akk, double* Aik, double* Tik, double* Ypi, double* Tpi) {
-  using C = Cfg<B, S>;
-  using L = Layout<B, S>;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
-  double* P = sm + L::Y1;
-  double* Ys = sm + L::Y0;
-  double* Tp = sm + L::T1;
-  double* Ts = sm + L::T0;
-  double* Rb = sm + L::RB;
-  double* Z = sm + L::ZZ;
-  double* tau = sm + L::TAU;
-#ifdef TQR_PROFILE_PHASES
-  long long* s_ph = (long long*)(sm + Layout<B, S>::TOTAL);
-#endif
-  PH_T0;
-  for (int l = 0; l < B / S; ++l) {
-    const int c0 = l * S;
-    const double* src = Aik + (size_t)c0 * B;
-    for (int e = tid; e < B * S; e += C::NT) P[e] = __ldcg(src + e);
-    for (int e = tid; e < S * S; e += C::NT) {
-      const int r = e % S, c = e / S;
-      Rb[e] = (r <= c) ? __ldcg(Akk + (size_t)(c0 + c) * B + c0 + r) : 0.0;
-    }
-    __syncthreads();
-    PH_MARK(0);
-    panel_factor<B, S, C::NWARP, true>(P, B, Rb, tau, Z);
-    PH_MARK(1);
-    if (warp == 0) build_t<S>(Tp, tau, Z);
-    __syncthreads();
-    PH_MARK(2);
-    double* dst = Aik + (size_t)c0 * B;
-    for (int e = tid; e < B * S; e += C::NT) {
-      const double v = P[e];
-      __stcg(dst + e, v);
-      Ys[swz<B>(e % B, e / B)] = v;
-    }
-    for (int e = tid; e < S * S; e += C::NT) {
-      const int r = e % S, c = e / S;
-      if (r <= c) __stcg(Akk + (size_t)(c0 + c) * B + c0 + r, Rb[e]);
-      const double v = Tp[e];
-      __stcg(Tik + (size_t)l * S * S + e, v);
-      Ts[swz<S>(r, c)] = v;
-    }
-    __syncthreads();  // Rb/Z/tau dead from here: their space is reused by c1s / xbuf
-    for (int e = tid; e < B * S; e += C::NT) __stcg(Ypi + (size_t)l * B * S + e, Ys[e]);
-    for (int e = tid; e < S * S; e += C::NT) __stcg(Tpi + (size_t)l * S * S + e, Ts[e]);
-    PH_MARK(3);
-    double* c1s = sm + L::C1S + gi * C::C1W;
-    for (int g = (c0 + S) / 8 + gi; g < B / 8; g += C::GPS) {
-      double acc[C::RW / 8][2];
-      load_cols<B, C::RW>(acc, Aik, 8 * g, t0);
-      if (rpart == 0) {
-        c1_fetch<B, S>(c1s, Akk, c0, 8 * g);
-        cp_async_wait<0>();
-        __syncwarp();
-      }
-      group_apply<B, S, C::RW, C::RS, true, true, true>(acc, Ys, Ts, c1s, Akk, c0, 8 * g, t0, gi, rpart,
-                                                        sm + L::XBUF + gi * C::RS * C::XW);
-      store_cols<B, C::RW>(acc, Aik, 8 * g, t0);
-    }
-    __syncthreads();
-    PH_MARK(4);
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// Update task on one column slice (PAPER.md:395-402 DLARFB, PAPER.md:430-466 DSSRFB):
-//   SS = false: C <- (I - U_l T_l^{T or 1} U_l^T) C for each l (U_l unit lower of V)
-//   SS = true : [C1; C] <- (I - [E_l; V_l] T_l^{T or 1} [E_l; V_l]^T) [C1; C]
-// QT = true: Q^T direction (l ascending, T_l^T); false: Q direction (l descending, T_l).
-// Y_l, T_l and (SS) the slice's C1 block are staged by cp.async into double buffers; the
-// slice stays in registers for the whole task; one __syncthreads per inner block.
-// ---------------------------------------------------------------------------------------
 // Stage panel l (Y_l: B*S doubles, T_l: S*S) from the packed workspace into buffer `buf`
 // with two TMA bulk copies completing on mbarrier full[buf].  One thread.
 template <int B, int S>
@@ -220,85 +87,150 @@ __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const 
   bulk_g2s(sm + (buf ? L::T1 : L::T0), Tp + (size_t)l * S * S, TB, full + buf);
 }
 
-// Pipeline: two buffers; panels l0, l1 are issued at task start; the LAST warp to finish
-// with a buffer (shared-memory counter) issues its refill two panels ahead, so no
-// __syncthreads is needed inside the panel loop and the refill overlaps a whole panel of
-// math.  C1 (SS) is prefetched into registers one panel ahead by the group's rpart-0 warp.
-template <int B, int S, bool SS, bool QT>
-__device__ __forceinline__ void task_update(double* sm, const double* Yp, const double* Tp, double* C1, double* Ct,
-                                            int slice) {
+// Update phase shared by every task kind (one inlined copy per executor instance):
+// load the column groups [col0, col0 + 8*gact) of tile Ct into registers, then apply the
+// nb packed reflector blocks (Yp, Tp) to them -- blocks 0..nb-1 (DESC: nb-1..0) -- each
+// as W = [C1] + Y^T C; W <- T^{T|1} W; [C1 -= W]; C -= Y W, with the C1 rows of block l
+// taken from tile C1 (nullptr: LARFB / GEQRT type).
+// Pipeline: two buffers; blocks 0 and 1 are issued at phase start; the LAST warp to finish
+// with a buffer (shared-memory counter) issues its refill two blocks ahead, so there is no
+// __syncthreads inside the block loop and every refill overlaps a whole block of math.
+// C1 is fetched one block ahead by the group's rpart-0 warp (cp.async).
+template <int B, int S, bool QT, bool DESC>
+__device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>::RW / 8][2], const double* Yp,
+                                             const double* Tp, int nb, double* C1, const double* Ct, int col0,
+                                             int gact) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
-  constexpr int NL = B / S;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
-  const int cg0 = slice * C::SLICE + gi * 8;
-  const bool active = cg0 < B;
-  const bool top_owner = SS && active && rpart == 0;
-  double* c1s0 = sm + L::C1S + gi * C::C1W;           // C1 buffer for even li
-  double* c1s1 = sm + L::C1S + L::C1SZ + gi * C::C1W;  // C1 buffer for odd li
+  const int cg0 = col0 + gi * 8;
+  const bool active = gi < gact;
+  const bool top_owner = C1 != nullptr && active && rpart == 0;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
   int* done = reinterpret_cast<int*>(full + 2);
-#ifdef TQR_PROFILE_PHASES
-  long long* s_ph = (long long*)(sm + Layout<B, S>::TOTAL);
-#endif
-  PH_T0;
-  double acc[C::RW / 8][2];
-  if (top_owner) c1_fetch<B, S>(c1s0, C1, (QT ? 0 : NL - 1) * S, cg0);
+  double* c1s0 = sm + L::C1S + gi * C::C1W;           // C1 buffer for even li
+  double* c1s1 = sm + L::C1S + L::C1SZ + gi * C::C1W;  // C1 buffer for odd li
   if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
+  if (nb == 0) return;
+  if (top_owner) c1_fetch<B, S>(c1s0, C1, (DESC ? nb - 1 : 0) * S, cg0);
   if (threadIdx.x == 0) {
     mbar_init(full, 1);
     mbar_init(full + 1, 1);
     done[0] = 0;
     done[1] = 0;
     fence_mbar_init();
-    issue_panel<B, S>(sm, Yp, Tp, QT ? 0 : NL - 1, 0);
-    if (NL > 1) issue_panel<B, S>(sm, Yp, Tp, QT ? 1 : NL - 2, 1);
+    issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 1 : 0, 0);
+    if (nb > 1) issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 2 : 1, 1);
   }
   __syncthreads();
-  PH_MARK(0);
-  for (int li = 0; li < NL; ++li) {
-    const int l = QT ? li : NL - 1 - li;
+  for (int li = 0; li < nb; ++li) {
+    const int l = DESC ? nb - 1 - li : li;
     const int buf = li & 1;
     if (top_owner) {
-      cp_async_wait<0>();  // this panel's C1 block
+      cp_async_wait<0>();  // this block's C1
       __syncwarp();
-      if (li + 1 < NL) c1_fetch<B, S>(buf ? c1s0 : c1s1, C1, (QT ? li + 1 : NL - 2 - li) * S, cg0);
+      if (li + 1 < nb) c1_fetch<B, S>(buf ? c1s0 : c1s1, C1, (DESC ? l - 1 : l + 1) * S, cg0);
     }
     mbar_wait(full + buf, (li >> 1) & 1);
-    PH_MARK(1);
-    if (active) {
-      group_apply<B, S, C::RW, C::RS, QT, true, SS>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
-                                                     buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
-                                                     sm + L::XBUF + gi * C::RS * C::XW);
-    }
-    PH_MARK(4);
+    if (active)
+      group_apply<B, S, C::RW, C::RS, QT, true>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
+                                                buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
+                                                sm + L::XBUF + gi * C::RS * C::XW);
     __syncwarp();
-    if (lane == 0 && li + 2 < NL) {
+    if (lane == 0 && li + 2 < nb) {
       if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
         done[buf] = 0;
-        issue_panel<B, S>(sm, Yp, Tp, QT ? li + 2 : NL - 3 - li, buf);
+        issue_panel<B, S>(sm, Yp, Tp, DESC ? l - 2 : l + 2, buf);
       }
     }
-    PH_MARK(3);
   }
-  if (active) store_cols<B, C::RW>(acc, Ct, cg0, t0);
-  __syncthreads();  // all reads of the staging buffers done before the next task reuses them
-  PH_MARK(5);
+  __syncthreads();  // every staged buffer consumed before anyone reuses the staging space
 }
 
-// LARFB body.  Every task body is inlined into the executor: with device-function calls
-// present, ptxas spilled the accumulators of the update path (call ABI register limits).
+// ---------------------------------------------------------------------------------------
+// Panel block l of GEQRT(k) (ts = false) or TSQRT(k,i) (PAPER.md:404-428,
+// ts = true).  The panel task is left-looking inside the tile: for block l the update
+// phase has already applied this task's blocks 0..l-1 to the block's columns (acc); here
+// they go to shared memory, the block is factored (panel_factor), V / R / T are written
+// out and the packed Y_l / T_l are published for blocks l+1.. and for every update task.
+// TSQRT reads and writes only the upper triangle of A(k,k).
+// ---------------------------------------------------------------------------------------
 template <int B, int S>
-__device__ __forceinline__ void task_larfb(double* sm, const double* Yp, const double* Tp, double* Ct, int slice) {
-  task_update<B, S, false, true>(sm, Yp, Tp, nullptr, Ct, slice);
+__device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2], const bool ts,
+                                            double* Akk, double* Ab, double* Tslot, double* Ypt, double* Tps, int l) {
+  using C = Cfg<B, S>;
+  using L = Layout<B, S>;
+  constexpr int LDP = L::LDP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
+  const int c0 = l * S;
+  double* P = sm + L::Y1;
+  double* Ys = sm + L::Y0;
+  double* Rb = sm + L::RB;
+  double* Tp = sm + L::RB;  // after Rb is written back
+  double* Z = sm + L::ZZ;
+  double* tau = sm + L::TAU;
+  // block columns -> P (shared memory); GEQRT: rows above the block are final R
+  if (gi < S / 8) {
+    const int col = 8 * gi + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < C::RW / 8; ++t)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * (t0 + t) + 4 * h + (lane & 3);
+        if (ts || r >= c0) P[r + col * LDP] = acc[t][h];
+        else __stcg(Ab + (size_t)(c0 + col) * B + r, acc[t][h]);
+      }
+  }
+  if (ts)
+    for (int e = tid; e < S * S; e += C::NT) {
+      const int r = e % S, c = e / S;
+      Rb[e] = (r <= c) ? __ldcg(Akk + (size_t)(c0 + c) * B + c0 + r) : 0.0;
+    }
+  __syncthreads();
+  panel_factor<B, S, C::NWARP, LDP>(P, c0, Rb, tau, ts);
+  // V / R out, packed Y_l (Ys), Gram -> T_l, packed T_l
+  for (int e = tid; e < B * S; e += C::NT) {
+    const int r = e % B, c = e / B;
+    double y = 0.0;
+    if (ts) {
+      y = P[r + c * LDP];
+      __stcg(Ab + (size_t)(c0 + c) * B + r, y);
+    } else if (r >= c0) {
+      const double v = P[r + c * LDP];
+      __stcg(Ab + (size_t)(c0 + c) * B + r, v);
+      y = (r - c0 == c) ? 1.0 : (r - c0 > c ? v : 0.0);
+    }
+    Ys[swz<B>(r, c)] = y;
+  }
+  if (ts)
+    for (int e = tid; e < S * S; e += C::NT) {
+      const int r = e % S, c = e / S;
+      if (r <= c) __stcg(Akk + (size_t)(c0 + c) * B + c0 + r, Rb[e]);
+    }
+  __syncthreads();
+  gram_upper<B, S, C::NWARP>(Ys, Z);
+  for (int e = tid; e < B * S; e += C::NT) __stcg(Ypt + (size_t)l * B * S + e, Ys[e]);
+  __syncthreads();
+  if (warp == 0) build_t<S>(Tp, tau, Z);
+  __syncthreads();
+  for (int e = tid; e < S * S; e += C::NT) {
+    const int r = e % S, c = e / S;
+    const double v = Tp[e];
+    __stcg(Tslot + (size_t)l * S * S + e, v);
+    __stcg(Tps + (size_t)l * S * S + swz<S>(r, c), v);
+  }
+  fence_proxy_async();  // packed panels (generic stores) -> later TMA reads
+  __syncthreads();
 }
 
 // ---------------------------------------------------------------------------------------
 // Persistent executor.
 // ---------------------------------------------------------------------------------------
-// MODE 0: factorization (GEQRT/TSQRT out of line, LARFB/SSRFB inlined); MODE 1: apply Q^T;
-// MODE 2: apply Q.  Separate instances keep device-function calls out of the update paths.
+// MODE 0: factorization; MODE 1: apply Q^T; MODE 2: apply Q.  No device-function calls:
+// every task kind runs through ONE inlined update phase (plus the panel block for GEQRT /
+// TSQRT), so ptxas allocates the column-group accumulators once, without spills.
 template <int B, int S, int MODE>
 __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
   extern __shared__ __align__(16) double sm[];
@@ -350,35 +282,47 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
     if (a.trace && tid == 0) t_start = globaltimer();
     const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
     const int p = a.p;
-    if (MODE == 0) {
-      switch (kind) {
-        case K_G:
-          task_geqrt<B, S>(sm, tile_ptr(a.A, k, k, p, B), tslot_ptr(a.T, k, k, p, B, S), tile_ptr(a.Yp, k, k, p, B),
-                           tslot_ptr(a.Tp, k, k, p, B, S));
-          break;
-        case K_T:
-          task_tsqrt<B, S>(sm, tile_ptr(a.A, k, k, p, B), tile_ptr(a.A, i, k, p, B), tslot_ptr(a.T, i, k, p, B, S),
-                           tile_ptr(a.Yp, i, k, p, B), tslot_ptr(a.Tp, i, k, p, B, S));
-          break;
-        case K_L:
-          task_larfb<B, S>(sm, tile_ptr(a.Yp, k, k, p, B), tslot_ptr(a.Tp, k, k, p, B, S), tile_ptr(a.A, k, j, p, B),
-                           sl);
-          break;
-        case K_S:
-          task_update<B, S, true, true>(sm, tile_ptr(a.Yp, i, k, p, B), tslot_ptr(a.Tp, i, k, p, B, S),
-                                        tile_ptr(a.A, k, j, p, B), tile_ptr(a.A, i, j, p, B), sl);
-          break;
-        default:
-          break;
+    {
+      constexpr int NL = B / S;
+      const bool panel = MODE == 0 && (kind == K_G || kind == K_T);
+      const bool ts = kind == K_T;
+      const bool lkind = kind == K_L || kind == K_LQT || kind == K_LQ;
+      double* Bt = MODE == 0 ? a.A : a.Bt;
+      double* Akk = tile_ptr(a.A, k, k, p, B);
+      double* Ab = ts ? tile_ptr(a.A, i, k, p, B) : Akk;  // panel tasks: the tile being factored
+      const int vrow = (panel && !ts) || lkind ? k : i;     // tile row of the reflectors applied
+      double* Tslot = tslot_ptr(a.T, vrow, k, p, B, S);
+      double* Ypt = tile_ptr(a.Yp, vrow, k, p, B);
+      double* Tps = tslot_ptr(a.Tp, vrow, k, p, B, S);
+      const int nsub = panel ? NL : 1;
+      for (int sub = 0; sub < nsub; ++sub) {
+        double acc[Cfg<B, S>::RW / 8][2];
+        double* C1;
+        double* Ct;
+        int col0, nb, gact;
+        if (panel) {
+          C1 = ts ? Akk : nullptr;
+          Ct = Ab;
+          col0 = sub * S;
+          nb = sub;
+          gact = S / 8;
+        } else {
+          C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
+          Ct = lkind ? tile_ptr(Bt, k, j, p, B) : tile_ptr(Bt, i, j, p, B);
+          col0 = sl * Cfg<B, S>::SLICE;
+          nb = NL;
+          gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
+        }
+        update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact);
+        PH_MARK(4);
+        if (panel) {
+          panel_block<B, S>(sm, acc, ts, Akk, Ab, Tslot, Ypt, Tps, sub);
+        } else if (warp / Cfg<B, S>::RS < gact) {
+          store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
+                                       (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
+        }
+        PH_MARK(panel ? 1 : 5);
       }
-    } else {
-      constexpr bool QT = MODE == 1;
-      if (kind == K_LQT || kind == K_LQ)
-        task_update<B, S, false, QT>(sm, tile_ptr(a.Yp, k, k, p, B), tslot_ptr(a.Tp, k, k, p, B, S), nullptr,
-                                     tile_ptr(a.Bt, k, j, p, B), sl);
-      else
-        task_update<B, S, true, QT>(sm, tile_ptr(a.Yp, i, k, p, B), tslot_ptr(a.Tp, i, k, p, B, S),
-                                    tile_ptr(a.Bt, k, j, p, B), tile_ptr(a.Bt, i, j, p, B), sl);
     }
     __syncthreads();
     if (tid == 0) {

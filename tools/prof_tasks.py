@@ -50,8 +50,7 @@ for kind in [int(x) for x in a.kinds.split(",")]:
         v = PH.cpu().tolist()
         PH.zero_()
         tot = sum(v)
-        names = (["load", "panel", "build_t", "writeback", "trailing", "-", "dispatch+deps", "-"] if kind in (0, 1) else
-                 ["prologue", "wait", "-", "release", "apply", "epilogue", "dispatch+deps", "-"])
+        names = ["-", "panel block", "-", "-", "update phase", "store", "dispatch+deps", "-"]
         print("   phases (% of warp-0 cycles, all reps): " + ", ".join(f"{n} {100*x/tot:.1f}" for n, x in zip(names, v) if x))
     per_task_us = ms * 1e3 / waves
     print(f"kind {['G','T','L','S','LQT','SQT','LQ','SQ'][kind]} b={b} s={s}: {count} tasks in {ms:.3f} ms -> {per_task_us:.1f} us/task/SM, "
