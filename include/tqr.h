@@ -144,9 +144,10 @@ tqr_status tqr_trace_fetch(tqr_plan* plan, int64_t* rec, int64_t cap, int64_t* n
 tqr_status tqr_profile_tasks(tqr_plan* plan, int32_t kind, int64_t count, double* At, double* T, void* work);
 
 /* Profiling builds only (libtqr_phases.so, compiled with -DTQR_PROFILE_PHASES): attach a
- * caller-owned device array of 8 int64 per-phase clock64 totals (warp 0 of every CTA adds
- * its cycles in: 0 prologue, 1 cp.async wait, 2 barrier, 3 staging issue, 4 apply,
- * 5 epilogue, 6 dispatch + dependency wait).  NULL detaches.  No-op in product builds. */
+ * caller-owned device array of 16 int64 per-phase clock64 totals (thread 0 of every CTA adds
+ * its cycles in: 4 update phase of an update task, 5 its epilogue, 6 dispatch + dependency
+ * wait, 7 update phase of a panel task, 8 panel staging, 9 panel factorization, 10 V/R out,
+ * 11 Gram + packed Y out, 12 T build, 13 T out).  NULL detaches.  No-op in product builds. */
 tqr_status tqr_phase_counters(tqr_plan* plan, long long* d_counters);
 
 #ifdef __cplusplus

@@ -334,20 +334,51 @@ __device__ __forceinline__ void c1_fetch(double* c1s, const double* tile, int ro
 //              reflector is [e_c; v], identity tops are mutually orthogonal.
 //   TS = false (GEQRT): P holds the tile rows, block columns; column jj's
 //              alpha is P[c0+jj][jj], its x is P[c0+jj+1 :][jj].
-// P column c at P + c*LDP.  Column jj belongs to warp jj % NW.  One __syncthreads per
-// column: the owner of column jj+1 updates it first and immediately generates the next
-// reflector, overlapping the other warps' updates.  Householder generator = DESIGN.md
-// R2-R4 (the oracle's), with v = x * (1/(alpha-beta)).  Outputs: P holds V_l (below the
-// diagonal for GEQRT), Rb / P's upper part the new R entries, tau[S].
+// P column c at P + c*LDP.  Column c belongs to warp c % NW and only that warp writes it.
+// No block-wide barrier inside the column loop: the owner of column jj publishes v_jj (in
+// place, P column jj is final once generated) and tau_jj, then ARRIVES (bar.arrive, no
+// wait) on hardware named barrier 1 + jj % 15; every other warp waits on it (bar.sync)
+// before applying reflector jj to its own columns.  The owner of column jj+1 updates that
+// column first and immediately generates the next reflector, so the critical path per
+// column is one dot/update plus one Householder generation; the other warps' columns are
+// updated off the critical path with their reductions interleaved.  (Measured with
+// tools/panel_bench.cu: a shared-memory flag handoff costs ~400 clk, a named barrier ~30.)
+// Householder generator = DESIGN.md R2-R4 (the oracle's), v = x * (1/(alpha-beta)).
+// Outputs: P holds V_l (below the diagonal for GEQRT), Rb / P's upper part the new R
+// entries, tau[S].  Uses named barriers 1..15 (all instances complete on return).
 // ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 template <int B, int S, int NW, int LDP>
 __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, double* tau, const bool TS) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NR = (B + 31) / 32;  // rows per lane
+  constexpr int NR = (B + 31) / 32;       // rows per lane
+  constexpr int NC = (S + NW - 1) / NW;   // columns per warp
   auto top = [&](int r, int c) -> double& { return TS ? Rb[r + c * S] : P[c0 + r + c * LDP]; };
   auto lo_of = [&](int jj) { return TS ? 0 : c0 + jj + 1; };
 
-  auto house = [&](int jj, double sigma) {
+  // Householder generation for column jj by its owner warp, then publish (release).
+  auto house_pub = [&](int jj) {
+    const int lo = lo_of(jj);
+    double xr[NR];
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int x = 0; x < NR; ++x) {
+      const int r = lane + 32 * x;
+      xr[x] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
+      if (x & 1) s1 += xr[x] * xr[x]; else s0 += xr[x] * xr[x];
+    }
+    const double sigma = warp_sum(s0 + s1);
     const double alpha = top(jj, jj);
     double beta, tv, scale;
     if (sigma == 0.0) {
@@ -358,29 +389,22 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       tv = (beta - alpha) / beta;
       scale = 1.0 / (alpha - beta);
     }
-    const int lo = lo_of(jj);
 #pragma unroll
     for (int x = 0; x < NR; ++x) {
       const int r = lane + 32 * x;
-      if (r >= lo && r < B) P[r + jj * LDP] *= scale;
+      if (r >= lo && r < B) P[r + jj * LDP] = xr[x] * scale;
     }
-    if (lane == 0) { top(jj, jj) = beta; tau[jj] = tv; }
-  };
-  auto colsq = [&](int jj) {
-    const int lo = lo_of(jj);
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int x = 0; x < NR; ++x) {
-      const int r = lane + 32 * x;
-      const double v = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
-      if (x & 1) s1 += v * v; else s0 += v * v;
+    __syncwarp();
+    if (lane == 0) {
+      top(jj, jj) = beta;
+      tau[jj] = tv;
     }
-    return warp_sum(s0 + s1);
+    named_arrive(1 + jj % 15, 32 * NW);  // publishes v_jj, tau_jj, beta_jj (no wait)
   };
 
-  if (warp == 0) house(0, colsq(0));
-  for (int jj = 0; jj < S; ++jj) {
-    __syncthreads();  // v_jj, tau_jj visible
+  if (warp == 0) house_pub(0);
+  for (int jj = 0; jj + 1 < S; ++jj) {
+    if (warp != jj % NW) named_bar(1 + jj % 15, 32 * NW);  // v_jj published
     const double tj = tau[jj];
     const int lo = lo_of(jj);
     double vr[NR];
@@ -389,41 +413,62 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       const int r = lane + 32 * x;
       vr[x] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
     }
-    // my columns c > jj: jj+1 first (it feeds the next reflector)
-    const int first = (jj + 1 < S && (jj + 1) % NW == warp) ? jj + 1 : -1;
-    for (int pass = 0; pass < 1 + (S + NW - 1) / NW; ++pass) {
-      int c;
-      if (pass == 0) { c = first; if (c < 0) continue; }
-      else { c = warp + (pass - 1) * NW; if (c <= jj || c == first || c >= S) continue; }
+    const int nxt = jj + 1;
+    if (nxt % NW == warp) {  // critical path: update column jj+1, generate reflector jj+1
       double xr[NR];
       double d0 = 0.0, d1 = 0.0;
 #pragma unroll
       for (int x = 0; x < NR; ++x) {
         const int r = lane + 32 * x;
-        xr[x] = (r >= lo && r < B) ? P[r + c * LDP] : 0.0;
+        xr[x] = (r >= lo && r < B) ? P[r + nxt * LDP] : 0.0;
         if (x & 1) d1 += vr[x] * xr[x]; else d0 += vr[x] * xr[x];
       }
-      const double d = warp_sum(d0 + d1);
-      const double tw = tj * (top(jj, c) + d);
-      const int nlo = TS ? 0 : c0 + jj + 2;  // rows of the next column's x (GEQRT: below its alpha)
-      double s0 = 0.0, s1 = 0.0;
+      const double tw = tj * (top(jj, nxt) + warp_sum(d0 + d1));
 #pragma unroll
       for (int x = 0; x < NR; ++x) {
         const int r = lane + 32 * x;
-        if (r >= lo && r < B) {
-          const double nv = xr[x] - tw * vr[x];
-          P[r + c * LDP] = nv;
-          if (r >= nlo) { if (x & 1) s1 += nv * nv; else s0 += nv * nv; }
+        if (r >= lo && r < B) P[r + nxt * LDP] = xr[x] - tw * vr[x];
+      }
+      __syncwarp();
+      if (lane == 0) top(jj, nxt) -= tw;
+      __syncwarp();
+      house_pub(nxt);
+    }
+    // the other columns c > jj+1 of this warp: dots, interleaved reductions, updates
+    double dc[NC];
+#pragma unroll
+    for (int ci = 0; ci < NC; ++ci) {
+      const int c = warp + NW * ci;
+      double d0 = 0.0, d1 = 0.0;
+      if (c > nxt && c < S) {
+#pragma unroll
+        for (int x = 0; x < NR; ++x) {
+          const int r = lane + 32 * x;
+          const double xv = (r >= lo && r < B) ? P[r + c * LDP] : 0.0;
+          if (x & 1) d1 += vr[x] * xv; else d0 += vr[x] * xv;
         }
       }
-      if (lane == 0) top(jj, c) -= tw;
-      if (c == jj + 1) {
-        const double sg = warp_sum(s0 + s1);
+      dc[ci] = d0 + d1;
+    }
+#pragma unroll
+    for (int ci = 0; ci < NC; ++ci) dc[ci] = warp_sum(dc[ci]);
+#pragma unroll
+    for (int ci = 0; ci < NC; ++ci) {
+      const int c = warp + NW * ci;
+      if (c > nxt && c < S) {
+        const double tw = tj * (top(jj, c) + dc[ci]);
+#pragma unroll
+        for (int x = 0; x < NR; ++x) {
+          const int r = lane + 32 * x;
+          if (r >= lo && r < B) P[r + c * LDP] -= tw * vr[x];
+        }
         __syncwarp();
-        house(c, sg);
+        if (lane == 0) top(jj, c) -= tw;
       }
     }
+    __syncwarp();
   }
+  if (warp != (S - 1) % NW) named_bar(1 + (S - 1) % 15, 32 * NW);  // complete the last instance
   __syncthreads();
 }
 
@@ -453,31 +498,29 @@ __device__ void gram_upper(const double* __restrict__ Ys, double* Z) {
   }
 }
 
-// T_l from tau and the Gram matrix Z (forward column-wise DLARFT, PAPER.md:153-157;
-// same recurrence as the oracle's larft_column, inner sums split in 4 for latency):
+// T_l from tau and the Gram matrix Z (forward column-wise DLARFT; the
+// oracle's larft_column recurrence):
 //   T[j][j] = tau_j ;  T[t][j] = -tau_j * sum_{t'=t}^{j-1} T[t][t'] Z[t'][j]
-// Tp: S x S plain column-major.  Executed by one warp.
+// Row t of T only needs row t itself (and Z), so each lane computes one row in registers
+// with no cross-lane dependency: lane t of warp w owns row 32w + t.  Called by warps
+// 0 .. ceil(S/32)-1.  Tp: S x S plain column-major.
 template <int S>
-__device__ void build_t(double* Tp, const double* tau, const double* Z) {
-  const int lane = threadIdx.x & 31;
-  for (int e = lane; e < S * S; e += 32) Tp[e] = 0.0;
-  __syncwarp();
-  for (int jj = 0; jj < S; ++jj) {
-    const double tj = tau[jj];
-    for (int t = lane; t < jj; t += 32) {
-      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int tp = t;
-      for (; tp + 3 < jj; tp += 4) {
-        a0 += Tp[t + tp * S] * Z[tp + jj * S];
-        a1 += Tp[t + (tp + 1) * S] * Z[tp + 1 + jj * S];
-        a2 += Tp[t + (tp + 2) * S] * Z[tp + 2 + jj * S];
-        a3 += Tp[t + (tp + 3) * S] * Z[tp + 3 + jj * S];
-      }
-      for (; tp < jj; ++tp) a0 += Tp[t + tp * S] * Z[tp + jj * S];
-      Tp[t + jj * S] = -tj * ((a0 + a1) + (a2 + a3));
+__device__ __forceinline__ void build_t(double* Tp, const double* tau, const double* Z) {
+  const int t = threadIdx.x;  // row of T (threads >= S compute nothing useful)
+  double row[S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    const double tj = tau[j];
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int tp = 0; tp < j; ++tp) {  // row[tp] == 0 for tp < t
+      if (tp & 1) a1 += row[tp] * Z[tp + j * S]; else a0 += row[tp] * Z[tp + j * S];
     }
-    if (lane == 0) Tp[jj + jj * S] = tj;
-    __syncwarp();
+    row[j] = (j == t) ? tj : (j > t ? -tj * (a0 + a1) : 0.0);
+  }
+  if (t < S) {
+#pragma unroll
+    for (int j = 0; j < S; ++j) Tp[t + j * S] = row[j];
   }
 }
 

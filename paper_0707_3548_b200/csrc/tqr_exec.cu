@@ -16,19 +16,23 @@ namespace tqr {
 // Optional phase timing (build with -DTQR_PROFILE_PHASES): warp 0 of every CTA accumulates
 // clock64 deltas per phase; totals are added to ExecArgs::phases at kernel exit.
 #ifdef TQR_PROFILE_PHASES
-#define PH_DECL __shared__ long long s_ph[8]
-#define PH_T0 long long ph_t = clock64()
-#define PH_MARK(idx)                                         \
-  do {                                                       \
-    if (threadIdx.x == 0) {                                  \
-      long long ph_n = clock64();                            \
-      s_ph[idx] += ph_n - ph_t;                              \
-      ph_t = ph_n;                                           \
-    }                                                        \
+constexpr int NPH = 16;
+__shared__ long long s_ph[NPH];  // per-CTA phase totals (thread 0)
+__shared__ long long s_pht;      // thread 0's last mark
+#define PH_T0                                 \
+  do {                                        \
+    if (threadIdx.x == 0) s_pht = clock64();  \
+  } while (0)
+#define PH_MARK(idx)                          \
+  do {                                        \
+    if (threadIdx.x == 0) {                   \
+      long long ph_n = clock64();             \
+      s_ph[idx] += ph_n - s_pht;              \
+      s_pht = ph_n;                           \
+    }                                         \
   } while (0)
 #else
-#define PH_DECL
-#define PH_T0
+#define PH_T0 do {} while (0)
 #define PH_MARK(idx) do {} while (0)
 #endif
 
@@ -53,11 +57,7 @@ struct Layout {
   // 2 "full" mbarriers (8 B each) + 2 int32 "done" counters
   static constexpr int MBAR = (PANEL_END > UPD_END ? PANEL_END : UPD_END);
   static constexpr int TOTAL = MBAR + 3;  // doubles
-#ifdef TQR_PROFILE_PHASES
-  static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double) + 64;
-#else
   static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double);
-#endif
   static_assert(BYTES <= 232448, "shared memory budget");
   static_assert((T0 % 2) == 0 && (Y1 % 2) == 0 && (MBAR % 1) == 0, "16-byte aligned TMA destinations");
 };
@@ -189,7 +189,9 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
       Rb[e] = (r <= c) ? __ldcg(Akk + (size_t)(c0 + c) * B + c0 + r) : 0.0;
     }
   __syncthreads();
+  PH_MARK(8);
   panel_factor<B, S, C::NWARP, LDP>(P, c0, Rb, tau, ts);
+  PH_MARK(9);
   // V / R out, packed Y_l (Ys), Gram -> T_l, packed T_l
   for (int e = tid; e < B * S; e += C::NT) {
     const int r = e % B, c = e / B;
@@ -210,11 +212,14 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
       if (r <= c) __stcg(Akk + (size_t)(c0 + c) * B + c0 + r, Rb[e]);
     }
   __syncthreads();
+  PH_MARK(10);
   gram_upper<B, S, C::NWARP>(Ys, Z);
   for (int e = tid; e < B * S; e += C::NT) __stcg(Ypt + (size_t)l * B * S + e, Ys[e]);
   __syncthreads();
-  if (warp == 0) build_t<S>(Tp, tau, Z);
+  PH_MARK(11);
+  if (warp < (S + 31) / 32) build_t<S>(Tp, tau, Z);
   __syncthreads();
+  PH_MARK(12);
   for (int e = tid; e < S * S; e += C::NT) {
     const int r = e % S, c = e / S;
     const double v = Tp[e];
@@ -223,6 +228,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   }
   fence_proxy_async();  // packed panels (generic stores) -> later TMA reads
   __syncthreads();
+  PH_MARK(13);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -238,8 +244,7 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
   __shared__ int s_ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 #ifdef TQR_PROFILE_PHASES
-  long long* s_ph = (long long*)(sm + Layout<B, S>::TOTAL);
-  if (tid < 8) s_ph[tid] = 0;
+  if (tid < NPH) s_ph[tid] = 0;
   __syncthreads();
 #endif
   for (;;) {
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
     const int tk = s_ticket;
 #ifdef TQR_PROFILE_PHASES
     if (tk >= a.ntasks) {
-      if (tid < 8 && a.phases) atomicAdd((unsigned long long*)&a.phases[tid], (unsigned long long)s_ph[tid]);
+      if (tid < NPH && a.phases) atomicAdd((unsigned long long*)&a.phases[tid], (unsigned long long)s_ph[tid]);
       return;
     }
 #else
@@ -314,14 +319,14 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }
         update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact);
-        PH_MARK(4);
+        if (panel) PH_MARK(7); else PH_MARK(4);
         if (panel) {
           panel_block<B, S>(sm, acc, ts, Akk, Ab, Tslot, Ypt, Tps, sub);
         } else if (warp / Cfg<B, S>::RS < gact) {
           store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
                                        (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
         }
-        PH_MARK(panel ? 1 : 5);
+        if (!panel) PH_MARK(5);
       }
     }
     __syncthreads();

@@ -203,7 +203,7 @@ class Plan:
         _check(lib().tqr_profile_tasks(self._h, kind, count, _ptr(At), _ptr(T), self.work().data_ptr()))
 
     def phase_counters(self, d_counters):
-        """Attach an int64 CUDA tensor of 8 phase-cycle totals (profiling builds only)."""
+        """Attach an int64 CUDA tensor of 16 phase-cycle totals (profiling builds only)."""
         _check(lib().tqr_phase_counters(self._h, None if d_counters is None else d_counters.data_ptr()))
 
     def trace(self, cap: int = 1 << 22):

@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(256, 1) kgroup(double* out, int iters) {
   double* c1s = sm + 2 * B * S + S * S + gi * 8 * (S + 4);
   double* xg = sm + 2 * B * S + S * S + 8 * 8 * (S + 4) + gi * RS * 256;
   for (int it = 0; it < iters; ++it) {
-    group_apply<B, S, RW, RS, true, false, HAS_C1>(acc, sm + (it & 1) * B * S, sm + 2 * B * S, c1s,
-                                                   out + 1024 * blockIdx.x, 0, 8 * gi, t0, gi, rpart, xg);
+    group_apply<B, S, RW, RS, true, true>(acc, sm + (it & 1) * B * S, sm + 2 * B * S, c1s,
+                                          HAS_C1 ? out + 1024 * blockIdx.x : nullptr, 0, 8 * gi, t0, gi, rpart, xg);
     __syncthreads();
   }
   double s = 0;

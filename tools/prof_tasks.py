@@ -24,7 +24,7 @@ plan = tqr.Plan(a.n, a.n, b, s)
 import os  # noqa: E402
 PH = None
 if os.environ.get("TQR_LIB", "").endswith("libtqr_phases.so"):
-    PH = torch.zeros(8, dtype=torch.int64, device="cuda")
+    PH = torch.zeros(16, dtype=torch.int64, device="cuda")
     plan.phase_counters(PH)
 At, T = plan.alloc()
 At.uniform_(-0.5, 0.5)
@@ -50,7 +50,8 @@ for kind in [int(x) for x in a.kinds.split(",")]:
         v = PH.cpu().tolist()
         PH.zero_()
         tot = sum(v)
-        names = ["-", "panel block", "-", "-", "update phase", "store", "dispatch+deps", "-"]
+        names = ["-", "-", "-", "-", "update", "store", "dispatch+deps", "panel-update", "stage", "factor",
+                 "V/R out", "gram+Yp", "build_t", "T out", "-", "-"]
         print("   phases (% of warp-0 cycles, all reps): " + ", ".join(f"{n} {100*x/tot:.1f}" for n, x in zip(names, v) if x))
     per_task_us = ms * 1e3 / waves
     print(f"kind {['G','T','L','S','LQT','SQT','LQ','SQ'][kind]} b={b} s={s}: {count} tasks in {ms:.3f} ms -> {per_task_us:.1f} us/task/SM, "
