@@ -8,10 +8,11 @@ in HBM: pack A into tiles (a1), the DAG-executed factorization GEQRT/TSQRT/LARFB
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C3] [--impl tqr|reference]
 
-N > 1 (torchrun): every rank factors its own matrix (independent replicas, weak scaling;
-DESIGN.md "Multi-GPU").  Timing: CUDA events on the plan's stream, barrier +
-synchronize on both sides, max over ranks.  Inputs (2 GiB at C3) exceed L2 (126 MB), so
-no flush is needed between steps.
+N > 1 (torchrun): ONE matrix factored by all ranks (strong scaling):
+tile columns 1D block-cyclic, the panel tasks store packed V/T into every rank's workspace
+over NVLink peer memory (CUDA IPC, exchanged once through torch.distributed).  Timing:
+CUDA events on the plan's stream, barrier + synchronize on both sides, max over ranks.
+Inputs (2 GiB at C3) exceed L2 (126 MB), so no flush is needed between steps.
 
 --impl reference times the CPU oracle (oracle/, the deliberately plain C implementation
 of the same algorithm) as it stands on the host cores, on a bounded sample per step.
@@ -52,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", default="", help="write a per-task execution trace (JSON) of one extra step")
+    ap.add_argument("--emulate-ranks", type=int, default=1,
+                    help="test mode: run the G-rank distributed schedule in one launch on one GPU")
     return ap.parse_args()
 
 
@@ -137,7 +140,7 @@ def run_reference(args, cfg, rank):
             vals.append(v)
     value = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": cfg["name"], "m": cfg["m"], "n": cfg["n"], "b": cfg["b"], "s": cfg["s"],
                        "sample": desc},
@@ -162,6 +165,7 @@ def main():
     import torch
     import torch.distributed as dist
     import paper_0707_3548_b200 as tqr
+    from paper_0707_3548_b200 import dist as tdist
 
     torch.cuda.set_device(local)
     if world > 1:
@@ -172,15 +176,22 @@ def main():
             dist.barrier()
 
     m, n, b, s = cfg["m"], cfg["n"], cfg["b"], cfg["s"]
+    G = world if world > 1 else args.emulate_ranks
     stream = torch.cuda.Stream()
-    plan = tqr.Plan(m, n, b, s, device=local, stream=stream)
-    A_host = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"] + 1000 * rank)   # replicas: one matrix per rank
-    A_pin = torch.from_numpy(np.ascontiguousarray(A_host.T)).pin_memory()       # column-major storage, pinned
+    plan = tqr.Plan(m, n, b, s, device=local, stream=stream, nranks=G, rank=rank if world > 1 else 0,
+                    emulate=world == 1 and G > 1)
+    if world > 1:
+        tdist.connect(plan)   # one-time CUDA IPC blob exchange
+    A_host = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"])                  # one matrix, every rank
+    A_pin = torch.from_numpy(np.ascontiguousarray(A_host.T)).pin_memory()     # column-major storage, pinned
     del A_host
+    # this rank's tile columns of A (column-major storage rows = matrix columns)
+    my_tiles = tdist.owned_columns(plan.q, G, rank) if world > 1 else list(range(plan.q))
+    my_cols = [(j * b, min(n, (j + 1) * b)) for j in my_tiles]
     with torch.cuda.stream(stream):
         A_dev = A_pin.to(f"cuda:{local}", non_blocking=True)
         At, T = plan.alloc()
-        R = torch.empty((n, min(m, n)), dtype=torch.float64, device=f"cuda:{local}")
+        R = torch.zeros((n, min(m, n)), dtype=torch.float64, device=f"cuda:{local}")
     stream.synchronize()
 
     def step():
@@ -218,24 +229,30 @@ def main():
         t = torch.tensor([ms, kern_ms], device=f"cuda:{local}", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms, kern_ms = t.tolist()
-    value = world * flops / (ms * 1e-3) / 1e9
+    value = flops / (ms * 1e-3) / 1e9     # one matrix for the whole job (strong scaling)
 
-    # ---- e2e: host buffers through the public API (H2D A, pack, factor, R, D2H R) ----
+    # ---- e2e: host buffers through the public API (H2D of this rank's columns of A, pack,
+    #      factor, R, D2H of this rank's columns of R) ----
     e2e = None
     if not args.no_e2e:
         R_pin = torch.empty((n, min(m, n)), dtype=torch.float64).pin_memory()
+
+        def e2e_step():
+            for c0, c1 in my_cols:
+                A_dev[c0:c1].copy_(A_pin[c0:c1], non_blocking=True)
+            step()
+            for c0, c1 in my_cols:
+                R_pin[c0:c1].copy_(R[c0:c1], non_blocking=True)
+
         with torch.cuda.stream(stream):
-            for _ in range(1):
-                A_dev.copy_(A_pin, non_blocking=True); step(); R_pin.copy_(R, non_blocking=True)
+            e2e_step()
         stream.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             f0.record(stream)
             for _ in range(args.steps):
-                A_dev.copy_(A_pin, non_blocking=True)
-                step()
-                R_pin.copy_(R, non_blocking=True)
+                e2e_step()
             f1.record(stream)
         stream.synchronize()
         barrier()
@@ -244,13 +261,14 @@ def main():
             t = torch.tensor([ems], device=f"cuda:{local}", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = t.item()
-        e2e = {"value": world * flops / (ems * 1e-3) / 1e9, "unit": "GFLOP/s",
-               "h2d_bytes_per_step": A_pin.numel() * 8, "d2h_bytes_per_step": R_pin.numel() * 8,
-               "ms_per_step": ems}
+        e2e = {"value": flops / (ems * 1e-3) / 1e9, "unit": "GFLOP/s",
+               "h2d_bytes_per_step": sum(c1 - c0 for c0, c1 in my_cols) * m * 8,
+               "d2h_bytes_per_step": sum(c1 - c0 for c0, c1 in my_cols) * min(m, n) * 8,
+               "ms_per_step": ems, "note": "per rank: its own tile columns of A in, of R out"}
 
     # ---- optional trace of one extra step ----
-    if args.trace and rank == 0:
-        tplan = tqr.Plan(m, n, b, s, device=local, stream=stream, trace=True)
+    if args.trace and rank == 0 and world == 1:
+        tplan = tqr.Plan(m, n, b, s, device=local, stream=stream, trace=True, nranks=G, emulate=G > 1)
         tplan.pack(A_dev, At)
         tplan.geqrf(At, T)
         tplan.sync()
@@ -272,27 +290,30 @@ def main():
         v, dt, desc = cpu_baseline_sample(cfg, threads)
         cpu = {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc, "seconds": dt}
 
-    achieved = flops / (kern_ms * 1e-3) / 1e12
+    achieved = flops / world / (kern_ms * 1e-3) / 1e12   # this GPU's share of the job, per launch
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": cfg["name"], "m": m, "n": n, "b": b, "s": s, "dist": cfg["dist"],
-                   "seed": cfg["seed"], "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                   "seed": cfg["seed"],
+                   "parallelism": (f"1D block-cyclic tile columns over {world} GPUs, V/T by NVLink peer stores"
+                                   if world > 1 else ("1 GPU" if G == 1 else f"1 GPU, {G} emulated ranks")),
                    "l2": "inputs 2 GiB > 126 MB L2; no flush between steps" if m * n * 8 > (1 << 28)
                    else "inputs smaller than L2 (not flushed)",
                    "step": "pack + geqrf (persistent DAG executor) + get_r"},
         "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
-        "executed_gflops": world * flops_exec / (ms * 1e-3) / 1e9,
+        "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
                      "kernel": f"exec_kernel<{b},{s}> (tqr_geqrf)", "kernel_ms": kern_ms,
-                     "flops_per_launch": flops,
+                     "flops_per_launch": flops / world,
                      "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": 3 * args.steps,
+        "gpu_launches": (4 if world > 1 else 3) * args.steps,   # pack, [rank barrier,] executor, get_r
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)

@@ -56,12 +56,16 @@ typedef struct {
   int32_t s;       /* inner block size: 1 <= s <= b, s divides b */
   int32_t device;  /* CUDA device ordinal */
   void* stream;    /* cudaStream_t to enqueue on; NULL = legacy default stream */
-  int32_t nranks;  /* 1 (single GPU).  >1 reserved for the 1D block-cyclic multi-GPU layout */
-  int32_t rank;    /* 0 <= rank < nranks */
+  int32_t nranks;  /* ranks of the job, 1..8: tile columns are 1D block-cyclic, rank r owns
+                      columns j == r (mod nranks) (multi-GPU section below) */
+  int32_t rank;    /* 0 <= rank < nranks (0 with TQR_FLAG_EMULATE_RANKS) */
   uint32_t flags;  /* TQR_FLAG_* */
 } tqr_params;
 
-#define TQR_FLAG_TRACE 1u /* record per-task (sm, start, end) %globaltimer stamps */
+#define TQR_FLAG_TRACE 1u          /* record per-task (sm, start, end) %globaltimer stamps */
+#define TQR_FLAG_EMULATE_RANKS 2u  /* nranks > 1 on ONE device in ONE launch: every rank's task
+                                      stream, counters and workspace, the same peer-store protocol
+                                      (test mode for the multi-GPU path on a single GPU) */
 
 /* ---- plan -------------------------------------------------------------------------- */
 /* Validates p (argument 2's fields: m=1, n=2, b=3, s=4, device=5, nranks=7, rank=8 are
@@ -70,19 +74,24 @@ typedef struct {
 tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p);
 tqr_status tqr_plan_destroy(tqr_plan* plan);
 
-/* Sizes of the caller-owned tile arrays, in doubles: At = p*q*b*b, T = p*q*s*b
- * (m rounded up to p = ceil(m/b) tiles, n to q = ceil(n/b)). */
+/* Sizes of the caller-owned tile arrays, in doubles: At = p*ql*b*b, T = p*ql*s*b
+ * (m rounded up to p = ceil(m/b) tiles, n to q = ceil(n/b)); ql = q, except on a real
+ * multi-rank plan, where ql = number of tile columns this rank owns (its storage column jl
+ * holds global tile column rank + jl*nranks). */
 tqr_status tqr_tiles_size(const tqr_plan* plan, size_t* a_doubles, size_t* t_doubles);
 /* Device workspace the caller must pass as `work` to geqrf/ormqr/orgqr (bytes):
  * (p*q*b*b + p*q*s*b) doubles holding packed (shared-memory-layout) copies of every
  * reflector panel and T block, written once by the panel tasks and streamed by TMA bulk
- * copies into every update task.  Not needed after the call returns. */
+ * copies into every update task.  Not needed after the call returns.  Multi-rank plans
+ * (nranks > 1) own a peer-visible workspace per rank instead: 0 bytes, `work` may be NULL. */
 tqr_status tqr_workspace_size(const tqr_plan* plan, size_t* bytes);
 
 /* ---- layout ------------------------------------------------------ */
-/* Column-major m x n A (lda >= m) -> tile-major At, zero padding beyond m, n. */
+/* Column-major m x n A (lda >= m) -> tile-major At, zero padding beyond m, n.  On a real
+ * multi-rank plan A is the whole matrix and only this rank's tile columns are packed. */
 tqr_status tqr_pack(tqr_plan* plan, const double* A, int64_t lda, double* At);
-/* Tile-major At -> column-major m x n A (lda >= m); padding is dropped. */
+/* Tile-major At -> column-major m x n A (lda >= m); padding is dropped (multi-rank: only
+ * this rank's columns of A are written). */
 tqr_status tqr_unpack(tqr_plan* plan, const double* At, double* A, int64_t ldr);
 
 /* ---- factorization (Algorithm 1) ---------------------------------- */
@@ -94,7 +103,7 @@ tqr_status tqr_unpack(tqr_plan* plan, const double* At, double* A, int64_t ldr);
 tqr_status tqr_geqrf(tqr_plan* plan, double* At, double* T, void* work);  /* work: see tqr_workspace_size */
 
 /* R = upper trapezoid of the factored tiles, min(m,n) x n column-major (ldr >= min(m,n)),
- * zeros below the diagonal. */
+ * zeros below the diagonal (multi-rank: only this rank's columns of R are written). */
 tqr_status tqr_get_r(tqr_plan* plan, const double* At, double* R, int64_t ldr);
 
 /* Apply Q^T (trans = 'T') or Q (trans = 'N') from the factors (At, T) to a tile-major
@@ -107,6 +116,25 @@ tqr_status tqr_ormqr(tqr_plan* plan, char trans, const double* At, const double*
  * (p row tiles, ceil(k/b) tile columns); 1 <= k <= m.  (DORGQR analogue.) */
 tqr_status tqr_orgqr(tqr_plan* plan, const double* At, const double* T, int64_t k,
                      double* Qt, void* work);
+
+/* ---- multi-GPU ---------------------------------------
+ * One process per GPU, tile columns 1D block-cyclic.  The panel tasks of step k (GEQRT(k),
+ * TSQRT(k,i)) run on owner(k) = k mod nranks and store their packed V/T tiles directly into
+ * every rank's workspace over NVLink peer memory, then release-store that rank's panel-k
+ * progress counter at system scope: the per-tile V/T broadcast is fused into the panel task
+ * (no separate collective).  LARFB/SSRFB run on the owner of the updated column.  R, V and T
+ * are bitwise identical to the single-GPU factorization.
+ *
+ * Connection, once per plan, after every rank created its plan with the same (m, n, b, s,
+ * nranks): tqr_comm_export writes this rank's TQR_IPC_BLOB_BYTES-byte CUDA IPC blob;
+ * the caller all-gathers the blobs (any transport, e.g. torch.distributed) in rank order
+ * and passes the concatenation to tqr_comm_connect.  Errors: TQR_ERR_UNSUPPORTED on
+ * single-rank or emulated plans; TQR_ERR_INVALID_ARG(2) if a blob does not match the plan;
+ * TQR_ERR_CUDA if the IPC mapping fails.  Every tqr_geqrf of a connected plan starts with a
+ * device-side entry barrier across ranks (a rank that never arrives traps after 60 s). */
+#define TQR_IPC_BLOB_BYTES 256
+tqr_status tqr_comm_export(tqr_plan* plan, void* blob /* TQR_IPC_BLOB_BYTES, host */);
+tqr_status tqr_comm_connect(tqr_plan* plan, const void* blobs /* nranks * TQR_IPC_BLOB_BYTES, host */);
 
 /* ---- flop models -------------------------------------------------------------------- */
 /* Standard count 2n^2(m - n/3) for m >= n, 2m^2(n - m/3) otherwise. */
@@ -130,6 +158,14 @@ int32_t tqr_supported(int32_t b, int32_t s);      /* 1 if a kernel instance exis
  * Returns TQR_OK when the order is a valid topological order of the DAG. */
 tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
                                 int64_t counts[4], int64_t* n_edges);
+
+/* The per-rank dispatch records (16 int32 per task, layout of csrc/tqr_internal.h) of the
+ * factorization schedule for a p x q grid with `nslice` slices, `workers` CTAs per rank and
+ * `nranks` ranks (real multi-rank storage columns for nranks > 1); *n = task count of
+ * `rank`, *nctr = its counter count; up to `cap` records copied to rec (host).  Pure host:
+ * lets CPU tests replay the distributed protocol. */
+tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, int32_t rank,
+                                int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr);
 
 /* Trace of the last tqr_geqrf with TQR_FLAG_TRACE: up to `cap` records of
  * {kind, k, i, j, slice, sm, start_ns, end_ns} as 8 int64 each (host memory);

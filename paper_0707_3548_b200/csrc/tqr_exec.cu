@@ -158,7 +158,8 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
 // ---------------------------------------------------------------------------------------
 template <int B, int S>
 __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2], const bool ts,
-                                            double* Akk, double* Ab, double* Tslot, double* Ypt, double* Tps, int l) {
+                                            double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
+                                            size_t toff, int l) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   constexpr int LDP = L::LDP;
@@ -214,7 +215,12 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   __syncthreads();
   PH_MARK(10);
   gram_upper<B, S, C::NWARP>(Ys, Z);
-  for (int e = tid; e < B * S; e += C::NT) __stcg(Ypt + (size_t)l * B * S + e, Ys[e]);
+  // packed Y_l to every rank's workspace (the V broadcast of SURVEY 8(e), fused into the
+  // panel task: peer stores over NVLink on a multi-GPU job, local stores otherwise)
+  for (int g = 0; g < a.nranks; ++g) {
+    double* dst = a.Yp[g] + yoff + (size_t)l * B * S;
+    for (int e = tid; e < B * S; e += C::NT) __stcg(dst + e, Ys[e]);
+  }
   __syncthreads();
   PH_MARK(11);
   if (warp < (S + 31) / 32) build_t<S>(Tp, tau, Z);
@@ -224,8 +230,9 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     const int r = e % S, c = e / S;
     const double v = Tp[e];
     __stcg(Tslot + (size_t)l * S * S + e, v);
-    __stcg(Tps + (size_t)l * S * S + swz<S>(r, c), v);
+    for (int g = 0; g < a.nranks; ++g) __stcg(a.Tp[g] + toff + (size_t)l * S * S + swz<S>(r, c), v);
   }
+  if (a.sys) __threadfence_system();  // peer stores ordered before the counter release
   fence_proxy_async();  // packed panels (generic stores) -> later TMA reads
   __syncthreads();
   PH_MARK(13);
@@ -238,41 +245,45 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
 // every task kind runs through ONE inlined update phase (plus the panel block for GEQRT /
 // TSQRT), so ptxas allocates the column-group accumulators once, without spills.
 template <int B, int S, int MODE>
-__global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
+__global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(const __grid_constant__ ExecArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_task[TASK_INTS];
   __shared__ int s_ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const RankLocal& R = a.loc[blockIdx.x % a.nloc];  // the rank this CTA serves
+  double* const Yme = a.Yp[R.rank];
+  double* const Tme = a.Tp[R.rank];
 #ifdef TQR_PROFILE_PHASES
   if (tid < NPH) s_ph[tid] = 0;
   __syncthreads();
 #endif
   for (;;) {
     PH_T0;
-    if (tid == 0) s_ticket = atomicAdd(a.ticket, 1);
+    if (tid == 0) s_ticket = atomicAdd(R.ticket, 1);
     __syncthreads();
     const int tk = s_ticket;
 #ifdef TQR_PROFILE_PHASES
-    if (tk >= a.ntasks) {
+    if (tk >= R.ntasks) {
       if (tid < NPH && a.phases) atomicAdd((unsigned long long*)&a.phases[tid], (unsigned long long)s_ph[tid]);
       return;
     }
 #else
-    if (tk >= a.ntasks) return;
+    if (tk >= R.ntasks) return;
 #endif
-    if (tid < TASK_INTS) s_task[tid] = a.tasks[(size_t)tk * TASK_INTS + tid];
+    if (tid < TASK_INTS) s_task[tid] = R.tasks[(size_t)tk * TASK_INTS + tid];
     __syncthreads();
     unsigned long long t_grab = 0, t_start = 0;
-    if (a.trace && tid == 0) t_grab = globaltimer();
+    if (R.trace && tid == 0) t_grab = globaltimer();
     if (warp == 0) {
 #pragma unroll
       for (int d = 0; d < TASK_NDEP; ++d) {
-        const int code = s_task[8 + 2 * d], val = s_task[9 + 2 * d];
+        const int code = s_task[8 + 2 * d], val = a.base + s_task[9 + 2 * d];
         const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
         for (int x = lane; x < cnt; x += 32) {
-          if (ld_acquire(a.ctr + idx + x) >= val) continue;
+          const int* c = R.ctr + idx + x;
+          if ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) >= val) continue;
           const unsigned long long t0w = globaltimer();
-          while (ld_acquire(a.ctr + idx + x) < val) {
+          while ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < val) {
             __nanosleep(200);
             // watchdog: a dependency that never resolves is a schedule bug; fail loudly
             if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
@@ -284,21 +295,24 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
     }
     __syncthreads();
     PH_MARK(6);
-    if (a.trace && tid == 0) t_start = globaltimer();
-    const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
+    if (R.trace && tid == 0) t_start = globaltimer();
+    const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4], kc = s_task[7];
     const int p = a.p;
     {
       constexpr int NL = B / S;
       const bool panel = MODE == 0 && (kind == K_G || kind == K_T);
       const bool ts = kind == K_T;
       const bool lkind = kind == K_L || kind == K_LQT || kind == K_LQ;
-      double* Bt = MODE == 0 ? a.A : a.Bt;
-      double* Akk = tile_ptr(a.A, k, k, p, B);
-      double* Ab = ts ? tile_ptr(a.A, i, k, p, B) : Akk;  // panel tasks: the tile being factored
+      double* Bt = MODE == 0 ? R.A : R.Bt;
+      double* Akk = tile_ptr(R.A, k, kc, p, B);
+      double* Ab = ts ? tile_ptr(R.A, i, kc, p, B) : Akk;  // panel tasks: the tile being factored
       const int vrow = (panel && !ts) || lkind ? k : i;     // tile row of the reflectors applied
-      double* Tslot = tslot_ptr(a.T, vrow, k, p, B, S);
-      double* Ypt = tile_ptr(a.Yp, vrow, k, p, B);
-      double* Tps = tslot_ptr(a.Tp, vrow, k, p, B, S);
+      double* Tslot = tslot_ptr(R.T, vrow, kc, p, B, S);
+      // reflector workspace, indexed by the global step k (every rank holds every panel)
+      const size_t yoff = ((size_t)vrow + (size_t)k * p) * (size_t)B * B;
+      const size_t toff = ((size_t)vrow + (size_t)k * p) * (size_t)S * B;
+      const double* Ypt = Yme + yoff;
+      const double* Tps = Tme + toff;
       const int nsub = panel ? NL : 1;
       for (int sub = 0; sub < nsub; ++sub) {
         double acc[Cfg<B, S>::RW / 8][2];
@@ -321,7 +335,7 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
         update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (panel) {
-          panel_block<B, S>(sm, acc, ts, Akk, Ab, Tslot, Ypt, Tps, sub);
+          panel_block<B, S>(sm, acc, ts, Akk, Ab, Tslot, a, yoff, toff, sub);
         } else if (warp / Cfg<B, S>::RS < gact) {
           store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
                                        (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
@@ -333,9 +347,20 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(ExecArgs a) {
     if (tid == 0) {
       __threadfence();
       fence_proxy_async();
-      st_release(a.ctr + s_task[5], s_task[6]);
-      if (a.trace) {
-        unsigned long long* tr = a.trace + (size_t)tk * 4;
+      const int oidx = s_task[5], oval = a.base + s_task[6];
+      if ((s_task[14] & 1) && a.nranks > 1) {
+        // panel progress: release on every rank (the V/T tiles it covers are already there)
+        if (a.sys) {
+          __threadfence_system();
+          for (int g = 0; g < a.nranks; ++g) st_release_sys(a.ctr[g] + oidx, oval);
+        } else {
+          for (int g = 0; g < a.nranks; ++g) st_release(a.ctr[g] + oidx, oval);
+        }
+      } else {
+        st_release(R.ctr + oidx, oval);
+      }
+      if (R.trace) {
+        unsigned long long* tr = R.trace + (size_t)tk * 4;
         tr[0] = ((unsigned long long)smid() << 32) | (unsigned)tk;
         tr[1] = t_grab;
         tr[2] = t_start;
@@ -423,33 +448,40 @@ int exec_max_ctas(int b, int s, int device) {
 // element, tile-row index fastest so both the column-major and the tile-major side are
 // contiguous runs of b doubles.
 // ---------------------------------------------------------------------------------------
+// tile-major element e of a (p x qloc tiles) storage array -> global (r, c); storage
+// column jl holds global tile column coff + jl*cstride
+__device__ __forceinline__ void tile_elem(int64_t e, int b, int64_t p, int cstride, int coff, int64_t& r, int64_t& c) {
+  const int64_t bb = (int64_t)b * b;
+  const int64_t tile = e / bb, in = e % bb;
+  const int64_t i = tile % p, jl = tile / p;
+  r = i * b + in % b;
+  c = ((int64_t)coff + jl * cstride) * b + in / b;
+}
 __global__ void pack_kernel(const double* __restrict__ A, int64_t lda, double* __restrict__ At, int64_t m, int64_t n,
-                            int b, int64_t p, int64_t total) {
+                            int b, int64_t p, int cstride, int coff, int64_t total) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t bb = (int64_t)b * b;
-    const int64_t tile = e / bb, in = e % bb;
-    const int64_t i = tile % p, jt = tile / p;
-    const int64_t r = i * b + in % b, c = jt * b + in / b;
+    int64_t r, c;
+    tile_elem(e, b, p, cstride, coff, r, c);
     At[e] = (r < m && c < n) ? A[r + c * lda] : 0.0;
   }
 }
 __global__ void unpack_kernel(const double* __restrict__ At, double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
-                              int b, int64_t p) {
-  const int64_t total = m * n;
+                              int b, int64_t p, int cstride, int coff, int64_t total) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e % m, c = e / m;
-    const int64_t i = r / b, jt = c / b;
-    A[r + c * lda] = At[((i + jt * p) * b + (c % b)) * b + (r % b)];
+    int64_t r, c;
+    tile_elem(e, b, p, cstride, coff, r, c);
+    if (r < m && c < n) A[r + c * lda] = At[e];
   }
 }
+// R = upper trapezoid (k = min(m,n) rows), zeros below the diagonal; only the tile columns
+// held by this storage array are written
 __global__ void get_r_kernel(const double* __restrict__ At, double* __restrict__ R, int64_t ldr, int64_t m, int64_t n,
-                             int b, int64_t p) {
+                             int b, int64_t p, int cstride, int coff, int64_t total) {
   const int64_t k = m < n ? m : n;
-  const int64_t total = k * n;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e % k, c = e / k;
-    const int64_t i = r / b, jt = c / b;
-    R[r + c * ldr] = (r <= c) ? At[((i + jt * p) * b + (c % b)) * b + (r % b)] : 0.0;
+    int64_t r, c;
+    tile_elem(e, b, p, cstride, coff, r, c);
+    if (r < k && c < n) R[r + c * ldr] = (r <= c) ? At[e] : 0.0;
   }
 }
 __global__ void eye_tiles_kernel(double* __restrict__ Qt, int64_t m, int64_t k, int b, int64_t p, int64_t total) {
@@ -499,6 +531,10 @@ __global__ void pack_factors_kernel(const double* __restrict__ A, const double* 
   }
 }
 
+struct RankPtrs {
+  int* p[MAX_RANKS];
+};
+
 static int grid_for(int64_t total) {
   int64_t g = (total + 255) / 256;
   if (g > 148 * 32) g = 148 * 32;
@@ -506,21 +542,48 @@ static int grid_for(int64_t total) {
   return (int)g;
 }
 
-cudaError_t launch_pack(const double* A, int64_t lda, double* At, int64_t m, int64_t n, int b, int64_t p, int64_t q,
-                        cudaStream_t st) {
-  const int64_t total = p * q * (int64_t)b * b;
-  pack_kernel<<<grid_for(total), 256, 0, st>>>(A, lda, At, m, n, b, p, total);
+cudaError_t launch_pack(const double* A, int64_t lda, double* At, int64_t m, int64_t n, int b, int64_t p,
+                        int64_t qloc, int cstride, int coff, cudaStream_t st) {
+  const int64_t total = p * qloc * (int64_t)b * b;
+  if (total == 0) return cudaSuccess;
+  pack_kernel<<<grid_for(total), 256, 0, st>>>(A, lda, At, m, n, b, p, cstride, coff, total);
   return cudaGetLastError();
 }
 cudaError_t launch_unpack(const double* At, double* A, int64_t lda, int64_t m, int64_t n, int b, int64_t p,
-                          cudaStream_t st) {
-  unpack_kernel<<<grid_for(m * n), 256, 0, st>>>(At, A, lda, m, n, b, p);
+                          int64_t qloc, int cstride, int coff, cudaStream_t st) {
+  const int64_t total = p * qloc * (int64_t)b * b;
+  if (total == 0) return cudaSuccess;
+  unpack_kernel<<<grid_for(total), 256, 0, st>>>(At, A, lda, m, n, b, p, cstride, coff, total);
   return cudaGetLastError();
 }
 cudaError_t launch_get_r(const double* At, double* R, int64_t ldr, int64_t m, int64_t n, int b, int64_t p,
-                         cudaStream_t st) {
-  const int64_t k = m < n ? m : n;
-  get_r_kernel<<<grid_for(k * n), 256, 0, st>>>(At, R, ldr, m, n, b, p);
+                         int64_t qloc, int cstride, int coff, cudaStream_t st) {
+  const int64_t total = p * qloc * (int64_t)b * b;
+  if (total == 0) return cudaSuccess;
+  get_r_kernel<<<grid_for(total), 256, 0, st>>>(At, R, ldr, m, n, b, p, cstride, coff, total);
+  return cudaGetLastError();
+}
+
+// Cross-rank entry barrier (real multi-GPU): every rank publishes `gen` into arrive[me] of
+// every rank, then waits for all ranks' arrivals in its own array.  A rank therefore starts
+// call `gen` only after every rank has finished call gen-1 (stream order), so no panel of
+// call gen can overwrite a workspace another rank is still reading.
+__global__ void rank_barrier_kernel(RankPtrs arr, int nranks, int me, int gen) {
+  const int g = threadIdx.x;
+  if (g < nranks) {
+    __threadfence_system();
+    st_release_sys(arr.p[g] + me, gen);
+    const unsigned long long t0 = globaltimer();
+    while (ld_acquire_sys(arr.p[me] + g) < gen) {
+      __nanosleep(500);
+      if (globaltimer() - t0 > 60ull * 1000000000ull) __trap();  // a rank never arrived
+    }
+  }
+}
+cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int gen, cudaStream_t st) {
+  RankPtrs arr;
+  for (int g = 0; g < MAX_RANKS; ++g) arr.p[g] = g < nranks ? arrive_all[g] : nullptr;
+  rank_barrier_kernel<<<1, 32, 0, st>>>(arr, nranks, me, gen);
   return cudaGetLastError();
 }
 cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, double* Tp, int b, int s, int64_t p,

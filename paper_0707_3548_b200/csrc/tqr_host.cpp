@@ -49,9 +49,9 @@ tqr_status cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 struct Sched {
-  std::vector<int> rec;  // TASK_INTS per task, dispatch order
+  std::vector<std::vector<int>> rec;  // per rank: TASK_INTS per task, dispatch order
+  std::vector<int> nctr;              // per rank: counters used
   int ntasks = 0;
-  int nctr = 0;
   int64_t nedges = 0;
   int64_t counts[4] = {0, 0, 0, 0};
   bool topo_ok = true;
@@ -61,6 +61,7 @@ struct Sched {
 struct TaskGen {
   struct T {
     int kind, k, i, j, sl;
+    int rank, kc, flags;  // executing rank, storage column of tile column k, TASK flags
     int out_idx, out_val;
     int dep_idx[TASK_NDEP], dep_cnt[TASK_NDEP], dep_val[TASK_NDEP];
     int ndep;
@@ -72,6 +73,7 @@ struct TaskGen {
   int add(int kind, int k, int i, int j, int sl, int out_idx, int out_val, double dur, int cls) {
     T x{};
     x.kind = kind; x.k = k; x.i = i; x.j = j; x.sl = sl;
+    x.rank = 0; x.kc = k; x.flags = 0;
     x.out_idx = out_idx; x.out_val = out_val; x.ndep = 0; x.dur = dur; x.cls = cls;
     x.key[0] = k; x.key[1] = i; x.key[2] = j; x.key[3] = sl;
     t.push_back(x);
@@ -85,14 +87,25 @@ struct TaskGen {
 
 static inline uint64_t ckey(int idx, int val) { return ((uint64_t)(uint32_t)idx << 32) | (uint32_t)val; }
 
-// Builds successor lists from counter deps (each (counter, value) has exactly one producer),
-// then list-schedules on `workers` identical workers.  Returns false if the dependency
+// Builds successor lists from counter deps (each (rank, counter, value) has exactly one
+// producer; panel counters published to every rank resolve to their producer on any rank),
+// then list-schedules the whole job on `workers[r]` identical workers per rank.  Each rank's
+// dispatch order is the restriction of ONE global topological order, so per-rank ticket
+// streams cannot deadlock across ranks.  Returns false if the dependency
 // structure is inconsistent (missing producer or cycle).
-static bool list_schedule(TaskGen& G, int workers, int nctr, Sched& out) {
+static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& out) {
   const int n = (int)G.t.size();
+  const int nr = (int)workers.size();
   std::unordered_map<uint64_t, int> producer;
   producer.reserve(n * 2);
-  for (int id = 0; id < n; ++id) producer[ckey(G.t[id].out_idx, G.t[id].out_val)] = id;
+  auto pkey = [](int rank, int idx, int val) { return ((uint64_t)(uint32_t)rank << 56) ^ ckey(idx, val); };
+  for (int id = 0; id < n; ++id) {
+    const auto& x = G.t[id];
+    if (x.flags & 1)
+      for (int r = 0; r < nr; ++r) producer[pkey(r, x.out_idx, x.out_val)] = id;
+    else
+      producer[pkey(x.rank, x.out_idx, x.out_val)] = id;
+  }
   std::vector<int> indeg(n, 0);
   std::vector<std::vector<int>> succ(n);
   int64_t nedges = 0;
@@ -100,7 +113,7 @@ static bool list_schedule(TaskGen& G, int workers, int nctr, Sched& out) {
     const auto& x = G.t[id];
     for (int d = 0; d < x.ndep; ++d)
       for (int c = 0; c < x.dep_cnt[d]; ++c) {
-        auto it = producer.find(ckey(x.dep_idx[d] + c, x.dep_val[d]));
+        auto it = producer.find(pkey(x.rank, x.dep_idx[d] + c, x.dep_val[d]));
         if (it == producer.end()) return false;
         succ[it->second].push_back(id);
         indeg[id]++;
@@ -114,52 +127,60 @@ static bool list_schedule(TaskGen& G, int workers, int nctr, Sched& out) {
       if (x.key[c] != y.key[c]) return x.key[c] > y.key[c];
     return a > b;
   };
-  std::priority_queue<int, std::vector<int>, decltype(prio_less)> ready(prio_less);
+  using PQ = std::priority_queue<int, std::vector<int>, decltype(prio_less)>;
+  std::vector<PQ> ready;
+  for (int r = 0; r < nr; ++r) ready.emplace_back(prio_less);
   using Ev = std::pair<double, int>;
   std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> events;
   for (int id = 0; id < n; ++id)
-    if (indeg[id] == 0) ready.push(id);
+    if (indeg[id] == 0) ready[G.t[id].rank].push(id);
   std::vector<int> order;
   order.reserve(n);
-  int free_w = std::max(1, workers);
+  std::vector<int> free_w(nr);
+  for (int r = 0; r < nr; ++r) free_w[r] = std::max(1, workers[r]);
   double now = 0.0;
   int done = 0;
   while (done < n) {
-    while (free_w > 0 && !ready.empty()) {
-      int id = ready.top();
-      ready.pop();
-      order.push_back(id);
-      events.push({now + G.t[id].dur, id});
-      free_w--;
-    }
+    for (int r = 0; r < nr; ++r)
+      while (free_w[r] > 0 && !ready[r].empty()) {
+        int id = ready[r].top();
+        ready[r].pop();
+        order.push_back(id);
+        events.push({now + G.t[id].dur, id});
+        free_w[r]--;
+      }
     if (events.empty()) return false;  // cycle
     Ev e = events.top();
     events.pop();
     now = e.first;
     done++;
-    free_w++;
-    for (int s : succ[e.second])
-      if (--indeg[s] == 0) ready.push(s);
+    free_w[G.t[e.second].rank]++;
+    for (int sidx : succ[e.second])
+      if (--indeg[sidx] == 0) ready[G.t[sidx].rank].push(sidx);
   }
-  // emit records; verify topological order against the counter semantics
+  // emit per-rank records; verify the global order is topological
   std::vector<int> pos(n);
   for (int r = 0; r < n; ++r) pos[order[r]] = r;
-  out.rec.assign((size_t)n * TASK_INTS, 0);
+  out.rec.assign(nr, {});
   out.topo_ok = true;
   for (int r = 0; r < n; ++r) {
     const auto& x = G.t[order[r]];
-    int* q = &out.rec[(size_t)r * TASK_INTS];
+    auto& v = out.rec[x.rank];
+    const size_t o = v.size();
+    v.resize(o + TASK_INTS, 0);
+    int* q = &v[o];
     q[0] = x.kind; q[1] = x.k; q[2] = x.i; q[3] = x.j; q[4] = x.sl; q[5] = x.out_idx; q[6] = x.out_val;
+    q[7] = x.kc;
     for (int d = 0; d < x.ndep; ++d) {
       q[8 + 2 * d] = x.dep_idx[d] | (x.dep_cnt[d] << 24);
       q[9 + 2 * d] = x.dep_val[d];
     }
+    q[14] = x.flags;
   }
   for (int id = 0; id < n; ++id)
-    for (int s : succ[id])
-      if (pos[id] >= pos[s]) out.topo_ok = false;
+    for (int sidx : succ[id])
+      if (pos[id] >= pos[sidx]) out.topo_ok = false;
   out.ntasks = n;
-  out.nctr = nctr;
   out.nedges = nedges;
   return true;
 }
@@ -178,42 +199,60 @@ struct DurModel {
   }
 };
 
-static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, int workers, Sched& out) {
+// Ranks own tile columns j == r (mod G): the panel tasks G(k), T(k,i) run on
+// owner(k) and publish the panel counter on every rank; L(k,j), S(k,i,j) run on owner(j).
+// Counter layout per rank: panel[k] at k (K entries, a copy on every rank), then the local
+// column counters col[k][jl][sl] (jl = j / G).  `real_layout`: tile storage holds only the
+// rank's own columns (storage column jl); otherwise the full global grid (column j).
+static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
+                               bool real_layout, Sched& out) {
   const int K = (int)std::min(p, q);
+  const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
   DurModel dm(b, s, w);
-  TaskGen G;
+  TaskGen T;
+  auto own = [&](int64_t j) { return (int)(j % G); };
+  auto qloc = [&](int r) { return r < q ? (int)((q - r + G - 1) / G) : 0; };
+  auto scol = [&](int64_t j) { return real_layout ? (int)(j / G) : (int)j; };
   auto PANEL = [&](int k) { return k; };
-  auto COL = [&](int k, int j, int sl) { return K + (int)(((int64_t)k * q + j) * nsl + sl); };
-  const int nctr = K + (int)((int64_t)K * q * nsl);
+  auto COL = [&](int k, int64_t j, int sl) { return K + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl); };
+  out.nctr.assign(G, 0);
+  for (int r = 0; r < G; ++r) out.nctr[r] = K + (int)((int64_t)K * qloc(r) * nsl);
   for (int k = 0; k < K; ++k) {
-    int id = G.add(K_G, k, k, k, 0, PANEL(k), 1, dm.g, 0);
-    if (k > 0) G.dep(id, COL(k - 1, k, 0), nsl, 2);
+    const int ok = own(k);
+    int id = T.add(K_G, k, k, scol(k), 0, PANEL(k), 1, dm.g, 0);
+    T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
+    if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, 2);
     out.counts[0]++;
     for (int j = k + 1; j < q; ++j)
       for (int sl = 0; sl < nsl; ++sl) {
         // lookahead (R10): updates of column k+1 feed panel k+1 -> critical path
-        id = G.add(K_L, k, k, j, sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
-        G.dep(id, PANEL(k), 1, 1);
-        if (k > 0) G.dep(id, COL(k - 1, j, sl), 1, 2);
+        id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
+        T.t[id].rank = own(j); T.t[id].kc = scol(k);
+        T.t[id].key[2] = j;
+        T.dep(id, PANEL(k), 1, 1);
+        if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, 2);
         out.counts[2]++;
       }
     for (int i = k + 1; i < p; ++i) {
-      id = G.add(K_T, k, i, k, 0, PANEL(k), i - k + 1, dm.t, 1);
-      G.dep(id, PANEL(k), 1, i - k);
-      if (k > 0) G.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
+      id = T.add(K_T, k, i, scol(k), 0, PANEL(k), i - k + 1, dm.t, 1);
+      T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
+      T.dep(id, PANEL(k), 1, i - k);
+      if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
       out.counts[1]++;
       for (int j = k + 1; j < q; ++j)
         for (int sl = 0; sl < nsl; ++sl) {
-          id = G.add(K_S, k, i, j, sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
-          G.dep(id, PANEL(k), 1, i - k + 1);
-          G.dep(id, COL(k, j, sl), 1, i - k);
-          if (k > 0) G.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
+          id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
+          T.t[id].rank = own(j); T.t[id].kc = scol(k);
+          T.t[id].key[2] = j;
+          T.dep(id, PANEL(k), 1, i - k + 1);
+          T.dep(id, COL(k, j, sl), 1, i - k);
+          if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
           out.counts[3]++;
         }
     }
   }
-  if (!list_schedule(G, workers, nctr, out)) out.topo_ok = false;
+  if (!list_schedule(T, workers, out)) out.topo_ok = false;
 }
 
 // apply-Q^T (trans) or apply-Q to a tile-major B with qb tile columns.
@@ -223,12 +262,13 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, int 
 //        cnt[k][jb][sl]: S(k,i) -> p-i, L -> p-k.
 static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nsl, bool trans, int workers,
                             Sched& out) {
+  out.nctr.assign(1, 0);
   const int K = (int)std::min(p, q);
   const int w = (b + nsl - 1) / nsl;
   DurModel dm(b, s, w);
   TaskGen G;
   auto CNT = [&](int k, int jb, int sl) { return (int)(((int64_t)k * qb + jb) * nsl + sl); };
-  const int nctr = (int)((int64_t)K * qb * nsl);
+  out.nctr[0] = (int)((int64_t)K * qb * nsl);
   for (int jb = 0; jb < qb; ++jb)
     for (int sl = 0; sl < nsl; ++sl) {
       if (trans) {
@@ -256,72 +296,156 @@ static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int 
         }
       }
     }
-  if (!list_schedule(G, workers, nctr, out)) out.topo_ok = false;
+  if (!list_schedule(G, std::vector<int>{workers}, out)) out.topo_ok = false;
 }
 
 struct DevSched {
-  int* d_tasks = nullptr;
-  int ntasks = 0;
-  int nctr = 0;
+  std::vector<int*> d_tasks;  // per local rank
+  std::vector<int> ntasks;
   int mode = 0;  // executor instance: 0 factorization, 1 apply Q^T, 2 apply Q
 };
 
 }  // namespace
+
+// Per-rank symmetric buffer (multi-rank plans): counters | arrive flags | reflector workspace.
+struct SymLayout {
+  size_t ctr_off, arrive_off, yp_off, tp_off, bytes;
+};
 
 struct tqr_plan {
   tqr_params prm;
   int64_t p, q, K;
   int nsl, workers;
   cudaStream_t st;
+  int G = 1, me = 0;          // job ranks, this process's rank
+  bool emulate = false;       // all G ranks in this process, one launch on one device
+  bool real = false;          // G > 1, one rank per process / GPU
+  int nloc = 1;               // ranks run by this process
+  int nctr_max = 0;
   DevSched fact;
   std::map<std::pair<int, int64_t>, DevSched> orm;
-  int* d_ctr = nullptr;   // sized for the largest schedule so far
-  int nctr_cap = 0;
-  int* d_ticket = nullptr;
+  // device state per job rank (index = rank); local ranks own their allocations
+  int* ctr[MAX_RANKS] = {};
+  int* arrive[MAX_RANKS] = {};
+  double* Yp[MAX_RANKS] = {};
+  double* Tp[MAX_RANKS] = {};
+  void* sym_own[MAX_RANKS] = {};   // allocations owned by this process (multi-rank)
+  void* sym_peer[MAX_RANKS] = {};  // IPC-opened peer allocations (real multi-rank)
+  SymLayout lay{};
+  bool connected = false;
+  int* d_ctr1 = nullptr;      // single-rank counters
+  int* d_ticket = nullptr;    // one per local rank
+  int gen = 0;                // call generation (counter base = gen * (p + 2))
   unsigned long long* d_trace = nullptr;
+  std::vector<int64_t> trace_off;  // per local rank: offset (tasks) into d_trace
+  int64_t trace_cap = 0;
+  bool trace_valid = false;
   long long* d_phases = nullptr;  // set by tqr_phase_counters (profiling builds)
-  int trace_cap = 0;
-  int trace_n = 0;
 };
 
-static tqr_status upload(tqr_plan* P, const Sched& s, DevSched& d) {
-  CU(cudaMalloc(&d.d_tasks, s.rec.size() * sizeof(int) + 16));
-  CU(cudaMemcpy(d.d_tasks, s.rec.data(), s.rec.size() * sizeof(int), cudaMemcpyHostToDevice));
-  d.ntasks = s.ntasks;
-  d.nctr = s.nctr;  // (mode is set by the caller)
-  if (s.nctr > P->nctr_cap) {
-    if (P->d_ctr) cudaFree(P->d_ctr);
-    CU(cudaMalloc(&P->d_ctr, sizeof(int) * (size_t)std::max(1, s.nctr)));
-    P->nctr_cap = s.nctr;
+static int64_t qloc_of(const tqr_plan* P, int r) {
+  return P->real ? (r < P->q ? (P->q - r + P->G - 1) / P->G : 0) : P->q;
+}
+
+static tqr_status upload(const Sched& s, const std::vector<int>& ranks, DevSched& d) {
+  d.d_tasks.assign(ranks.size(), nullptr);
+  d.ntasks.assign(ranks.size(), 0);
+  for (size_t li = 0; li < ranks.size(); ++li) {
+    const auto& v = s.rec[ranks[li]];
+    CU(cudaMalloc(&d.d_tasks[li], v.size() * sizeof(int) + 16));
+    if (!v.empty()) CU(cudaMemcpy(d.d_tasks[li], v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+    d.ntasks[li] = (int)(v.size() / TASK_INTS);
   }
   return TQR_OK;
 }
 
-static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, double* Bt, void* work, bool trace) {
-  if (d.ntasks == 0) return TQR_OK;
-  CU(cudaMemsetAsync(P->d_ctr, 0, sizeof(int) * (size_t)std::max(1, d.nctr), P->st));
-  CU(cudaMemsetAsync(P->d_ticket, 0, sizeof(int), P->st));
-  ExecArgs a;
-  a.A = A; a.T = T; a.Bt = Bt;
-  a.Yp = reinterpret_cast<double*>(work);
-  a.Tp = a.Yp + (size_t)P->p * P->q * P->prm.b * P->prm.b;
-  a.tasks = d.d_tasks;
-  a.ntasks = d.ntasks;
-  a.p = (int)P->p;
-  a.ticket = P->d_ticket;
-  a.ctr = P->d_ctr;
-  a.trace = nullptr;
-  a.phases = P->d_phases;
-  if (trace) {
-    if (P->trace_cap < d.ntasks) {
-      if (P->d_trace) cudaFree(P->d_trace);
-      CU(cudaMalloc(&P->d_trace, sizeof(unsigned long long) * 4 * (size_t)d.ntasks));
-      P->trace_cap = d.ntasks;
+static void free_sched(DevSched& d) {
+  for (int* t : d.d_tasks)
+    if (t) cudaFree(t);
+  d.d_tasks.clear();
+}
+
+static std::vector<int> local_ranks(const tqr_plan* P) {
+  std::vector<int> v;
+  if (P->emulate)
+    for (int r = 0; r < P->G; ++r) v.push_back(r);
+  else
+    v.push_back(P->me);
+  return v;
+}
+
+// Counter generation: counters are never reset; each call waits for / publishes base + v,
+// base = gen * (p + 2) > every value of the previous call.
+static tqr_status next_base(tqr_plan* P, int* base) {
+  const int64_t step = P->p + 2;
+  if ((int64_t)(P->gen + 2) * step >= (int64_t)INT32_MAX) {
+    if (P->real) {
+      g_err = "counter generations exhausted (re-create the plan)";
+      return TQR_ERR_UNSUPPORTED;
     }
-    a.trace = P->d_trace;
-    P->trace_n = d.ntasks;
+    for (int r = 0; r < MAX_RANKS; ++r)
+      if (P->ctr[r] && (P->emulate || r == P->me))
+        CU(cudaMemsetAsync(P->ctr[r], 0, sizeof(int) * (size_t)std::max(1, P->nctr_max), P->st));
+    P->gen = 0;
   }
-  const int grid = std::min(P->workers, std::max(1, d.ntasks));
+  P->gen++;
+  *base = (int)(P->gen * step);
+  return TQR_OK;
+}
+
+static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, double* Bt, void* work, bool trace) {
+  int total = 0;
+  for (int n : d.ntasks) total += n;
+  if (total == 0) return TQR_OK;
+  int base = 0;
+  tqr_status stx = next_base(P, &base);
+  if (stx != TQR_OK) return stx;
+  const int nl = (int)d.d_tasks.size();
+  CU(cudaMemsetAsync(P->d_ticket, 0, sizeof(int) * MAX_RANKS, P->st));
+  ExecArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.nloc = nl;
+  a.nranks = P->G;
+  a.p = (int)P->p;
+  a.base = base;
+  a.sys = P->real ? 1 : 0;
+  a.phases = P->d_phases;
+  if (P->G == 1) {
+    a.Yp[0] = reinterpret_cast<double*>(work);
+    a.Tp[0] = a.Yp[0] + (size_t)P->p * P->q * P->prm.b * P->prm.b;
+    a.ctr[0] = P->d_ctr1;
+  } else {
+    for (int r = 0; r < P->G; ++r) {
+      a.Yp[r] = P->Yp[r];
+      a.Tp[r] = P->Tp[r];
+      a.ctr[r] = P->ctr[r];
+    }
+  }
+  if (trace) {
+    if (P->trace_cap < total) {
+      if (P->d_trace) cudaFree(P->d_trace);
+      CU(cudaMalloc(&P->d_trace, sizeof(unsigned long long) * 4 * (size_t)total));
+      P->trace_cap = total;
+    }
+    P->trace_off.assign(nl, 0);
+    for (int li = 1; li < nl; ++li) P->trace_off[li] = P->trace_off[li - 1] + d.ntasks[li - 1];
+    P->trace_valid = true;
+  }
+  const std::vector<int> lr = local_ranks(P);
+  for (int li = 0; li < nl; ++li) {
+    RankLocal& R = a.loc[li];
+    R.tasks = d.d_tasks[li];
+    R.ntasks = d.ntasks[li];
+    R.rank = P->G == 1 ? 0 : lr[li];
+    R.ticket = P->d_ticket + li;
+    R.ctr = a.ctr[R.rank];
+    R.A = A;
+    R.T = T;
+    R.Bt = Bt;
+    R.trace = trace ? P->d_trace + 4 * P->trace_off[li] : nullptr;
+  }
+  if (P->real) CU(launch_rank_barrier(P->arrive, P->G, P->me, P->gen, P->st));
+  const int grid = std::max(nl, std::min(P->workers, std::max(1, total)));
   CU(launch_exec(P->prm.b, P->prm.s, d.mode, a, grid, P->st));
   return TQR_OK;
 }
@@ -359,6 +483,19 @@ double tqr_flops_tiled(int64_t m, int64_t n, int32_t b, int32_t s) {
   return tot;
 }
 
+static void destroy_plan(tqr_plan* P) {
+  free_sched(P->fact);
+  for (auto& kv : P->orm) free_sched(kv.second);
+  for (int r = 0; r < MAX_RANKS; ++r) {
+    if (P->sym_peer[r]) cudaIpcCloseMemHandle(P->sym_peer[r]);
+    if (P->sym_own[r]) cudaFree(P->sym_own[r]);
+  }
+  if (P->d_ctr1) cudaFree(P->d_ctr1);
+  if (P->d_ticket) cudaFree(P->d_ticket);
+  if (P->d_trace) cudaFree(P->d_trace);
+  delete P;
+}
+
 tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   g_badarg = 0;
   if (!out) return bad_arg(1, "out is NULL");
@@ -368,12 +505,10 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (p->n < 1) return bad_arg(2, "n < 1");
   if (p->b < 1) return bad_arg(3, "b < 1");
   if (p->s < 1 || p->s > p->b || p->b % p->s != 0) return bad_arg(4, "s must satisfy 1 <= s <= b and s | b");
-  if (p->nranks < 1) return bad_arg(7, "nranks < 1");
+  if (p->nranks < 1 || p->nranks > MAX_RANKS) return bad_arg(7, "nranks outside [1, 8]");
   if (p->rank < 0 || p->rank >= p->nranks) return bad_arg(8, "rank outside [0, nranks)");
-  if (p->nranks != 1) {
-    g_err = "multi-GPU plans are not built in this version";
-    return TQR_ERR_UNSUPPORTED;
-  }
+  const bool emulate = (p->flags & TQR_FLAG_EMULATE_RANKS) != 0 && p->nranks > 1;
+  if (emulate && p->rank != 0) return bad_arg(8, "emulated multi-rank plans run every rank: rank must be 0");
   if (!exec_supported(p->b, p->s)) {
     g_err = "no kernel instance for this (b, s)";
     return TQR_ERR_UNSUPPORTED;
@@ -387,52 +522,145 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   P->p = (p->m + p->b - 1) / p->b;
   P->q = (p->n + p->b - 1) / p->b;
   P->K = std::min(P->p, P->q);
+  P->G = p->nranks;
+  P->me = p->rank;
+  P->emulate = emulate;
+  P->real = P->G > 1 && !emulate;
+  P->nloc = emulate ? P->G : 1;
   P->nsl = (p->b + exec_slice(p->b, p->s) - 1) / exec_slice(p->b, p->s);
   P->st = (cudaStream_t)p->stream;
   P->workers = exec_max_ctas(p->b, p->s, p->device);
-  if (P->workers < 1) {
-    delete P;
+  if (P->workers < P->nloc) {
+    destroy_plan(P);
     g_err = "executor does not fit on this device";
     return TQR_ERR_UNSUPPORTED;
   }
   if ((int64_t)P->K * P->q * P->nsl + P->K >= (1 << 24)) {
-    delete P;
+    destroy_plan(P);
     g_err = "problem too large for 24-bit counter indices";
     return TQR_ERR_UNSUPPORTED;
   }
+  // worker pools: emulation splits this device's CTAs c -> rank c % G; real ranks each own a GPU
+  std::vector<int> workers(P->G, P->workers);
+  if (emulate)
+    for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, P->workers, s);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, s);
   if (!s.topo_ok) {
-    delete P;
+    destroy_plan(P);
     g_err = "internal: schedule is not topological";
     return TQR_ERR_UNSUPPORTED;
   }
-  tqr_status st = upload(P, s, P->fact);
-  if (st != TQR_OK) { delete P; return st; }
-  if (cudaMalloc(&P->d_ticket, sizeof(int)) != cudaSuccess) { delete P; return TQR_ERR_OOM; }
+  for (int c : s.nctr) P->nctr_max = std::max(P->nctr_max, c);
+  tqr_status st = upload(s, local_ranks(P), P->fact);
+  if (st != TQR_OK) { destroy_plan(P); return st; }
+  if (cudaMalloc(&P->d_ticket, sizeof(int) * MAX_RANKS) != cudaSuccess) { destroy_plan(P); return TQR_ERR_OOM; }
+  if (P->G == 1) {
+    if (cudaMalloc(&P->d_ctr1, sizeof(int) * (size_t)std::max(1, P->nctr_max)) != cudaSuccess) {
+      destroy_plan(P);
+      return TQR_ERR_OOM;
+    }
+    CU(cudaMemset(P->d_ctr1, 0, sizeof(int) * (size_t)std::max(1, P->nctr_max)));
+  } else {
+    // symmetric per-rank buffer: counters | arrive | Yp (p*K tiles) | Tp (p*K slots)
+    const size_t b = p->b, sb = p->s;
+    SymLayout& L = P->lay;
+    L.ctr_off = 0;
+    L.arrive_off = ((sizeof(int) * (size_t)P->nctr_max + 255) / 256) * 256;
+    L.yp_off = L.arrive_off + 256;
+    L.tp_off = L.yp_off + (size_t)P->p * P->K * b * b * sizeof(double);
+    L.bytes = L.tp_off + (size_t)P->p * P->K * sb * b * sizeof(double);
+    for (int r : local_ranks(P)) {
+      if (cudaMalloc(&P->sym_own[r], L.bytes) != cudaSuccess) { destroy_plan(P); return TQR_ERR_OOM; }
+      CU(cudaMemset(P->sym_own[r], 0, L.yp_off));
+      char* base = (char*)P->sym_own[r];
+      P->ctr[r] = (int*)(base + L.ctr_off);
+      P->arrive[r] = (int*)(base + L.arrive_off);
+      P->Yp[r] = (double*)(base + L.yp_off);
+      P->Tp[r] = (double*)(base + L.tp_off);
+    }
+    P->connected = emulate;
+  }
   *out = P;
   return TQR_OK;
 }
 
 tqr_status tqr_plan_destroy(tqr_plan* P) {
   if (!P) return bad_arg(1, "plan is NULL");
-  if (P->fact.d_tasks) cudaFree(P->fact.d_tasks);
-  for (auto& kv : P->orm) cudaFree(kv.second.d_tasks);
-  if (P->d_ctr) cudaFree(P->d_ctr);
-  if (P->d_ticket) cudaFree(P->d_ticket);
-  if (P->d_trace) cudaFree(P->d_trace);
-  delete P;
+  destroy_plan(P);
+  return TQR_OK;
+}
+
+// ---- real multi-GPU: peer-memory connection (CUDA IPC over NVLink / NVSwitch) ----------------
+struct IpcBlob {
+  char magic[8];
+  int32_t rank, nranks;
+  uint64_t bytes;
+  int64_t m, n;
+  int32_t b, s;
+  cudaIpcMemHandle_t h;
+};
+static_assert(sizeof(IpcBlob) <= TQR_IPC_BLOB_BYTES, "blob size");
+
+tqr_status tqr_comm_export(tqr_plan* P, void* blob) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (!blob) return bad_arg(2, "blob is NULL");
+  if (!P->real) {
+    g_err = "tqr_comm_export: only multi-rank plans without TQR_FLAG_EMULATE_RANKS exchange peer memory";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  IpcBlob x;
+  std::memset(&x, 0, sizeof(x));
+  std::memcpy(x.magic, "TQRIPC1", 8);
+  x.rank = P->me;
+  x.nranks = P->G;
+  x.bytes = P->lay.bytes;
+  x.m = P->prm.m; x.n = P->prm.n; x.b = P->prm.b; x.s = P->prm.s;
+  CU(cudaIpcGetMemHandle(&x.h, P->sym_own[P->me]));
+  std::memset(blob, 0, TQR_IPC_BLOB_BYTES);
+  std::memcpy(blob, &x, sizeof(x));
+  return TQR_OK;
+}
+
+tqr_status tqr_comm_connect(tqr_plan* P, const void* blobs) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (!blobs) return bad_arg(2, "blobs is NULL");
+  if (!P->real) {
+    g_err = "tqr_comm_connect: not a real multi-rank plan";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  if (P->connected) return TQR_OK;
+  CU(cudaSetDevice(P->prm.device));
+  for (int g = 0; g < P->G; ++g) {
+    IpcBlob x;
+    std::memcpy(&x, (const char*)blobs + (size_t)g * TQR_IPC_BLOB_BYTES, sizeof(x));
+    if (std::memcmp(x.magic, "TQRIPC1", 8) != 0 || x.rank != g || x.nranks != P->G || x.bytes != P->lay.bytes ||
+        x.m != P->prm.m || x.n != P->prm.n || x.b != P->prm.b || x.s != P->prm.s)
+      return bad_arg(2, "blob of some rank does not match this plan (order blobs by rank)");
+    if (g == P->me) continue;
+    void* ptr = nullptr;
+    CU(cudaIpcOpenMemHandle(&ptr, x.h, cudaIpcMemLazyEnablePeerAccess));
+    P->sym_peer[g] = ptr;
+    char* base = (char*)ptr;
+    P->ctr[g] = (int*)(base + P->lay.ctr_off);
+    P->arrive[g] = (int*)(base + P->lay.arrive_off);
+    P->Yp[g] = (double*)(base + P->lay.yp_off);
+    P->Tp[g] = (double*)(base + P->lay.tp_off);
+  }
+  P->connected = true;
   return TQR_OK;
 }
 
 tqr_status tqr_tiles_size(const tqr_plan* P, size_t* a, size_t* t) {
   if (!P) return bad_arg(1, "plan is NULL");
   const size_t b = (size_t)P->prm.b, s = (size_t)P->prm.s;
-  if (a) *a = (size_t)P->p * P->q * b * b;
-  if (t) *t = (size_t)P->p * P->q * s * b;
+  const size_t ql = (size_t)qloc_of(P, P->me);
+  if (a) *a = (size_t)P->p * ql * b * b;
+  if (t) *t = (size_t)P->p * ql * s * b;
   return TQR_OK;
 }
 static size_t work_bytes(const tqr_plan* P) {
+  if (P->G > 1) return 0;  // multi-rank plans own their (peer-visible) workspace
   const size_t b = (size_t)P->prm.b, s = (size_t)P->prm.s;
   return ((size_t)P->p * P->q * b * b + (size_t)P->p * P->q * s * b) * sizeof(double);
 }
@@ -442,12 +670,19 @@ tqr_status tqr_workspace_size(const tqr_plan* P, size_t* bytes) {
   return TQR_OK;
 }
 
+static void colmap(const tqr_plan* P, int* cstride, int* coff) {
+  *cstride = P->real ? P->G : 1;
+  *coff = P->real ? P->me : 0;
+}
+
 tqr_status tqr_pack(tqr_plan* P, const double* A, int64_t lda, double* At) {
   if (!P) return bad_arg(1, "plan is NULL");
   if (!A) return bad_arg(2, "A is NULL");
   if (lda < P->prm.m) return bad_arg(3, "lda < m");
   if (!At) return bad_arg(4, "At is NULL");
-  CU(launch_pack(A, lda, At, P->prm.m, P->prm.n, P->prm.b, P->p, P->q, P->st));
+  int cs, co;
+  colmap(P, &cs, &co);
+  CU(launch_pack(A, lda, At, P->prm.m, P->prm.n, P->prm.b, P->p, qloc_of(P, P->me), cs, co, P->st));
   return TQR_OK;
 }
 tqr_status tqr_unpack(tqr_plan* P, const double* At, double* A, int64_t lda) {
@@ -455,7 +690,9 @@ tqr_status tqr_unpack(tqr_plan* P, const double* At, double* A, int64_t lda) {
   if (!At) return bad_arg(2, "At is NULL");
   if (!A) return bad_arg(3, "A is NULL");
   if (lda < P->prm.m) return bad_arg(4, "lda < m");
-  CU(launch_unpack(At, A, lda, P->prm.m, P->prm.n, P->prm.b, P->p, P->st));
+  int cs, co;
+  colmap(P, &cs, &co);
+  CU(launch_unpack(At, A, lda, P->prm.m, P->prm.n, P->prm.b, P->p, qloc_of(P, P->me), cs, co, P->st));
   return TQR_OK;
 }
 tqr_status tqr_get_r(tqr_plan* P, const double* At, double* R, int64_t ldr) {
@@ -463,7 +700,9 @@ tqr_status tqr_get_r(tqr_plan* P, const double* At, double* R, int64_t ldr) {
   if (!At) return bad_arg(2, "At is NULL");
   if (!R) return bad_arg(3, "R is NULL");
   if (ldr < std::min(P->prm.m, P->prm.n)) return bad_arg(4, "ldr < min(m, n)");
-  CU(launch_get_r(At, R, ldr, P->prm.m, P->prm.n, P->prm.b, P->p, P->st));
+  int cs, co;
+  colmap(P, &cs, &co);
+  CU(launch_get_r(At, R, ldr, P->prm.m, P->prm.n, P->prm.b, P->p, qloc_of(P, P->me), cs, co, P->st));
   return TQR_OK;
 }
 
@@ -471,9 +710,14 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   if (!P) return bad_arg(1, "plan is NULL");
   if (!At) return bad_arg(2, "At is NULL");
   if (!T) return bad_arg(3, "T is NULL");
-  if (!work) return bad_arg(4, "work is NULL (tqr_workspace_size bytes required)");
-  const size_t tsz = (size_t)P->p * P->q * P->prm.s * P->prm.b;
-  CU(cudaMemsetAsync(T, 0, tsz * sizeof(double), P->st));
+  if (!work && P->G == 1) return bad_arg(4, "work is NULL (tqr_workspace_size bytes required)");
+  if (P->real && !P->connected) {
+    g_err = "multi-rank plan not connected (tqr_comm_export / tqr_comm_connect)";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  size_t tsz = 0;
+  tqr_tiles_size(P, nullptr, &tsz);
+  if (tsz) CU(cudaMemsetAsync(T, 0, tsz * sizeof(double), P->st));
   return run(P, P->fact, At, T, nullptr, work, (P->prm.flags & TQR_FLAG_TRACE) != 0);
 }
 
@@ -492,9 +736,19 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
       g_err = "internal: apply-Q schedule is not topological";
       return TQR_ERR_UNSUPPORTED;
     }
+    if (s.nctr[0] > P->nctr_max) {
+      // grow the single-rank counter array (fresh zeros; the generation base stays valid)
+      int* nc = nullptr;
+      CU(cudaMalloc(&nc, sizeof(int) * (size_t)s.nctr[0]));
+      CU(cudaMemset(nc, 0, sizeof(int) * (size_t)s.nctr[0]));
+      CU(cudaStreamSynchronize(P->st));
+      cudaFree(P->d_ctr1);
+      P->d_ctr1 = nc;
+      P->nctr_max = s.nctr[0];
+    }
     DevSched d;
     d.mode = trans ? 1 : 2;
-    tqr_status st = upload(P, s, d);
+    tqr_status st = upload(s, std::vector<int>{0}, d);
     if (st != TQR_OK) return st;
     it = P->orm.emplace(key, d).first;
   }
@@ -511,6 +765,10 @@ tqr_status tqr_ormqr(tqr_plan* P, char trans, const double* At, const double* T,
   if (!Bt) return bad_arg(5, "Bt is NULL");
   if (nrhs < 1) return bad_arg(6, "nrhs < 1");
   if (!work) return bad_arg(7, "work is NULL (tqr_workspace_size bytes required)");
+  if (P->G > 1) {
+    g_err = "apply-Q is single-GPU in this version";
+    return TQR_ERR_UNSUPPORTED;
+  }
   DevSched* d = nullptr;
   tqr_status st = orm_sched(P, trans == 'T' || trans == 't', nrhs, &d);
   if (st != TQR_OK) return st;
@@ -527,6 +785,10 @@ tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, 
   if (k < 1 || k > P->prm.m) return bad_arg(4, "k outside [1, m]");
   if (!Qt) return bad_arg(5, "Qt is NULL");
   if (!work) return bad_arg(6, "work is NULL (tqr_workspace_size bytes required)");
+  if (P->G > 1) {
+    g_err = "form-Q is single-GPU in this version";
+    return TQR_ERR_UNSUPPORTED;
+  }
   const int64_t qb = (k + P->prm.b - 1) / P->prm.b;
   CU(launch_eye_tiles(Qt, P->prm.m, k, P->prm.b, P->p, qb, P->st));
   return tqr_ormqr(P, 'N', At, T, Qt, k, work);
@@ -539,22 +801,42 @@ tqr_status tqr_sync(tqr_plan* P) {
   return TQR_OK;
 }
 
-tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers, int64_t counts[4],
-                                int64_t* n_edges) {
+static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, Sched& s) {
   g_badarg = 0;
   if (p < 1) return bad_arg(1, "p < 1");
   if (q < 1) return bad_arg(2, "q < 1");
   if (nslice < 1) return bad_arg(3, "nslice < 1");
   if (workers < 1) return bad_arg(4, "workers < 1");
-  Sched s;
-  build_factor_sched(p, q, 64 * nslice, 8, nslice, workers, s);
-  if (counts)
-    for (int c = 0; c < 4; ++c) counts[c] = s.counts[c];
-  if (n_edges) *n_edges = s.nedges;
+  if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
+  build_factor_sched(p, q, 64 * nslice, 8, nslice, std::vector<int>(nranks, workers), nranks > 1, s);
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
   }
+  return TQR_OK;
+}
+
+tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers, int64_t counts[4],
+                                int64_t* n_edges) {
+  Sched s;
+  tqr_status st = inspect(p, q, nslice, workers, 1, s);
+  if (counts)
+    for (int c = 0; c < 4; ++c) counts[c] = s.counts[c];
+  if (n_edges) *n_edges = s.nedges;
+  return st;
+}
+
+tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, int32_t rank,
+                                int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr) {
+  if (rank < 0 || rank >= nranks) return bad_arg(6, "rank outside [0, nranks)");
+  if (!n) return bad_arg(9, "n is NULL");
+  Sched s;
+  tqr_status st = inspect(p, q, nslice, workers, nranks, s);
+  if (st != TQR_OK) return st;
+  const auto& v = s.rec[rank];
+  *n = (int64_t)(v.size() / TASK_INTS);
+  if (nctr) *nctr = s.nctr[rank];
+  if (rec) std::memcpy(rec, v.data(), sizeof(int32_t) * (size_t)std::min<int64_t>(cap, *n) * TASK_INTS);
   return TQR_OK;
 }
 
@@ -563,22 +845,27 @@ tqr_status tqr_trace_fetch(tqr_plan* P, int64_t* rec, int64_t cap, int64_t* n) {
   if (!rec && cap > 0) return bad_arg(2, "rec is NULL");
   if (!n) return bad_arg(4, "n is NULL");
   *n = 0;
-  if (!P->d_trace || P->trace_n == 0) return TQR_OK;
-  const int64_t cnt = std::min<int64_t>(cap, P->trace_n);
-  std::vector<unsigned long long> raw((size_t)cnt * 4);
-  std::vector<int> tasks((size_t)cnt * TASK_INTS);
+  if (!P->d_trace || !P->trace_valid) return TQR_OK;
   CU(cudaStreamSynchronize(P->st));
-  CU(cudaMemcpy(raw.data(), P->d_trace, raw.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
-  CU(cudaMemcpy(tasks.data(), P->fact.d_tasks, tasks.size() * sizeof(int), cudaMemcpyDeviceToHost));
-  for (int64_t r = 0; r < cnt; ++r) {
-    const int* t = &tasks[(size_t)r * TASK_INTS];
-    int64_t* o = rec + r * 8;
-    o[0] = t[0]; o[1] = t[1]; o[2] = t[2]; o[3] = t[3]; o[4] = t[4];
-    o[5] = (int64_t)(raw[r * 4] >> 32);
-    o[6] = (int64_t)raw[r * 4 + 2];
-    o[7] = (int64_t)raw[r * 4 + 3];
+  int64_t w = 0;
+  for (size_t li = 0; li < P->fact.d_tasks.size() && w < cap; ++li) {
+    const int64_t cnt = std::min<int64_t>(cap - w, P->fact.ntasks[li]);
+    std::vector<unsigned long long> raw((size_t)cnt * 4);
+    std::vector<int> tasks((size_t)cnt * TASK_INTS);
+    CU(cudaMemcpy(raw.data(), P->d_trace + 4 * P->trace_off[li], raw.size() * sizeof(unsigned long long),
+                  cudaMemcpyDeviceToHost));
+    CU(cudaMemcpy(tasks.data(), P->fact.d_tasks[li], tasks.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int64_t r = 0; r < cnt; ++r) {
+      const int* t = &tasks[(size_t)r * TASK_INTS];
+      int64_t* o = rec + (w + r) * 8;
+      o[0] = t[0]; o[1] = t[1]; o[2] = t[2]; o[3] = t[3]; o[4] = t[4];
+      o[5] = (int64_t)(raw[r * 4] >> 32);
+      o[6] = (int64_t)raw[r * 4 + 2];
+      o[7] = (int64_t)raw[r * 4 + 3];
+    }
+    w += cnt;
   }
-  *n = cnt;
+  *n = w;
   return TQR_OK;
 }
 
@@ -588,14 +875,15 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
   if (count < 1 || count > (1 << 24)) return bad_arg(3, "count outside [1, 2^24]");
   if (!At) return bad_arg(4, "At is NULL");
   if (!T) return bad_arg(5, "T is NULL");
-  if (P->p < 2 || P->q < 2) {
-    g_err = "profiling needs p >= 2 and q >= 2";
+  if (!work) return bad_arg(6, "work is NULL");
+  if (P->p < 2 || P->q < 2 || P->G > 1) {
+    g_err = "profiling needs a single-rank plan with p >= 2 and q >= 2";
     return TQR_ERR_UNSUPPORTED;
   }
   Sched s;
-  s.rec.assign((size_t)count * TASK_INTS, 0);
+  s.rec.assign(1, std::vector<int>((size_t)count * TASK_INTS, 0));
   for (int64_t t = 0; t < count; ++t) {
-    int* q = &s.rec[(size_t)t * TASK_INTS];
+    int* q = &s.rec[0][(size_t)t * TASK_INTS];
     const int i = 1 + (int)(t % (P->p - 1));
     const int j = 1 + (int)((t / (P->p - 1)) % (P->q - 1));
     q[0] = kind;
@@ -606,22 +894,20 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
     q[4] = (int)(t % P->nsl);
     q[5] = 0;
     q[6] = 1;
+    q[7] = q[1];
   }
-  s.ntasks = (int)count;
-  s.nctr = 1;
   DevSched d;
   d.mode = kind >= 6 ? 2 : (kind >= 4 ? 1 : 0);
-  tqr_status st = upload(P, s, d);
+  tqr_status st = upload(s, std::vector<int>{0}, d);
   if (st != TQR_OK) return st;
-  if (!work) return bad_arg(6, "work is NULL");
   st = run(P, d, At, T, At, work, false);
   cudaStreamSynchronize(P->st);
-  cudaFree(d.d_tasks);
+  free_sched(d);
   return st;
 }
 
-// Profiling builds (-DTQR_PROFILE_PHASES): attach a device array of 8 int64 phase-cycle
-// totals (NULL detaches).  Not declared in tqr.h: development aid only.
+// Profiling builds (-DTQR_PROFILE_PHASES): attach a device array of 16 int64 phase-cycle
+// totals (NULL detaches).
 tqr_status tqr_phase_counters(tqr_plan* P, long long* d_counters) {
   if (!P) return bad_arg(1, "plan is NULL");
   P->d_phases = d_counters;

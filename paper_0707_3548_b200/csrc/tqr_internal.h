@@ -19,29 +19,49 @@ enum Kind : int {
 };
 
 // One task record = 16 int32:
-//   [0] kind [1] k [2] i [3] j [4] slice [5] out counter index [6] out value [7] unused
+//   [0] kind [1] k (global step; indexes the reflector workspace) [2] i
+//   [3] j: STORAGE tile column of the updated tile (L/S/apply-Q kinds)
+//   [4] slice [5] out counter index [6] out value
+//   [7] kc: STORAGE tile column of tile column k (A(k,k), A(i,k), T(., k))
 //   [8 + 2d], [9 + 2d], d = 0..2: dependency d = (index | count << 24, value):
-//   wait until ctr[index + x] >= value for x in [0, count); count == 0 means no dependency.
+//       wait until ctr[index + x] >= base + value for x in [0, count); count 0 = none
+//   [14] flags: bit 0 = publish the out counter on every rank (panel progress, multi-GPU)
+//   [15] unused
+// Counter values of one factorization are base + v with v in [1, p + 1]; the base grows by
+// (p + 2) per call, so counters are never reset (no cross-rank reset race).
 constexpr int TASK_INTS = 16;
 constexpr int TASK_NDEP = 3;
+constexpr int MAX_RANKS = 8;
 
-struct ExecArgs {
-  double* A;          // tile-major factors (p x q tiles)
-  double* T;          // T slots (p x q slots of s*b)
-  double* Bt;         // apply-Q target, tile-major with p row tiles
-  double* Yp;         // workspace: packed reflector panels (p x q tiles of b*b)
-  double* Tp;         // workspace: packed T blocks (p x q slots of s*b)
+// One rank's task stream and its tile storage.  In the single-launch multi-rank
+// emulation every rank of the job is a RankLocal of the same launch; on a real multi-GPU
+// job each process runs exactly one.
+struct RankLocal {
   const int* tasks;   // TASK_INTS per task, dispatch order
   int ntasks;
-  int p;              // row tiles (same for A and Bt)
+  int rank;           // job rank id (index into ExecArgs::Yp/Tp/ctr)
   int* ticket;        // next ticket (reset to 0 before the launch)
-  int* ctr;           // monotone progress counters (reset to 0)
+  int* ctr;           // this rank's progress counters
+  double* A;          // tile-major factors (p row tiles, storage columns)
+  double* T;          // T slots (p x storage columns, s*b each)
+  double* Bt;         // apply-Q target, tile-major with p row tiles (single rank only)
   unsigned long long* trace;  // 4 per task or nullptr
-  long long* phases;          // TQR_PROFILE_PHASES builds: 8 phase-cycle totals, or nullptr
 };
 
-// Launch the persistent executor for tile size b, inner block s.  Returns cudaSuccess or
-// the launch error; *grid_out receives the co-resident grid used.
+struct ExecArgs {
+  RankLocal loc[MAX_RANKS];
+  int nloc;                 // ranks run by this launch (CTA c serves loc[c % nloc])
+  int nranks;               // ranks of the job
+  double* Yp[MAX_RANKS];    // every rank's workspace: packed reflector panels (p x K tiles of b*b)
+  double* Tp[MAX_RANKS];    //   and packed T blocks (p x K slots of s*b)
+  int* ctr[MAX_RANKS];      // every rank's counters (panel progress is published to all)
+  int p;                    // row tiles (same for A and Bt)
+  int base;                 // counter generation base of this call
+  int sys;                  // 1: peers on other GPUs (system-scope acquire/release)
+  long long* phases;        // TQR_PROFILE_PHASES builds: 16 phase-cycle totals, or nullptr
+};
+
+// Launch the persistent executor for tile size b, inner block s (cooperative launch).
 // mode: 0 factorization, 1 apply Q^T, 2 apply Q.
 cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cudaStream_t st);
 // Max co-resident CTAs for (b, s) on this device (0 if no instance).
@@ -50,14 +70,19 @@ bool exec_supported(int b, int s);
 // Columns per LARFB/SSRFB slice task for (b, s) (0 if no instance).
 int exec_slice(int b, int s);
 
-cudaError_t launch_pack(const double* A, int64_t lda, double* At, int64_t m, int64_t n, int b, int64_t p, int64_t q,
-                        cudaStream_t st);
+// Layout kernels.  Tile-major arrays hold the tile columns j = coff + jl*cstride of the
+// global p x q grid at storage column jl (single GPU / emulation: cstride 1, coff 0).
+cudaError_t launch_pack(const double* A, int64_t lda, double* At, int64_t m, int64_t n, int b, int64_t p,
+                        int64_t qloc, int cstride, int coff, cudaStream_t st);
 cudaError_t launch_unpack(const double* At, double* A, int64_t lda, int64_t m, int64_t n, int b, int64_t p,
-                          cudaStream_t st);
+                          int64_t qloc, int cstride, int coff, cudaStream_t st);
 cudaError_t launch_get_r(const double* At, double* R, int64_t ldr, int64_t m, int64_t n, int b, int64_t p,
-                         cudaStream_t st);
+                         int64_t qloc, int cstride, int coff, cudaStream_t st);
 cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, double* Tp, int b, int s, int64_t p,
                                 int64_t K, cudaStream_t st);
 cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qb, cudaStream_t st);
+// Cross-rank entry barrier of one call (real multi-GPU): publish `gen` into every rank's
+// arrive[me] (system scope), wait until arrive[g] >= gen for all g on this rank.
+cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int gen, cudaStream_t st);
 
 }  // namespace tqr

@@ -14,6 +14,9 @@ LIB_PATH = os.environ.get("TQR_LIB") or os.path.join(HERE, "libtqr.so")
 
 TQR_OK = 0
 TQR_FLAG_TRACE = 1
+TQR_FLAG_EMULATE_RANKS = 2
+TQR_IPC_BLOB_BYTES = 256
+TASK_INTS = 16
 _STATUS = {0: "TQR_OK", 1: "TQR_ERR_INVALID_ARG", 2: "TQR_ERR_CUDA", 3: "TQR_ERR_NCCL", 4: "TQR_ERR_OOM",
            5: "TQR_ERR_UNSUPPORTED"}
 
@@ -68,6 +71,10 @@ def lib():
         L.tqr_trace_fetch.argtypes = [_vp, ctypes.POINTER(_i64), _i64, ctypes.POINTER(_i64)]
         L.tqr_profile_tasks.argtypes = [_vp, _i32, _i64, _vp, _vp, _vp]
         L.tqr_phase_counters.argtypes = [_vp, _vp]
+        L.tqr_comm_export.argtypes = [_vp, _vp]
+        L.tqr_comm_connect.argtypes = [_vp, _vp]
+        L.tqr_schedule_records.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _vp, _i64, ctypes.POINTER(_i64),
+                                           ctypes.POINTER(_i32)]
         _lib = L
     return _lib
 
@@ -113,6 +120,18 @@ def schedule_inspect(p: int, q: int, nslice: int, workers: int):
     return dict(G=c[0], T=c[1], L=c[2], S=c[3]), ne.value
 
 
+def schedule_records(p: int, q: int, nslice: int, workers: int, nranks: int, rank: int):
+    """Dispatch records (numpy int32 (ntasks, 16)) of `rank` in the nranks-rank factorization
+    schedule, and that rank's counter count (pure host; include/tqr.h)."""
+    import numpy as np
+    n, nc = _i64(), _i32()
+    _check(lib().tqr_schedule_records(p, q, nslice, workers, nranks, rank, None, 0, ctypes.byref(n), ctypes.byref(nc)))
+    rec = np.zeros((max(1, n.value), TASK_INTS), dtype=np.int32)
+    _check(lib().tqr_schedule_records(p, q, nslice, workers, nranks, rank, rec.ctypes.data, n.value, ctypes.byref(n),
+                                      ctypes.byref(nc)))
+    return rec[: n.value], nc.value
+
+
 # ---- plan ----------------------------------------------------------------------------------
 
 class Plan:
@@ -123,15 +142,20 @@ class Plan:
     current torch stream).
     """
 
-    def __init__(self, m: int, n: int, b: int, s: int, device: int = 0, stream=None, trace: bool = False):
+    def __init__(self, m: int, n: int, b: int, s: int, device: int = 0, stream=None, trace: bool = False,
+                 nranks: int = 1, rank: int = 0, emulate: bool = False):
+        """nranks > 1: 1D block-cyclic multi-GPU plan for `rank` (connect it with
+        paper_0707_3548_b200.dist.connect), or with emulate=True all nranks ranks in one
+        launch on this device (tile arrays then keep the global layout)."""
         import torch
         self.m, self.n, self.b, self.s = m, n, b, s
         self.p, self.q = -(-m // b), -(-n // b)
+        self.nranks, self.rank, self.emulate = nranks, rank, emulate
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
-        prm = _Params(m, n, b, s, device, ctypes.c_void_p(stream.cuda_stream), 1, 0,
-                      TQR_FLAG_TRACE if trace else 0)
+        flags = (TQR_FLAG_TRACE if trace else 0) | (TQR_FLAG_EMULATE_RANKS if emulate else 0)
+        prm = _Params(m, n, b, s, device, ctypes.c_void_p(stream.cuda_stream), nranks, rank, flags)
         h = _vp()
         _check(lib().tqr_plan_create(ctypes.byref(h), ctypes.byref(prm)))
         self._h = h
@@ -183,6 +207,18 @@ class Plan:
     def geqrf(self, At, T, work=None):
         w = self.work() if work is None else work
         _check(lib().tqr_geqrf(self._h, _ptr(At), _ptr(T), w.data_ptr()))
+
+    def comm_export(self) -> bytes:
+        """This rank's CUDA IPC blob (TQR_IPC_BLOB_BYTES) for tqr_comm_connect."""
+        buf = ctypes.create_string_buffer(TQR_IPC_BLOB_BYTES)
+        _check(lib().tqr_comm_export(self._h, buf))
+        return buf.raw
+
+    def comm_connect(self, blobs: bytes):
+        """blobs: every rank's comm_export() blob, concatenated in rank order."""
+        if len(blobs) != self.nranks * TQR_IPC_BLOB_BYTES:
+            raise ValueError("need nranks * TQR_IPC_BLOB_BYTES bytes")
+        _check(lib().tqr_comm_connect(self._h, blobs))
 
     def get_r(self, At, R):
         _check(lib().tqr_get_r(self._h, _ptr(At), _ptr(R), min(self.m, self.n)))
