@@ -156,7 +156,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
 // out and the packed Y_l / T_l are published for blocks l+1.. and for every update task.
 // TSQRT reads and writes only the upper triangle of A(k,k).
 // ---------------------------------------------------------------------------------------
-template <int B, int S>
+template <int B, int S, int SO>
 __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2], const bool ts,
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
                                             size_t toff, int l) {
@@ -226,10 +226,14 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   if (warp < (S + 31) / 32) build_t<S>(Tp, tau, Z);
   __syncthreads();
   PH_MARK(12);
+  // output slot: T_L (SO x SO) in columns [L*SO, L*SO+SO); this SI-block is its diagonal
+  // block m (the off-diagonal blocks of SO > SI are formed after the factorization)
+  constexpr int RB_ = SO / S;
+  const int Lo = l / RB_, mo = (l % RB_) * S;
   for (int e = tid; e < S * S; e += C::NT) {
     const int r = e % S, c = e / S;
     const double v = Tp[e];
-    __stcg(Tslot + (size_t)l * S * S + e, v);
+    __stcg(Tslot + ((size_t)Lo * SO + mo + c) * SO + mo + r, v);
     for (int g = 0; g < a.nranks; ++g) __stcg(a.Tp[g] + toff + (size_t)l * S * S + swz<S>(r, c), v);
   }
   if (a.sys) __threadfence_system();  // peer stores ordered before the counter release
@@ -244,8 +248,9 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
 // MODE 0: factorization; MODE 1: apply Q^T; MODE 2: apply Q.  No device-function calls:
 // every task kind runs through ONE inlined update phase (plus the panel block for GEQRT /
 // TSQRT), so ptxas allocates the column-group accumulators once, without spills.
-template <int B, int S, int MODE>
-__global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(const __grid_constant__ ExecArgs a) {
+template <int B, int SO, int MODE>
+__global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(const __grid_constant__ ExecArgs a) {
+  constexpr int S = Inner<B, SO>::SI;  // internal inner block (== SO up to b = 256)
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_task[TASK_INTS];
   __shared__ int s_ticket;
@@ -307,13 +312,14 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(const __grid_con
       double* Akk = tile_ptr(R.A, k, kc, p, B);
       double* Ab = ts ? tile_ptr(R.A, i, kc, p, B) : Akk;  // panel tasks: the tile being factored
       const int vrow = (panel && !ts) || lkind ? k : i;     // tile row of the reflectors applied
-      double* Tslot = tslot_ptr(R.T, vrow, kc, p, B, S);
-      // reflector workspace, indexed by the global step k (every rank holds every panel)
+      double* Tslot = tslot_ptr(R.T, vrow, kc, p, B, SO);
+      // reflector workspace, indexed by the global step k (every rank holds every panel);
+      // T slots of SO*B doubles holding the B/S internal S x S blocks
       const size_t yoff = ((size_t)vrow + (size_t)k * p) * (size_t)B * B;
-      const size_t toff = ((size_t)vrow + (size_t)k * p) * (size_t)S * B;
+      const size_t toff = ((size_t)vrow + (size_t)k * p) * (size_t)SO * B;
       const double* Ypt = Yme + yoff;
       const double* Tps = Tme + toff;
-      const int nsub = panel ? NL : 1;
+      const int nsub = panel ? NL : Cfg<B, S>::TSL / Cfg<B, S>::SLICE;
       for (int sub = 0; sub < nsub; ++sub) {
         double acc[Cfg<B, S>::RW / 8][2];
         double* C1;
@@ -328,14 +334,14 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(const __grid_con
         } else {
           C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
           Ct = lkind ? tile_ptr(Bt, k, j, p, B) : tile_ptr(Bt, i, j, p, B);
-          col0 = sl * Cfg<B, S>::SLICE;
+          col0 = sl * Cfg<B, S>::TSL + sub * Cfg<B, S>::SLICE;
           nb = NL;
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }
         update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (panel) {
-          panel_block<B, S>(sm, acc, ts, Akk, Ab, Tslot, a, yoff, toff, sub);
+          panel_block<B, S, SO>(sm, acc, ts, Akk, Ab, Tslot, a, yoff, toff, sub);
         } else if (warp / Cfg<B, S>::RS < gact) {
           store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
                                        (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
@@ -375,11 +381,11 @@ __global__ void __launch_bounds__(Cfg<B, S>::NT, 1) exec_kernel(const __grid_con
 // (128,32), (256,32) plus small/test shapes and s == b (the paper's unblocked kernels).
 // ---------------------------------------------------------------------------------------
 #define TQR_INSTANCES(X) \
-  X(16, 8) X(16, 16) X(32, 8) X(32, 32) X(64, 16) X(64, 64) X(128, 32) X(256, 32)
+  X(16, 8) X(16, 16) X(32, 8) X(32, 32) X(64, 16) X(64, 64) X(128, 32) X(256, 32) X(512, 64)
 
 template <int B, int S, int MODE>
 static cudaError_t launch_mode(const ExecArgs& a, int grid, cudaStream_t st) {
-  using L = Layout<B, S>;
+  using L = Layout<B, Inner<B, S>::SI>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e =
@@ -389,8 +395,8 @@ static cudaError_t launch_mode(const ExecArgs& a, int grid, cudaStream_t st) {
   }
   ExecArgs args = a;
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((const void*)exec_kernel<B, S, MODE>, dim3(grid), dim3(Cfg<B, S>::NT), params,
-                                     L::BYTES, st);
+  return cudaLaunchCooperativeKernel((const void*)exec_kernel<B, S, MODE>, dim3(grid),
+                                     dim3(Cfg<B, Inner<B, S>::SI>::NT), params, L::BYTES, st);
 }
 template <int B, int S>
 static cudaError_t launch_one(const ExecArgs& a, int mode, int grid, cudaStream_t st) {
@@ -401,13 +407,15 @@ static cudaError_t launch_one(const ExecArgs& a, int mode, int grid, cudaStream_
 
 template <int B, int S>
 static int max_ctas_one(int device) {
-  using L = Layout<B, S>;
+  using L = Layout<B, Inner<B, S>::SI>;
   int per_sm = 0, sms = 0, worst = 1 << 30;
   const void* fns[3] = {(const void*)exec_kernel<B, S, 0>, (const void*)exec_kernel<B, S, 1>,
                         (const void*)exec_kernel<B, S, 2>};
   for (const void* f : fns) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, Cfg<B, S>::NT, L::BYTES) != cudaSuccess) return 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, Cfg<B, Inner<B, S>::SI>::NT, L::BYTES) !=
+        cudaSuccess)
+      return 0;
     worst = per_sm < worst ? per_sm : worst;
   }
   per_sm = worst;
@@ -430,7 +438,7 @@ cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cud
 }
 
 int exec_slice(int b, int s) {
-#define X(BB, SS) if (b == BB && s == SS) return Cfg<BB, SS>::SLICE;
+#define X(BB, SS) if (b == BB && s == SS) return Cfg<BB, Inner<BB, SS>::SI>::TSL;
   TQR_INSTANCES(X)
 #undef X
   return 0;
@@ -496,9 +504,11 @@ __global__ void eye_tiles_kernel(double* __restrict__ Qt, int64_t m, int64_t k, 
 
 // Packed reflector panels for apply-Q from the boundary factors (At, T): the same Yp/Tp
 // contents the factorization writes, one thread per element of the lower tile triangle.
-template <int B, int S>
+// The internal S x S blocks are the diagonal blocks of the output T_L (SO x SO).
+template <int B, int SO>
 __global__ void pack_factors_kernel(const double* __restrict__ A, const double* __restrict__ T, double* __restrict__ Yp,
                                     double* __restrict__ Tp, int p, int K) {
+  constexpr int S = Inner<B, SO>::SI, RB_ = SO / S;
   const int64_t bb = (int64_t)B * B;
   const int64_t total = (int64_t)p * K * bb;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
@@ -521,13 +531,69 @@ __global__ void pack_factors_kernel(const double* __restrict__ A, const double* 
       y = r < gc ? 0.0 : (r == gc ? 1.0 : At[(size_t)gc * B + r]);
     }
     Yp[tile * bb + in] = y;
-    if (q < S * S) {  // T block l of slot (i, k) in swz<S>
+    if (q < S * S) {  // internal T block l of slot (i, k) in swz<S>
       const int tb = q >> 6, tw = q & 63;
       const int tcb = tb / (S / 8), trb = tb % (S / 8);
       const int tc = tcb * 8 + (tw >> 3), tr = trb * 8 + ((tw & 7) ^ (tc & 6));
-      const int64_t slot = tile * (int64_t)S * B;
-      Tp[slot + (int64_t)l * S * S + q] = T[slot + (int64_t)l * S * S + (int64_t)tc * S + tr];
+      const int64_t slot = tile * (int64_t)SO * B;
+      const int Lo = l / RB_, mo = (l % RB_) * S;
+      Tp[slot + (int64_t)l * S * S + q] = T[slot + ((int64_t)Lo * SO + mo + tc) * SO + mo + tr];
     }
+  }
+}
+
+// Output T_L blocks when the executor ran with SI < SO (b = 512, s = 64): the off-diagonal
+// SI x SI blocks of T_L = (diag(1/tau) + striu(Z))^{-1}, Z = U_L^T U_L (the forward
+// column-wise DLARFT recurrence over SO columns; build_t).  The diagonal
+// blocks -- what the factorization applied -- are kept as written; tau_j = T_L[j][j].
+// One CTA per (slot (i, k), L); Z accumulated over 64-row chunks of the reflectors.
+template <int B, int SO>
+__global__ void __launch_bounds__(256) form_t_kernel(const double* __restrict__ A, double* __restrict__ T, int p,
+                                                     int qloc, int cstride, int coff) {
+  constexpr int SI = Inner<B, SO>::SI, NLO = B / SO, RC = 64;
+  extern __shared__ double fsm[];
+  double(*U)[SO + 1] = reinterpret_cast<double(*)[SO + 1]>(fsm);  // RC x (SO+1)
+  double* Z = fsm + RC * (SO + 1);
+  double* tau = Z + SO * SO;
+  double* Tf = fsm;  // aliases U once Z is complete
+  int64_t idx = blockIdx.x;
+  const int L = (int)(idx % NLO);
+  idx /= NLO;
+  const int i = (int)(idx % p), kc = (int)(idx / p);
+  const int k = coff + kc * cstride;  // global tile column
+  if (i < k || kc >= qloc) return;
+  const double* At = A + ((size_t)i + (size_t)kc * p) * B * B;
+  double* Ts = T + ((size_t)i + (size_t)kc * p) * (size_t)SO * B + (size_t)L * SO * SO;
+  const bool diag = i == k;
+  const int c0 = L * SO, tid = threadIdx.x;
+  const int a = tid % SO, bg = tid / SO, NBG = 256 / SO;
+  double acc[SO / (256 / SO)];
+#pragma unroll
+  for (int x = 0; x < SO / NBG; ++x) acc[x] = 0.0;
+  for (int r0 = diag ? c0 : 0; r0 < B; r0 += RC) {
+    __syncthreads();
+    for (int e = tid; e < RC * SO; e += 256) {
+      const int rr = e % RC, c = e / RC, r = r0 + rr, gc = c0 + c;
+      double u = 0.0;
+      if (r < B) u = diag ? (r < gc ? 0.0 : (r == gc ? 1.0 : At[(size_t)gc * B + r])) : At[(size_t)gc * B + r];
+      U[rr][c] = u;
+    }
+    __syncthreads();
+    for (int rr = 0; rr < RC; ++rr) {
+      const double ua = U[rr][a];
+#pragma unroll
+      for (int x = 0; x < SO / NBG; ++x) acc[x] += ua * U[rr][bg + NBG * x];
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < SO / NBG; ++x) Z[a + (bg + NBG * x) * SO] = acc[x];
+  if (tid < SO) tau[tid] = Ts[(size_t)tid * SO + tid];
+  __syncthreads();  // (U no longer read: Tf may overwrite it)
+  if (tid < 32 * ((SO + 31) / 32)) build_t<SO>(Tf, tau, Z);
+  __syncthreads();
+  for (int e = tid; e < SO * SO; e += 256) {
+    const int r = e % SO, c = e / SO;
+    if (r / SI < c / SI) Ts[e] = Tf[e];
   }
 }
 
@@ -591,6 +657,36 @@ cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, do
   const int64_t total = p * K * (int64_t)b * b;
 #define X(BB, SS) \
   if (b == BB && s == SS) { pack_factors_kernel<BB, SS><<<grid_for(total), 256, 0, st>>>(A, T, Yp, Tp, (int)p, (int)K); return cudaGetLastError(); }
+  TQR_INSTANCES(X)
+#undef X
+  return cudaErrorInvalidValue;
+}
+
+int exec_inner(int b, int s) {
+#define X(BB, SS) if (b == BB && s == SS) return Inner<BB, SS>::SI;
+  TQR_INSTANCES(X)
+#undef X
+  return 0;
+}
+template <int B, int SO>
+static cudaError_t form_t_one(const double* A, double* T, int64_t p, int64_t qloc, int cstride, int coff,
+                              cudaStream_t st) {
+  if constexpr (Inner<B, SO>::SI == SO) {
+    return cudaSuccess;
+  } else {
+    const int64_t nblk = p * qloc * (B / SO);
+    if (nblk == 0) return cudaSuccess;
+    constexpr size_t smem = (size_t)(64 * (SO + 1) + SO * SO + SO) * sizeof(double);
+    static_assert(64 * (SO + 1) >= SO * SO, "Tf alias");
+    cudaError_t e = cudaFuncSetAttribute(form_t_kernel<B, SO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    form_t_kernel<B, SO><<<(unsigned)nblk, 256, smem, st>>>(A, T, (int)p, (int)qloc, cstride, coff);
+    return cudaGetLastError();
+  }
+}
+cudaError_t launch_form_t(const double* A, double* T, int b, int s, int64_t p, int64_t qloc, int cstride, int coff,
+                          cudaStream_t st) {
+#define X(BB, SS) if (b == BB && s == SS) return form_t_one<BB, SS>(A, T, p, qloc, cstride, coff, st);
   TQR_INSTANCES(X)
 #undef X
   return cudaErrorInvalidValue;

@@ -718,7 +718,17 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   size_t tsz = 0;
   tqr_tiles_size(P, nullptr, &tsz);
   if (tsz) CU(cudaMemsetAsync(T, 0, tsz * sizeof(double), P->st));
-  return run(P, P->fact, At, T, nullptr, work, (P->prm.flags & TQR_FLAG_TRACE) != 0);
+  tqr_status st = run(P, P->fact, At, T, nullptr, work, (P->prm.flags & TQR_FLAG_TRACE) != 0);
+  if (st != TQR_OK) return st;
+  if (exec_inner(P->prm.b, P->prm.s) != P->prm.s) {
+    int cs, co;
+    colmap(P, &cs, &co);
+    if (P->emulate || P->G == 1)
+      CU(launch_form_t(At, T, P->prm.b, P->prm.s, P->p, P->q, 1, 0, P->st));
+    else
+      CU(launch_form_t(At, T, P->prm.b, P->prm.s, P->p, qloc_of(P, P->me), cs, co, P->st));
+  }
+  return TQR_OK;
 }
 
 static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** out) {

@@ -69,6 +69,11 @@ int exec_max_ctas(int b, int s, int device);
 bool exec_supported(int b, int s);
 // Columns per LARFB/SSRFB slice task for (b, s) (0 if no instance).
 int exec_slice(int b, int s);
+// Internal inner block SI of the executor for (b, s) (== s except b = 512).
+int exec_inner(int b, int s);
+// Off-diagonal blocks of the output T_L when SI < s (no-op otherwise).
+cudaError_t launch_form_t(const double* A, double* T, int b, int s, int64_t p, int64_t qloc, int cstride, int coff,
+                          cudaStream_t st);
 
 // Layout kernels.  Tile-major arrays hold the tile columns j = coff + jl*cstride of the
 // global p x q grid at storage column jl (single GPU / emulation: cstride 1, coff 0).

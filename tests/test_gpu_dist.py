@@ -34,7 +34,7 @@ def _factor_emulated(A, b, s, G):
 
 @pytest.mark.parametrize("m,n,b,s,G", [(256, 256, 64, 16, 2), (256, 256, 64, 16, 3), (700, 600, 256, 32, 2),
                                        (700, 600, 256, 32, 4), (1280, 300, 256, 32, 2), (520, 300, 128, 32, 8),
-                                       (67, 41, 16, 8, 3), (2048, 2048, 128, 32, 8)])
+                                       (67, 41, 16, 8, 3), (2048, 2048, 128, 32, 8), (1100, 1030, 512, 64, 2)])
 def test_emulated_ranks_bitwise_equal_single_gpu(m, n, b, s, G):
     A = tqr_inputs.uniform(m, n, 31 + m + G)
     g1 = run_factor(A, b, s)

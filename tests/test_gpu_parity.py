@@ -25,6 +25,7 @@ def _cases():
         (520, 300, 128, 32, "uniform"),
         (700, 600, 256, 32, "uniform"),  # C3 tiling, ragged
         (1280, 300, 256, 32, "normal"),  # C4-shaped tall-skinny
+        (1100, 1030, 512, 64, "uniform"),  # C5 tiling (internal 16-column blocks + form_t), ragged
     ]
 
 
@@ -56,7 +57,7 @@ def test_factor_deterministic():
 
 
 @pytest.mark.parametrize("m,n,b,s,nrhs", [(256, 256, 64, 16, 100), (700, 600, 256, 32, 300), (67, 41, 16, 8, 20),
-                                           (520, 300, 128, 32, 128)])
+                                           (520, 300, 128, 32, 128), (1100, 700, 512, 64, 200)])
 @pytest.mark.parametrize("trans", ["T", "N"])
 def test_ormqr_parity(m, n, b, s, nrhs, trans):
     import torch
@@ -73,7 +74,8 @@ def test_ormqr_parity(m, n, b, s, nrhs, trans):
     assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.linalg.norm(Bm)) * m
 
 
-@pytest.mark.parametrize("m,n,b,s", [(256, 256, 64, 16), (700, 600, 256, 32), (520, 300, 128, 32)])
+@pytest.mark.parametrize("m,n,b,s", [(256, 256, 64, 16), (700, 600, 256, 32), (520, 300, 128, 32),
+                                     (1100, 700, 512, 64)])
 def test_orgqr_and_backward_error_on_gpu(m, n, b, s):
     import torch
     A = tqr_inputs.uniform(m, n, 23 + m)
