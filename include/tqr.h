@@ -181,9 +181,11 @@ tqr_status tqr_profile_tasks(tqr_plan* plan, int32_t kind, int64_t count, double
 
 /* Profiling builds only (libtqr_phases.so, compiled with -DTQR_PROFILE_PHASES): attach a
  * caller-owned device array of 16 int64 per-phase clock64 totals (thread 0 of every CTA adds
- * its cycles in: 4 update phase of an update task, 5 its epilogue, 6 dispatch + dependency
- * wait, 7 update phase of a panel task, 8 panel staging, 9 panel factorization, 10 V/R out,
- * 11 Gram + packed Y out, 12 T build, 13 T out).  NULL detaches.  No-op in product builds. */
+ * its cycles in: 0 update prologue up to the first staged block, 1 ticket + task record,
+ * 2 end-of-task barrier, 3 release, 4 update phase of an update task, 5 its epilogue,
+ * 6 dependency wait, 7 update phase of a panel task, 8 panel staging, 9 panel factorization,
+ * 10 V/R out, 11 Gram + packed Y out, 12 T build, 13 T out).  NULL detaches.  No-op in
+ * product builds. */
 tqr_status tqr_phase_counters(tqr_plan* plan, long long* d_counters);
 
 #ifdef __cplusplus

@@ -75,13 +75,16 @@ __device__ __forceinline__ double* tslot_ptr(double* base, int i, int k, int p, 
 //   Tp slot (i,k), block l: S*S doubles at tslot_ptr(Tp, i, k) + l*S*S, swz<S> layout.
 
 // Stage panel l (Y_l: B*S doubles, T_l: S*S) from the packed workspace into buffer `buf`
-// with two TMA bulk copies completing on mbarrier full[buf].  One thread.
+// with two TMA bulk copies completing on mbarrier full[buf].  One thread.  No proxy fence
+// here: the generic-proxy writes of the packed panels are ordered before these async-proxy
+// reads by the fence.proxy.async after the dependency acquire (or after panel_block), and a
+// buffer refill after generic reads (WAR) needs none.  (A fence here also waited for the
+// thread's outstanding acc loads -- 6% of C3 time.)
 template <int B, int S>
 __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const double* Tp, int l, int buf) {
   using L = Layout<B, S>;
   constexpr unsigned YB = B * S * 8, TB = S * S * 8;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
-  fence_proxy_async();
   mbar_expect_tx(full + buf, YB + TB);
   bulk_g2s(sm + (buf ? L::Y1 : L::Y0), Yp + (size_t)l * B * S, YB, full + buf);
   bulk_g2s(sm + (buf ? L::T1 : L::T0), Tp + (size_t)l * S * S, TB, full + buf);
@@ -96,10 +99,11 @@ __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const 
 // with a buffer (shared-memory counter) issues its refill two blocks ahead, so there is no
 // __syncthreads inside the block loop and every refill overlaps a whole block of math.
 // C1 is fetched one block ahead by the group's rpart-0 warp (cp.async).
-template <int B, int S, bool QT, bool DESC>
+// `pf(li, nb)` is called by thread 0 once per block (cross-task prefetch hook).
+template <int B, int S, bool QT, bool DESC, class PF>
 __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>::RW / 8][2], const double* Yp,
                                              const double* Tp, int nb, double* C1, const double* Ct, int col0,
-                                             int gact) {
+                                             int gact, PF&& pf) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -111,19 +115,21 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
   int* done = reinterpret_cast<int*>(full + 2);
   double* c1s0 = sm + L::C1S + gi * C::C1W;           // C1 buffer for even li
   double* c1s1 = sm + L::C1S + L::C1SZ + gi * C::C1W;  // C1 buffer for odd li
-  if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
-  if (nb == 0) return;
-  if (top_owner) c1_fetch<B, S>(c1s0, C1, (DESC ? nb - 1 : 0) * S, cg0);
-  if (threadIdx.x == 0) {
+  if (nb > 0 && threadIdx.x == 0) {  // staging first: nothing outstanding to wait for
     mbar_init(full, 1);
     mbar_init(full + 1, 1);
     done[0] = 0;
     done[1] = 0;
     fence_mbar_init();
+    fence_proxy_async();
     issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 1 : 0, 0);
     if (nb > 1) issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 2 : 1, 1);
   }
+  if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
+  if (nb == 0) return;
+  if (top_owner) c1_fetch<B, S>(c1s0, C1, (DESC ? nb - 1 : 0) * S, cg0);
   __syncthreads();
+  PH_MARK(14);
   for (int li = 0; li < nb; ++li) {
     const int l = DESC ? nb - 1 - li : li;
     const int buf = li & 1;
@@ -132,7 +138,10 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
       __syncwarp();
       if (li + 1 < nb) c1_fetch<B, S>(buf ? c1s0 : c1s1, C1, (DESC ? l - 1 : l + 1) * S, cg0);
     }
+    if (li == 0) PH_MARK(15);
     mbar_wait(full + buf, (li >> 1) & 1);
+    if (li == 0) PH_MARK(0);
+    if (threadIdx.x == 0) pf(li, nb);
     if (active)
       group_apply<B, S, C::RW, C::RS, QT, true>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
                                                 buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
@@ -242,6 +251,29 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   PH_MARK(13);
 }
 
+// L2 prefetch of the inputs of a (not yet started) task record q: the tile column slice it
+// updates (+ its C1 slice), or the tile a panel task factors, and its first two packed
+// reflector blocks.  Safe before the task's dependencies hold (L2 is coherent).
+template <int B, int S, int SO, int MODE>
+__device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, const double* Yme, int p) {
+  using C = Cfg<B, S>;
+  const int kind = q[0], k = q[1], i = q[2], j = q[3], sl = q[4], kc = q[7];
+  if (MODE == 0 && (kind == K_G || kind == K_T)) {
+    prefetch_l2(tile_ptr(R.A, kind == K_T ? i : k, kc, p, B), (unsigned)(B * B * 8));
+    return;
+  }
+  const bool lkind = kind == K_L || kind == K_LQT || kind == K_LQ;
+  double* Bt = MODE == 0 ? R.A : R.Bt;
+  const size_t off = (size_t)sl * C::TSL * B;
+  prefetch_l2(tile_ptr(Bt, lkind ? k : i, j, p, B) + off, (unsigned)(C::TSL * B * 8));
+  if (!lkind) prefetch_l2(tile_ptr(Bt, k, j, p, B) + off, (unsigned)(C::TSL * B * 8));
+  const int vrow = lkind ? k : i;
+  const double* Y = Yme + ((size_t)vrow + (size_t)k * p) * (size_t)B * B;
+  constexpr int NL = B / S;
+  const int l0 = MODE == 2 ? (NL >= 2 ? NL - 2 : 0) : 0;
+  prefetch_l2(Y + (size_t)l0 * B * S, (unsigned)((NL >= 2 ? 2 : 1) * B * S * 8));
+}
+
 // ---------------------------------------------------------------------------------------
 // Persistent executor.
 // ---------------------------------------------------------------------------------------
@@ -262,9 +294,23 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
   if (tid < NPH) s_ph[tid] = 0;
   __syncthreads();
 #endif
+  // Cross-task pipelining (thread 0): half-way through the last pass of an update the next
+  // ticket is taken, one block later its record is fetched (cp.async), one more block later
+  // its input tiles are prefetched into L2, so the next prologue (acc / C1 loads, first
+  // TMA) reads from L2 and the dispatch round trips overlap math.  Holding one ticket ahead cannot
+  // deadlock: every wait is on a smaller ticket, and the smallest unfinished ticket is running.
+  __shared__ __align__(16) int s_next[TASK_INTS];
+  __shared__ int s_have;
+  int next_tk = -1, rec_for = -1;  // thread 0
   for (;;) {
     PH_T0;
-    if (tid == 0) s_ticket = atomicAdd(R.ticket, 1);
+    if (tid == 0) {
+      if (next_tk < 0) next_tk = atomicAdd(R.ticket, 1);
+      cp_async_wait<0>();  // a prefetched record has landed
+      s_ticket = next_tk;
+      s_have = rec_for == next_tk;
+      next_tk = -1;
+    }
     __syncthreads();
     const int tk = s_ticket;
 #ifdef TQR_PROFILE_PHASES
@@ -275,8 +321,9 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
 #else
     if (tk >= R.ntasks) return;
 #endif
-    if (tid < TASK_INTS) s_task[tid] = R.tasks[(size_t)tk * TASK_INTS + tid];
+    if (tid < TASK_INTS) s_task[tid] = s_have ? s_next[tid] : R.tasks[(size_t)tk * TASK_INTS + tid];
     __syncthreads();
+    PH_MARK(1);
     unsigned long long t_grab = 0, t_start = 0;
     if (R.trace && tid == 0) t_grab = globaltimer();
     if (warp == 0) {
@@ -338,7 +385,23 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
           nb = NL;
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }
-        update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact);
+        auto pf = [&](int li, int nbb) {
+          if (sub != nsub - 1 || nbb < 4) return;
+          const int l0 = nbb / 2;
+          if (li == l0) next_tk = atomicAdd(R.ticket, 1);  // next ticket, half a pass early
+          if (li == l0 + 1 && next_tk < R.ntasks) {       // its record -> s_next (async)
+#pragma unroll
+            for (int x = 0; x < TASK_INTS; x += 4)  // 4 x 16 bytes
+              cp_async16(s_next + x, R.tasks + (size_t)next_tk * TASK_INTS + x);
+            cp_async_commit();
+            rec_for = next_tk;
+          }
+          if (li == l0 + 2 && rec_for == next_tk && next_tk < R.ntasks) {
+            cp_async_wait<0>();
+            prefetch_task<B, S, SO, MODE>(s_next, R, Yme, p);
+          }
+        };
+        update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact, pf);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (panel) {
           panel_block<B, S, SO>(sm, acc, ts, Akk, Ab, Tslot, a, yoff, toff, sub);
@@ -350,6 +413,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
       }
     }
     __syncthreads();
+    PH_MARK(2);
     if (tid == 0) {
       __threadfence();
       fence_proxy_async();
@@ -365,6 +429,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
       } else {
         st_release(R.ctr + oidx, oval);
       }
+      PH_MARK(3);
       if (R.trace) {
         unsigned long long* tr = R.trace + (size_t)tk * 4;
         tr[0] = ((unsigned long long)smid() << 32) | (unsigned)tk;

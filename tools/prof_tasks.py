@@ -11,6 +11,9 @@ import torch  # noqa: E402
 
 import paper_0707_3548_b200 as tqr  # noqa: E402
 
+PHASE_NAMES = ["prologue", "ticket+record", "end barrier", "release", "update blocks", "store", "dep wait",
+               "panel-update", "stage", "factor", "V/R out", "gram+Yp", "build_t", "T out", "upd setup",
+         "C1 wait"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--b", type=int, default=256)
 ap.add_argument("--s", type=int, default=32)
@@ -50,8 +53,7 @@ for kind in [int(x) for x in a.kinds.split(",")]:
         v = PH.cpu().tolist()
         PH.zero_()
         tot = sum(v)
-        names = ["-", "-", "-", "-", "update", "store", "dispatch+deps", "panel-update", "stage", "factor",
-                 "V/R out", "gram+Yp", "build_t", "T out", "-", "-"]
+        names = PHASE_NAMES
         print("   phases (% of warp-0 cycles, all reps): " + ", ".join(f"{n} {100*x/tot:.1f}" for n, x in zip(names, v) if x))
     per_task_us = ms * 1e3 / waves
     print(f"kind {['G','T','L','S','LQT','SQT','LQ','SQ'][kind]} b={b} s={s}: {count} tasks in {ms:.3f} ms -> {per_task_us:.1f} us/task/SM, "
