@@ -291,6 +291,14 @@ def main():
         cpu = {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc, "seconds": dt}
 
     achieved = flops / world / (kern_ms * 1e-3) / 1e12   # this GPU's share of the job, per launch
+    traffic = None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
+        if tr and world == 1:
+            traffic = {"bytes_per_launch": tr["bytes"], "source": tr["source"],
+                       "algorithmic_flop_per_byte": flops / tr["bytes"]}
+    except (OSError, ValueError):
+        pass
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -306,7 +314,7 @@ def main():
         "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
         "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                      "kernel": f"exec_kernel<{b},{s}> (tqr_geqrf)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops / world,
                      "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt); "

@@ -393,26 +393,19 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
   auto top = [&](int r, int c) -> double& { return TS ? Rb[r + c * S] : P[c0 + r + c * LDP]; };
   auto lo_of = [&](int jj) { return TS ? 0 : c0 + jj + 1; };
 
-  // Householder generation for column jj by its owner warp, then publish (release).
-  auto house_pub = [&](int jj) {
+  // Householder generation (R2-R4, R17, R20) from alpha and sigma = ||x||^2, x in
+  // registers (rows >= lo); stores v, beta, tau and publishes (bar.arrive).
+  auto house_pub = [&](int jj, double alpha, double sigma, const double (&xr)[NR]) {
     const int lo = lo_of(jj);
-    double xr[NR];
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int x = 0; x < NR; ++x) {
-      const int r = lane + 32 * x;
-      xr[x] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
-      if (x & 1) s1 += xr[x] * xr[x]; else s0 += xr[x] * xr[x];
-    }
-    const double sigma = warp_sum(s0 + s1);
-    const double alpha = top(jj, jj);
     double beta, tv, scale;
     if (sigma == 0.0) {
       beta = alpha; tv = 0.0; scale = 0.0;
     } else {
-      const double nu = sqrt(alpha * alpha + sigma);
+      const double nn = alpha * alpha + sigma;
+      const double rn = rsqrt(nn);                // 1/nu
+      const double nu = nn * rn;
       beta = (alpha >= 0.0) ? -nu : nu;
-      tv = (beta - alpha) / beta;
+      tv = 1.0 + fabs(alpha) * rn;                 // (beta - alpha)/beta = 1 + |alpha|/nu
       scale = 1.0 / (alpha - beta);
     }
 #pragma unroll
@@ -427,38 +420,93 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
     }
     named_arrive(1 + jj % 15, 32 * NW);  // publishes v_jj, tau_jj, beta_jj (no wait)
   };
+  auto load_x = [&](int c, int lo, double (&xr)[NR]) {
+#pragma unroll
+    for (int x = 0; x < NR; ++x) {
+      const int r = lane + 32 * x;
+      xr[x] = (r >= lo && r < B) ? P[r + c * LDP] : 0.0;
+    }
+  };
 
-  if (warp == 0) house_pub(0);
+  if (warp == 0) {
+    double xr[NR];
+    load_x(0, lo_of(0), xr);
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int x = 0; x < NR; ++x) { if (x & 1) s1 += xr[x] * xr[x]; else s0 += xr[x] * xr[x]; }
+    house_pub(0, top(0, 0), warp_sum(s0 + s1), xr);
+  }
   for (int jj = 0; jj + 1 < S; ++jj) {
     if (warp != jj % NW) named_bar(1 + jj % 15, 32 * NW);  // v_jj published
     const double tj = tau[jj];
     const int lo = lo_of(jj);
     double vr[NR];
-#pragma unroll
-    for (int x = 0; x < NR; ++x) {
-      const int r = lane + 32 * x;
-      vr[x] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
-    }
+    load_x(jj, lo, vr);
     const int nxt = jj + 1;
-    if (nxt % NW == warp) {  // critical path: update column jj+1, generate reflector jj+1
+    if (nxt % NW == warp) {
+      // Critical path: update column jj+1 and generate reflector jj+1.  One interleaved
+      // reduction of (x.v, x.x, v.v) gives the dot product AND the new sub-column norm by
+      // downdating, sigma' = x.x - 2 tw x.v + tw^2 v.v [- alpha'^2 for GEQRT]; if that may
+      // have cancelled (sigma' below 5% of the magnitude of its terms) it is recomputed
+      // directly from the updated column (R20, the xGEQP3 safeguard).
       double xr[NR];
-      double d0 = 0.0, d1 = 0.0;
+      load_x(nxt, lo, xr);
+      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
       for (int x = 0; x < NR; ++x) {
-        const int r = lane + 32 * x;
-        xr[x] = (r >= lo && r < B) ? P[r + nxt * LDP] : 0.0;
-        if (x & 1) d1 += vr[x] * xr[x]; else d0 += vr[x] * xr[x];
+        if (x & 1) { a1 += vr[x] * xr[x]; b1 += xr[x] * xr[x]; e1 += vr[x] * vr[x]; }
+        else { a0 += vr[x] * xr[x]; b0 += xr[x] * xr[x]; e0 += vr[x] * vr[x]; }
       }
-      const double tw = tj * (top(jj, nxt) + warp_sum(d0 + d1));
+      double sxv = a0 + a1, sxx = b0 + b1, svv = e0 + e1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        sxv += __shfl_xor_sync(0xffffffffu, sxv, o);
+        sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+        svv += __shfl_xor_sync(0xffffffffu, svv, o);
+      }
+      const double tw = tj * (top(jj, nxt) + sxv);
 #pragma unroll
       for (int x = 0; x < NR; ++x) {
         const int r = lane + 32 * x;
-        if (r >= lo && r < B) P[r + nxt * LDP] = xr[x] - tw * vr[x];
+        if (r >= lo && r < B) {
+          xr[x] -= tw * vr[x];
+          P[r + nxt * LDP] = xr[x];
+        }
       }
       __syncwarp();
       if (lane == 0) top(jj, nxt) -= tw;
       __syncwarp();
-      house_pub(nxt);
+      // alpha of column jj+1: R[jj+1][jj+1] (TSQRT) or the updated row c0+jj+1 (GEQRT)
+      double alpha, a2 = 0.0;
+      if (TS) {
+        alpha = top(nxt, nxt);
+      } else {
+        double t = 0.0;
+#pragma unroll
+        for (int x = 0; x < NR; ++x)
+          if ((lo >> 5) == x) t = xr[x];
+        alpha = __shfl_sync(0xffffffffu, t, lo & 31);
+        a2 = alpha * alpha;
+      }
+      double sigma = sxx - 2.0 * tw * sxv + tw * tw * svv - a2;
+      const double mag = sxx + 2.0 * fabs(tw * sxv) + tw * tw * svv + a2;
+      const int lon = lo_of(nxt);
+      if (!(sigma >= 0.05 * mag)) {  // possible cancellation (or NaN): direct norm
+        double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+        for (int x = 0; x < NR; ++x) {
+          const int r = lane + 32 * x;
+          const double v = (r >= lon && r < B) ? xr[x] : 0.0;
+          if (x & 1) s1 += v * v; else s0 += v * v;
+        }
+        sigma = warp_sum(s0 + s1);
+      }
+      if (!TS) {  // x of column jj+1 starts one row lower
+#pragma unroll
+        for (int x = 0; x < NR; ++x)
+          if (lane + 32 * x < lon) xr[x] = 0.0;
+      }
+      house_pub(nxt, alpha, sigma, xr);
     }
     // the other columns c > jj+1 of this warp: dots, interleaved reductions, updates
     double dc[NC];

@@ -366,8 +366,12 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
       const size_t toff = ((size_t)vrow + (size_t)k * p) * (size_t)SO * B;
       const double* Ypt = Yme + yoff;
       const double* Tps = Tme + toff;
-      const int nsub = panel ? NL : Cfg<B, S>::TSL / Cfg<B, S>::SLICE;
-      for (int sub = 0; sub < nsub; ++sub) {
+      // panel task: inner blocks [sub0, sub1) of the tile (one output T block per task, or the
+      // whole tile when sl < 0); update task: TSL / SLICE register passes of its slice
+      constexpr int SPT = SO / S;  // internal blocks per output T block
+      const int sub0 = panel ? (sl < 0 ? 0 : sl * SPT) : 0;
+      const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : Cfg<B, S>::TSL / Cfg<B, S>::SLICE;
+      for (int sub = sub0; sub < nsub; ++sub) {
         double acc[Cfg<B, S>::RW / 8][2];
         double* C1;
         double* Ct;
@@ -381,7 +385,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
         } else {
           C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
           Ct = lkind ? tile_ptr(Bt, k, j, p, B) : tile_ptr(Bt, i, j, p, B);
-          col0 = sl * Cfg<B, S>::TSL + sub * Cfg<B, S>::SLICE;
+          col0 = sl * Cfg<B, S>::TSL + sub * Cfg<B, S>::SLICE;  // (update tasks: sl >= 0)
           nb = NL;
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }

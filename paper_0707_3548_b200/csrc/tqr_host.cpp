@@ -1,13 +1,15 @@
 // tqr_host.cpp -- host runtime of the tiled QR library: plan, DAG task tables, list-schedule
 // dispatch order, and the C ABI declared in include/tqr.h.
 //
-// DAG (edges derived from each kernel's read/write sets, SPEC dag module):
-//   G(k)        <- S(k-1,k,k,*)
-//   L(k,j,sl)   <- G(k), S(k-1,k,j,sl)
-//   T(k,i)      <- G(k) | T(k,i-1), S(k-1,i,k,*)
-//   S(k,i,j,sl) <- T(k,i), L(k,j,sl) | S(k,i-1,j,sl), S(k-1,i,j,sl)
+// DAG (edges derived from each kernel's read/write sets, SPEC dag module),
+// with the panel tasks split by inner block l (R21):
+//   G(k,l)      <- G(k,l-1) | S(k-1,k,k,*) (l = 0)
+//   T(k,i,l)    <- G(k,l) | T(k,i-1,l);  T(k,i,l-1) | S(k-1,i,k,*) (l = 0)
+//   L(k,j,sl)   <- G(k, last), S(k-1,k,j,sl)
+//   S(k,i,j,sl) <- T(k,i, last), L(k,j,sl) | S(k,i-1,j,sl), S(k-1,i,j,sl)
 // Every dependency is a chain, so it is expressed on the device as "progress counter >=
-// value": panel[k] counts G(k), T(k,k+1), ... ; col[k][j][sl] counts L(k,j,sl), S(k,k+1,j,sl), ...
+// value": pblk[k][l] counts G(k,l), T(k,k+1,l), ... ; col[k][j][sl] counts L(k,j,sl),
+// S(k,k+1,j,sl), ...
 // The dispatch (ticket) order is a list schedule of the DAG on `workers` CTAs with the
 // paper's priorities G > T > L > S, ties by (k, i, j, slice); it is
 // topological by construction, so with all CTAs co-resident no ticket can wait forever.
@@ -209,43 +211,57 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
+  const int NPT = b / s;  // panel sub-tasks per tile: one per inner block l (one output T_l)
   DurModel dm(b, s, w);
   TaskGen T;
   auto own = [&](int64_t j) { return (int)(j % G); };
   auto qloc = [&](int r) { return r < q ? (int)((q - r + G - 1) / G) : 0; };
   auto scol = [&](int64_t j) { return real_layout ? (int)(j / G) : (int)j; };
-  auto PANEL = [&](int k) { return k; };
-  auto COL = [&](int k, int64_t j, int sl) { return K + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl); };
+  // pblk[k][l]: how many panel tasks of step k (GEQRT(k), TSQRT(k,k+1), ...) have finished
+  // inner block l (a copy on every rank)
+  auto PBLK = [&](int k, int l) { return k * NPT + l; };
+  auto COL = [&](int k, int64_t j, int sl) {
+    return K * NPT + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl);
+  };
   out.nctr.assign(G, 0);
-  for (int r = 0; r < G; ++r) out.nctr[r] = K + (int)((int64_t)K * qloc(r) * nsl);
+  for (int r = 0; r < G; ++r) out.nctr[r] = K * NPT + (int)((int64_t)K * qloc(r) * nsl);
   for (int k = 0; k < K; ++k) {
     const int ok = own(k);
-    int id = T.add(K_G, k, k, scol(k), 0, PANEL(k), 1, dm.g, 0);
-    T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
-    if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, 2);
+    // GEQRT(k) block l: own block l-1 first; block 0 needs tile (k,k) updated by step k-1
+    for (int l = 0; l < NPT; ++l) {
+      int id = T.add(K_G, k, k, scol(k), l, PBLK(k, l), 1, dm.g / NPT, 0);
+      T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
+      if (l > 0) T.dep(id, PBLK(k, l - 1), 1, 1);
+      else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, 2);
+    }
     out.counts[0]++;
     for (int j = k + 1; j < q; ++j)
       for (int sl = 0; sl < nsl; ++sl) {
         // lookahead (R10): updates of column k+1 feed panel k+1 -> critical path
-        id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
+        int id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
         T.t[id].rank = own(j); T.t[id].kc = scol(k);
         T.t[id].key[2] = j;
-        T.dep(id, PANEL(k), 1, 1);
+        T.dep(id, PBLK(k, NPT - 1), 1, 1);
         if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, 2);
         out.counts[2]++;
       }
     for (int i = k + 1; i < p; ++i) {
-      id = T.add(K_T, k, i, scol(k), 0, PANEL(k), i - k + 1, dm.t, 1);
-      T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
-      T.dep(id, PANEL(k), 1, i - k);
-      if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
+      // TSQRT(k,i) block l touches only column block l of R_kk (and tile (i,k)): it follows
+      // TSQRT(k,i-1) block l and its own block l-1 -- a wavefront over (i, l) (R21)
+      for (int l = 0; l < NPT; ++l) {
+        int id = T.add(K_T, k, i, scol(k), l, PBLK(k, l), i - k + 1, dm.t / NPT, 1);
+        T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
+        T.dep(id, PBLK(k, l), 1, i - k);
+        if (l > 0) T.dep(id, PBLK(k, l - 1), 1, i - k + 1);
+        else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
+      }
       out.counts[1]++;
       for (int j = k + 1; j < q; ++j)
         for (int sl = 0; sl < nsl; ++sl) {
-          id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
+          int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
-          T.dep(id, PANEL(k), 1, i - k + 1);
+          T.dep(id, PBLK(k, NPT - 1), 1, i - k + 1);
           T.dep(id, COL(k, j, sl), 1, i - k);
           if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
           out.counts[3]++;
@@ -818,7 +834,7 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   if (nslice < 1) return bad_arg(3, "nslice < 1");
   if (workers < 1) return bad_arg(4, "workers < 1");
   if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
-  build_factor_sched(p, q, 64 * nslice, 8, nslice, std::vector<int>(nranks, workers), nranks > 1, s);
+  build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1, s);
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
@@ -901,7 +917,7 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
     const bool lkind = kind == 2 || kind == 4 || kind == 6;
     q[2] = (kind == 0 || lkind) ? q[1] : i;
     q[3] = (kind == 0 || kind == 1) ? q[1] : j;
-    q[4] = (int)(t % P->nsl);
+    q[4] = (kind == 0 || kind == 1) ? -1 : (int)(t % P->nsl);  // -1: a panel task over the whole tile
     q[5] = 0;
     q[6] = 1;
     q[7] = q[1];

@@ -14,6 +14,7 @@ import numpy as np
 import pytest
 
 K_G, K_T, K_L, K_S = 0, 1, 2, 3
+NPT = 2  # panel sub-tasks per tile in the inspected schedules (b / s = 64n / 32n; R21)
 
 
 @pytest.fixture(scope="module")
@@ -32,7 +33,7 @@ def _global_j(rec, G, r):
 def _task_key(rec, G, r):
     kind = int(rec[0])
     j = _global_j(rec, G, r) if kind in (K_L, K_S) else int(rec[1])
-    return (kind, int(rec[1]), int(rec[2]), int(j), int(rec[4]) if kind in (K_L, K_S) else 0)
+    return (kind, int(rec[1]), int(rec[2]), int(j), int(rec[4]))
 
 
 def _deps(rec):
@@ -120,7 +121,8 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
     for g, sim in enumerate(sims):
         # every rank ends with the complete panel progress of every step, received exactly once
         for k in range(K):
-            assert sim.ctr[k] == max(1, p - k)
+            for l in range(NPT):
+                assert sim.ctr[k * NPT + l] == max(1, p - k)
         assert all(v == 1 for v in seen[g].values())
 
 
@@ -158,7 +160,7 @@ def _gloo_rank(rank, world, port, p, q, nsl, workers, out):
             rounds += 1
             # nobody ran a task this round and some rank is unfinished: cross-rank deadlock
             assert rounds < 100000 and any(r for _, _, r in allp), "deadlock across ranks"
-        out.put((rank, sim.done, len(recs), sim.ctr[:min(p, q)].tolist()))
+        out.put((rank, sim.done, len(recs), sim.ctr[:min(p, q) * NPT].tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -181,7 +183,7 @@ def test_gloo_two_ranks_replay(L, p, q, nsl, workers):
     K = min(p, q)
     for rank, done, n, ctr in res:
         assert done == n
-        assert ctr == [max(1, p - k) for k in range(K)]
+        assert ctr == [max(1, p - k) for k in range(K) for _ in range(NPT)]
 
 
 def test_exchange_blobs_gloo():
