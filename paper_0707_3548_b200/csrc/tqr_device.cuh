@@ -26,6 +26,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 namespace tqr {
 
 // Per-(b, s) CTA shape.  A column group (8 columns) is held by RS warps, each owning
@@ -60,6 +62,16 @@ struct Inner {
 };
 
 __device__ __forceinline__ int phi(int n) { return ((n & 1) << 2) | (n >> 1); }
+
+// f(std::integral_constant<int, I>) for I = 0 .. N-1: register-array indices stay compile-time
+// constants inside lambdas (a runtime index would move the array to local memory)
+template <int N, int I = 0, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<N, I + 1>(f);
+  }
+}
 
 // 8x8-block swizzled layout of an R x C operand (R, C multiples of 8): element (r, c) at
 // block (r/8, c/8) (blocks column-major), inside the block column-major with the row
@@ -388,14 +400,51 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 template <int B, int S, int NW, int LDP>
 __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, double* tau, const bool TS) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NR = (B + 31) / 32;       // rows per lane
-  constexpr int NC = (S + NW - 1) / NW;   // columns per warp
-  auto top = [&](int r, int c) -> double& { return TS ? Rb[r + c * S] : P[c0 + r + c * LDP]; };
-  auto lo_of = [&](int jj) { return TS ? 0 : c0 + jj + 1; };
+  constexpr int NR = (B + 31) / 32;       // rows per lane: row r = lane + 32 x
+  constexpr int NC = (S + NW - 1) / NW;   // columns per warp: column c = warp + NW ci
+  const int lo0 = TS ? 0 : c0;             // first panel row held in P
+  auto lo_of = [&](int jj) __attribute__((always_inline)) { return TS ? 0 : c0 + jj + 1; };
+  // The warp's columns live in registers for the whole panel (a column step would otherwise
+  // read + write the whole panel in shared memory: 128 KiB per step, ~1000 clk at b = 256).
+  double x[NC][NR];
+#pragma unroll
+  for (int ci = 0; ci < NC; ++ci)
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q, c = warp + NW * ci;
+      x[ci][q] = (c < S && r >= lo0 && r < B) ? P[r + c * LDP] : 0.0;
+    }
+  // (all lambdas below take the column index as std::integral_constant: see static_for)
+  // row r of column CI, broadcast to the warp
+  auto get_row = [&](auto CI, int r) __attribute__((always_inline)) -> double {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+      if ((r >> 5) == q) t = x[decltype(CI)::value][q];
+    return __shfl_sync(0xffffffffu, t, r & 31);
+  };
+  auto add_row = [&](auto CI, int r, double v) __attribute__((always_inline)) {
+#pragma unroll
+    for (int q = 0; q < NR; ++q)
+      if ((r >> 5) == q && lane == (r & 31)) x[decltype(CI)::value][q] += v;
+  };
+  // "top" entry of reflector jj in column CI: R[jj][c] (TSQRT, in Rb) or tile row c0+jj
+  auto top_get = [&](auto CI, int jj) __attribute__((always_inline)) -> double {
+    return TS ? Rb[jj + (warp + NW * decltype(CI)::value) * S] : get_row(CI, c0 + jj);
+  };
+  auto top_sub = [&](auto CI, int jj, double w) __attribute__((always_inline)) {
+    if (TS) {
+      __syncwarp();
+      if (lane == 0) Rb[jj + (warp + NW * decltype(CI)::value) * S] -= w;
+    } else {
+      add_row(CI, c0 + jj, -w);
+    }
+  };
 
-  // Householder generation (R2-R4, R17, R20) from alpha and sigma = ||x||^2, x in
-  // registers (rows >= lo); stores v, beta, tau and publishes (bar.arrive).
-  auto house_pub = [&](int jj, double alpha, double sigma, const double (&xr)[NR]) {
+  // Householder generation (R2-R4, R17, R20) for column jj = warp + NW ci from alpha
+  // and sigma = ||x||^2 (rows >= lo_of(jj)); stores v into P, beta, tau; publishes (bar.arrive).
+  auto house_pub = [&](auto CI, int jj, double alpha, double sigma) __attribute__((always_inline)) {
+    constexpr int ci = decltype(CI)::value;
     const int lo = lo_of(jj);
     double beta, tv, scale;
     if (sigma == 0.0) {
@@ -409,39 +458,40 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       scale = 1.0 / (alpha - beta);
     }
 #pragma unroll
-    for (int x = 0; x < NR; ++x) {
-      const int r = lane + 32 * x;
-      if (r >= lo && r < B) P[r + jj * LDP] = xr[x] * scale;
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q;
+      if (r >= lo && r < B) P[r + jj * LDP] = x[ci][q] * scale;
     }
-    __syncwarp();
     if (lane == 0) {
-      top(jj, jj) = beta;
+      if (TS) Rb[jj + jj * S] = beta; else P[c0 + jj + jj * LDP] = beta;
       tau[jj] = tv;
     }
     named_arrive(1 + jj % 15, 32 * NW);  // publishes v_jj, tau_jj, beta_jj (no wait)
   };
-  auto load_x = [&](int c, int lo, double (&xr)[NR]) {
-#pragma unroll
-    for (int x = 0; x < NR; ++x) {
-      const int r = lane + 32 * x;
-      xr[x] = (r >= lo && r < B) ? P[r + c * LDP] : 0.0;
-    }
-  };
 
   if (warp == 0) {
-    double xr[NR];
-    load_x(0, lo_of(0), xr);
+    const int lo = lo_of(0);
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-    for (int x = 0; x < NR; ++x) { if (x & 1) s1 += xr[x] * xr[x]; else s0 += xr[x] * xr[x]; }
-    house_pub(0, top(0, 0), warp_sum(s0 + s1), xr);
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q;
+      const double v = (r >= lo && r < B) ? x[0][q] : 0.0;
+      if (q & 1) s1 += v * v; else s0 += v * v;
+    }
+    const double sg = warp_sum(s0 + s1);
+    const std::integral_constant<int, 0> C0;
+    house_pub(C0, 0, top_get(C0, 0), sg);
   }
   for (int jj = 0; jj + 1 < S; ++jj) {
     if (warp != jj % NW) named_bar(1 + jj % 15, 32 * NW);  // v_jj published
     const double tj = tau[jj];
     const int lo = lo_of(jj);
     double vr[NR];
-    load_x(jj, lo, vr);
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q;
+      vr[q] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
+    }
     const int nxt = jj + 1;
     if (nxt % NW == warp) {
       // Critical path: update column jj+1 and generate reflector jj+1.  One interleaved
@@ -449,66 +499,49 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       // downdating, sigma' = x.x - 2 tw x.v + tw^2 v.v [- alpha'^2 for GEQRT]; if that may
       // have cancelled (sigma' below 5% of the magnitude of its terms) it is recomputed
       // directly from the updated column (R20, the xGEQP3 safeguard).
-      double xr[NR];
-      load_x(nxt, lo, xr);
-      double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
+      static_for<NC>([&](auto CI) __attribute__((always_inline)) {
+        constexpr int ci = decltype(CI)::value;
+        if (warp + NW * ci != nxt) return;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
-      for (int x = 0; x < NR; ++x) {
-        if (x & 1) { a1 += vr[x] * xr[x]; b1 += xr[x] * xr[x]; e1 += vr[x] * vr[x]; }
-        else { a0 += vr[x] * xr[x]; b0 += xr[x] * xr[x]; e0 += vr[x] * vr[x]; }
-      }
-      double sxv = a0 + a1, sxx = b0 + b1, svv = e0 + e1;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        sxv += __shfl_xor_sync(0xffffffffu, sxv, o);
-        sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
-        svv += __shfl_xor_sync(0xffffffffu, svv, o);
-      }
-      const double tw = tj * (top(jj, nxt) + sxv);
-#pragma unroll
-      for (int x = 0; x < NR; ++x) {
-        const int r = lane + 32 * x;
-        if (r >= lo && r < B) {
-          xr[x] -= tw * vr[x];
-          P[r + nxt * LDP] = xr[x];
+        for (int q = 0; q < NR; ++q) {
+          const int r = lane + 32 * q;
+          const double xv = (r >= lo && r < B) ? x[ci][q] : 0.0;
+          if (q & 1) { a1 += vr[q] * xv; b1 += xv * xv; e1 += vr[q] * vr[q]; }
+          else { a0 += vr[q] * xv; b0 += xv * xv; e0 += vr[q] * vr[q]; }
         }
-      }
-      __syncwarp();
-      if (lane == 0) top(jj, nxt) -= tw;
-      __syncwarp();
-      // alpha of column jj+1: R[jj+1][jj+1] (TSQRT) or the updated row c0+jj+1 (GEQRT)
-      double alpha, a2 = 0.0;
-      if (TS) {
-        alpha = top(nxt, nxt);
-      } else {
-        double t = 0.0;
+        double sxv = a0 + a1, sxx = b0 + b1, svv = e0 + e1;
 #pragma unroll
-        for (int x = 0; x < NR; ++x)
-          if ((lo >> 5) == x) t = xr[x];
-        alpha = __shfl_sync(0xffffffffu, t, lo & 31);
-        a2 = alpha * alpha;
-      }
-      double sigma = sxx - 2.0 * tw * sxv + tw * tw * svv - a2;
-      const double mag = sxx + 2.0 * fabs(tw * sxv) + tw * tw * svv + a2;
-      const int lon = lo_of(nxt);
-      if (!(sigma >= 0.05 * mag)) {  // possible cancellation (or NaN): direct norm
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int x = 0; x < NR; ++x) {
-          const int r = lane + 32 * x;
-          const double v = (r >= lon && r < B) ? xr[x] : 0.0;
-          if (x & 1) s1 += v * v; else s0 += v * v;
+        for (int o = 16; o > 0; o >>= 1) {
+          sxv += __shfl_xor_sync(0xffffffffu, sxv, o);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+          svv += __shfl_xor_sync(0xffffffffu, svv, o);
         }
-        sigma = warp_sum(s0 + s1);
-      }
-      if (!TS) {  // x of column jj+1 starts one row lower
+        const double tw = tj * (top_get(CI, jj) + sxv);
 #pragma unroll
-        for (int x = 0; x < NR; ++x)
-          if (lane + 32 * x < lon) xr[x] = 0.0;
-      }
-      house_pub(nxt, alpha, sigma, xr);
+        for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];  // vr == 0 outside rows >= lo
+        top_sub(CI, jj, tw);
+        // alpha of column jj+1: R[jj+1][jj+1] (TSQRT) or the updated tile row c0+jj+1 (GEQRT)
+        __syncwarp();
+        const double alpha = top_get(CI, nxt);
+        const double a2 = TS ? 0.0 : alpha * alpha;
+        double sigma = sxx - 2.0 * tw * sxv + tw * tw * svv - a2;
+        const double mag = sxx + 2.0 * fabs(tw * sxv) + tw * tw * svv + a2;
+        if (!(sigma >= 0.05 * mag)) {  // possible cancellation (or NaN): direct norm
+          const int lon = lo_of(nxt);
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int q = 0; q < NR; ++q) {
+            const int r = lane + 32 * q;
+            const double v = (r >= lon && r < B) ? x[ci][q] : 0.0;
+            if (q & 1) s1 += v * v; else s0 += v * v;
+          }
+          sigma = warp_sum(s0 + s1);
+        }
+        house_pub(CI, nxt, alpha, sigma);
+      });
     }
-    // the other columns c > jj+1 of this warp: dots, interleaved reductions, updates
+    // the warp's other columns c > jj+1: dots, one interleaved butterfly, register updates
     double dc[NC];
 #pragma unroll
     for (int ci = 0; ci < NC; ++ci) {
@@ -516,33 +549,37 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       double d0 = 0.0, d1 = 0.0;
       if (c > nxt && c < S) {
 #pragma unroll
-        for (int x = 0; x < NR; ++x) {
-          const int r = lane + 32 * x;
-          const double xv = (r >= lo && r < B) ? P[r + c * LDP] : 0.0;
-          if (x & 1) d1 += vr[x] * xv; else d0 += vr[x] * xv;
+        for (int q = 0; q < NR; ++q) {
+          if (q & 1) d1 += vr[q] * x[ci][q]; else d0 += vr[q] * x[ci][q];
         }
       }
       dc[ci] = d0 + d1;
     }
 #pragma unroll
-    for (int ci = 0; ci < NC; ++ci) dc[ci] = warp_sum(dc[ci]);
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int ci = 0; ci < NC; ++ci) {
+      for (int ci = 0; ci < NC; ++ci) dc[ci] += __shfl_xor_sync(0xffffffffu, dc[ci], o);
+    static_for<NC>([&](auto CI) __attribute__((always_inline)) {
+      constexpr int ci = decltype(CI)::value;
       const int c = warp + NW * ci;
       if (c > nxt && c < S) {
-        const double tw = tj * (top(jj, c) + dc[ci]);
+        const double tw = tj * (top_get(CI, jj) + dc[ci]);
 #pragma unroll
-        for (int x = 0; x < NR; ++x) {
-          const int r = lane + 32 * x;
-          if (r >= lo && r < B) P[r + c * LDP] -= tw * vr[x];
-        }
-        __syncwarp();
-        if (lane == 0) top(jj, c) -= tw;
+        for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];
+        top_sub(CI, jj, tw);
       }
-    }
-    __syncwarp();
+    });
   }
   if (warp != (S - 1) % NW) named_bar(1 + (S - 1) % 15, 32 * NW);  // complete the last instance
+  if (!TS) {  // GEQRT: R entries above the diagonal (rows c0 .. c0+c-1) back to P
+#pragma unroll
+    for (int ci = 0; ci < NC; ++ci)
+#pragma unroll
+      for (int q = 0; q < NR; ++q) {
+        const int r = lane + 32 * q, c = warp + NW * ci;
+        if (c < S && r >= c0 && r < c0 + c) P[r + c * LDP] = x[ci][q];
+      }
+  }
   __syncthreads();
 }
 

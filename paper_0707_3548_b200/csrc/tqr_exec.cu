@@ -165,8 +165,8 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
 // out and the packed Y_l / T_l are published for blocks l+1.. and for every update task.
 // TSQRT reads and writes only the upper triangle of A(k,k).
 // ---------------------------------------------------------------------------------------
-template <int B, int S, int SO>
-__device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2], const bool ts,
+template <int B, int S, int SO, bool ts>
+__device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2],
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
                                             size_t toff, int l) {
   using C = Cfg<B, S>;
@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
         update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact, pf);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (panel) {
-          panel_block<B, S, SO>(sm, acc, ts, Akk, Ab, Tslot, a, yoff, toff, sub);
+          // TS as a template argument: each flavour is register-allocated on its own
+          if (ts) panel_block<B, S, SO, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub);
+          else panel_block<B, S, SO, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub);
         } else if (warp / Cfg<B, S>::RS < gact) {
           store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
                                        (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
