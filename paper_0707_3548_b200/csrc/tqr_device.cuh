@@ -399,53 +399,50 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
 
 template <int B, int S, int NW, int LDP>
 __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, double* tau, const bool TS) {
+  static_assert(S <= 64, "top block rows: two per lane at most");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NR = (B + 31) / 32;       // rows per lane: row r = lane + 32 x
+  constexpr int NR = (B + 31) / 32;       // x-part rows per lane: row r = lane + 32 q
   constexpr int NC = (S + NW - 1) / NW;   // columns per warp: column c = warp + NW ci
-  const int lo0 = TS ? 0 : c0;             // first panel row held in P
-  auto lo_of = [&](int jj) __attribute__((always_inline)) { return TS ? 0 : c0 + jj + 1; };
-  // The warp's columns live in registers for the whole panel (a column step would otherwise
-  // read + write the whole panel in shared memory: 128 KiB per step, ~1000 clk at b = 256).
-  double x[NC][NR];
+  constexpr int NTR = (S + 31) / 32;      // top-block rows per lane: block row L = lane + 32 h
+  // Column c of the panel = [top block (S rows); x part].  TSQRT: top = R_kk's diagonal block
+  // (Rb, upper triangle), x = the B rows of A(i,k); the reflector is [e_j; v_j].  GEQRT: top =
+  // tile rows [c0, c0+S), x = tile rows [c0+S, B); the reflector is [0; 1; v_j] with v_j's
+  // leading part inside the top block.  Every warp keeps its columns in registers (x and
+  // top), so no register row index is ever dynamic (row jj of the top block is a shuffle
+  // from lane jj) and no column step touches shared memory except v_j.
+  const int lox = TS ? 0 : c0 + S;  // first x-part row
+  double x[NC][NR], tr[NC][NTR];
 #pragma unroll
-  for (int ci = 0; ci < NC; ++ci)
+  for (int ci = 0; ci < NC; ++ci) {
+    const int c = warp + NW * ci;
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
-      const int r = lane + 32 * q, c = warp + NW * ci;
-      x[ci][q] = (c < S && r >= lo0 && r < B) ? P[r + c * LDP] : 0.0;
+      const int r = lane + 32 * q;
+      x[ci][q] = (c < S && r >= lox && r < B) ? P[r + c * LDP] : 0.0;
     }
-  // (all lambdas below take the column index as std::integral_constant: see static_for)
-  // row r of column CI, broadcast to the warp
-  auto get_row = [&](auto CI, int r) __attribute__((always_inline)) -> double {
-    double t = 0.0;
 #pragma unroll
-    for (int q = 0; q < NR; ++q)
-      if ((r >> 5) == q) t = x[decltype(CI)::value][q];
-    return __shfl_sync(0xffffffffu, t, r & 31);
+    for (int h = 0; h < NTR; ++h) {
+      const int L = lane + 32 * h;
+      tr[ci][h] = (c < S && L < S && (!TS || L <= c)) ? (TS ? Rb[L + c * S] : P[c0 + L + c * LDP]) : 0.0;
+    }
+  }
+  // block row L of column CI, broadcast to the warp
+  auto getT = [&](auto CI, int L) __attribute__((always_inline)) -> double {
+    constexpr int ci = decltype(CI)::value;
+    const double t = (NTR == 1 || L < 32) ? tr[ci][0] : tr[ci][NTR - 1];
+    return __shfl_sync(0xffffffffu, t, L & 31);
   };
-  auto add_row = [&](auto CI, int r, double v) __attribute__((always_inline)) {
-#pragma unroll
-    for (int q = 0; q < NR; ++q)
-      if ((r >> 5) == q && lane == (r & 31)) x[decltype(CI)::value][q] += v;
-  };
-  // "top" entry of reflector jj in column CI: R[jj][c] (TSQRT, in Rb) or tile row c0+jj
-  auto top_get = [&](auto CI, int jj) __attribute__((always_inline)) -> double {
-    return TS ? Rb[jj + (warp + NW * decltype(CI)::value) * S] : get_row(CI, c0 + jj);
-  };
-  auto top_sub = [&](auto CI, int jj, double w) __attribute__((always_inline)) {
-    if (TS) {
-      __syncwarp();
-      if (lane == 0) Rb[jj + (warp + NW * decltype(CI)::value) * S] -= w;
-    } else {
-      add_row(CI, c0 + jj, -w);
+  auto subT = [&](auto CI, int L, double w) __attribute__((always_inline)) {
+    constexpr int ci = decltype(CI)::value;
+    if (lane == (L & 31)) {
+      if (NTR == 1 || L < 32) tr[ci][0] -= w; else tr[ci][NTR - 1] -= w;
     }
   };
 
-  // Householder generation (R2-R4, R17, R20) for column jj = warp + NW ci from alpha
-  // and sigma = ||x||^2 (rows >= lo_of(jj)); stores v into P, beta, tau; publishes (bar.arrive).
+  // Householder generation (R2-R4, R17, R20) for column jj (in CI) from alpha and
+  // sigma = ||x||^2 over its rows below the pivot; stores v into P, beta, tau; publishes.
   auto house_pub = [&](auto CI, int jj, double alpha, double sigma) __attribute__((always_inline)) {
     constexpr int ci = decltype(CI)::value;
-    const int lo = lo_of(jj);
     double beta, tv, scale;
     if (sigma == 0.0) {
       beta = alpha; tv = 0.0; scale = 0.0;
@@ -460,7 +457,14 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
       const int r = lane + 32 * q;
-      if (r >= lo && r < B) P[r + jj * LDP] = x[ci][q] * scale;
+      if (r >= lox && r < B) P[r + jj * LDP] = x[ci][q] * scale;
+    }
+    if (!TS) {
+#pragma unroll
+      for (int h = 0; h < NTR; ++h) {
+        const int L = lane + 32 * h;
+        if (L > jj && L < S) P[c0 + L + jj * LDP] = tr[ci][h] * scale;
+      }
     }
     if (lane == 0) {
       if (TS) Rb[jj + jj * S] = beta; else P[c0 + jj + jj * LDP] = beta;
@@ -468,47 +472,66 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
     }
     named_arrive(1 + jj % 15, 32 * NW);  // publishes v_jj, tau_jj, beta_jj (no wait)
   };
-
-  if (warp == 0) {
-    const int lo = lo_of(0);
+  // ||column CI below block row j||^2: x part, plus (GEQRT) top-block rows L > j
+  auto norm_below = [&](auto CI, int j) __attribute__((always_inline)) -> double {
+    constexpr int ci = decltype(CI)::value;
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
-      const int r = lane + 32 * q;
-      const double v = (r >= lo && r < B) ? x[0][q] : 0.0;
-      if (q & 1) s1 += v * v; else s0 += v * v;
+      if (q & 1) s1 += x[ci][q] * x[ci][q]; else s0 += x[ci][q] * x[ci][q];
     }
-    const double sg = warp_sum(s0 + s1);
+    if (!TS) {
+#pragma unroll
+      for (int h = 0; h < NTR; ++h) {
+        const int L = lane + 32 * h;
+        if (L > j && L < S) s0 += tr[ci][h] * tr[ci][h];
+      }
+    }
+    return warp_sum(s0 + s1);
+  };
+
+  if (warp == 0) {
     const std::integral_constant<int, 0> C0;
-    house_pub(C0, 0, top_get(C0, 0), sg);
+    const double sg = norm_below(C0, 0);
+    house_pub(C0, 0, getT(C0, 0), sg);
   }
   for (int jj = 0; jj + 1 < S; ++jj) {
     if (warp != jj % NW) named_bar(1 + jj % 15, 32 * NW);  // v_jj published
     const double tj = tau[jj];
-    const int lo = lo_of(jj);
-    double vr[NR];
+    double vr[NR], vt[NTR];
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
       const int r = lane + 32 * q;
-      vr[q] = (r >= lo && r < B) ? P[r + jj * LDP] : 0.0;
+      vr[q] = (r >= lox && r < B) ? P[r + jj * LDP] : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < NTR; ++h) {  // v_jj inside the top block (GEQRT only; TSQRT: e_jj)
+      const int L = lane + 32 * h;
+      vt[h] = (!TS && L > jj && L < S) ? P[c0 + L + jj * LDP] : 0.0;
     }
     const int nxt = jj + 1;
     if (nxt % NW == warp) {
       // Critical path: update column jj+1 and generate reflector jj+1.  One interleaved
-      // reduction of (x.v, x.x, v.v) gives the dot product AND the new sub-column norm by
-      // downdating, sigma' = x.x - 2 tw x.v + tw^2 v.v [- alpha'^2 for GEQRT]; if that may
-      // have cancelled (sigma' below 5% of the magnitude of its terms) it is recomputed
-      // directly from the updated column (R20, the xGEQP3 safeguard).
+      // reduction of (x.v, x.x, v.v) over the rows below the pivot jj gives the dot product
+      // AND the new norm by downdating, sigma' = x.x - 2 tw x.v + tw^2 v.v [- alpha'^2 for
+      // GEQRT, whose alpha' is one of those rows]; if it may have cancelled (below 5% of the
+      // magnitude of its terms) it is recomputed from the updated column (R20).
       static_for<NC>([&](auto CI) __attribute__((always_inline)) {
         constexpr int ci = decltype(CI)::value;
         if (warp + NW * ci != nxt) return;
         double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
 #pragma unroll
         for (int q = 0; q < NR; ++q) {
-          const int r = lane + 32 * q;
-          const double xv = (r >= lo && r < B) ? x[ci][q] : 0.0;
-          if (q & 1) { a1 += vr[q] * xv; b1 += xv * xv; e1 += vr[q] * vr[q]; }
-          else { a0 += vr[q] * xv; b0 += xv * xv; e0 += vr[q] * vr[q]; }
+          if (q & 1) { a1 += vr[q] * x[ci][q]; b1 += x[ci][q] * x[ci][q]; e1 += vr[q] * vr[q]; }
+          else { a0 += vr[q] * x[ci][q]; b0 += x[ci][q] * x[ci][q]; e0 += vr[q] * vr[q]; }
+        }
+        if (!TS) {
+#pragma unroll
+          for (int h = 0; h < NTR; ++h) {
+            const int L = lane + 32 * h;
+            const double tv_ = (L > jj && L < S) ? tr[ci][h] : 0.0;
+            a0 += vt[h] * tv_; b0 += tv_ * tv_; e0 += vt[h] * vt[h];
+          }
         }
         double sxv = a0 + a1, sxx = b0 + b1, svv = e0 + e1;
 #pragma unroll
@@ -517,27 +540,17 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
           sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
           svv += __shfl_xor_sync(0xffffffffu, svv, o);
         }
-        const double tw = tj * (top_get(CI, jj) + sxv);
+        const double tw = tj * (getT(CI, jj) + sxv);
 #pragma unroll
-        for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];  // vr == 0 outside rows >= lo
-        top_sub(CI, jj, tw);
-        // alpha of column jj+1: R[jj+1][jj+1] (TSQRT) or the updated tile row c0+jj+1 (GEQRT)
-        __syncwarp();
-        const double alpha = top_get(CI, nxt);
+        for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];
+#pragma unroll
+        for (int h = 0; h < NTR; ++h) tr[ci][h] -= tw * vt[h];
+        subT(CI, jj, tw);
+        const double alpha = getT(CI, nxt);
         const double a2 = TS ? 0.0 : alpha * alpha;
         double sigma = sxx - 2.0 * tw * sxv + tw * tw * svv - a2;
         const double mag = sxx + 2.0 * fabs(tw * sxv) + tw * tw * svv + a2;
-        if (!(sigma >= 0.05 * mag)) {  // possible cancellation (or NaN): direct norm
-          const int lon = lo_of(nxt);
-          double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-          for (int q = 0; q < NR; ++q) {
-            const int r = lane + 32 * q;
-            const double v = (r >= lon && r < B) ? x[ci][q] : 0.0;
-            if (q & 1) s1 += v * v; else s0 += v * v;
-          }
-          sigma = warp_sum(s0 + s1);
-        }
+        if (!(sigma >= 0.05 * mag)) sigma = norm_below(CI, nxt);  // possible cancellation / NaN
         house_pub(CI, nxt, alpha, sigma);
       });
     }
@@ -552,6 +565,8 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
         for (int q = 0; q < NR; ++q) {
           if (q & 1) d1 += vr[q] * x[ci][q]; else d0 += vr[q] * x[ci][q];
         }
+#pragma unroll
+        for (int h = 0; h < NTR; ++h) d0 += vt[h] * tr[ci][h];
       }
       dc[ci] = d0 + d1;
     }
@@ -563,22 +578,28 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       constexpr int ci = decltype(CI)::value;
       const int c = warp + NW * ci;
       if (c > nxt && c < S) {
-        const double tw = tj * (top_get(CI, jj) + dc[ci]);
+        const double tw = tj * (getT(CI, jj) + dc[ci]);
 #pragma unroll
         for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];
-        top_sub(CI, jj, tw);
+#pragma unroll
+        for (int h = 0; h < NTR; ++h) tr[ci][h] -= tw * vt[h];
+        subT(CI, jj, tw);
       }
     });
   }
   if (warp != (S - 1) % NW) named_bar(1 + (S - 1) % 15, 32 * NW);  // complete the last instance
-  if (!TS) {  // GEQRT: R entries above the diagonal (rows c0 .. c0+c-1) back to P
+  // R entries above the diagonal of the top block back to shared memory (the diagonal (beta)
+  // and V were stored by house_pub)
 #pragma unroll
-    for (int ci = 0; ci < NC; ++ci)
+  for (int ci = 0; ci < NC; ++ci) {
+    const int c = warp + NW * ci;
 #pragma unroll
-      for (int q = 0; q < NR; ++q) {
-        const int r = lane + 32 * q, c = warp + NW * ci;
-        if (c < S && r >= c0 && r < c0 + c) P[r + c * LDP] = x[ci][q];
+    for (int h = 0; h < NTR; ++h) {
+      const int L = lane + 32 * h;
+      if (c < S && L < c) {
+        if (TS) Rb[L + c * S] = tr[ci][h]; else P[c0 + L + c * LDP] = tr[ci][h];
       }
+    }
   }
   __syncthreads();
 }

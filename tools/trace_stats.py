@@ -35,3 +35,10 @@ u = []
 for a, b in zip(bins[:-1], bins[1:]):
     u.append(np.clip(np.minimum(en, b) - np.maximum(st, a), 0, None).sum() / (nsm * (b - a)))
 print("  utilisation by decile:", " ".join(f"{x:.2f}" for x in u))
+
+# panel sub-tasks by inner block l (slice field)
+for kd, name in ((0, "G"), (1, "T")):
+    m = kind == kd
+    if m.any() and sl[m].max() > 0:
+        print(f"  {name} sub-task median by block l:", " ".join(f"{np.median(dur[m & (sl == l)]):.0f}"
+                                                            for l in range(sl[m].max() + 1)))
