@@ -124,7 +124,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 // L2 prefetch of a contiguous global range (bytes % 16 == 0, 16-byte aligned); no SMEM, no
 // completion tracking -- a hint that turns the next task's HBM reads into L2 hits
 __device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+  // issued in chunks of <= 64 KiB
+  const char* p = static_cast<const char*>(src);
+  for (unsigned off = 0; off < bytes; off += 65536u) {
+    const unsigned n = bytes - off < 65536u ? bytes - off : 65536u;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
+  }
 }
 // order this thread's generic-proxy accesses before subsequent async-proxy (TMA) accesses
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }

@@ -102,8 +102,10 @@ __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const 
 // `pf(li, nb)` is called by thread 0 once per block (cross-task prefetch hook).
 template <int B, int S, bool QT, bool DESC, class PF>
 __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>::RW / 8][2], const double* Yp,
-                                             const double* Tp, int nb, double* C1, const double* Ct, int col0,
-                                             int gact, PF&& pf) {
+                                             const double* Tp, int lb0, int nbe, double* C1, const double* Ct,
+                                             int col0, int gact, PF&& pf) {
+  // blocks lb0 .. nbe-1 (DESC: nbe-1 .. 0, lb0 must be 0)
+  const int nb = nbe - lb0;
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -122,16 +124,16 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
     done[1] = 0;
     fence_mbar_init();
     fence_proxy_async();
-    issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 1 : 0, 0);
-    if (nb > 1) issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 2 : 1, 1);
+    issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);
+    if (nb > 1) issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
   }
   if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
-  if (nb == 0) return;
-  if (top_owner) c1_fetch<B, S>(c1s0, C1, (DESC ? nb - 1 : 0) * S, cg0);
+  if (nb <= 0) return;
+  if (top_owner) c1_fetch<B, S>(c1s0, C1, (DESC ? nb - 1 : lb0) * S, cg0);
   __syncthreads();
   PH_MARK(14);
   for (int li = 0; li < nb; ++li) {
-    const int l = DESC ? nb - 1 - li : li;
+    const int l = DESC ? nb - 1 - li : lb0 + li;
     const int buf = li & 1;
     if (top_owner) {
       cp_async_wait<0>();  // this block's C1
@@ -168,7 +170,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
 template <int B, int S, int SO, bool ts>
 __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2],
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
-                                            size_t toff, int l) {
+                                            size_t toff, int l, bool more, int rlo) {
   using C = Cfg<B, S>;
   using L = Layout<B, S>;
   constexpr int LDP = L::LDP;
@@ -181,7 +183,9 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   double* Tp = sm + L::RB;  // after Rb is written back
   double* Z = sm + L::ZZ;
   double* tau = sm + L::TAU;
-  // block columns -> P (shared memory); GEQRT: rows above the block are final R
+  // block columns -> P (shared memory); GEQRT: rows above the block are final R -- written
+  // back only from row rlo: rows above the task's first block belong to the apply part,
+  // which the next tile's apply part (TSQRT A(k,k+1,.)) may already be updating (R21)
   if (gi < S / 8) {
     const int col = 8 * gi + (lane >> 2);
 #pragma unroll
@@ -190,7 +194,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
       for (int h = 0; h < 2; ++h) {
         const int r = 8 * (t0 + t) + 4 * h + (lane & 3);
         if (ts || r >= c0) P[r + col * LDP] = acc[t][h];
-        else __stcg(Ab + (size_t)(c0 + col) * B + r, acc[t][h]);
+        else if (r >= rlo) __stcg(Ab + (size_t)(c0 + col) * B + r, acc[t][h]);
       }
   }
   if (ts)
@@ -224,15 +228,20 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   __syncthreads();
   PH_MARK(10);
   gram_upper<B, S, C::NWARP>(Ys, Z);
-  // packed Y_l to every rank's workspace (the V broadcast of SURVEY 8(e), fused into the
-  // panel task: peer stores over NVLink on a multi-GPU job, local stores otherwise)
-  for (int g = 0; g < a.nranks; ++g) {
-    double* dst = a.Yp[g] + yoff + (size_t)l * B * S;
-    for (int e = tid; e < B * S; e += C::NT) __stcg(dst + e, Ys[e]);
-  }
   __syncthreads();
   PH_MARK(11);
-  if (warp < (S + 31) / 32) build_t<S>(Tp, tau, Z);
+  constexpr int NTW = (S + 31) / 32;  // warps building T_l
+  if (warp < NTW) {
+    build_t<S>(Tp, tau, Z);
+  } else {
+    // meanwhile the other warps store the packed Y_l into every rank's workspace (the V
+    // broadcast of SURVEY 8(e), fused into the panel task: peer stores over NVLink on a
+    // multi-GPU job, local stores otherwise)
+    for (int g = 0; g < a.nranks; ++g) {
+      double* dst = a.Yp[g] + yoff + (size_t)l * B * S;
+      for (int e = tid - 32 * NTW; e < B * S; e += C::NT - 32 * NTW) __stcg(dst + e, Ys[e]);
+    }
+  }
   __syncthreads();
   PH_MARK(12);
   // output slot: T_L (SO x SO) in columns [L*SO, L*SO+SO); this SI-block is its diagonal
@@ -246,7 +255,9 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     for (int g = 0; g < a.nranks; ++g) __stcg(a.Tp[g] + toff + (size_t)l * S * S + swz<S>(r, c), v);
   }
   if (a.sys) __threadfence_system();  // peer stores ordered before the counter release
-  fence_proxy_async();  // packed panels (generic stores) -> later TMA reads
+  // packed panels (generic stores) -> TMA reads of the next block of THIS task; a later task
+  // orders them with its own fence after acquiring the panel counter
+  if (more) fence_proxy_async();
   __syncthreads();
   PH_MARK(13);
 }
@@ -371,16 +382,20 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
       constexpr int SPT = SO / S;  // internal blocks per output T block
       const int sub0 = panel ? (sl < 0 ? 0 : sl * SPT) : 0;
       const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : Cfg<B, S>::TSL / Cfg<B, S>::SLICE;
+      // panel split (R21): flags bit 1 = apply part only (left-looking update of the
+      // block columns with this tile's earlier blocks, stored back), bit 2 = factor part only
+      const bool a_part = panel && (s_task[14] & 2), f_part = panel && (s_task[14] & 4);
       for (int sub = sub0; sub < nsub; ++sub) {
         double acc[Cfg<B, S>::RW / 8][2];
         double* C1;
         double* Ct;
-        int col0, nb, gact;
+        int col0, nb, gact, lb0 = 0;
         if (panel) {
           C1 = ts ? Akk : nullptr;
           Ct = Ab;
           col0 = sub * S;
-          nb = sub;
+          nb = a_part ? sub0 : sub;   // A: blocks < sub0; F: this task's blocks [sub0, sub)
+          lb0 = f_part ? sub0 : 0;
           gact = S / 8;
         } else {
           C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
@@ -390,7 +405,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }
         auto pf = [&](int li, int nbb) {
-          if (sub != nsub - 1 || nbb < 4) return;
+          if (sub != nsub - 1 || nbb < 4) return;  // (nbb: blocks this pass applies)
           const int l0 = nbb / 2;
           if (li == l0) next_tk = atomicAdd(R.ticket, 1);  // next ticket, half a pass early
           if (li == l0 + 1 && next_tk < R.ntasks) {       // its record -> s_next (async)
@@ -405,12 +420,17 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
             prefetch_task<B, S, SO, MODE>(s_next, R, Yme, p);
           }
         };
-        update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, nb, C1, Ct, col0, gact, pf);
+        update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf);
         if (panel) PH_MARK(7); else PH_MARK(4);
-        if (panel) {
+        if (a_part) {
+          if (warp / Cfg<B, S>::RS < gact)
+            store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
+                                         (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
+        } else if (panel) {
           // TS as a template argument: each flavour is register-allocated on its own
-          if (ts) panel_block<B, S, SO, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub);
-          else panel_block<B, S, SO, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub);
+          const int rlo = f_part ? sub0 * S : 0;
+          if (ts) panel_block<B, S, SO, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
+          else panel_block<B, S, SO, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
         } else if (warp / Cfg<B, S>::RS < gact) {
           store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
                                        (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));

@@ -2,14 +2,15 @@
 // dispatch order, and the C ABI declared in include/tqr.h.
 //
 // DAG (edges derived from each kernel's read/write sets, SPEC dag module),
-// with the panel tasks split by inner block l (R21):
-//   G(k,l)      <- G(k,l-1) | S(k-1,k,k,*) (l = 0)
-//   T(k,i,l)    <- G(k,l) | T(k,i-1,l);  T(k,i,l-1) | S(k-1,i,k,*) (l = 0)
-//   L(k,j,sl)   <- G(k, last), S(k-1,k,j,sl)
-//   S(k,i,j,sl) <- T(k,i, last), L(k,j,sl) | S(k,i-1,j,sl), S(k-1,i,j,sl)
+// with the panel tasks split by inner block l into an apply part A and a factor part F
+// (R21; P(k,i) = GEQRT(k) for i = k, TSQRT(k,i) for i > k):
+//   A(k,i,l)    <- F(k,i,l-1);  A(k,i-1,l)                       (l >= 1)
+//   F(k,i,l)    <- F(k,i-1,l);  A(k,i,l) | S(k-1,i,k,*) (l = 0)
+//   L(k,j,sl)   <- F(k,k, last), S(k-1,k,j,sl)
+//   S(k,i,j,sl) <- F(k,i, last), L(k,j,sl) | S(k,i-1,j,sl), S(k-1,i,j,sl)
 // Every dependency is a chain, so it is expressed on the device as "progress counter >=
-// value": pblk[k][l] counts G(k,l), T(k,k+1,l), ... ; col[k][j][sl] counts L(k,j,sl),
-// S(k,k+1,j,sl), ...
+// value": PF(k,l) / PA(k,l) count the F / A parts of P(k,k), P(k,k+1), ... ; col[k][j][sl]
+// counts L(k,j,sl), S(k,k+1,j,sl), ...
 // The dispatch (ticket) order is a list schedule of the DAG on `workers` CTAs with the
 // paper's priorities G > T > L > S, ties by (k, i, j, slice); it is
 // topological by construction, so with all CTAs co-resident no ticket can wait forever.
@@ -187,18 +188,22 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
   return true;
 }
 
-// Rough per-task durations (ns) for the list schedule only (never affect results):
-// fp64 DMMA peak per SM ~251 GFLOP/s (M0 probe), efficiencies per kind as measured by
-// tools/prof_tasks.py (r01: GEQRT ~9%, TSQRT ~14%, LARFB ~34%, SSRFB ~60% of the SM peak).
+// Per-task durations (ns) for the list schedule only (never affect results), fitted to the
+// B200 traces (tools/trace_stats.py, r01): fp64 DMMA peak per SM ~251 GFLOP/s; a panel
+// sub-task for inner block l = ~10 us fixed + ~0.7 us per factored column + l block applies
+// of its columns at ~80% of the SM peak; update tasks run at ~78% (the LARFB form applies
+// the zero rows of U above block l as well, so it costs like SSRFB without C1).
 struct DurModel {
-  double g, t, l, s;
-  DurModel(int b, int s_, int w) {
-    const double B = b, Sv = s_, W = w, sm = 251.0;  // GFLOP/s per SM == flop/ns
-    g = 3000 + (4.0 / 3 * B * B * B + 2.0 / 3 * Sv * B * B) / (0.09 * sm);
-    t = 3000 + (2.0 * B * B * B + 4.0 / 3 * Sv * B * B) / (0.14 * sm);
-    l = 1500 + (2.0 * B * B * W + Sv * B * W) / (0.34 * sm);
-    s = 1500 + (4.0 * B * B * W + Sv * B * W) / (0.6 * sm);
+  double B, Sv, W, l, s, apply;
+  DurModel(int b, int s_, int w) : B(b), Sv(s_), W(w) {
+    const double sm = 251.0;  // GFLOP/s per SM == flop/ns
+    l = 3000 + (4.0 * B * B * W) / (0.78 * sm);
+    s = 3000 + (4.0 * B * B * W + Sv * B * W) / (0.78 * sm);
+    apply = 4.0 * B * Sv * Sv / (0.8 * sm);
   }
+  double panel(int lb) const { return 10000 + Sv * (B >= 256 ? 720 : 630) + lb * apply; }
+  double apply_part(int lb) const { return 5000 + lb * apply; }
+  double factor_part(bool split) const { return (split ? 11000 : 10000) + Sv * (B >= 256 ? 720 : 630); }
 };
 
 // Ranks own tile columns j == r (mod G): the panel tasks G(k), T(k,i) run on
@@ -217,23 +222,37 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   auto own = [&](int64_t j) { return (int)(j % G); };
   auto qloc = [&](int r) { return r < q ? (int)((q - r + G - 1) / G) : 0; };
   auto scol = [&](int64_t j) { return real_layout ? (int)(j / G) : (int)j; };
-  // pblk[k][l]: how many panel tasks of step k (GEQRT(k), TSQRT(k,k+1), ...) have finished
-  // inner block l (a copy on every rank)
-  auto PBLK = [&](int k, int l) { return k * NPT + l; };
+  // Panel progress of step k, per inner block l (a copy on every rank, R21):
+  //   PF(k,l): factor parts done (GEQRT(k) then TSQRT(k,k+1), ...: value i-k+1 after TSQRT(k,i))
+  //   PA(k,l): apply parts done, l >= 1 (left-looking update of block l's columns; owner only)
+  auto PF = [&](int k, int l) { return k * 2 * NPT + l; };
+  auto PA = [&](int k, int l) { return k * 2 * NPT + NPT + l; };
   auto COL = [&](int k, int64_t j, int sl) {
-    return K * NPT + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl);
+    return K * 2 * NPT + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl);
   };
   out.nctr.assign(G, 0);
-  for (int r = 0; r < G; ++r) out.nctr[r] = K * NPT + (int)((int64_t)K * qloc(r) * nsl);
-  for (int k = 0; k < K; ++k) {
-    const int ok = own(k);
-    // GEQRT(k) block l: own block l-1 first; block 0 needs tile (k,k) updated by step k-1
+  for (int r = 0; r < G; ++r) out.nctr[r] = K * 2 * NPT + (int)((int64_t)K * qloc(r) * nsl);
+  // One panel task on tile (i,k) block l in two parts: A (apply this tile's blocks < l to
+  // block l's columns: touches the rows of R_kk ABOVE the diagonal block) and F (factor: the
+  // diagonal block).  A(k,i+1,l) may overlap F(k,i,l), which halves the TSQRT chain's step.
+  auto panel = [&](int kind, int k, int i, int cls) {
+    const int ok = own(k), v = i - k + 1;
     for (int l = 0; l < NPT; ++l) {
-      int id = T.add(K_G, k, k, scol(k), l, PBLK(k, l), 1, dm.g / NPT, 0);
-      T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
-      if (l > 0) T.dep(id, PBLK(k, l - 1), 1, 1);
-      else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, 2);
+      if (l > 0) {
+        int id = T.add(kind, k, i, scol(k), l, PA(k, l), v, dm.apply_part(l), cls);
+        T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
+        T.dep(id, PF(k, l - 1), 1, v);                 // this tile's blocks < l factored
+        if (v > 1) T.dep(id, PA(k, l), 1, v - 1);      // R_kk rows above block l: previous tile
+      }
+      int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(l > 0), cls);
+      T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
+      if (v > 1) T.dep(id, PF(k, l), 1, v - 1);        // R_kk diagonal block l: previous tile
+      if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part
+      else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);  // tile updated by step k-1
     }
+  };
+  for (int k = 0; k < K; ++k) {
+    panel(K_G, k, k, 0);
     out.counts[0]++;
     for (int j = k + 1; j < q; ++j)
       for (int sl = 0; sl < nsl; ++sl) {
@@ -241,27 +260,21 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         int id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
         T.t[id].rank = own(j); T.t[id].kc = scol(k);
         T.t[id].key[2] = j;
-        T.dep(id, PBLK(k, NPT - 1), 1, 1);
+        T.dep(id, PF(k, NPT - 1), 1, 1);
         if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, 2);
         out.counts[2]++;
       }
     for (int i = k + 1; i < p; ++i) {
-      // TSQRT(k,i) block l touches only column block l of R_kk (and tile (i,k)): it follows
-      // TSQRT(k,i-1) block l and its own block l-1 -- a wavefront over (i, l) (R21)
-      for (int l = 0; l < NPT; ++l) {
-        int id = T.add(K_T, k, i, scol(k), l, PBLK(k, l), i - k + 1, dm.t / NPT, 1);
-        T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
-        T.dep(id, PBLK(k, l), 1, i - k);
-        if (l > 0) T.dep(id, PBLK(k, l - 1), 1, i - k + 1);
-        else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
-      }
+      // TSQRT(k,i) block l touches only column block l of R_kk (and tile (i,k)): a wavefront
+      // over (i, l) (R21)
+      panel(K_T, k, i, 1);
       out.counts[1]++;
       for (int j = k + 1; j < q; ++j)
         for (int sl = 0; sl < nsl; ++sl) {
           int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
-          T.dep(id, PBLK(k, NPT - 1), 1, i - k + 1);
+          T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
           T.dep(id, COL(k, j, sl), 1, i - k);
           if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
           out.counts[3]++;

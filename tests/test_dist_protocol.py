@@ -95,7 +95,9 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
             kind = int(rec[0])
             k = int(rec[1])
             if kind in (K_G, K_T):
-                assert k % G == r and rec[14] & 1 and rec[7] == k // G  # panel on owner(k), published
+                assert k % G == r and rec[7] == k // G  # panel parts on owner(k)
+                # factor parts publish their progress to every rank, apply parts stay local
+                assert bool(rec[14] & 1) == bool(rec[14] & 4) and bool(rec[14] & 2) != bool(rec[14] & 4)
             else:
                 assert _global_j(rec, G, r) % G == r and not rec[14] & 1  # update on owner(j), local
             keys.append(_task_key(rec, G, r))
@@ -121,8 +123,8 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
     for g, sim in enumerate(sims):
         # every rank ends with the complete panel progress of every step, received exactly once
         for k in range(K):
-            for l in range(NPT):
-                assert sim.ctr[k * NPT + l] == max(1, p - k)
+            for l in range(NPT):  # PF(k, l) at k*2*NPT + l
+                assert sim.ctr[k * 2 * NPT + l] == max(1, p - k)
         assert all(v == 1 for v in seen[g].values())
 
 
@@ -160,7 +162,8 @@ def _gloo_rank(rank, world, port, p, q, nsl, workers, out):
             rounds += 1
             # nobody ran a task this round and some rank is unfinished: cross-rank deadlock
             assert rounds < 100000 and any(r for _, _, r in allp), "deadlock across ranks"
-        out.put((rank, sim.done, len(recs), sim.ctr[:min(p, q) * NPT].tolist()))
+        out.put((rank, sim.done, len(recs), [int(sim.ctr[k * 2 * NPT + l]) for k in range(min(p, q))
+                                             for l in range(NPT)]))
     finally:
         dist.destroy_process_group()
 

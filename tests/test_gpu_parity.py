@@ -104,3 +104,15 @@ def test_identity_and_zero_columns():
     g = run_factor(A, 64, 16)
     At_o, T_o = oracle.geqrf(A, 64, 16)
     assert np.max(np.abs(g["R"] - oracle.get_r(At_o, 200, 150, 64))) <= 1e-10 * np.linalg.norm(A)
+
+
+@pytest.mark.parametrize("m,n,b,s,reps", [(4096, 4096, 128, 32, 4), (8192, 1024, 256, 32, 4), (3000, 2100, 512, 64, 3),
+                                          (1024, 1024, 64, 16, 6)])
+def test_repeat_bitwise_stress(m, n, b, s, reps):
+    """Races show up as run-to-run differences: the out-of-order executor must give bitwise
+    identical R/V/T on every run (each tile's operation sequence is fixed by the DAG)."""
+    A = tqr_inputs.uniform(m, n, 99 + m)
+    g0 = run_factor(A, b, s)
+    for _ in range(reps - 1):
+        g = run_factor(A, b, s)
+        assert np.array_equal(g["At"], g0["At"]) and np.array_equal(g["T"], g0["T"])
