@@ -405,6 +405,11 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }
         auto pf = [&](int li, int nbb) {
+          if (!panel && sub + 1 < nsub && li == nbb / 2) {  // next register pass of this task
+            const size_t nxt_off = (size_t)(col0 + Cfg<B, S>::SLICE) * B;
+            prefetch_l2(Ct + nxt_off, (unsigned)(Cfg<B, S>::SLICE * B * 8));
+            if (C1) prefetch_l2(C1 + nxt_off, (unsigned)(Cfg<B, S>::SLICE * B * 8));
+          }
           if (sub != nsub - 1 || nbb < 4) return;  // (nbb: blocks this pass applies)
           const int l0 = nbb / 2;
           if (li == l0) next_tk = atomicAdd(R.ticket, 1);  // next ticket, half a pass early
