@@ -8,12 +8,15 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 PHASES = os.environ.get("TQR_PHASES", "0") == "1"   # profiling variant with phase timers
-LIB = os.path.join(HERE, "libtqr_phases.so" if PHASES else "libtqr.so")
+# experiment variants (development only): extra -D flags and their own library name
+VARIANT_DEFS = os.environ.get("TQR_VARIANT_DEFS", "").split()
+VARIANT = os.environ.get("TQR_VARIANT", "")
+LIB = os.path.join(HERE, f"libtqr_{VARIANT}.so" if VARIANT else ("libtqr_phases.so" if PHASES else "libtqr.so"))
 SOURCES = ["tqr_exec.cu", "tqr_host.cpp"]
 HEADERS = ["tqr_device.cuh", "tqr_internal.h", os.path.join("..", "..", "include", "tqr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"] + (["-DTQR_PROFILE_PHASES"] if PHASES else [])
+         "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"] + (["-DTQR_PROFILE_PHASES"] if PHASES else []) + VARIANT_DEFS
 
 
 def _stale() -> bool:
@@ -30,7 +33,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     objs = []
     procs = []
     for src in SOURCES:
-        obj = os.path.join(CSRC, src + (".ph" if PHASES else "") + ".o")
+        obj = os.path.join(CSRC, src + (f".{VARIANT}" if VARIANT else (".ph" if PHASES else "")) + ".o")
         cmd = [NVCC, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)

@@ -44,9 +44,6 @@ struct Cfg {
   static constexpr int NT = NWARP * 32;
   static constexpr int GPS = NWARP / RS;
   static constexpr int SLICE = 8 * GPS;
-  // columns per LARFB/SSRFB task: SLICE (one register-resident pass) up to b = 256; for
-  // b = 512 a task walks 8 such passes (keeps the DAG of C5 at 2.8 M tasks)
-  static constexpr int TSL = B >= 512 ? 8 * SLICE : SLICE;
   static constexpr int XW = (S / 8) * 2 * 32;  // doubles per warp for a W fragment set
   static constexpr int C1W = 8 * (S + 4);      // doubles per group for a staged C1 block
   static_assert(GPS >= 1 && (RS == 1 || GPS <= 15), "named barriers 1..15");

@@ -266,7 +266,8 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
 // updates (+ its C1 slice), or the tile a panel task factors, and its first two packed
 // reflector blocks.  Safe before the task's dependencies hold (L2 is coherent).
 template <int B, int S, int SO, int MODE>
-__device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, const double* Yme, int p) {
+__device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, const double* Yme, int p,
+                                              int tsl) {
   using C = Cfg<B, S>;
   const int kind = q[0], k = q[1], i = q[2], j = q[3], sl = q[4], kc = q[7];
   if (MODE == 0 && (kind == K_G || kind == K_T)) {
@@ -275,9 +276,10 @@ __device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, 
   }
   const bool lkind = kind == K_L || kind == K_LQT || kind == K_LQ;
   double* Bt = MODE == 0 ? R.A : R.Bt;
-  const size_t off = (size_t)sl * C::TSL * B;
-  prefetch_l2(tile_ptr(Bt, lkind ? k : i, j, p, B) + off, (unsigned)(C::TSL * B * 8));
-  if (!lkind) prefetch_l2(tile_ptr(Bt, k, j, p, B) + off, (unsigned)(C::TSL * B * 8));
+  const size_t off = (size_t)sl * tsl * B;
+  const unsigned bytes = (unsigned)(C::SLICE * B * 8);  // the first pass's columns
+  prefetch_l2(tile_ptr(Bt, lkind ? k : i, j, p, B) + off, bytes);
+  if (!lkind) prefetch_l2(tile_ptr(Bt, k, j, p, B) + off, bytes);
   const int vrow = lkind ? k : i;
   const double* Y = Yme + ((size_t)vrow + (size_t)k * p) * (size_t)B * B;
   constexpr int NL = B / S;
@@ -381,7 +383,8 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
       // whole tile when sl < 0); update task: TSL / SLICE register passes of its slice
       constexpr int SPT = SO / S;  // internal blocks per output T block
       const int sub0 = panel ? (sl < 0 ? 0 : sl * SPT) : 0;
-      const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : Cfg<B, S>::TSL / Cfg<B, S>::SLICE;
+      const int tsl = a.passes * Cfg<B, S>::SLICE;  // columns per update task
+      const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : a.passes;
       // panel split (R21): flags bit 1 = apply part only (left-looking update of the
       // block columns with this tile's earlier blocks, stored back), bit 2 = factor part only
       const bool a_part = panel && (s_task[14] & 2), f_part = panel && (s_task[14] & 4);
@@ -400,7 +403,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
         } else {
           C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
           Ct = lkind ? tile_ptr(Bt, k, j, p, B) : tile_ptr(Bt, i, j, p, B);
-          col0 = sl * Cfg<B, S>::TSL + sub * Cfg<B, S>::SLICE;  // (update tasks: sl >= 0)
+          col0 = sl * tsl + sub * Cfg<B, S>::SLICE;  // (update tasks: sl >= 0)
           nb = NL;
           gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
         }
@@ -422,7 +425,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
           }
           if (li == l0 + 2 && rec_for == next_tk && next_tk < R.ntasks) {
             cp_async_wait<0>();
-            prefetch_task<B, S, SO, MODE>(s_next, R, Yme, p);
+            prefetch_task<B, S, SO, MODE>(s_next, R, Yme, p, tsl);
           }
         };
         update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf);
@@ -534,7 +537,7 @@ cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cud
 }
 
 int exec_slice(int b, int s) {
-#define X(BB, SS) if (b == BB && s == SS) return Cfg<BB, Inner<BB, SS>::SI>::TSL;
+#define X(BB, SS) if (b == BB && s == SS) return Cfg<BB, Inner<BB, SS>::SI>::SLICE;
   TQR_INSTANCES(X)
 #undef X
   return 0;

@@ -212,7 +212,7 @@ struct DurModel {
 // column counters col[k][jl][sl] (jl = j / G).  `real_layout`: tile storage holds only the
 // rank's own columns (storage column jl); otherwise the full global grid (column j).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
-                               bool real_layout, Sched& out) {
+                               bool real_layout, bool split, Sched& out) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -238,6 +238,14 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   auto panel = [&](int kind, int k, int i, int cls) {
     const int ok = own(k), v = i - k + 1;
     for (int l = 0; l < NPT; ++l) {
+      if (!split) {  // fused apply + factor per block (R21 without the A/F split)
+        int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l), cls);
+        T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
+        if (v > 1) T.dep(id, PF(k, l), 1, v - 1);
+        if (l > 0) T.dep(id, PF(k, l - 1), 1, v);
+        else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
+        continue;
+      }
       if (l > 0) {
         int id = T.add(kind, k, i, scol(k), l, PA(k, l), v, dm.apply_part(l), cls);
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
@@ -345,6 +353,8 @@ struct tqr_plan {
   tqr_params prm;
   int64_t p, q, K;
   int nsl, workers;
+  int passes = 1;      // register passes per update task (policy below)
+  bool split = true;   // panel A/F split (R21)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -438,6 +448,7 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
   a.p = (int)P->p;
   a.base = base;
   a.sys = P->real ? 1 : 0;
+  a.passes = P->passes;
   a.phases = P->d_phases;
   if (P->G == 1) {
     a.Yp[0] = reinterpret_cast<double*>(work);
@@ -556,7 +567,18 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   P->emulate = emulate;
   P->real = P->G > 1 && !emulate;
   P->nloc = emulate ? P->G : 1;
-  P->nsl = (p->b + exec_slice(p->b, p->s) - 1) / exec_slice(p->b, p->s);
+  // Granularity policy (measured on B200, r01): b = 512 tasks walk 8 register passes (C5 DAG
+  // stays at 2.8 M tasks); tall-skinny grids (p >= 4q) are bound by the TSQRT chain and want
+  // fine update tasks plus the panel A/F split (C4: 60 vs 64-68 ms); square grids at b = 256
+  // prefer 2-pass update tasks and fused panel blocks (C3: 232 vs 238 ms); at b <= 128 the
+  // GEQRT/TSQRT chain dominates and the split helps (C2: 7.6 vs 7.9 ms).
+  const bool tall = P->p >= 4 * P->q;
+  P->passes = p->b >= 512 ? 8 : (p->b >= 256 && !tall ? 2 : 1);
+  P->split = tall || p->b >= 512 || p->b <= 128;
+  {
+    const int w = exec_slice(p->b, p->s) * P->passes;
+    P->nsl = (int)((p->b + w - 1) / w);
+  }
   P->st = (cudaStream_t)p->stream;
   P->workers = exec_max_ctas(p->b, p->s, p->device);
   if (P->workers < P->nloc) {
@@ -574,7 +596,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate)
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, s);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -847,7 +869,8 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   if (nslice < 1) return bad_arg(3, "nslice < 1");
   if (workers < 1) return bad_arg(4, "workers < 1");
   if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
-  build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1, s);
+  build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1,
+                     (p + q) % 2 == 0, s);  // both panel forms are exercised by the inspected shapes
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;

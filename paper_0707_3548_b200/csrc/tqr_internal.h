@@ -58,6 +58,7 @@ struct ExecArgs {
   int p;                    // row tiles (same for A and Bt)
   int base;                 // counter generation base of this call
   int sys;                  // 1: peers on other GPUs (system-scope acquire/release)
+  int passes;               // register passes (SLICE columns each) per LARFB/SSRFB task
   long long* phases;        // TQR_PROFILE_PHASES builds: 16 phase-cycle totals, or nullptr
 };
 
@@ -67,7 +68,8 @@ cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cud
 // Max co-resident CTAs for (b, s) on this device (0 if no instance).
 int exec_max_ctas(int b, int s, int device);
 bool exec_supported(int b, int s);
-// Columns per LARFB/SSRFB slice task for (b, s) (0 if no instance).
+// Columns of one register-resident pass of a LARFB/SSRFB task for (b, s) (0 if no instance);
+// a task covers `passes` consecutive passes (host policy, ExecArgs::passes).
 int exec_slice(int b, int s);
 // Internal inner block SI of the executor for (b, s) (== s except b = 512).
 int exec_inner(int b, int s);

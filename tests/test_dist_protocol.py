@@ -96,8 +96,9 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
             k = int(rec[1])
             if kind in (K_G, K_T):
                 assert k % G == r and rec[7] == k // G  # panel parts on owner(k)
-                # factor parts publish their progress to every rank, apply parts stay local
-                assert bool(rec[14] & 1) == bool(rec[14] & 4) and bool(rec[14] & 2) != bool(rec[14] & 4)
+                # factor parts (bit 2) and fused blocks publish their progress to every rank,
+                # apply parts (bit 1) stay local
+                assert rec[14] in (1, 2, 1 | 4)
             else:
                 assert _global_j(rec, G, r) % G == r and not rec[14] & 1  # update on owner(j), local
             keys.append(_task_key(rec, G, r))
