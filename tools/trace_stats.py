@@ -42,3 +42,15 @@ for kd, name in ((0, "G"), (1, "T")):
     if m.any() and sl[m].max() > 0:
         print(f"  {name} sub-task median by block l:", " ".join(f"{np.median(dur[m & (sl == l)]):.0f}"
                                                             for l in range(sl[m].max() + 1)))
+
+# per-SM gaps (dispatch + dependency wait) attributed to the task that follows the gap
+order = np.lexsort((st, sm))
+gap = np.zeros(len(r))
+same = sm[order][1:] == sm[order][:-1]
+g = (st[order][1:] - en[order][:-1])
+gap[order[1:][same]] = g[same]
+for kd, name in enumerate("GTLS"):
+    m = kind == kd
+    if m.any():
+        print(f"  gap before {name}: mean {gap[m].mean():7.1f} us, p90 {np.percentile(gap[m], 90):7.1f} us, "
+              f"total {gap[m].sum() / 1e3:8.1f} SM-ms")
