@@ -231,40 +231,88 @@ def main():
         ms, kern_ms = t.tolist()
     value = flops / (ms * 1e-3) / 1e9     # one matrix for the whole job (strong scaling)
 
-    # ---- e2e: host buffers through the public API (H2D of this rank's columns of A, pack,
-    #      factor, R, D2H of this rank's columns of R) ----
+    # ---- e2e: host buffers through the public API.  Every step copies its own input in
+    #      (H2D of this rank's columns of A from pinned memory), packs, factors, extracts R
+    #      and copies its own result out (D2H of this rank's columns of R).  The copies run on
+    #      a second stream with double-buffered device A and R, so step s+1's H2D and step
+    #      s-1's D2H overlap step s's factorization (a serving pipeline). ----
     e2e = None
     if not args.no_e2e:
-        R_pin = torch.empty((n, min(m, n)), dtype=torch.float64).pin_memory()
+        dev = f"cuda:{local}"
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        dbl = free_b > 1.15 * (A_dev.numel() + R.numel()) * 8   # room for the second buffers?
+        A_bufs = [A_dev, torch.empty_like(A_dev) if dbl else A_dev]
+        R_bufs = [R, torch.zeros_like(R) if dbl else R]
+        R_pins = [torch.empty((n, min(m, n)), dtype=torch.float64).pin_memory() for _ in range(2)]
+        cst = torch.cuda.Stream(device=dev)   # H2D
+        dst = torch.cuda.Stream(device=dev)   # D2H
+        ev = {key: [torch.cuda.Event() for _ in range(2)] for key in ("h2d", "packed", "r", "d2h")}
+        issued = {key: [False, False] for key in ev}
 
-        def e2e_step():
-            for c0, c1 in my_cols:
-                A_dev[c0:c1].copy_(A_pin[c0:c1], non_blocking=True)
-            step()
-            for c0, c1 in my_cols:
-                R_pin[c0:c1].copy_(R[c0:c1], non_blocking=True)
+        def e2e_run(nsteps):
+            for st_ in range(nsteps):
+                bf = st_ % 2
+                with torch.cuda.stream(cst):   # H2D of this step's A once its buffer is free
+                    if issued["packed"][bf]:
+                        cst.wait_event(ev["packed"][bf])
+                    for c0, c1 in my_cols:
+                        A_bufs[bf][c0:c1].copy_(A_pin[c0:c1], non_blocking=True)
+                    ev["h2d"][bf].record(cst); issued["h2d"][bf] = True
+                stream.wait_event(ev["h2d"][bf])
+                plan.pack(A_bufs[bf], At)
+                ev["packed"][bf].record(stream); issued["packed"][bf] = True
+                plan.geqrf(At, T)
+                if issued["d2h"][bf]:
+                    stream.wait_event(ev["d2h"][bf])   # R buffer read out by step s-2
+                plan.get_r(At, R_bufs[bf])
+                ev["r"][bf].record(stream); issued["r"][bf] = True
+                with torch.cuda.stream(dst):   # D2H of this step's R
+                    dst.wait_event(ev["r"][bf])
+                    for c0, c1 in my_cols:
+                        R_pins[bf][c0:c1].copy_(R_bufs[bf][c0:c1], non_blocking=True)
+                    ev["d2h"][bf].record(dst); issued["d2h"][bf] = True
 
-        with torch.cuda.stream(stream):
-            e2e_step()
-        stream.synchronize()
+        e2e_run(2)
+        torch.cuda.synchronize()
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            f0.record(stream)
-            for _ in range(args.steps):
-                e2e_step()
-            f1.record(stream)
-        stream.synchronize()
+        f0.record(cst)
+        e2e_run(args.steps)
+        f1.record(dst)       # after the last D2H (D2H stream order)
+        torch.cuda.synchronize()
         barrier()
         ems = f0.elapsed_time(f1) / args.steps
         if world > 1:
-            t = torch.tensor([ems], device=f"cuda:{local}", dtype=torch.float64)
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = t.item()
-        e2e = {"value": flops / (ems * 1e-3) / 1e9, "unit": "GFLOP/s",
+        del A_bufs[1], R_bufs[1]
+        e2e = {"value": flops / (ems * 1e-3) / 1e9, "unit": "GFLOP/s", "double_buffered": dbl,
                "h2d_bytes_per_step": sum(c1 - c0 for c0, c1 in my_cols) * m * 8,
                "d2h_bytes_per_step": sum(c1 - c0 for c0, c1 in my_cols) * min(m, n) * 8,
-               "ms_per_step": ems, "note": "per rank: its own tile columns of A in, of R out"}
+               "ms_per_step": ems,
+               "note": "per rank: its own tile columns of A in, of R out, every step; H2D and D2H on their "
+                       "own streams, double-buffered, overlapping the neighbouring steps' factorization"}
+
+    # ---- form Q explicitly (tqr_orgqr), once, after the timed region ----
+    form_q = None
+    if world == 1 and not args.no_e2e:
+        qb = -(-n // b)
+        free_b, _ = torch.cuda.mem_get_info(f"cuda:{local}")
+        if free_b > 1.2 * plan.p * qb * b * b * 8:
+            Qt = torch.empty(plan.p * qb * b * b, dtype=torch.float64, device=f"cuda:{local}")
+            plan.orgqr(At, T, n, Qt)      # warm-up (builds the apply-Q schedule)
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(stream)
+            plan.orgqr(At, T, n, Qt)
+            q1.record(stream)
+            stream.synchronize()
+            qms = q0.elapsed_time(q1)
+            k_ = min(m, n)
+            qfl = 4.0 * m * n * k_ - 2.0 * (m + n) * k_ * k_ + 4.0 / 3.0 * k_ ** 3   # DORGQR count
+            form_q = {"ms": qms, "gflops": qfl / (qms * 1e-3) / 1e9, "flop_model": "4mnk-2(m+n)k^2+4k^3/3, k=n",
+                      "pct_of_fp64_peak": 100.0 * qfl / (qms * 1e-3) / (FP64_PEAK_TFLOPS * 1e12)}
+            del Qt
 
     # ---- optional trace of one extra step ----
     if args.trace and rank == 0 and world == 1:
@@ -321,6 +369,7 @@ def main():
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "cpu_baseline": cpu,
         "e2e": e2e,
+        "form_q": form_q,
         "gpu_launches": (4 if world > 1 else 3) * args.steps,   # pack, [rank barrier,] executor, get_r
         "clocks": clk.summary(),
     }

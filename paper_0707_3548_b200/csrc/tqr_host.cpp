@@ -297,8 +297,11 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
 //        cnt[k][jb][sl]: L -> 1, S(k,i) -> i-k+1.
 //   Q  : step k descending: S(k,i,jb,sl) for i descending, then L(k,jb,sl).
 //        cnt[k][jb][sl]: S(k,i) -> p-i, L -> p-k.
+// form_q (Q applied to [I; 0], tqr_orgqr): backward accumulation leaves the tile columns
+// left of step k untouched (they are still unit vectors in rows >= k b), so the tasks
+// (k, jb < k) are skipped -- the DORGQR saving, half the work of a dense Q*B.
 static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nsl, bool trans, int workers,
-                            Sched& out) {
+                            Sched& out, bool form_q = false) {
   out.nctr.assign(1, 0);
   const int K = (int)std::min(p, q);
   const int w = (b + nsl - 1) / nsl;
@@ -320,12 +323,14 @@ static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int 
         }
       } else {
         for (int k = K - 1; k >= 0; --k) {
+          if (form_q && jb < k) continue;                       // untouched unit columns
+          const bool prev = k + 1 < K && !(form_q && jb < k + 1);  // step k+1 had tasks here
           for (int i = (int)p - 1; i > k; --i) {
             int id = G.add(K_SQ, k, i, jb, sl, CNT(k, jb, sl), (int)p - i, dm.s, 1);
             G.t[id].key[0] = K - 1 - k;  // reverse order: later steps first
             G.t[id].key[1] = (int)p - 1 - i;
             if (i < p - 1) G.dep(id, CNT(k, jb, sl), 1, (int)p - i - 1);
-            if (k + 1 < K) G.dep(id, CNT(k + 1, jb, sl), 1, (int)p - i);
+            if (prev) G.dep(id, CNT(k + 1, jb, sl), 1, (int)p - i);
           }
           int id = G.add(K_LQ, k, k, jb, sl, CNT(k, jb, sl), (int)p - k, dm.l, 0);
           G.t[id].key[0] = K - 1 - k;
@@ -782,8 +787,8 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   return TQR_OK;
 }
 
-static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** out) {
-  auto key = std::make_pair(trans ? 1 : 0, nrhs);
+static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** out, bool form_q = false) {
+  auto key = std::make_pair(trans ? 1 : (form_q ? 2 : 0), nrhs);
   auto it = P->orm.find(key);
   if (it == P->orm.end()) {
     const int64_t qb = (nrhs + P->prm.b - 1) / P->prm.b;
@@ -792,7 +797,7 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
       return TQR_ERR_UNSUPPORTED;
     }
     Sched s;
-    build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, P->workers, s);
+    build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, P->workers, s, form_q);
     if (!s.topo_ok) {
       g_err = "internal: apply-Q schedule is not topological";
       return TQR_ERR_UNSUPPORTED;
@@ -817,8 +822,8 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
   return TQR_OK;
 }
 
-tqr_status tqr_ormqr(tqr_plan* P, char trans, const double* At, const double* T, double* Bt, int64_t nrhs,
-                     void* work) {
+static tqr_status ormqr_impl(tqr_plan* P, char trans, const double* At, const double* T, double* Bt, int64_t nrhs,
+                             void* work, bool form_q) {
   if (!P) return bad_arg(1, "plan is NULL");
   if (trans != 'T' && trans != 'N' && trans != 't' && trans != 'n') return bad_arg(2, "trans must be 'T' or 'N'");
   if (!At) return bad_arg(3, "At is NULL");
@@ -831,12 +836,17 @@ tqr_status tqr_ormqr(tqr_plan* P, char trans, const double* At, const double* T,
     return TQR_ERR_UNSUPPORTED;
   }
   DevSched* d = nullptr;
-  tqr_status st = orm_sched(P, trans == 'T' || trans == 't', nrhs, &d);
+  tqr_status st = orm_sched(P, trans == 'T' || trans == 't', nrhs, &d, form_q);
   if (st != TQR_OK) return st;
   double* Yp = reinterpret_cast<double*>(work);
   double* Tp = Yp + (size_t)P->p * P->q * P->prm.b * P->prm.b;
   CU(launch_pack_factors(At, T, Yp, Tp, P->prm.b, P->prm.s, P->p, P->K, P->st));
   return run(P, *d, const_cast<double*>(At), const_cast<double*>(T), Bt, work, false);
+}
+
+tqr_status tqr_ormqr(tqr_plan* P, char trans, const double* At, const double* T, double* Bt, int64_t nrhs,
+                     void* work) {
+  return ormqr_impl(P, trans, At, T, Bt, nrhs, work, false);
 }
 
 tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, double* Qt, void* work) {
@@ -852,7 +862,7 @@ tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, 
   }
   const int64_t qb = (k + P->prm.b - 1) / P->prm.b;
   CU(launch_eye_tiles(Qt, P->prm.m, k, P->prm.b, P->p, qb, P->st));
-  return tqr_ormqr(P, 'N', At, T, Qt, k, work);
+  return ormqr_impl(P, 'N', At, T, Qt, k, work, true);
 }
 
 tqr_status tqr_sync(tqr_plan* P) {
