@@ -135,6 +135,13 @@ tqr_status tqr_orgqr(tqr_plan* plan, const double* At, const double* T, int64_t 
 #define TQR_IPC_BLOB_BYTES 256
 tqr_status tqr_comm_export(tqr_plan* plan, void* blob /* TQR_IPC_BLOB_BYTES, host */);
 tqr_status tqr_comm_connect(tqr_plan* plan, const void* blobs /* nranks * TQR_IPC_BLOB_BYTES, host */);
+/* Connectivity check of a connected plan, no waiting on peers: tqr_comm_ping stores
+ * magic + rank into slot `rank` of every rank's ping array through the peer mappings
+ * (system-scope release stores; synchronous); after a host-side barrier, tqr_comm_flags
+ * copies this rank's nranks ping slots to host memory `out` (slot g == magic + g when rank g's
+ * stores arrived).  TQR_ERR_UNSUPPORTED on plans that are not real multi-rank. */
+tqr_status tqr_comm_ping(tqr_plan* plan, int32_t magic);
+tqr_status tqr_comm_flags(tqr_plan* plan, int32_t* out /* nranks, host */);
 
 /* ---- flop models -------------------------------------------------------------------- */
 /* Standard count 2n^2(m - n/3) for m >= n, 2m^2(n - m/3) otherwise. */

@@ -745,6 +745,18 @@ __global__ void rank_barrier_kernel(RankPtrs arr, int nranks, int me, int gen) {
     }
   }
 }
+// Connectivity check of the peer mappings (no waiting): rank `me` stores magic + me into
+// slot me of every rank's ping array (system-scope release, over NVLink on a real job).
+__global__ void ping_kernel(RankPtrs arr, int nranks, int me, int magic) {
+  const int g = threadIdx.x;
+  if (g < nranks) st_release_sys(arr.p[g] + me, magic + me);
+}
+cudaError_t launch_ping(int* const* ping_all, int nranks, int me, int magic, cudaStream_t st) {
+  RankPtrs arr;
+  for (int g = 0; g < MAX_RANKS; ++g) arr.p[g] = g < nranks ? ping_all[g] : nullptr;
+  ping_kernel<<<1, 32, 0, st>>>(arr, nranks, me, magic);
+  return cudaGetLastError();
+}
 cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int gen, cudaStream_t st) {
   RankPtrs arr;
   for (int g = 0; g < MAX_RANKS; ++g) arr.p[g] = g < nranks ? arrive_all[g] : nullptr;

@@ -707,6 +707,33 @@ tqr_status tqr_comm_connect(tqr_plan* P, const void* blobs) {
   return TQR_OK;
 }
 
+// ping slots: 8 ints right after the 8 arrive flags (same 256-byte block)
+static int* ping_of(int* arrive) { return arrive ? arrive + MAX_RANKS : nullptr; }
+
+tqr_status tqr_comm_ping(tqr_plan* P, int32_t magic) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (!P->real || !P->connected) {
+    g_err = "tqr_comm_ping: needs a connected real multi-rank plan";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  int* pings[MAX_RANKS] = {};
+  for (int g = 0; g < P->G; ++g) pings[g] = ping_of(P->arrive[g]);
+  CU(launch_ping(pings, P->G, P->me, magic, P->st));
+  CU(cudaStreamSynchronize(P->st));
+  return TQR_OK;
+}
+
+tqr_status tqr_comm_flags(tqr_plan* P, int32_t* out) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (!out) return bad_arg(2, "out is NULL");
+  if (!P->real) {
+    g_err = "tqr_comm_flags: needs a real multi-rank plan";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  CU(cudaMemcpy(out, ping_of(P->arrive[P->me]), sizeof(int32_t) * P->G, cudaMemcpyDeviceToHost));
+  return TQR_OK;
+}
+
 tqr_status tqr_tiles_size(const tqr_plan* P, size_t* a, size_t* t) {
   if (!P) return bad_arg(1, "plan is NULL");
   const size_t b = (size_t)P->prm.b, s = (size_t)P->prm.s;

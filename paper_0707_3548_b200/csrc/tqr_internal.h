@@ -91,5 +91,7 @@ cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p,
 // Cross-rank entry barrier of one call (real multi-GPU): publish `gen` into every rank's
 // arrive[me] (system scope), wait until arrive[g] >= gen for all g on this rank.
 cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int gen, cudaStream_t st);
+// Store magic + me into slot me of every rank's ping array (tqr_comm_ping).
+cudaError_t launch_ping(int* const* ping_all, int nranks, int me, int magic, cudaStream_t st);
 
 }  // namespace tqr

@@ -73,6 +73,8 @@ def lib():
         L.tqr_phase_counters.argtypes = [_vp, _vp]
         L.tqr_comm_export.argtypes = [_vp, _vp]
         L.tqr_comm_connect.argtypes = [_vp, _vp]
+        L.tqr_comm_ping.argtypes = [_vp, _i32]
+        L.tqr_comm_flags.argtypes = [_vp, _vp]
         L.tqr_schedule_records.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _vp, _i64, ctypes.POINTER(_i64),
                                            ctypes.POINTER(_i32)]
         _lib = L
@@ -213,6 +215,16 @@ class Plan:
         buf = ctypes.create_string_buffer(TQR_IPC_BLOB_BYTES)
         _check(lib().tqr_comm_export(self._h, buf))
         return buf.raw
+
+    def comm_ping(self, magic: int):
+        """Store magic + rank into every rank's ping slot (peer-store connectivity check)."""
+        _check(lib().tqr_comm_ping(self._h, magic))
+
+    def comm_flags(self):
+        """This rank's ping slots (after a host barrier following every rank's comm_ping)."""
+        out = (_i32 * self.nranks)()
+        _check(lib().tqr_comm_flags(self._h, out))
+        return list(out)
 
     def comm_connect(self, blobs: bytes):
         """blobs: every rank's comm_export() blob, concatenated in rank order."""

@@ -106,3 +106,44 @@ def test_real_rank_layout_pack_unpack_get_r(G):
             plan.geqrf(At, T)  # not connected to its peers
         plan.close()
     assert np.array_equal(back.cpu().numpy(), Ac.cpu().numpy())
+
+
+def _ipc_rank(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+    from paper_0707_3548_b200 import Plan
+    from paper_0707_3548_b200 import dist as tdist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    try:
+        plan = Plan(1024, 1024, 128, 32, nranks=world, rank=rank)
+        tdist.connect(plan)               # CUDA IPC blobs over torch.distributed
+        plan.comm_ping(7000)              # peer stores into every rank's ping slots
+        dist.barrier()
+        out.put((rank, plan.comm_flags()))
+        dist.barrier()
+        plan.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_real_ranks_ipc_connect_and_peer_stores():
+    """The real multi-GPU connection path, two processes on ONE GPU (no kernel waits on
+    another rank, as the profiling recipe requires): export/exchange/open the CUDA IPC
+    handles of each rank's symmetric buffer and store through the peer mappings at system
+    scope; every rank must see every rank's store in its own ping slots."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_rank, args=(r, 2, port, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    res = dict(q.get(timeout=300) for _ in procs)
+    for p_ in procs:
+        p_.join(timeout=120)
+        assert p_.exitcode == 0
+    assert res[0] == [7000, 7001] and res[1] == [7000, 7001], res
