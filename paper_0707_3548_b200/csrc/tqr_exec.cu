@@ -8,6 +8,8 @@
 // completion it publishes its counter (release).  Task granularity: GEQRT(k) and
 // TSQRT(k,i) are whole-tile single-CTA tasks; LARFB and SSRFB are split into 64-column
 // slices (one 8-column group per warp, register resident).
+#include <cstdio>
+
 #include "tqr_device.cuh"
 #include "tqr_internal.h"
 
@@ -362,6 +364,23 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
     PH_MARK(6);
     if (R.trace && tid == 0) t_start = globaltimer();
     const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4], kc = s_task[7];
+#ifdef TQR_CHECKS
+    // checked build: every field of the record and every counter range in bounds
+    if (tid == 0) {
+      bool bad = kind < 0 || kind > 7 || k < 0 || k >= a.p || i < k || i >= a.p || kc < 0 || kc >= a.qcols ||
+                 j < 0 || j >= a.qcols || sl < -1 || sl >= (kind >= K_L ? a.nsl : B / SO) ||
+                 s_task[5] < 0 || s_task[5] >= a.nctr || (MODE == 0) != (kind <= K_S);
+      for (int d = 0; d < TASK_NDEP; ++d) {
+        const int code = s_task[8 + 2 * d], cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+        if (cnt && (idx + cnt > a.nctr)) bad = true;
+      }
+      if (bad) {
+        printf("tqr checked build: bad task record %d: kind %d k %d i %d j %d sl %d kc %d out %d\n", tk, kind, k, i,
+               j, sl, kc, s_task[5]);
+        __trap();
+      }
+    }
+#endif
     const int p = a.p;
     {
       constexpr int NL = B / S;

@@ -19,6 +19,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <queue>
@@ -454,6 +455,9 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
   a.base = base;
   a.sys = P->real ? 1 : 0;
   a.passes = P->passes;
+  a.nctr = P->nctr_max;
+  a.qcols = (int)std::max<int64_t>(qloc_of(P, P->me), Bt ? (int64_t)(1 << 30) : 0);  // Bt width unknown here
+  a.nsl = P->nsl;
   a.phases = P->d_phases;
   if (P->G == 1) {
     a.Yp[0] = reinterpret_cast<double*>(work);
@@ -580,6 +584,8 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   const bool tall = P->p >= 4 * P->q;
   P->passes = p->b >= 512 ? 8 : (p->b >= 256 && !tall ? 2 : 1);
   P->split = tall || p->b >= 512 || p->b <= 128;
+  if (const char* e = getenv("TQR_DEV_PASSES")) P->passes = std::max(1, atoi(e));   // development knobs
+  if (const char* e = getenv("TQR_DEV_SPLIT")) P->split = atoi(e) != 0;
   {
     const int w = exec_slice(p->b, p->s) * P->passes;
     P->nsl = (int)((p->b + w - 1) / w);

@@ -59,6 +59,9 @@ struct ExecArgs {
   int base;                 // counter generation base of this call
   int sys;                  // 1: peers on other GPUs (system-scope acquire/release)
   int passes;               // register passes (SLICE columns each) per LARFB/SSRFB task
+  int nctr;                 // counters per rank (TQR_CHECKS builds: bounds of every counter access)
+  int qcols;                // storage tile columns of A (and of Bt in apply-Q) (TQR_CHECKS)
+  int nsl;                  // update tasks per tile (TQR_CHECKS)
   long long* phases;        // TQR_PROFILE_PHASES builds: 16 phase-cycle totals, or nullptr
 };
 
