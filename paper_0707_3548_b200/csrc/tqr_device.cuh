@@ -36,9 +36,9 @@ namespace tqr {
 // 8 warps (up to 255 registers per thread: the executor contains device-function calls,
 // and ptxas spilled the accumulators of the inlined update path at a 128-register cap)
 // and holds GPS groups = SLICE columns.
-template <int B, int S>
+template <int B, int S, int RWM = 128>
 struct Cfg {
-  static constexpr int RW = B < 128 ? B : 128;
+  static constexpr int RW = B < RWM ? B : RWM;  // rows of a column group held by one warp
   static constexpr int RS = B / RW;
   static constexpr int NWARP = 8;  // 255-register budget: no spills in the DMMA paths
   static constexpr int NT = NWARP * 32;

@@ -38,9 +38,9 @@ __shared__ long long s_pht;      // thread 0's last mark
 #define PH_MARK(idx) do {} while (0)
 #endif
 
-template <int B, int S>
+template <int B, int S, int RWM>
 struct Layout {
-  using C = Cfg<B, S>;
+  using C = Cfg<B, S, RWM>;
   static constexpr int YSZ = B * S;          // one Y buffer (swizzled panel)
   static constexpr int TSZ = S * S;
   // Y0 T0 | Y1 T1: the panel tasks overlay P (ld B+4) on the contiguous (Y1, T1) region
@@ -82,9 +82,9 @@ __device__ __forceinline__ double* tslot_ptr(double* base, int i, int k, int p, 
 // reads by the fence.proxy.async after the dependency acquire (or after panel_block), and a
 // buffer refill after generic reads (WAR) needs none.  (A fence here also waited for the
 // thread's outstanding acc loads -- 6% of C3 time.)
-template <int B, int S>
+template <int B, int S, int RWM>
 __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const double* Tp, int l, int buf) {
-  using L = Layout<B, S>;
+  using L = Layout<B, S, RWM>;
   constexpr unsigned YB = B * S * 8, TB = S * S * 8;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
   mbar_expect_tx(full + buf, YB + TB);
@@ -102,14 +102,14 @@ __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const 
 // __syncthreads inside the block loop and every refill overlaps a whole block of math.
 // C1 is fetched one block ahead by the group's rpart-0 warp (cp.async).
 // `pf(li, nb)` is called by thread 0 once per block (cross-task prefetch hook).
-template <int B, int S, bool QT, bool DESC, class PF>
-__device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>::RW / 8][2], const double* Yp,
+template <int B, int S, int RWM, bool QT, bool DESC, class PF>
+__device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S, RWM>::RW / 8][2], const double* Yp,
                                              const double* Tp, int lb0, int nbe, double* C1, const double* Ct,
                                              int col0, int gact, PF&& pf) {
   // blocks lb0 .. nbe-1 (DESC: nbe-1 .. 0, lb0 must be 0)
   const int nb = nbe - lb0;
-  using C = Cfg<B, S>;
-  using L = Layout<B, S>;
+  using C = Cfg<B, S, RWM>;
+  using L = Layout<B, S, RWM>;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
   const int cg0 = col0 + gi * 8;
@@ -126,8 +126,8 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
     done[1] = 0;
     fence_mbar_init();
     fence_proxy_async();
-    issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);
-    if (nb > 1) issue_panel<B, S>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
+    issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);
+    if (nb > 1) issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
   }
   if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
   if (nb <= 0) return;
@@ -154,7 +154,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
     if (lane == 0 && li + 2 < nb) {
       if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
         done[buf] = 0;
-        issue_panel<B, S>(sm, Yp, Tp, DESC ? l - 2 : l + 2, buf);
+        issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? l - 2 : l + 2, buf);
       }
     }
   }
@@ -169,12 +169,12 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S>
 // out and the packed Y_l / T_l are published for blocks l+1.. and for every update task.
 // TSQRT reads and writes only the upper triangle of A(k,k).
 // ---------------------------------------------------------------------------------------
-template <int B, int S, int SO, bool ts>
-__device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S>::RW / 8][2],
+template <int B, int S, int SO, int RWM, bool ts>
+__device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S, RWM>::RW / 8][2],
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
                                             size_t toff, int l, bool more, int rlo) {
-  using C = Cfg<B, S>;
-  using L = Layout<B, S>;
+  using C = Cfg<B, S, RWM>;
+  using L = Layout<B, S, RWM>;
   constexpr int LDP = L::LDP;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
@@ -267,10 +267,10 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
 // L2 prefetch of the inputs of a (not yet started) task record q: the tile column slice it
 // updates (+ its C1 slice), or the tile a panel task factors, and its first two packed
 // reflector blocks.  Safe before the task's dependencies hold (L2 is coherent).
-template <int B, int S, int SO, int MODE>
+template <int B, int S, int SO, int RWM, int MODE>
 __device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, const double* Yme, int p,
                                               int tsl) {
-  using C = Cfg<B, S>;
+  using C = Cfg<B, S, RWM>;
   const int kind = q[0], k = q[1], i = q[2], j = q[3], sl = q[4], kc = q[7];
   if (MODE == 0 && (kind == K_G || kind == K_T)) {
     prefetch_l2(tile_ptr(R.A, kind == K_T ? i : k, kc, p, B), (unsigned)(B * B * 8));
@@ -295,8 +295,8 @@ __device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, 
 // MODE 0: factorization; MODE 1: apply Q^T; MODE 2: apply Q.  No device-function calls:
 // every task kind runs through ONE inlined update phase (plus the panel block for GEQRT /
 // TSQRT), so ptxas allocates the column-group accumulators once, without spills.
-template <int B, int SO, int MODE>
-__global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(const __grid_constant__ ExecArgs a) {
+template <int B, int SO, int MODE, int RWM>
+__global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_kernel(const __grid_constant__ ExecArgs a) {
   constexpr int S = Inner<B, SO>::SI;  // internal inner block (== SO up to b = 256)
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_task[TASK_INTS];
@@ -402,13 +402,13 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
       // whole tile when sl < 0); update task: TSL / SLICE register passes of its slice
       constexpr int SPT = SO / S;  // internal blocks per output T block
       const int sub0 = panel ? (sl < 0 ? 0 : sl * SPT) : 0;
-      const int tsl = a.passes * Cfg<B, S>::SLICE;  // columns per update task
+      const int tsl = a.passes * Cfg<B, S, RWM>::SLICE;  // columns per update task
       const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : a.passes;
       // panel split (R21): flags bit 1 = apply part only (left-looking update of the
       // block columns with this tile's earlier blocks, stored back), bit 2 = factor part only
       const bool a_part = panel && (s_task[14] & 2), f_part = panel && (s_task[14] & 4);
       for (int sub = sub0; sub < nsub; ++sub) {
-        double acc[Cfg<B, S>::RW / 8][2];
+        double acc[Cfg<B, S, RWM>::RW / 8][2];
         double* C1;
         double* Ct;
         int col0, nb, gact, lb0 = 0;
@@ -422,15 +422,15 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
         } else {
           C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
           Ct = lkind ? tile_ptr(Bt, k, j, p, B) : tile_ptr(Bt, i, j, p, B);
-          col0 = sl * tsl + sub * Cfg<B, S>::SLICE;  // (update tasks: sl >= 0)
+          col0 = sl * tsl + sub * Cfg<B, S, RWM>::SLICE;  // (update tasks: sl >= 0)
           nb = NL;
-          gact = (B - col0) / 8 < Cfg<B, S>::GPS ? (B - col0) / 8 : Cfg<B, S>::GPS;
+          gact = (B - col0) / 8 < Cfg<B, S, RWM>::GPS ? (B - col0) / 8 : Cfg<B, S, RWM>::GPS;
         }
         auto pf = [&](int li, int nbb) {
           if (!panel && sub + 1 < nsub && li == nbb / 2) {  // next register pass of this task
-            const size_t nxt_off = (size_t)(col0 + Cfg<B, S>::SLICE) * B;
-            prefetch_l2(Ct + nxt_off, (unsigned)(Cfg<B, S>::SLICE * B * 8));
-            if (C1) prefetch_l2(C1 + nxt_off, (unsigned)(Cfg<B, S>::SLICE * B * 8));
+            const size_t nxt_off = (size_t)(col0 + Cfg<B, S, RWM>::SLICE) * B;
+            prefetch_l2(Ct + nxt_off, (unsigned)(Cfg<B, S, RWM>::SLICE * B * 8));
+            if (C1) prefetch_l2(C1 + nxt_off, (unsigned)(Cfg<B, S, RWM>::SLICE * B * 8));
           }
           if (sub != nsub - 1 || nbb < 4) return;  // (nbb: blocks this pass applies)
           const int l0 = nbb / 2;
@@ -444,23 +444,23 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
           }
           if (li == l0 + 2 && rec_for == next_tk && next_tk < R.ntasks) {
             cp_async_wait<0>();
-            prefetch_task<B, S, SO, MODE>(s_next, R, Yme, p, tsl);
+            prefetch_task<B, S, SO, RWM, MODE>(s_next, R, Yme, p, tsl);
           }
         };
-        update_phase<B, S, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf);
+        update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (a_part) {
-          if (warp / Cfg<B, S>::RS < gact)
-            store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
-                                         (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
+          if (warp / Cfg<B, S, RWM>::RS < gact)
+            store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
+                                         (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8));
         } else if (panel) {
           // TS as a template argument: each flavour is register-allocated on its own
           const int rlo = f_part ? sub0 * S : 0;
-          if (ts) panel_block<B, S, SO, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
-          else panel_block<B, S, SO, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
-        } else if (warp / Cfg<B, S>::RS < gact) {
-          store_cols<B, Cfg<B, S>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S>::RS),
-                                       (warp % Cfg<B, S>::RS) * (Cfg<B, S>::RW / 8));
+          if (ts) panel_block<B, S, SO, RWM, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
+          else panel_block<B, S, SO, RWM, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
+        } else if (warp / Cfg<B, S, RWM>::RS < gact) {
+          store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
+                                       (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8));
         }
         if (!panel) PH_MARK(5);
       }
@@ -501,37 +501,41 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI>::NT, 1) exec_kernel(c
 #define TQR_INSTANCES(X) \
   X(16, 8) X(16, 16) X(32, 8) X(32, 32) X(64, 16) X(64, 64) X(128, 32) X(256, 32) X(512, 64)
 
-template <int B, int S, int MODE>
+// RWM: rows per warp cap (Cfg::RW = min(B, RWM)).  b >= 256 tiles are built twice: RWM = 256
+// (one warp holds a whole 256-row column group: no row-partial exchange, 64-column passes --
+// square grids) and RWM = 128 (32-column passes -- tall-skinny grids want the finer tasks);
+// the plan chooses (tqr_host.cpp).  b <= 128 has RW = B either way.
+template <int B, int S, int MODE, int RWM>
 static cudaError_t launch_mode(const ExecArgs& a, int grid, cudaStream_t st) {
-  using L = Layout<B, Inner<B, S>::SI>;
+  using L = Layout<B, Inner<B, S>::SI, RWM>;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(exec_kernel<B, S, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
+    cudaError_t e = cudaFuncSetAttribute(exec_kernel<B, S, MODE, RWM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)L::BYTES);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   ExecArgs args = a;
   void* params[] = {&args};
-  return cudaLaunchCooperativeKernel((const void*)exec_kernel<B, S, MODE>, dim3(grid),
-                                     dim3(Cfg<B, Inner<B, S>::SI>::NT), params, L::BYTES, st);
+  return cudaLaunchCooperativeKernel((const void*)exec_kernel<B, S, MODE, RWM>, dim3(grid),
+                                     dim3(Cfg<B, Inner<B, S>::SI, RWM>::NT), params, L::BYTES, st);
 }
-template <int B, int S>
+template <int B, int S, int RWM>
 static cudaError_t launch_one(const ExecArgs& a, int mode, int grid, cudaStream_t st) {
-  if (mode == 1) return launch_mode<B, S, 1>(a, grid, st);
-  if (mode == 2) return launch_mode<B, S, 2>(a, grid, st);
-  return launch_mode<B, S, 0>(a, grid, st);
+  if (mode == 1) return launch_mode<B, S, 1, RWM>(a, grid, st);
+  if (mode == 2) return launch_mode<B, S, 2, RWM>(a, grid, st);
+  return launch_mode<B, S, 0, RWM>(a, grid, st);
 }
 
-template <int B, int S>
+template <int B, int S, int RWM>
 static int max_ctas_one(int device) {
-  using L = Layout<B, Inner<B, S>::SI>;
+  using L = Layout<B, Inner<B, S>::SI, RWM>;
   int per_sm = 0, sms = 0, worst = 1 << 30;
-  const void* fns[3] = {(const void*)exec_kernel<B, S, 0>, (const void*)exec_kernel<B, S, 1>,
-                        (const void*)exec_kernel<B, S, 2>};
+  const void* fns[3] = {(const void*)exec_kernel<B, S, 0, RWM>, (const void*)exec_kernel<B, S, 1, RWM>,
+                        (const void*)exec_kernel<B, S, 2, RWM>};
   for (const void* f : fns) {
     cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, Cfg<B, Inner<B, S>::SI>::NT, L::BYTES) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, Cfg<B, Inner<B, S>::SI, RWM>::NT, L::BYTES) !=
         cudaSuccess)
       return 0;
     worst = per_sm < worst ? per_sm : worst;
@@ -547,23 +551,37 @@ bool exec_supported(int b, int s) {
 #undef X
   return false;
 }
+int exec_rw_variant(int b, int rwm) { return (b >= 256 && rwm >= 256) ? 256 : 128; }
 
-cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cudaStream_t st) {
-#define X(BB, SS) if (b == BB && s == SS) return launch_one<BB, SS>(a, mode, grid, st);
+cudaError_t launch_exec(int b, int s, int mode, int rwm, const ExecArgs& a, int grid, cudaStream_t st) {
+#define X(BB, SS)                                                              \
+  if (b == BB && s == SS) {                                                    \
+    if constexpr (BB >= 256)                                                   \
+      if (exec_rw_variant(b, rwm) == 256) return launch_one<BB, SS, 256>(a, mode, grid, st); \
+    return launch_one<BB, SS, 128>(a, mode, grid, st);                         \
+  }
   TQR_INSTANCES(X)
 #undef X
   return cudaErrorInvalidValue;
 }
 
-int exec_slice(int b, int s) {
-#define X(BB, SS) if (b == BB && s == SS) return Cfg<BB, Inner<BB, SS>::SI>::SLICE;
+int exec_slice(int b, int s, int rwm) {
+#define X(BB, SS)                                                                         \
+  if (b == BB && s == SS)                                                                 \
+    return exec_rw_variant(b, rwm) == 256 ? Cfg<BB, Inner<BB, SS>::SI, 256>::SLICE        \
+                                          : Cfg<BB, Inner<BB, SS>::SI, 128>::SLICE;
   TQR_INSTANCES(X)
 #undef X
   return 0;
 }
 
-int exec_max_ctas(int b, int s, int device) {
-#define X(BB, SS) if (b == BB && s == SS) return max_ctas_one<BB, SS>(device);
+int exec_max_ctas(int b, int s, int rwm, int device) {
+#define X(BB, SS)                                                          \
+  if (b == BB && s == SS) {                                                \
+    if constexpr (BB >= 256)                                               \
+      if (exec_rw_variant(b, rwm) == 256) return max_ctas_one<BB, SS, 256>(device); \
+    return max_ctas_one<BB, SS, 128>(device);                              \
+  }
   TQR_INSTANCES(X)
 #undef X
   return 0;

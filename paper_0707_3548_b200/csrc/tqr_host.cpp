@@ -360,6 +360,7 @@ struct tqr_plan {
   int64_t p, q, K;
   int nsl, workers;
   int passes = 1;      // register passes per update task (policy below)
+  int rwm = 128;       // rows-per-warp variant of the executor (policy below)
   bool split = true;   // panel A/F split (R21)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
@@ -495,7 +496,7 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
   }
   if (P->real) CU(launch_rank_barrier(P->arrive, P->G, P->me, P->gen, P->st));
   const int grid = std::max(nl, std::min(P->workers, std::max(1, total)));
-  CU(launch_exec(P->prm.b, P->prm.s, d.mode, a, grid, P->st));
+  CU(launch_exec(P->prm.b, P->prm.s, d.mode, P->rwm, a, grid, P->st));
   return TQR_OK;
 }
 
@@ -576,22 +577,27 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   P->emulate = emulate;
   P->real = P->G > 1 && !emulate;
   P->nloc = emulate ? P->G : 1;
-  // Granularity policy (measured on B200, r01): b = 512 tasks walk 8 register passes (C5 DAG
-  // stays at 2.8 M tasks); tall-skinny grids (p >= 4q) are bound by the TSQRT chain and want
-  // fine update tasks plus the panel A/F split (C4: 60 vs 64-68 ms); square grids at b = 256
-  // prefer 2-pass update tasks and fused panel blocks (C3: 232 vs 238 ms); at b <= 128 the
-  // GEQRT/TSQRT chain dominates and the split helps (C2: 7.6 vs 7.9 ms).
+  // Granularity policy (measured on B200, r01):
+  //  * square grids, b >= 256: the RW = 256 executor (a warp holds all 256 rows of its column
+  //    group: no row-partial exchange) with 128-column update tasks -- C3 224 ms (70.5%),
+  //    C5 12.5 s (80.7%) vs 232 ms / 13.7 s with RW = 128;
+  //  * tall-skinny grids (p >= 4q) are bound by the TSQRT chain: the RW = 128 executor with
+  //    32-column update tasks and the panel A/F split (C4: 60 ms vs 77 with RW = 256);
+  //  * b <= 128: RW = b, 1-pass tasks, A/F split (the GEQRT/TSQRT chain dominates C2).
   const bool tall = P->p >= 4 * P->q;
-  P->passes = p->b >= 512 ? 8 : (p->b >= 256 && !tall ? 2 : 1);
-  P->split = tall || p->b >= 512 || p->b <= 128;
+  P->rwm = (p->b >= 256 && !tall) ? 256 : 128;
+  P->passes = p->b >= 256 ? (128 / exec_slice(p->b, p->s, P->rwm)) : 1;  // 128-column tasks
+  if (tall && p->b <= 256) P->passes = 1;
+  P->split = tall || p->b <= 128;
   if (const char* e = getenv("TQR_DEV_PASSES")) P->passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P->split = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_RW")) P->rwm = atoi(e);
   {
-    const int w = exec_slice(p->b, p->s) * P->passes;
+    const int w = exec_slice(p->b, p->s, P->rwm) * P->passes;
     P->nsl = (int)((p->b + w - 1) / w);
   }
   P->st = (cudaStream_t)p->stream;
-  P->workers = exec_max_ctas(p->b, p->s, p->device);
+  P->workers = exec_max_ctas(p->b, p->s, P->rwm, p->device);
   if (P->workers < P->nloc) {
     destroy_plan(P);
     g_err = "executor does not fit on this device";

@@ -67,13 +67,14 @@ struct ExecArgs {
 
 // Launch the persistent executor for tile size b, inner block s (cooperative launch).
 // mode: 0 factorization, 1 apply Q^T, 2 apply Q.
-cudaError_t launch_exec(int b, int s, int mode, const ExecArgs& a, int grid, cudaStream_t st);
-// Max co-resident CTAs for (b, s) on this device (0 if no instance).
-int exec_max_ctas(int b, int s, int device);
+// rwm: rows-per-warp variant (128 or 256; b >= 256 only, otherwise ignored).
+cudaError_t launch_exec(int b, int s, int mode, int rwm, const ExecArgs& a, int grid, cudaStream_t st);
+// Max co-resident CTAs for (b, s, rwm) on this device (0 if no instance).
+int exec_max_ctas(int b, int s, int rwm, int device);
 bool exec_supported(int b, int s);
 // Columns of one register-resident pass of a LARFB/SSRFB task for (b, s) (0 if no instance);
 // a task covers `passes` consecutive passes (host policy, ExecArgs::passes).
-int exec_slice(int b, int s);
+int exec_slice(int b, int s, int rwm);
 // Internal inner block SI of the executor for (b, s) (== s except b = 512).
 int exec_inner(int b, int s);
 // Off-diagonal blocks of the output T_L when SI < s (no-op otherwise).
