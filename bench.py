@@ -363,7 +363,7 @@ def main():
         "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                     "kernel": f"exec_kernel<{b},{s}> (tqr_geqrf)", "kernel_ms": kern_ms,
+                     "kernel": f"exec_kernel<{b},{s},mode 0> (tqr_geqrf)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops / world,
                      "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},

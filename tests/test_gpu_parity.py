@@ -26,6 +26,9 @@ def _cases():
         (700, 600, 256, 32, "uniform"),  # C3 tiling, ragged
         (1280, 300, 256, 32, "normal"),  # C4-shaped tall-skinny
         (1100, 1030, 512, 64, "uniform"),  # C5 tiling (internal 16-column blocks + form_t), ragged
+        # degenerate shapes: 1x1, one row, one column, one exact tile, a tile + 1-element tail
+        (1, 1, 16, 8, "uniform"), (1, 50, 16, 8, "uniform"), (50, 1, 16, 8, "uniform"),
+        (64, 64, 64, 16, "normal"), (65, 65, 64, 16, "uniform"), (257, 3, 256, 32, "normal"),
     ]
 
 
