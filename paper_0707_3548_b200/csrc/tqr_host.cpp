@@ -97,7 +97,20 @@ static inline uint64_t ckey(int idx, int val) { return ((uint64_t)(uint32_t)idx 
 // dispatch order is the restriction of ONE global topological order, so per-rank ticket
 // streams cannot deadlock across ranks.  Returns false if the dependency
 // structure is inconsistent (missing producer or cycle).
-static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& out) {
+// Priority of the list schedule (never affects results, only the ticket order):
+//  * PRIO_CLASS: the paper's classes G > T > L > S with the lookahead of
+//    DESIGN.md R10, ties by (k, i, j, slice);
+//  * PRIO_BLEVEL: critical-path priority -- the task's bottom level (its duration plus the
+//    longest duration-weighted path to the end of the DAG, `lat` ns per edge for the counter
+//    handoff), ties as above.  The paper motivates its classes by the critical path
+//    ("nodes that have the higher number of outgoing edges"); the bottom
+//    level is that criterion computed exactly on the task graph.  It matters when many panel
+//    chains are in flight at once (tall-skinny grids, R22): the updates of column
+//    j at step k < j - 1 feed panel j's chain and outrank later-column work of earlier steps.
+enum Prio { PRIO_CLASS = 0, PRIO_BLEVEL = 1 };
+
+static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& out, int prio = PRIO_CLASS,
+                          double lat = 0.0) {
   const int n = (int)G.t.size();
   const int nr = (int)workers.size();
   std::unordered_map<uint64_t, int> producer;
@@ -124,9 +137,31 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
         nedges++;
       }
   }
+  std::vector<double> blevel;
+  if (prio == PRIO_BLEVEL) {  // reverse topological DP (Kahn order)
+    std::vector<int> topo, deg(indeg);
+    topo.reserve(n);
+    for (int id = 0; id < n; ++id)
+      if (deg[id] == 0) topo.push_back(id);
+    for (size_t h = 0; h < topo.size(); ++h)
+      for (int sidx : succ[topo[h]])
+        if (--deg[sidx] == 0) topo.push_back(sidx);
+    if ((int)topo.size() != n) return false;  // cycle
+    blevel.assign(n, 0.0);
+    for (int h = n - 1; h >= 0; --h) {
+      const int id = topo[h];
+      double m = 0.0;
+      for (int sidx : succ[id]) m = std::max(m, blevel[sidx] + lat);
+      blevel[id] = G.t[id].dur + m;
+    }
+  }
   auto prio_less = [&](int a, int b) {  // true if a has LOWER priority than b (for max-heap)
     const auto &x = G.t[a], &y = G.t[b];
-    if (x.cls != y.cls) return x.cls > y.cls;
+    if (prio == PRIO_BLEVEL) {
+      if (blevel[a] != blevel[b]) return blevel[a] < blevel[b];
+    } else if (x.cls != y.cls) {
+      return x.cls > y.cls;
+    }
     for (int c = 0; c < 4; ++c)
       if (x.key[c] != y.key[c]) return x.key[c] > y.key[c];
     return a > b;
@@ -150,7 +185,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
         int id = ready[r].top();
         ready[r].pop();
         order.push_back(id);
-        events.push({now + G.t[id].dur, id});
+        events.push({now + G.t[id].dur + lat, id});
         free_w[r]--;
       }
     if (events.empty()) return false;  // cycle
@@ -213,7 +248,7 @@ struct DurModel {
 // column counters col[k][jl][sl] (jl = j / G).  `real_layout`: tile storage holds only the
 // rank's own columns (storage column jl); otherwise the full global grid (column j).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
-                               bool real_layout, bool split, Sched& out) {
+                               bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -290,7 +325,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         }
     }
   }
-  if (!list_schedule(T, workers, out)) out.topo_ok = false;
+  if (!list_schedule(T, workers, out, prio, lat)) out.topo_ok = false;
 }
 
 // apply-Q^T (trans) or apply-Q to a tile-major B with qb tile columns.
@@ -362,6 +397,8 @@ struct tqr_plan {
   int passes = 1;      // register passes per update task (policy below)
   int rwm = 128;       // rows-per-warp variant of the executor (policy below)
   bool split = true;   // panel A/F split (R21)
+  int prio = PRIO_BLEVEL;  // list-schedule priority (policy below)
+  double lat = 4000.0;     // modelled per-task handoff latency of the list schedule (ns)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -583,7 +620,9 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   //    C5 12.5 s (80.7%) vs 232 ms / 13.7 s with RW = 128;
   //  * tall-skinny grids (p >= 4q) are bound by the TSQRT chain: the RW = 128 executor with
   //    32-column update tasks and the panel A/F split (C4: 60 ms vs 77 with RW = 256);
-  //  * b <= 128: RW = b, 1-pass tasks, A/F split (the GEQRT/TSQRT chain dominates C2).
+  //  * b <= 128: RW = b, 1-pass tasks, A/F split (the GEQRT/TSQRT chain dominates C2);
+  //  * dispatch order by bottom level (critical path) with a 4 us handoff per task, not by the
+  //    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
   const bool tall = P->p >= 4 * P->q;
   P->rwm = (p->b >= 256 && !tall) ? 256 : 128;
   P->passes = p->b >= 256 ? (128 / exec_slice(p->b, p->s, P->rwm)) : 1;  // 128-column tasks
@@ -592,6 +631,8 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (const char* e = getenv("TQR_DEV_PASSES")) P->passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P->split = atoi(e) != 0;
   if (const char* e = getenv("TQR_DEV_RW")) P->rwm = atoi(e);
+  if (const char* e = getenv("TQR_DEV_PRIO")) P->prio = atoi(e);
+  if (const char* e = getenv("TQR_DEV_LAT")) P->lat = atof(e);
   {
     const int w = exec_slice(p->b, p->s, P->rwm) * P->passes;
     P->nsl = (int)((p->b + w - 1) / w);
@@ -613,7 +654,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate)
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -919,7 +960,8 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   if (workers < 1) return bad_arg(4, "workers < 1");
   if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
   build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1,
-                     (p + q) % 2 == 0, s);  // both panel forms are exercised by the inspected shapes
+                     (p + q) % 2 == 0, s, p % 2 == 0 ? PRIO_BLEVEL : PRIO_CLASS,
+                     4000.0);  // both panel forms and both priorities are exercised by the inspected shapes
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
