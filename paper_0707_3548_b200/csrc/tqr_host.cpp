@@ -225,21 +225,27 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
 }
 
 // Per-task durations (ns) for the list schedule only (never affect results), fitted to the
-// B200 traces (tools/trace_stats.py, r01): fp64 DMMA peak per SM ~251 GFLOP/s; a panel
-// sub-task for inner block l = ~10 us fixed + ~0.7 us per factored column + l block applies
-// of its columns at ~80% of the SM peak; update tasks run at ~78% (the LARFB form applies
-// the zero rows of U above block l as well, so it costs like SSRFB without C1).
+// B200 traces of the r01 executor (tools/trace_stats.py; b = 256 / 128, s = 32):
+//  * update tasks (LARFB, SSRFB, apply-Q): ~2 us fixed + the task's flops at 88% (RW = 256
+//    executor) / 79% (RW = 128) of the 251 GFLOP/s per-SM fp64 DMMA peak (the LARFB form
+//    applies the zero rows of U above block l as well, so it costs like SSRFB without C1);
+//  * panel factor part (R21 F): ~15.5 us fixed + s columns at (0.25 + 0.0018 b) us each
+//    (TSQRT b = 256: 38.6 us, b = 128: 30.7 us); GEQRT + 0.03 b us;
+//  * panel apply part of block l (R21 A): (1.5 + 0.012 b) us + l block applies at 78%;
+//  * fused panel sub-task (no A/F split): factor part + 9 us + 1.35 x the l block applies.
 struct DurModel {
   double B, Sv, W, l, s, apply;
-  DurModel(int b, int s_, int w) : B(b), Sv(s_), W(w) {
+  DurModel(int b, int s_, int w, int rwm = 128) : B(b), Sv(s_), W(w) {
     const double sm = 251.0;  // GFLOP/s per SM == flop/ns
-    l = 3000 + (4.0 * B * B * W) / (0.78 * sm);
-    s = 3000 + (4.0 * B * B * W + Sv * B * W) / (0.78 * sm);
-    apply = 4.0 * B * Sv * Sv / (0.8 * sm);
+    const double eff = (rwm >= 256 && b >= 256) ? 0.88 : 0.79;
+    l = 2000 + (4.0 * B * B * W) / (eff * sm);
+    s = 2000 + (4.0 * B * B * W + Sv * B * W) / (eff * sm);
+    apply = 4.0 * B * Sv * Sv / (0.78 * sm);
   }
-  double panel(int lb) const { return 10000 + Sv * (B >= 256 ? 720 : 630) + lb * apply; }
-  double apply_part(int lb) const { return 5000 + lb * apply; }
-  double factor_part(bool split) const { return (split ? 11000 : 10000) + Sv * (B >= 256 ? 720 : 630); }
+  double factor(bool geqrt) const { return 15500 + Sv * (250 + 1.8 * B) + (geqrt ? 30 * B : 0); }
+  double panel(int lb, bool geqrt) const { return factor(geqrt) + 9000 + 1.35 * lb * apply; }
+  double apply_part(int lb) const { return 1500 + 12 * B + lb * apply; }
+  double factor_part(bool geqrt) const { return factor(geqrt); }
 };
 
 // Ranks own tile columns j == r (mod G): the panel tasks G(k), T(k,i) run on
@@ -248,12 +254,13 @@ struct DurModel {
 // column counters col[k][jl][sl] (jl = j / G).  `real_layout`: tile storage holds only the
 // rank's own columns (storage column jl); otherwise the full global grid (column j).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
-                               bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0) {
+                               bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
+                               int rwm = 128) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
   const int NPT = b / s;  // panel sub-tasks per tile: one per inner block l (one output T_l)
-  DurModel dm(b, s, w);
+  DurModel dm(b, s, w, rwm);
   TaskGen T;
   auto own = [&](int64_t j) { return (int)(j % G); };
   auto qloc = [&](int r) { return r < q ? (int)((q - r + G - 1) / G) : 0; };
@@ -275,7 +282,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
     const int ok = own(k), v = i - k + 1;
     for (int l = 0; l < NPT; ++l) {
       if (!split) {  // fused apply + factor per block (R21 without the A/F split)
-        int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l), cls);
+        int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l, kind == K_G), cls);
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
         if (v > 1) T.dep(id, PF(k, l), 1, v - 1);
         if (l > 0) T.dep(id, PF(k, l - 1), 1, v);
@@ -288,7 +295,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         T.dep(id, PF(k, l - 1), 1, v);                 // this tile's blocks < l factored
         if (v > 1) T.dep(id, PA(k, l), 1, v - 1);      // R_kk rows above block l: previous tile
       }
-      int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(l > 0), cls);
+      int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(kind == K_G), cls);
       T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
       if (v > 1) T.dep(id, PF(k, l), 1, v - 1);        // R_kk diagonal block l: previous tile
       if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part
@@ -337,11 +344,12 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
 // left of step k untouched (they are still unit vectors in rows >= k b), so the tasks
 // (k, jb < k) are skipped -- the DORGQR saving, half the work of a dense Q*B.
 static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nsl, bool trans, int workers,
-                            Sched& out, bool form_q = false) {
+                            Sched& out, bool form_q = false, int prio = PRIO_CLASS, double lat = 0.0,
+                            int rwm = 128) {
   out.nctr.assign(1, 0);
   const int K = (int)std::min(p, q);
   const int w = (b + nsl - 1) / nsl;
-  DurModel dm(b, s, w);
+  DurModel dm(b, s, w, rwm);
   TaskGen G;
   auto CNT = [&](int k, int jb, int sl) { return (int)(((int64_t)k * qb + jb) * nsl + sl); };
   out.nctr[0] = (int)((int64_t)K * qb * nsl);
@@ -374,7 +382,7 @@ static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int 
         }
       }
     }
-  if (!list_schedule(G, std::vector<int>{workers}, out)) out.topo_ok = false;
+  if (!list_schedule(G, std::vector<int>{workers}, out, prio, lat)) out.topo_ok = false;
 }
 
 struct DevSched {
@@ -399,6 +407,7 @@ struct tqr_plan {
   bool split = true;   // panel A/F split (R21)
   int prio = PRIO_BLEVEL;  // list-schedule priority (policy below)
   double lat = 4000.0;     // modelled per-task handoff latency of the list schedule (ns)
+  int orm_prio = PRIO_BLEVEL;  // list-schedule priority of apply-Q / form-Q
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -633,6 +642,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (const char* e = getenv("TQR_DEV_RW")) P->rwm = atoi(e);
   if (const char* e = getenv("TQR_DEV_PRIO")) P->prio = atoi(e);
   if (const char* e = getenv("TQR_DEV_LAT")) P->lat = atof(e);
+  if (const char* e = getenv("TQR_DEV_ORM_PRIO")) P->orm_prio = atoi(e);
   {
     const int w = exec_slice(p->b, p->s, P->rwm) * P->passes;
     P->nsl = (int)((p->b + w - 1) / w);
@@ -654,7 +664,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate)
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -877,7 +887,8 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
       return TQR_ERR_UNSUPPORTED;
     }
     Sched s;
-    build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, P->workers, s, form_q);
+    build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, P->workers, s, form_q, P->orm_prio, P->lat,
+                    P->rwm);
     if (!s.topo_ok) {
       g_err = "internal: apply-Q schedule is not topological";
       return TQR_ERR_UNSUPPORTED;
