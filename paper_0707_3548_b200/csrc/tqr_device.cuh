@@ -9,17 +9,19 @@
 // inside GEQRT/TSQRT, and apply-Q) is "apply a block reflector (Y_l, T_l) to a set of
 // columns".  Each warp owns a group of 8 columns of the target tile and keeps the
 // whole b x 8 group in DMMA accumulator registers, transposed: the group is C^T
-// (8 x b), accumulator tile t covers tile rows [8t, 8t+8).  With the column mapping
-// phi(n) below, an accumulator fragment is ALSO a valid A-operand fragment for the
-// k-step over the same rows, so W^T = C^T Y (GEMM1), W^T <- W^T T_l (T multiply) and
-// C^T -= W^T Y^T (GEMM2) chain through registers with no shuffles and no shared
-// memory round trip.  Shared memory only holds the reflector panel Y_l (b x s) and
-// T_l (s x s) in the bank-conflict-free 8x8-block swizzle swz<R>().
+// (8 x b), accumulator tile t covers tile rows [8t, 8t+8): fragment element h of lane j
+// (j = lane&3) holds row 8t + 2j + h, which is both the accumulator's column 2j+h and, for
+// the k-step h over rows {8t + 2j + h}, the A-operand index j.  So an accumulator fragment
+// is ALSO a valid A-operand fragment for GEMM1 over the same rows, and W^T = C^T Y (GEMM1),
+// W^T <- W^T T_l (T multiply) and C^T -= W^T Y^T (GEMM2) chain through registers with no
+// shuffles and no shared memory round trip.  Shared memory only holds the reflector panel
+// Y_l (b x s, swizzle swy<R>()) and T_l (s x s, swizzle swz<R>()), both bank-conflict-free.
 //
 // DMMA m8n8k4 fragment layouts (PTX ISA, mma.m8n8k4 .f64):
 //   A 8x4 : a0 = A[lane>>2][lane&3]          B 4x8 : b0 = B[lane&3][lane>>2]
 //   C 8x8 : c0,c1 = C[lane>>2][2*(lane&3) + {0,1}]
-// Accumulator column n (0..7) of an 8-wide block maps to block-local index phi(n):
+// On the reflector-column side (W, T_l) accumulator column n (0..7) of an 8-wide block maps
+// to block-local index phi(n):
 //   phi(2j+h) = 4h + j  -> fragment element h of lane (j = lane&3) holds index 4h+j,
 // which is exactly the k index (lane&3) of a k-step over indices {4h .. 4h+3}.
 #pragma once
@@ -72,12 +74,22 @@ __device__ __forceinline__ void static_for(F&& f) {
 
 // 8x8-block swizzled layout of an R x C operand (R, C multiples of 8): element (r, c) at
 // block (r/8, c/8) (blocks column-major), inside the block column-major with the row
-// index XOR-ed by (c & 6).  Conflict-free (one wavefront per half warp) for both the
-// GEMM1 pattern (rows 4h+j, cols phi(n)) and the GEMM2 pattern (rows phi(n), cols
-// 4h+j); row pairs (2m, 2m+1) stay adjacent, so 16-byte cp.async fills work.
+// index XOR-ed by (c & 6).  Conflict-free (one wavefront per half warp) for the T-multiply
+// patterns (rows 4h+j, cols phi(n)) and (rows phi(n), cols 4h+j).
 template <int R>
 __device__ __forceinline__ int swz(int r, int c) {
   return ((((c >> 3) * (R >> 3)) + (r >> 3)) << 6) + ((c & 7) << 3) + ((r & 7) ^ (c & 6));
+}
+
+// Layout of the packed reflector panels Y (R x C): the same 8x8 blocks, inside a block
+// column-major with the row index XOR-ed by xy(c) = (c bit 2) | (c bit 1) << 2.  The
+// accumulators map tile row 8t + 2j + h to fragment element h of lane j (see load_cols),
+// so GEMM1 reads rows {2j + h} x cols phi(n) and GEMM2 rows n x cols {4h + j}: both are
+// conflict-free under xy (the c & 6 swizzle above is conflict-free for the T blocks' pattern).
+__device__ __forceinline__ int xy(int c) { return ((c >> 2) & 1) | ((c & 2) << 1); }
+template <int R>
+__device__ __forceinline__ int swy(int r, int c) {
+  return ((((c >> 3) * (R >> 3)) + (r >> 3)) << 6) + ((c & 7) << 3) + ((r & 7) ^ xy(c & 7));
 }
 
 __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
@@ -166,30 +178,31 @@ __device__ __forceinline__ double warp_sum(double x) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Column-group register I/O.  acc[t][h] <-> C[8t + 4h + (lane&3)][col0 + (lane>>2)] of a
-// column-major tile with leading dimension B.  Global tile data is always read with .cg
-// (L2, never L1): tiles are rewritten by other CTAs during the persistent launch.
+// Column-group register I/O.  acc[t][h] <-> C[8t + 2(lane&3) + h][col0 + (lane>>2)] of a
+// column-major tile with leading dimension B: the two elements of a lane are adjacent rows,
+// so every access is one 16-byte LDG/STG (half the instructions and L1 wavefronts of the
+// 4h + j row map).  DMMA k-step h of 8-row block t therefore covers rows {8t + 2j + h}.
+// Global tile data is always read with .cg (L2, never L1): tiles are rewritten by other CTAs
+// during the persistent launch.
 // ---------------------------------------------------------------------------------------
 // acc covers rows [8*t0, 8*t0 + RW) of the tile.
 template <int B, int RW>
 __device__ __forceinline__ void load_cols(double (&acc)[RW / 8][2], const double* tile, int col0, int t0) {
   const int lane = threadIdx.x & 31;
-  const double* col = tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + (lane & 3);
+  const double2* col = reinterpret_cast<const double2*>(tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + 2 * (lane & 3));
 #pragma unroll
   for (int t = 0; t < RW / 8; ++t) {
-    acc[t][0] = __ldcg(col + 8 * t);
-    acc[t][1] = __ldcg(col + 8 * t + 4);
+    const double2 v = __ldcg(col + 4 * t);
+    acc[t][0] = v.x;
+    acc[t][1] = v.y;
   }
 }
 template <int B, int RW>
 __device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], double* tile, int col0, int t0) {
   const int lane = threadIdx.x & 31;
-  double* col = tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + (lane & 3);
+  double2* col = reinterpret_cast<double2*>(tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + 2 * (lane & 3));
 #pragma unroll
-  for (int t = 0; t < RW / 8; ++t) {
-    __stcg(col + 8 * t, acc[t][0]);
-    __stcg(col + 8 * t + 4, acc[t][1]);
-  }
+  for (int t = 0; t < RW / 8; ++t) __stcg(col + 4 * t, make_double2(acc[t][0], acc[t][1]));
 }
 template <int S>
 __device__ __forceinline__ void negate(double (&wn)[S / 8][2]) {
@@ -259,7 +272,7 @@ __device__ __forceinline__ void gemm1(const double (&acc)[RW / 8][2], double (&w
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int u = 0; u < S / 8; ++u) dmma(w[u], acc[t][h], Ys[swz<B>(8 * (t0 + t) + 4 * h + j, 8 * u + pn)]);
+      for (int u = 0; u < S / 8; ++u) dmma(w[u], acc[t][h], Ys[swy<B>(8 * (t0 + t) + 2 * j + h, 8 * u + pn)]);
 }
 
 // T multiply: wn = W^T T_l (QT: W <- T_l^T W) or W^T T_l^T (!QT: W <- T_l W)
@@ -286,13 +299,14 @@ __device__ __forceinline__ void t_multiply(const double (&w)[S / 8][2], double (
 template <int B, int S, int RW>
 __device__ __forceinline__ void gemm2(double (&acc)[RW / 8][2], const double (&nwn)[S / 8][2],
                                       const double* __restrict__ Ys, int t0) {
-  const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
+  const int lane = threadIdx.x & 31, j = lane & 3, g = lane >> 2;
+  // accumulator column n of block t = tile row 8t + n (fragment element h of lane j: n = 2j+h)
 #pragma unroll
   for (int u = 0; u < S / 8; ++u)
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int t = 0; t < RW / 8; ++t) dmma(acc[t], nwn[u][h], Ys[swz<B>(8 * (t0 + t) + pn, 8 * u + 4 * h + j)]);
+      for (int t = 0; t < RW / 8; ++t) dmma(acc[t], nwn[u][h], Ys[swy<B>(8 * (t0 + t) + g, 8 * u + 4 * h + j)]);
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -622,8 +636,8 @@ __device__ void gram_upper(const double* __restrict__ Ys, double* Z) {
     for (int t = 0; t < B / 8; ++t)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const double a = Ys[swz<B>(8 * t + 4 * h + j, 8 * u1 + pn)];
-        const double bb = Ys[swz<B>(8 * t + 4 * h + j, 8 * u2 + pn)];
+        const double a = Ys[swy<B>(8 * t + 2 * j + h, 8 * u1 + pn)];
+        const double bb = Ys[swy<B>(8 * t + 2 * j + h, 8 * u2 + pn)];
         if (t & 1) dmma(g1, a, bb); else dmma(g0, a, bb);
       }
     // element (m = lane>>2, n = 2j+h): Z[8u1 + phi(m)][8u2 + phi(2j+h)], phi(2j+h) = 4h+j

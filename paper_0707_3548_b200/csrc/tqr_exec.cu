@@ -72,7 +72,7 @@ __device__ __forceinline__ double* tslot_ptr(double* base, int i, int k, int p, 
 }
 // Workspace: packed copies of every reflector panel, written once by the panel
 // task that creates it, read by every update task through TMA bulk copies.
-//   Yp tile (i,k), panel l: B*S doubles at tile_ptr(Yp, i, k) + l*B*S, swz<B> layout;
+//   Yp tile (i,k), panel l: B*S doubles at tile_ptr(Yp, i, k) + l*B*S, swy<B> layout;
 //     diagonal tiles hold U_l (0 above the block, unit-lower top block, V below).
 //   Tp slot (i,k), block l: S*S doubles at tslot_ptr(Tp, i, k) + l*S*S, swz<S> layout.
 
@@ -194,7 +194,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     for (int t = 0; t < C::RW / 8; ++t)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int r = 8 * (t0 + t) + 4 * h + (lane & 3);
+        const int r = 8 * (t0 + t) + 2 * (lane & 3) + h;
         if (ts || r >= c0) P[r + col * LDP] = acc[t][h];
         else if (r >= rlo) __stcg(Ab + (size_t)(c0 + col) * B + r, acc[t][h]);
       }
@@ -220,7 +220,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
       __stcg(Ab + (size_t)(c0 + c) * B + r, v);
       y = (r - c0 == c) ? 1.0 : (r - c0 > c ? v : 0.0);
     }
-    Ys[swz<B>(r, c)] = y;
+    Ys[swy<B>(r, c)] = y;
   }
   if (ts)
     for (int e = tid; e < S * S; e += C::NT) {
@@ -657,7 +657,7 @@ __global__ void pack_factors_kernel(const double* __restrict__ A, const double* 
     const int blk = q >> 6, w = q & 63;
     const int cb = blk / (B / 8), rb = blk % (B / 8);
     const int cc = w >> 3;
-    const int c = cb * 8 + cc, r = rb * 8 + ((w & 7) ^ (c & 6));
+    const int c = cb * 8 + cc, r = rb * 8 + ((w & 7) ^ xy(cc));
     const double* At = A + tile * bb;
     const int gc = l * S + c;  // column inside the tile
     double y;

@@ -175,6 +175,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
     if (indeg[id] == 0) ready[G.t[id].rank].push(id);
   std::vector<int> order;
   order.reserve(n);
+  std::vector<double> sim_start(n, 0.0);  // development aid: TQR_DEV_SIMDUMP=<file>
   std::vector<int> free_w(nr);
   for (int r = 0; r < nr; ++r) free_w[r] = std::max(1, workers[r]);
   double now = 0.0;
@@ -185,6 +186,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
         int id = ready[r].top();
         ready[r].pop();
         order.push_back(id);
+        sim_start[id] = now;
         events.push({now + G.t[id].dur + lat, id});
         free_w[r]--;
       }
@@ -196,6 +198,15 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
     free_w[G.t[e.second].rank]++;
     for (int sidx : succ[e.second])
       if (--indeg[sidx] == 0) ready[G.t[sidx].rank].push(sidx);
+  }
+  if (const char* f = getenv("TQR_DEV_SIMDUMP")) {  // modelled start/end per task (ns), dispatch order
+    if (FILE* fp = fopen(f, "w")) {
+      for (int id : order) {
+        const auto& x = G.t[id];
+        fprintf(fp, "%d %d %d %d %d %.0f %.0f\n", x.kind, x.k, x.i, x.j, x.sl, sim_start[id], sim_start[id] + x.dur);
+      }
+      fclose(fp);
+    }
   }
   // emit per-rank records; verify the global order is topological
   std::vector<int> pos(n);

@@ -21,7 +21,7 @@ __device__ __forceinline__ void core(double (&acc)[MT][RW / 8][2], const double*
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int u = 0; u < S / 8; ++u) {
-        const double bv = Ys[swz<B>(8 * (t0 + t) + 4 * h + j, 8 * u + pn)];
+        const double bv = Ys[swy<B>(8 * (t0 + t) + 2 * j + h, 8 * u + pn)];
 #pragma unroll
         for (int m = 0; m < MT; ++m) dmma(w[m][u], acc[m][t][h], bv);
       }
@@ -45,7 +45,7 @@ __device__ __forceinline__ void core(double (&acc)[MT][RW / 8][2], const double*
     for (int h = 0; h < 2; ++h)
 #pragma unroll
       for (int t = 0; t < RW / 8; ++t) {
-        const double bv = Ys[swz<B>(8 * (t0 + t) + pn, 8 * u + 4 * h + j)];
+        const double bv = Ys[swy<B>(8 * (t0 + t) + (lane >> 2), 8 * u + 4 * h + j)];
 #pragma unroll
         for (int m = 0; m < MT; ++m) dmma(acc[m][t], wn[m][u][h], bv);
       }
