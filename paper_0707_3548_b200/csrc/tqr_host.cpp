@@ -72,6 +72,7 @@ struct TaskGen {
     double dur;
     int cls;
     int key[4];  // priority keys after cls (smaller first); default (k, i, j, sl)
+    int64_t group;  // PRIO_BLEVEL: tasks of one group share the group's highest bottom level (-1: none)
   };
   std::vector<T> t;
   int add(int kind, int k, int i, int j, int sl, int out_idx, int out_val, double dur, int cls) {
@@ -80,6 +81,7 @@ struct TaskGen {
     x.rank = 0; x.kc = k; x.flags = 0;
     x.out_idx = out_idx; x.out_val = out_val; x.ndep = 0; x.dur = dur; x.cls = cls;
     x.key[0] = k; x.key[1] = i; x.key[2] = j; x.key[3] = sl;
+    x.group = -1;
     t.push_back(x);
     return (int)t.size() - 1;
   }
@@ -110,7 +112,7 @@ static inline uint64_t ckey(int idx, int val) { return ((uint64_t)(uint32_t)idx 
 enum Prio { PRIO_CLASS = 0, PRIO_BLEVEL = 1 };
 
 static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& out, int prio = PRIO_CLASS,
-                          double lat = 0.0) {
+                          double lat = 0.0, double blq = 0.0) {
   const int n = (int)G.t.size();
   const int nr = (int)workers.size();
   std::unordered_map<uint64_t, int> producer;
@@ -154,6 +156,20 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
       for (int sidx : succ[id]) m = std::max(m, blevel[sidx] + lat);
       blevel[id] = G.t[id].dur + m;
     }
+    // grouped tasks (the updates that read one reflector panel, R22) take their
+    // group's highest bottom level, so they are dispatched together and share the panel in L2
+    std::unordered_map<int64_t, double> gmax;
+    for (int id = 0; id < n; ++id)
+      if (G.t[id].group >= 0) {
+        double& g = gmax[G.t[id].group];
+        g = std::max(g, blevel[id]);
+      }
+    for (int id = 0; id < n; ++id)
+      if (G.t[id].group >= 0) blevel[id] = gmax[G.t[id].group];
+    // quantised (blq > 0): tasks within one quantum keep the (k, i, j, slice) order, so the
+    // updates sharing one reflector panel (k, i) run together and reuse it from L2
+    if (blq > 0.0)
+      for (double& x : blevel) x = std::floor(x / blq);
   }
   auto prio_less = [&](int a, int b) {  // true if a has LOWER priority than b (for max-heap)
     const auto &x = G.t[a], &y = G.t[b];
@@ -266,7 +282,7 @@ struct DurModel {
 // rank's own columns (storage column jl); otherwise the full global grid (column j).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
-                               int rwm = 128) {
+                               int rwm = 128, double blq = 0.0, bool group = false) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -322,6 +338,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         int id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
         T.t[id].rank = own(j); T.t[id].kc = scol(k);
         T.t[id].key[2] = j;
+        if (group && j > k + 1) T.t[id].group = (int64_t)k * p + k;
         T.dep(id, PF(k, NPT - 1), 1, 1);
         if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, 2);
         out.counts[2]++;
@@ -336,6 +353,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
           int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
+          if (group && j > k + 1) T.t[id].group = (int64_t)k * p + i;
           T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
           T.dep(id, COL(k, j, sl), 1, i - k);
           if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
@@ -343,7 +361,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         }
     }
   }
-  if (!list_schedule(T, workers, out, prio, lat)) out.topo_ok = false;
+  if (!list_schedule(T, workers, out, prio, lat, blq)) out.topo_ok = false;
 }
 
 // apply-Q^T (trans) or apply-Q to a tile-major B with qb tile columns.
@@ -419,6 +437,8 @@ struct tqr_plan {
   int prio = PRIO_BLEVEL;  // list-schedule priority (policy below)
   double lat = 4000.0;     // modelled per-task handoff latency of the list schedule (ns)
   int orm_prio = PRIO_BLEVEL;  // list-schedule priority of apply-Q / form-Q
+  double blq = 0.0;            // bottom-level quantum (ns) of the factorization schedule
+  bool group = false;          // group the updates of one reflector panel (R22)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -654,6 +674,8 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (const char* e = getenv("TQR_DEV_PRIO")) P->prio = atoi(e);
   if (const char* e = getenv("TQR_DEV_LAT")) P->lat = atof(e);
   if (const char* e = getenv("TQR_DEV_ORM_PRIO")) P->orm_prio = atoi(e);
+  if (const char* e = getenv("TQR_DEV_BLQ")) P->blq = atof(e);
+  if (const char* e = getenv("TQR_DEV_GROUP")) P->group = atoi(e) != 0;
   {
     const int w = exec_slice(p->b, p->s, P->rwm) * P->passes;
     P->nsl = (int)((p->b + w - 1) / w);
@@ -675,7 +697,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate)
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
