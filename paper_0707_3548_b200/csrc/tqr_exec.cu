@@ -129,7 +129,15 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
     issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);
     if (nb > 1) issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
   }
-  if (active) load_cols<B, C::RW>(acc, Ct, cg0, t0);
+  if (active) {
+    load_cols<B, C::RW>(acc, Ct, cg0, t0);
+  } else {
+    // a def on every path: otherwise acc stays live (for the compiler) across the panel code
+    // of a panel task, which then rematerialises its indices (RW = 256: +40% instructions
+    // in the column loop)
+#pragma unroll
+    for (int t = 0; t < C::RW / 8; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+  }
   if (nb <= 0) return;
   if (top_owner) c1_fetch<B, S>(c1s0, C1, (DESC ? nb - 1 : lb0) * S, cg0);
   __syncthreads();
