@@ -343,8 +343,8 @@ def main():
     try:
         tr = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get(args.config)
         if tr and world == 1:
-            traffic = {"bytes_per_launch": tr["bytes"], "source": tr["source"],
-                       "algorithmic_flop_per_byte": flops / tr["bytes"]}
+            traffic = {"bytes": tr["bytes"], "source": tr["source"],
+                       "flop_per_dram_byte": flops / tr["bytes"]}
     except (OSError, ValueError):
         pass
     line = {
@@ -362,7 +362,10 @@ def main():
         "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
         "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic and traffic["bytes"],
+                     "traffic_source": traffic and (f"dram__bytes_read.sum + dram__bytes_write.sum per launch, "
+                                                    f"{traffic['source']} ({traffic['flop_per_dram_byte']:.1f} "
+                                                    f"flop per DRAM byte)"),
                      "kernel": f"exec_kernel<{b},{s},mode 0> (tqr_geqrf)", "kernel_ms": kern_ms,
                      "flops_per_launch": flops / world,
                      "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt); "
