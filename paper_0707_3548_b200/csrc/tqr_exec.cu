@@ -276,8 +276,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
 // updates (+ its C1 slice), or the tile a panel task factors, and its first two packed
 // reflector blocks.  Safe before the task's dependencies hold (L2 is coherent).
 template <int B, int S, int SO, int RWM, int MODE>
-__device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, const double* Yme, int p,
-                                              int tsl) {
+__device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, const double* Yme, int p) {
   using C = Cfg<B, S, RWM>;
   const int kind = q[0], k = q[1], i = q[2], j = q[3], sl = q[4], kc = q[7];
   if (MODE == 0 && (kind == K_G || kind == K_T)) {
@@ -286,7 +285,7 @@ __device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, 
   }
   const bool lkind = kind == K_L || kind == K_LQT || kind == K_LQ;
   double* Bt = MODE == 0 ? R.A : R.Bt;
-  const size_t off = (size_t)sl * tsl * B;
+  const size_t off = (size_t)sl * C::SLICE * B;
   const unsigned bytes = (unsigned)(C::SLICE * B * 8);  // the first pass's columns
   prefetch_l2(tile_ptr(Bt, lkind ? k : i, j, p, B) + off, bytes);
   if (!lkind) prefetch_l2(tile_ptr(Bt, k, j, p, B) + off, bytes);
@@ -377,7 +376,8 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
     if (tid == 0) {
       bool bad = kind < 0 || kind > 7 || k < 0 || k >= a.p || i < k || i >= a.p || kc < 0 || kc >= a.qcols ||
                  j < 0 || j >= a.qcols || sl < -1 || sl >= (kind >= K_L ? a.nsl : B / SO) ||
-                 s_task[5] < 0 || s_task[5] >= a.nctr || (MODE == 0) != (kind <= K_S);
+                 (kind >= K_L && ((s_task[15] & 0xFF) < 1 || sl + (s_task[15] & 0xFF) > a.nsl)) ||
+                 s_task[5] < 0 || s_task[5] + ((s_task[15] >> 8) & 0xFF) > a.nctr || (MODE == 0) != (kind <= K_S);
       for (int d = 0; d < TASK_NDEP; ++d) {
         const int code = s_task[8 + 2 * d], cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
         if (cnt && (idx + cnt > a.nctr)) bad = true;
@@ -407,11 +407,12 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
       const double* Ypt = Yme + yoff;
       const double* Tps = Tme + toff;
       // panel task: inner blocks [sub0, sub1) of the tile (one output T block per task, or the
-      // whole tile when sl < 0); update task: TSL / SLICE register passes of its slice
+      // whole tile when sl < 0); update task: np register passes from pass sl
       constexpr int SPT = SO / S;  // internal blocks per output T block
       const int sub0 = panel ? (sl < 0 ? 0 : sl * SPT) : 0;
-      const int tsl = a.passes * Cfg<B, S, RWM>::SLICE;  // columns per update task
-      const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : a.passes;
+      // update tasks: passes [sl, sl + np) of SLICE columns each (record [15] = np | ocnt << 8)
+      const int np = s_task[15] & 0xFF;
+      const int nsub = panel ? (sl < 0 ? NL : sub0 + SPT) : np;
       // panel split (R21): flags bit 1 = apply part only (left-looking update of the
       // block columns with this tile's earlier blocks, stored back), bit 2 = factor part only
       const bool a_part = panel && (s_task[14] & 2), f_part = panel && (s_task[14] & 4);
@@ -430,7 +431,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         } else {
           C1 = lkind ? nullptr : tile_ptr(Bt, k, j, p, B);
           Ct = lkind ? tile_ptr(Bt, k, j, p, B) : tile_ptr(Bt, i, j, p, B);
-          col0 = sl * tsl + sub * Cfg<B, S, RWM>::SLICE;  // (update tasks: sl >= 0)
+          col0 = (sl + sub) * Cfg<B, S, RWM>::SLICE;  // (update tasks: sl >= 0)
           nb = NL;
           gact = (B - col0) / 8 < Cfg<B, S, RWM>::GPS ? (B - col0) / 8 : Cfg<B, S, RWM>::GPS;
         }
@@ -452,7 +453,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
           }
           if (li == l0 + 2 && rec_for == next_tk && next_tk < R.ntasks) {
             cp_async_wait<0>();
-            prefetch_task<B, S, SO, RWM, MODE>(s_next, R, Yme, p, tsl);
+            prefetch_task<B, S, SO, RWM, MODE>(s_next, R, Yme, p);
           }
         };
         update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf);
@@ -488,7 +489,8 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
           for (int g = 0; g < a.nranks; ++g) st_release(a.ctr[g] + oidx, oval);
         }
       } else {
-        st_release(R.ctr + oidx, oval);
+        const int ocnt = (s_task[15] >> 8) & 0xFF;  // update tasks: one counter per pass
+        for (int x = 0; x < (ocnt > 0 ? ocnt : 1); ++x) st_release(R.ctr + oidx + x, oval);
       }
       PH_MARK(3);
       if (R.trace) {

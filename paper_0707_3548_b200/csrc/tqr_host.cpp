@@ -73,6 +73,7 @@ struct TaskGen {
     int cls;
     int key[4];  // priority keys after cls (smaller first); default (k, i, j, sl)
     int64_t group;  // PRIO_BLEVEL: tasks of one group share the group's highest bottom level (-1: none)
+    int np, ocnt;   // update tasks: register passes; consecutive out counters published (>= 1)
   };
   std::vector<T> t;
   int add(int kind, int k, int i, int j, int sl, int out_idx, int out_val, double dur, int cls) {
@@ -82,6 +83,7 @@ struct TaskGen {
     x.out_idx = out_idx; x.out_val = out_val; x.ndep = 0; x.dur = dur; x.cls = cls;
     x.key[0] = k; x.key[1] = i; x.key[2] = j; x.key[3] = sl;
     x.group = -1;
+    x.np = 1; x.ocnt = 1;
     t.push_back(x);
     return (int)t.size() - 1;
   }
@@ -123,7 +125,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
     if (x.flags & 1)
       for (int r = 0; r < nr; ++r) producer[pkey(r, x.out_idx, x.out_val)] = id;
     else
-      producer[pkey(x.rank, x.out_idx, x.out_val)] = id;
+      for (int c = 0; c < x.ocnt; ++c) producer[pkey(x.rank, x.out_idx + c, x.out_val)] = id;
   }
   std::vector<int> indeg(n, 0);
   std::vector<std::vector<int>> succ(n);
@@ -242,6 +244,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
       q[9 + 2 * d] = x.dep_val[d];
     }
     q[14] = x.flags;
+    q[15] = x.np | (x.ocnt << 8);
   }
   for (int id = 0; id < n; ++id)
     for (int sidx : succ[id])
@@ -280,14 +283,21 @@ struct DurModel {
 // Counter layout per rank: panel[k] at k (K entries, a copy on every rank), then the local
 // column counters col[k][jl][sl] (jl = j / G).  `real_layout`: tile storage holds only the
 // rank's own columns (storage column jl); otherwise the full global grid (column j).
+// nsl: column slices per tile (one register pass each; the unit of the progress counters);
+// np: register passes per update task (np | nsl); fine: 1 = the updates of the lookahead
+// column k+1 run as 1-pass tasks (they feed panel k+1: a shorter chain link), 2 = also every
+// update of the steps whose default-granularity task count is below two waves (the tail).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
-                               int rwm = 128, double blq = 0.0, bool group = false) {
+                               int rwm = 128, double blq = 0.0, bool group = false, int np = 1, int fine = 0) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
   const int NPT = b / s;  // panel sub-tasks per tile: one per inner block l (one output T_l)
-  DurModel dm(b, s, w, rwm);
+  if (np < 1 || nsl % np != 0) np = 1;
+  DurModel dm(b, s, w * np, rwm), dmf(b, s, w, rwm);
+  int64_t wtot = 0;
+  for (int x : workers) wtot += x;
   TaskGen T;
   auto own = [&](int64_t j) { return (int)(j % G); };
   auto qloc = [&](int r) { return r < q ? (int)((q - r + G - 1) / G) : 0; };
@@ -332,16 +342,21 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   for (int k = 0; k < K; ++k) {
     panel(K_G, k, k, 0);
     out.counts[0]++;
+    // task granularity of step k's updates (R23)
+    const bool tail = fine >= 2 && (int64_t)(q - k - 1) * (p - k) * (nsl / np) < 2 * wtot;
+    auto npj = [&](int64_t j) { return (fine >= 1 && j == k + 1) || tail ? 1 : np; };
     for (int j = k + 1; j < q; ++j)
-      for (int sl = 0; sl < nsl; ++sl) {
+      for (int sl = 0; sl < nsl; sl += npj(j)) {
+        const int n_ = npj(j);
         // lookahead (R10): updates of column k+1 feed panel k+1 -> critical path
-        int id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, dm.l, j == k + 1 ? 1 : 2);
+        int id = T.add(K_L, k, k, scol(j), sl, COL(k, j, sl), 1, (n_ == np ? dm : dmf).l, j == k + 1 ? 1 : 2);
         T.t[id].rank = own(j); T.t[id].kc = scol(k);
         T.t[id].key[2] = j;
+        T.t[id].np = n_; T.t[id].ocnt = n_;
         if (group && j > k + 1) T.t[id].group = (int64_t)k * p + k;
         T.dep(id, PF(k, NPT - 1), 1, 1);
-        if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, 2);
-        out.counts[2]++;
+        if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, 2);
+        out.counts[2] += n_;  // counted per register pass (column slice)
       }
     for (int i = k + 1; i < p; ++i) {
       // TSQRT(k,i) block l touches only column block l of R_kk (and tile (i,k)): a wavefront
@@ -349,15 +364,18 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
       panel(K_T, k, i, 1);
       out.counts[1]++;
       for (int j = k + 1; j < q; ++j)
-        for (int sl = 0; sl < nsl; ++sl) {
-          int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, dm.s, j == k + 1 ? 1 : 3);
+        for (int sl = 0; sl < nsl; sl += npj(j)) {
+          const int n_ = npj(j);
+          int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, (n_ == np ? dm : dmf).s,
+                         j == k + 1 ? 1 : 3);
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
+          T.t[id].np = n_; T.t[id].ocnt = n_;
           if (group && j > k + 1) T.t[id].group = (int64_t)k * p + i;
           T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
-          T.dep(id, COL(k, j, sl), 1, i - k);
-          if (k > 0) T.dep(id, COL(k - 1, j, sl), 1, i - k + 2);
-          out.counts[3]++;
+          T.dep(id, COL(k, j, sl), n_, i - k);
+          if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, i - k + 2);
+          out.counts[3] += n_;
         }
     }
   }
@@ -372,11 +390,14 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
 // form_q (Q applied to [I; 0], tqr_orgqr): backward accumulation leaves the tile columns
 // left of step k untouched (they are still unit vectors in rows >= k b), so the tasks
 // (k, jb < k) are skipped -- the DORGQR saving, half the work of a dense Q*B.
-static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nsl, bool trans, int workers,
+// nslf: column slices (register passes) per tile; tasks cover np of them (counters per task slice).
+static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nslf, bool trans, int workers,
                             Sched& out, bool form_q = false, int prio = PRIO_CLASS, double lat = 0.0,
-                            int rwm = 128) {
+                            int rwm = 128, int np = 1) {
   out.nctr.assign(1, 0);
   const int K = (int)std::min(p, q);
+  if (np < 1 || nslf % np != 0) np = 1;
+  const int nsl = nslf / np;
   const int w = (b + nsl - 1) / nsl;
   DurModel dm(b, s, w, rwm);
   TaskGen G;
@@ -411,6 +432,10 @@ static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int 
         }
       }
     }
+  for (auto& x : G.t) {  // record: first register pass (column slice of width b / nslf), passes
+    x.np = np;
+    x.sl *= np;
+  }
   if (!list_schedule(G, std::vector<int>{workers}, out, prio, lat)) out.topo_ok = false;
 }
 
@@ -432,6 +457,7 @@ struct tqr_plan {
   int64_t p, q, K;
   int nsl, workers;
   int passes = 1;      // register passes per update task (policy below)
+  int fine = 2;        // 1-pass tasks for the lookahead column (1) and the tail steps (2) (R23)
   int rwm = 128;       // rows-per-warp variant of the executor (policy below)
   bool split = true;   // panel A/F split (R21)
   int prio = PRIO_BLEVEL;  // list-schedule priority (policy below)
@@ -532,7 +558,6 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
   a.p = (int)P->p;
   a.base = base;
   a.sys = P->real ? 1 : 0;
-  a.passes = P->passes;
   a.nctr = P->nctr_max;
   a.qcols = (int)std::max<int64_t>(qloc_of(P, P->me), Bt ? (int64_t)(1 << 30) : 0);  // Bt width unknown here
   a.nsl = P->nsl;
@@ -677,9 +702,11 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (const char* e = getenv("TQR_DEV_BLQ")) P->blq = atof(e);
   if (const char* e = getenv("TQR_DEV_GROUP")) P->group = atoi(e) != 0;
   {
-    const int w = exec_slice(p->b, p->s, P->rwm) * P->passes;
+    const int w = exec_slice(p->b, p->s, P->rwm);  // one register pass
     P->nsl = (int)((p->b + w - 1) / w);
+    if (P->nsl % P->passes != 0) P->passes = 1;
   }
+  if (const char* e = getenv("TQR_DEV_FINE")) P->fine = atoi(e);
   P->st = (cudaStream_t)p->stream;
   P->workers = exec_max_ctas(p->b, p->s, P->rwm, p->device);
   if (P->workers < P->nloc) {
@@ -697,7 +724,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate)
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -921,7 +948,7 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
     }
     Sched s;
     build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, P->workers, s, form_q, P->orm_prio, P->lat,
-                    P->rwm);
+                    P->rwm, P->passes);
     if (!s.topo_ok) {
       g_err = "internal: apply-Q schedule is not topological";
       return TQR_ERR_UNSUPPORTED;
@@ -1003,9 +1030,11 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   if (nslice < 1) return bad_arg(3, "nslice < 1");
   if (workers < 1) return bad_arg(4, "workers < 1");
   if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
+  // both panel forms, both priorities and every task-granularity policy are exercised by the
+  // inspected shapes
   build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1,
-                     (p + q) % 2 == 0, s, p % 2 == 0 ? PRIO_BLEVEL : PRIO_CLASS,
-                     4000.0);  // both panel forms and both priorities are exercised by the inspected shapes
+                     (p + q) % 2 == 0, s, p % 2 == 0 ? PRIO_BLEVEL : PRIO_CLASS, 4000.0, 128, 0.0, false,
+                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3));
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
@@ -1088,7 +1117,9 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
     const bool lkind = kind == 2 || kind == 4 || kind == 6;
     q[2] = (kind == 0 || lkind) ? q[1] : i;
     q[3] = (kind == 0 || kind == 1) ? q[1] : j;
-    q[4] = (kind == 0 || kind == 1) ? -1 : (int)(t % P->nsl);  // -1: a panel task over the whole tile
+    // -1: a panel task over the whole tile; update tasks: first register pass, P->passes passes
+    q[4] = (kind == 0 || kind == 1) ? -1 : (int)(t % (P->nsl / P->passes)) * P->passes;
+    q[15] = P->passes | (1 << 8);
     q[5] = 0;
     q[6] = 1;
     q[7] = q[1];

@@ -26,7 +26,9 @@ enum Kind : int {
 //   [8 + 2d], [9 + 2d], d = 0..2: dependency d = (index | count << 24, value):
 //       wait until ctr[index + x] >= base + value for x in [0, count); count 0 = none
 //   [14] flags: bit 0 = publish the out counter on every rank (panel progress, multi-GPU)
-//   [15] unused
+//   [15] update tasks: np | ocnt << 8 -- register passes [slice, slice + np) (slice = [4], in
+//        units of SLICE columns), and ocnt consecutive out counters [5] .. [5] + ocnt - 1 set
+//        to [6] on completion (0 / panel tasks: one)
 // Counter values of one factorization are base + v with v in [1, p + 1]; the base grows by
 // (p + 2) per call, so counters are never reset (no cross-rank reset race).
 constexpr int TASK_INTS = 16;
@@ -58,7 +60,6 @@ struct ExecArgs {
   int p;                    // row tiles (same for A and Bt)
   int base;                 // counter generation base of this call
   int sys;                  // 1: peers on other GPUs (system-scope acquire/release)
-  int passes;               // register passes (SLICE columns each) per LARFB/SSRFB task
   int nctr;                 // counters per rank (TQR_CHECKS builds: bounds of every counter access)
   int qcols;                // storage tile columns of A (and of Bt in apply-Q) (TQR_CHECKS)
   int nsl;                  // update tasks per tile (TQR_CHECKS)
@@ -73,7 +74,7 @@ cudaError_t launch_exec(int b, int s, int mode, int rwm, const ExecArgs& a, int 
 int exec_max_ctas(int b, int s, int rwm, int device);
 bool exec_supported(int b, int s);
 // Columns of one register-resident pass of a LARFB/SSRFB task for (b, s) (0 if no instance);
-// a task covers `passes` consecutive passes (host policy, ExecArgs::passes).
+// a task covers np consecutive passes (host policy, task record [15]).
 int exec_slice(int b, int s, int rwm);
 // Internal inner block SI of the executor for (b, s) (== s except b = 512).
 int exec_inner(int b, int s);

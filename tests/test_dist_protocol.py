@@ -30,10 +30,19 @@ def _global_j(rec, G, r):
     return rec[3] * G + r if G > 1 else rec[3]
 
 
-def _task_key(rec, G, r):
+def _task_keys(rec, G, r):
+    """The DAG nodes a record covers: update tasks at register-pass granularity (a task covers
+    passes [rec[4], rec[4] + np), np = rec[15] & 0xFF; the per-step task granularity is a
+    scheduling policy that may differ between a 1-rank and a G-rank job)."""
     kind = int(rec[0])
-    j = _global_j(rec, G, r) if kind in (K_L, K_S) else int(rec[1])
-    return (kind, int(rec[1]), int(rec[2]), int(j), int(rec[4]))
+    if kind in (K_L, K_S):
+        j, npass = _global_j(rec, G, r), max(1, int(rec[15]) & 0xFF)
+        return [(kind, int(rec[1]), int(rec[2]), int(j), int(rec[4]) + x) for x in range(npass)]
+    return [(kind, int(rec[1]), int(rec[2]), int(rec[1]), int(rec[4]))]
+
+
+def _out_count(rec):
+    return max(1, (int(rec[15]) >> 8) & 0xFF)
 
 
 def _deps(rec):
@@ -72,7 +81,8 @@ class RankSim:
             rec = self.recs[t]
             if self.ready(rec):
                 self.held.remove(t)
-                self.publish(int(rec[5]), int(rec[6]))
+                for x in range(_out_count(rec)):  # update tasks: one counter per register pass
+                    self.publish(int(rec[5]) + x, int(rec[6]))
                 if rec[14] & 1:
                     self.published.append((int(rec[5]), int(rec[6])))
                 self.done += 1
@@ -87,7 +97,7 @@ class RankSim:
                                                (20, 20, 2, 2, 4), (3, 2, 1, 8, 1), (30, 4, 2, 4, 2)])
 def test_partition_and_replay(L, p, q, nsl, G, workers):
     single, _ = L.schedule_records(p, q, nsl, workers, 1, 0)
-    ref = sorted(_task_key(r, 1, 0) for r in single)
+    ref = sorted(key for rec in single for key in _task_keys(rec, 1, 0))
     sims, keys = [], []
     for r in range(G):
         recs, nctr = L.schedule_records(p, q, nsl, workers, G, r)
@@ -101,7 +111,7 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
                 assert rec[14] in (1, 2, 1 | 4)
             else:
                 assert _global_j(rec, G, r) % G == r and not rec[14] & 1  # update on owner(j), local
-            keys.append(_task_key(rec, G, r))
+            keys.extend(_task_keys(rec, G, r))
         sims.append(RankSim(recs, nctr, workers))
     assert sorted(keys) == ref, "the ranks' tasks are not exactly the single-GPU DAG"
     # in-process replay; panel publications reach the other ranks' counter copies at once
