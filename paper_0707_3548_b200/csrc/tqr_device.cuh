@@ -204,11 +204,6 @@ __device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], doubl
 #pragma unroll
   for (int t = 0; t < RW / 8; ++t) __stcg(col + 4 * t, make_double2(acc[t][0], acc[t][1]));
 }
-template <int S>
-__device__ __forceinline__ void negate(double (&wn)[S / 8][2]) {
-#pragma unroll
-  for (int u = 0; u < S / 8; ++u) { wn[u][0] = -wn[u][0]; wn[u][1] = -wn[u][1]; }
-}
 // w[u][h] <-> C1[row0 + 8u + 4h + (lane&3)][col0 + (lane>>2)]  (s rows of the "top" tile)
 template <int B, int S>
 __device__ __forceinline__ void load_top(double (&w)[S / 8][2], const double* tile, int row0, int col0) {
@@ -240,18 +235,6 @@ __device__ __forceinline__ void frag_put(double* st, const double (&w)[S / 8][2]
 #pragma unroll
   for (int u = 0; u < S / 8; ++u) { st[(2 * u) * 32 + lane] = w[u][0]; st[(2 * u + 1) * 32 + lane] = w[u][1]; }
 }
-// C1 <- C1 - W with C1 from its shared-memory stage (c1_idx layout)
-template <int B, int S>
-__device__ __forceinline__ void store_top_minus(const double* c1s, const double (&wn)[S / 8][2], double* tile,
-                                                int row0, int col0) {
-  const int lane = threadIdx.x & 31;
-  double* col = tile + (size_t)(col0 + (lane >> 2)) * B + row0 + (lane & 3);
-#pragma unroll
-  for (int u = 0; u < S / 8; ++u) {
-    __stcg(col + 8 * u, c1s[c1_idx<S>(u, 0, lane)] - wn[u][0]);
-    __stcg(col + 8 * u + 4, c1s[c1_idx<S>(u, 1, lane)] - wn[u][1]);
-  }
-}
 
 // ---------------------------------------------------------------------------------------
 // Block-reflector apply on one warp's column group (PAPER.md:395-402 DLARFB and
@@ -275,38 +258,65 @@ __device__ __forceinline__ void gemm1(const double (&acc)[RW / 8][2], double (&w
       for (int u = 0; u < S / 8; ++u) dmma(w[u], acc[t][h], Ys[swy<B>(8 * (t0 + t) + 2 * j + h, 8 * u + pn)]);
 }
 
-// T multiply: wn = W^T T_l (QT: W <- T_l^T W) or W^T T_l^T (!QT: W <- T_l W)
-template <int S, bool QT>
-__device__ __forceinline__ void t_multiply(const double (&w)[S / 8][2], double (&wn)[S / 8][2],
-                                           const double* __restrict__ Ts) {
-  const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2);
+// Fused T multiply + C1 store + GEMM2, software-pipelined.  QT (W <- T_l^T W): column block
+// u2 of W^T T_l needs only w[0..u2] (T_l upper triangular) and GEMM2's k-steps over u = u2
+// need only that block, so blocks are finished in the order u2 = 0, 1, ... and block u2+1's
+// T-multiply DMMAs are issued between GEMM2's DMMAs for u2 instead of draining the pipe
+// before GEMM2 starts (per block and warp: a chain of up to 2 s/8 dependent DMMAs that both
+// warps of an SMSP would otherwise wait out together).  !QT (W <- T_l W, apply Q): block u2
+// needs w[u2..], so the order is u2 = NU-1, ..., 0.  Each block's T products are summed over
+// (u, h) ascending; GEMM2 (C^T += (-W)^T Y^T, accumulators chained per row block t) runs its
+// k-steps in the block order.
+template <int B, int S, int RW, bool QT>
+__device__ __forceinline__ void tmul_gemm2(double (&acc)[RW / 8][2], const double (&w)[S / 8][2],
+                                           const double* __restrict__ Ys, const double* __restrict__ Ts,
+                                           const double* c1s, double* top, int row0, int col0, int t0,
+                                           bool store_c1) {
+  const int lane = threadIdx.x & 31, j = lane & 3, pn = phi(lane >> 2), g = lane >> 2;
+  constexpr int NU = S / 8, TT = RW / 8;
+  double wn[NU][2];
 #pragma unroll
-  for (int u = 0; u < S / 8; ++u) { wn[u][0] = 0.0; wn[u][1] = 0.0; }
+  for (int u = 0; u < NU; ++u) { wn[u][0] = 0.0; wn[u][1] = 0.0; }
+  // x-th block finished (x = 0 .. NU-1) and its T-multiply step q: (u, h)
+  auto blk = [](int x) { return QT ? x : NU - 1 - x; };
+  auto nsteps = [](int u2) { return QT ? 2 * (u2 + 1) : 2 * (NU - u2); };
+  auto tmul_step = [&](int u2, int q) __attribute__((always_inline)) {
+    const int u = (QT ? 0 : u2) + (q >> 1), h = q & 1;
+    const double tv = QT ? Ts[swz<S>(8 * u + 4 * h + j, 8 * u2 + pn)] : Ts[swz<S>(8 * u2 + pn, 8 * u + 4 * h + j)];
+    dmma(wn[u2], w[u][h], tv);
+  };
+  auto finish = [&](int u2) __attribute__((always_inline)) {  // C1 -= W (block u2), negate
+    if (store_c1) {
+      double* col = top + (size_t)(col0 + g) * B + row0 + j;
+      __stcg(col + 8 * u2, c1s[c1_idx<S>(u2, 0, lane)] - wn[u2][0]);
+      __stcg(col + 8 * u2 + 4, c1s[c1_idx<S>(u2, 1, lane)] - wn[u2][1]);
+    }
+    wn[u2][0] = -wn[u2][0];
+    wn[u2][1] = -wn[u2][1];
+  };
 #pragma unroll
-  for (int u = 0; u < S / 8; ++u)
+  for (int q = 0; q < nsteps(blk(0)); ++q) tmul_step(blk(0), q);
+  finish(blk(0));
+#pragma unroll
+  for (int x = 0; x < NU; ++x) {
+    const int u = blk(x);
+    const bool more = x + 1 < NU;
+    const int un = more ? blk(x + 1) : 0, nn = more ? nsteps(un) : 0;
+    // GEMM2 k-steps (u, h) over all row blocks t; the next block's T-multiply DMMAs are
+    // spread over them (one per 4 GEMM2 DMMAs), the rest (TT/4 < nn) issued after
 #pragma unroll
     for (int h = 0; h < 2; ++h)
 #pragma unroll
-      for (int u2 = 0; u2 < S / 8; ++u2) {
-        if (QT ? (u2 < u) : (u2 > u)) continue;  // T_l upper triangular
-        const double tv = QT ? Ts[swz<S>(8 * u + 4 * h + j, 8 * u2 + pn)] : Ts[swz<S>(8 * u2 + pn, 8 * u + 4 * h + j)];
-        dmma(wn[u2], w[u][h], tv);
+      for (int t = 0; t < TT; ++t) {
+        dmma(acc[t], wn[u][h], Ys[swy<B>(8 * (t0 + t) + g, 8 * u + 4 * h + j)]);
+        if (more && h == 0 && (t & 3) == 3 && (t >> 2) < nn) tmul_step(un, t >> 2);
       }
-}
-
-// GEMM2: C^T[8 x RW] += nwn^T[8 x S] * Y^T[S x RW], nwn = -W.  Loop order (u, h) outer so
-// consecutive DMMAs hit different accumulators (dependency distance RW/8).
-template <int B, int S, int RW>
-__device__ __forceinline__ void gemm2(double (&acc)[RW / 8][2], const double (&nwn)[S / 8][2],
-                                      const double* __restrict__ Ys, int t0) {
-  const int lane = threadIdx.x & 31, j = lane & 3, g = lane >> 2;
-  // accumulator column n of block t = tile row 8t + n (fragment element h of lane j: n = 2j+h)
+    if (more) {
 #pragma unroll
-  for (int u = 0; u < S / 8; ++u)
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int t = 0; t < RW / 8; ++t) dmma(acc[t], nwn[u][h], Ys[swy<B>(8 * (t0 + t) + g, 8 * u + 4 * h + j)]);
+      for (int q = TT / 4; q < nn; ++q) tmul_step(un, q);
+      finish(un);
+    }
+  }
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -339,7 +349,7 @@ __device__ __forceinline__ void group_apply(double (&acc)[RW / 8][2], const doub
   const int lane = threadIdx.x & 31;
   const bool HAS_C1 = top != nullptr;  // SSRFB / TSQRT type: C1 block staged in c1s
   constexpr int XW = (S / 8) * 2 * 32;
-  double w[S / 8][2], wn[S / 8][2];
+  double w[S / 8][2];
 #pragma unroll
   for (int u = 0; u < S / 8; ++u) {
     w[u][0] = (HAS_C1 && rpart == 0) ? c1s[c1_idx<S>(u, 0, lane)] : 0.0;
@@ -360,10 +370,7 @@ __device__ __forceinline__ void group_apply(double (&acc)[RW / 8][2], const doub
       }
     if (BAR2) named_bar(1 + gi, 32 * RS);
   }
-  t_multiply<S, QT>(w, wn, Ts);
-  if (HAS_C1 && rpart == 0) store_top_minus<B, S>(c1s, wn, top, row0, col0);
-  negate<S>(wn);
-  gemm2<B, S, RW>(acc, wn, Ys, t0);
+  tmul_gemm2<B, S, RW, QT>(acc, w, Ys, Ts, c1s, top, row0, col0, t0, HAS_C1 && rpart == 0);
 }
 
 // Warp-local cp.async of one group's C1 block (rows [row0, row0+S), 8 columns from col0)
