@@ -171,6 +171,43 @@ __device__ __forceinline__ unsigned smid() {
   return r;
 }
 
+// Sums of N values (N a power of two <= 32) over the 32 lanes, every lane receiving all N sums,
+// with fewer shuffles than N butterflies (5N): a reduce-scatter over lane bits 4, 3, ... (each
+// level halves the values a lane carries), a butterfly over the remaining bits, and N
+// broadcasts -- 2N - 1 + (5 - log2 N) shuffles (N = 4: 10 instead of 20).  The panel's
+// off-critical-path column updates are shuffle-bound (they share the SM with the critical
+// column's reductions).  Every sum is formed in one fixed order on every lane (deterministic).
+template <int N>
+__device__ __forceinline__ void warp_allreduce(double (&v)[N]) {
+  static_assert(N >= 1 && N <= 32 && (N & (N - 1)) == 0, "N: power of two");
+  const int lane = threadIdx.x & 31;
+  constexpr int K = N == 1 ? 0 : N == 2 ? 1 : N == 4 ? 2 : N == 8 ? 3 : N == 16 ? 4 : 5;
+  double r[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) r[i] = v[i];
+#pragma unroll
+  for (int lv = 0; lv < K; ++lv) {  // level lv: lane bit (4 - lv) selects the half kept
+    const int o = 16 >> lv, half = N >> (lv + 1);
+    const bool up = lane & o;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = up ? r[i] : r[i + half];
+      const double keep = up ? r[i + half] : r[i];
+      r[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = 16 >> K; o > 0; o >>= 1) r[0] += __shfl_xor_sync(0xffffffffu, r[0], o);
+  // lane L now holds sum c with bit (K-1-lv) of c = lane bit (4-lv)
+#pragma unroll
+  for (int c = 0; c < N; ++c) {
+    int src = 0;
+#pragma unroll
+    for (int lv = 0; lv < K; ++lv) src |= ((c >> (K - 1 - lv)) & 1) << (4 - lv);
+    v[c] = __shfl_sync(0xffffffffu, r[0], src);
+  }
+}
+
 __device__ __forceinline__ double warp_sum(double x) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
@@ -578,6 +615,9 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       });
     }
     // the warp's other columns c > jj+1: dots, one interleaved butterfly, register updates
+#ifdef TQR_PF_SKIP_NONCRIT  // tools/panel_bench.cu timing experiment only (wrong results)
+    continue;
+#endif
     double dc[NC];
 #pragma unroll
     for (int ci = 0; ci < NC; ++ci) {
@@ -594,9 +634,7 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       dc[ci] = d0 + d1;
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1)
-#pragma unroll
-      for (int ci = 0; ci < NC; ++ci) dc[ci] += __shfl_xor_sync(0xffffffffu, dc[ci], o);
+    warp_allreduce<NC>(dc);
     static_for<NC>([&](auto CI) __attribute__((always_inline)) {
       constexpr int ci = decltype(CI)::value;
       const int c = warp + NW * ci;
