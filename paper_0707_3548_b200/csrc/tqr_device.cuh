@@ -633,7 +633,6 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       }
       dc[ci] = d0 + d1;
     }
-#pragma unroll
     warp_allreduce<NC>(dc);
     static_for<NC>([&](auto CI) __attribute__((always_inline)) {
       constexpr int ci = decltype(CI)::value;
