@@ -99,7 +99,9 @@ tqr_status tqr_unpack(tqr_plan* plan, const double* At, double* A, int64_t ldr);
  * vectors V below it (V_kk strictly lower in diagonal tiles, V_ik full in tiles
  * below the diagonal); T receives every T slot.
  * GEQRT, TSQRT, LARFB and SSRFB tasks run out of order on the device in a
- * topological order of the DAG with the paper's G > T > L > S priorities. */
+ * topological order of the DAG, prioritised by critical-path length (the criterion behind
+ * the paper's G > T > L > S priorities; R10).  The order never
+ * changes the result: R, V and T are bitwise reproducible run to run. */
 tqr_status tqr_geqrf(tqr_plan* plan, double* At, double* T, void* work);  /* work: see tqr_workspace_size */
 
 /* R = upper trapezoid of the factored tiles, min(m,n) x n column-major (ldr >= min(m,n)),

@@ -3,11 +3,12 @@
 // The paper runs the tasks of Algorithm 1 out of order on CPU
 // threads that pick ready tasks by priority.  Here one persistent
 // CTA per SM (co-resident cooperative launch) takes tickets in a host-computed
-// topological order (list schedule with the paper's G > T > L > S priorities) and waits
+// topological order (a list schedule by critical-path priority, R10) and waits
 // on per-chain monotone progress counters (acquire) before running the task; on
-// completion it publishes its counter (release).  Task granularity: GEQRT(k) and
-// TSQRT(k,i) are whole-tile single-CTA tasks; LARFB and SSRFB are split into 64-column
-// slices (one 8-column group per warp, register resident).
+// completion it publishes its counter(s) (release).  Task granularity: GEQRT(k) and
+// TSQRT(k,i) run as one single-CTA task per inner block l (fused, or split into an apply
+// and a factor part, R21); LARFB and SSRFB tasks cover np register passes of a
+// tile's columns (one 8-column group per warp, register resident; R23).
 #include <cstdio>
 
 #include "tqr_device.cuh"

@@ -11,8 +11,9 @@
 // Every dependency is a chain, so it is expressed on the device as "progress counter >=
 // value": PF(k,l) / PA(k,l) count the F / A parts of P(k,k), P(k,k+1), ... ; col[k][j][sl]
 // counts L(k,j,sl), S(k,k+1,j,sl), ...
-// The dispatch (ticket) order is a list schedule of the DAG on `workers` CTAs with the
-// paper's priorities G > T > L > S, ties by (k, i, j, slice); it is
+// The dispatch (ticket) order is a list schedule of the DAG on `workers` CTAs by bottom
+// level (critical path, R10; the paper's fixed priorities G > T > L > S of
+// PAPER.md:606-615 remain selectable), ties by (k, i, j, slice); it is
 // topological by construction, so with all CTAs co-resident no ticket can wait forever.
 #include <cuda_runtime.h>
 
