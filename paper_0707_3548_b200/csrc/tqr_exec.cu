@@ -16,6 +16,10 @@
 
 namespace tqr {
 
+#ifndef TQR_POLL_NS
+#define TQR_POLL_NS 200  // back-off between polls of an unresolved dependency counter
+#endif
+
 // Optional phase timing (build with -DTQR_PROFILE_PHASES): warp 0 of every CTA accumulates
 // clock64 deltas per phase; totals are added to ExecArgs::phases at kernel exit.
 #ifdef TQR_PROFILE_PHASES
@@ -359,7 +363,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
           if ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) >= val) continue;
           const unsigned long long t0w = globaltimer();
           while ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < val) {
-            __nanosleep(200);
+            __nanosleep(TQR_POLL_NS);
             // watchdog: a dependency that never resolves is a schedule bug; fail loudly
             if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
           }
