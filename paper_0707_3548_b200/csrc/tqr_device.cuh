@@ -115,6 +115,9 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 __device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   asm volatile(
       "{\n .reg .pred p;\n"
@@ -457,8 +460,11 @@ __device__ __forceinline__ void named_arrive(int id, int nthreads) {
   asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// pmb: S mbarriers (one arrival each), initialised once per launch (pmb_init); every call
+// completes each of them exactly once, so call number g of the CTA waits on parity g & 1.
 template <int B, int S, int NW, int LDP>
-__device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, double* tau, const bool TS) {
+__device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, double* tau, const bool TS,
+                                             unsigned long long* pmb, unsigned parity) {
   static_assert(S <= 64, "top block rows: two per lane at most");
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NR = (B + 31) / 32;       // x-part rows per lane: row r = lane + 32 q
@@ -530,7 +536,8 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       if (TS) Rb[jj + jj * S] = beta; else P[c0 + jj + jj * LDP] = beta;
       tau[jj] = tv;
     }
-    named_arrive(1 + jj % 15, 32 * NW);  // publishes v_jj, tau_jj, beta_jj (no wait)
+    __syncwarp();                          // the warp's stores of v_jj, tau_jj, beta_jj ...
+    if (lane == 0) mbar_arrive(pmb + jj);  // ... published (release); the owner does not wait
   };
   // ||column CI below block row j||^2: x part, plus (GEQRT) top-block rows L > j
   auto norm_below = [&](auto CI, int j) __attribute__((always_inline)) -> double {
@@ -556,7 +563,7 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
     house_pub(C0, 0, getT(C0, 0), sg);
   }
   for (int jj = 0; jj + 1 < S; ++jj) {
-    if (warp != jj % NW) named_bar(1 + jj % 15, 32 * NW);  // v_jj published
+    if (warp != jj % NW) mbar_wait(pmb + jj, parity);  // v_jj published (acquire)
     const double tj = tau[jj];
     double vr[NR], vt[NTR];
 #pragma unroll
@@ -647,7 +654,6 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       }
     });
   }
-  if (warp != (S - 1) % NW) named_bar(1 + (S - 1) % 15, 32 * NW);  // complete the last instance
   // R entries above the diagonal of the top block back to shared memory (the diagonal (beta)
   // and V were stored by house_pub)
 #pragma unroll

@@ -63,7 +63,9 @@ struct Layout {
   static constexpr int UPD_END = C1S + 2 * C1SZ;
   // 2 "full" mbarriers (8 B each) + 2 int32 "done" counters
   static constexpr int MBAR = (PANEL_END > UPD_END ? PANEL_END : UPD_END);
-  static constexpr int TOTAL = MBAR + 3;  // doubles
+  // S mbarriers of the panel column handoff (panel_factor), initialised once per launch
+  static constexpr int PMB = MBAR + 4;
+  static constexpr int TOTAL = PMB + S;  // doubles
   static constexpr size_t BYTES = (size_t)TOTAL * sizeof(double);
   static_assert(BYTES <= 232448, "shared memory budget");
   static_assert((T0 % 2) == 0 && (Y1 % 2) == 0 && (MBAR % 1) == 0, "16-byte aligned TMA destinations");
@@ -185,7 +187,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
 template <int B, int S, int SO, int RWM, bool ts>
 __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S, RWM>::RW / 8][2],
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
-                                            size_t toff, int l, bool more, int rlo) {
+                                            size_t toff, int l, bool more, int rlo, unsigned& pf_gen) {
   using C = Cfg<B, S, RWM>;
   using L = Layout<B, S, RWM>;
   constexpr int LDP = L::LDP;
@@ -219,7 +221,9 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     }
   __syncthreads();
   PH_MARK(8);
-  panel_factor<B, S, C::NWARP, LDP>(P, c0, Rb, tau, ts);
+  panel_factor<B, S, C::NWARP, LDP>(P, c0, Rb, tau, ts, reinterpret_cast<unsigned long long*>(sm + L::PMB),
+                                    pf_gen & 1);
+  ++pf_gen;  // every call completes each column mbarrier once
   PH_MARK(9);
   // V / R out, packed Y_l (Ys), Gram -> T_l, packed T_l
   for (int e = tid; e < B * S; e += C::NT) {
@@ -328,6 +332,13 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
   // deadlock: every wait is on a smaller ticket, and the smallest unfinished ticket is running.
   __shared__ __align__(16) int s_next[TASK_INTS];
   __shared__ int s_have;
+  // panel column handoff mbarriers (panel_factor): one init per launch, parity by call count
+  unsigned pf_gen = 0;
+  if (MODE == 0) {
+    if (tid < S) mbar_init(reinterpret_cast<unsigned long long*>(sm + Layout<B, S, RWM>::PMB) + tid, 1);
+    fence_mbar_init();
+    __syncthreads();
+  }
   int next_tk = -1, rec_for = -1;  // thread 0
   for (;;) {
     PH_T0;
@@ -470,8 +481,10 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         } else if (panel) {
           // TS as a template argument: each flavour is register-allocated on its own
           const int rlo = f_part ? sub0 * S : 0;
-          if (ts) panel_block<B, S, SO, RWM, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
-          else panel_block<B, S, SO, RWM, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo);
+          if (ts)
+            panel_block<B, S, SO, RWM, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo, pf_gen);
+          else
+            panel_block<B, S, SO, RWM, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo, pf_gen);
         } else if (warp / Cfg<B, S, RWM>::RS < gact) {
           store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
                                        (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8));

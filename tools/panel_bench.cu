@@ -104,13 +104,18 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel(const double* src, long lo
   double* tau = Rb + S * S;
   int* flag = (int*)(tau + S);
   long long tot = 0;
+  unsigned long long* pmb = reinterpret_cast<unsigned long long*>(tau + S + 2);
+  if (threadIdx.x < S) mbar_init(pmb + threadIdx.x, 1);
+  fence_mbar_init();
+  __syncthreads();
   for (int rep = 0; rep < reps; ++rep) {
     for (int e = threadIdx.x; e < B * S; e += blockDim.x) P[(e % B) + (e / B) * LDP] = src[e];
     for (int e = threadIdx.x; e < S * S; e += blockDim.x) Rb[e] = ((e % S) <= (e / S)) ? src[e] + 3.0 : 0.0;
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     long long t0 = clock64();
-    if (OLD) panel_factor_old<B, S, NW, LDP>(P, 0, Rb, tau, TS); else panel_factor<B, S, NW, LDP>(P, 0, Rb, tau, TS);
+    if (OLD) panel_factor_old<B, S, NW, LDP>(P, 0, Rb, tau, TS);
+    else panel_factor<B, S, NW, LDP>(P, 0, Rb, tau, TS, pmb, rep & 1);
     long long t1 = clock64();
     tot += t1 - t0;
     __syncthreads();
@@ -136,7 +141,7 @@ int main() {
   double hs[256 * 32];
   for (int i = 0; i < 256 * 32; ++i) hs[i] = ((i * 7919) % 1000) / 1000.0 - 0.5;
   cudaMemcpy(src, hs, sizeof(hs), cudaMemcpyHostToDevice);
-  size_t smem = ((256 + 4) * 32 + 32 * 32 + 32 + 2) * 8;
+  size_t smem = ((256 + 4) * 32 + 32 * 32 + 32 + 2 + 32) * 8;
   cudaFuncSetAttribute(k_panel<256, 32, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k_panel<256, 32, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_panel<256, 32, 8, true><<<1, 256, smem>>>(src, d, 20);
@@ -152,7 +157,7 @@ int main() {
   cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
   printf("OLD panel_factor TS b=256 s=32: %lld clk (%.0f per column)  %s\n", h[0], h[0] / 32.0,
          cudaGetErrorString(cudaGetLastError()));
-  size_t smem2 = ((128 + 4) * 32 + 32 * 32 + 32 + 2) * 8;
+  size_t smem2 = ((128 + 4) * 32 + 32 * 32 + 32 + 2 + 32) * 8;
   cudaFuncSetAttribute(k_panel<128, 32, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   k_panel<128, 32, 8, true><<<1, 256, smem2>>>(src, d, 20);
   cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
