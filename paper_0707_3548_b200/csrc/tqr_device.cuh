@@ -518,7 +518,7 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
       const double nu = nn * rn;
       beta = (alpha >= 0.0) ? -nu : nu;
       tv = 1.0 + fabs(alpha) * rn;                 // (beta - alpha)/beta = 1 + |alpha|/nu
-      scale = 1.0 / (alpha - beta);
+      scale = __drcp_rn(alpha - beta);             // correctly rounded, == 1.0 / (alpha - beta)
     }
 #pragma unroll
     for (int q = 0; q < NR; ++q) {
