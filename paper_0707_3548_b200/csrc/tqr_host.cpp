@@ -260,10 +260,10 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
 //  * update tasks (LARFB, SSRFB, apply-Q): ~2 us fixed + the task's flops at 88% (RW = 256
 //    executor) / 79% (RW = 128) of the 251 GFLOP/s per-SM fp64 DMMA peak (the LARFB form
 //    applies the zero rows of U above block l as well, so it costs like SSRFB without C1);
-//  * panel factor part (R21 F): ~15.5 us fixed + s columns at (0.25 + 0.0018 b) us each
-//    (TSQRT b = 256: 38.6 us, b = 128: 30.7 us); GEQRT + 0.03 b us;
+//  * panel factor part (R21 F): ~14 us fixed + s columns at (0.25 + 0.00146 b) us each
+//    (TSQRT b = 256: 34 us, b = 128: 28 us, r01 v11); GEQRT + 0.04 b us;
 //  * panel apply part of block l (R21 A): (1.5 + 0.012 b) us + l block applies at 78%;
-//  * fused panel sub-task (no A/F split): factor part + 9 us + 1.35 x the l block applies.
+//  * fused panel sub-task (no A/F split): factor part + 1 us + 1.35 x the l block applies.
 struct DurModel {
   double B, Sv, W, l, s, apply;
   DurModel(int b, int s_, int w, int rwm = 128) : B(b), Sv(s_), W(w) {
@@ -273,8 +273,8 @@ struct DurModel {
     s = 2000 + (4.0 * B * B * W + Sv * B * W) / (eff * sm);
     apply = 4.0 * B * Sv * Sv / (0.78 * sm);
   }
-  double factor(bool geqrt) const { return 15500 + Sv * (250 + 1.8 * B) + (geqrt ? 30 * B : 0); }
-  double panel(int lb, bool geqrt) const { return factor(geqrt) + 9000 + 1.35 * lb * apply; }
+  double factor(bool geqrt) const { return 14000 + Sv * (250 + 1.46 * B) + (geqrt ? 40 * B : 0); }
+  double panel(int lb, bool geqrt) const { return factor(geqrt) + 1000 + 1.35 * lb * apply; }
   double apply_part(int lb) const { return 1500 + 12 * B + lb * apply; }
   double factor_part(bool geqrt) const { return factor(geqrt); }
 };
