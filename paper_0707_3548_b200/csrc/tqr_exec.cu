@@ -187,7 +187,8 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
 template <int B, int S, int SO, int RWM, bool ts>
 __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S, RWM>::RW / 8][2],
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
-                                            size_t toff, int l, bool more, int rlo, unsigned& pf_gen) {
+                                            size_t toff, int l, bool more, int rlo, unsigned& pf_gen,
+                                            int* pr_ctr, int pr_val) {
   using C = Cfg<B, S, RWM>;
   using L = Layout<B, S, RWM>;
   constexpr int LDP = L::LDP;
@@ -245,6 +246,13 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
       if (r <= c) __stcg(Akk + (size_t)(c0 + c) * B + c0 + r, Rb[e]);
     }
   __syncthreads();
+  // early release (R24): R_kk's rows of this block are final (V/R out above), which
+  // is all the next tile's factor part of this block reads -- it need not wait for the Gram,
+  // T and packed-panel work below
+  if (pr_ctr && !more && threadIdx.x == 0) {
+    __threadfence();
+    st_release(pr_ctr, pr_val);
+  }
   PH_MARK(10);
   gram_upper<B, S, C::NWARP>(Ys, Z);
   __syncthreads();
@@ -481,10 +489,15 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         } else if (panel) {
           // TS as a template argument: each flavour is register-allocated on its own
           const int rlo = f_part ? sub0 * S : 0;
+          const int pr = (s_task[14] >> 8) - 1;  // early-release counter (or -1)
+          int* const prc = pr >= 0 ? R.ctr + pr : nullptr;
+          const int prv = a.base + s_task[6];
           if (ts)
-            panel_block<B, S, SO, RWM, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo, pf_gen);
+            panel_block<B, S, SO, RWM, true>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo, pf_gen,
+                                             prc, prv);
           else
-            panel_block<B, S, SO, RWM, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo, pf_gen);
+            panel_block<B, S, SO, RWM, false>(sm, acc, Akk, Ab, Tslot, a, yoff, toff, sub, sub + 1 < nsub, rlo, pf_gen,
+                                              prc, prv);
         } else if (warp / Cfg<B, S, RWM>::RS < gact) {
           store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
                                        (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8));

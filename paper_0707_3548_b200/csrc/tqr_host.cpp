@@ -75,6 +75,7 @@ struct TaskGen {
     int key[4];  // priority keys after cls (smaller first); default (k, i, j, sl)
     int64_t group;  // PRIO_BLEVEL: tasks of one group share the group's highest bottom level (-1: none)
     int np, ocnt;   // update tasks: register passes; consecutive out counters published (>= 1)
+    int out2_idx;   // panel factor parts: early-release counter (set to out_val mid-task), or -1
   };
   std::vector<T> t;
   int add(int kind, int k, int i, int j, int sl, int out_idx, int out_val, double dur, int cls) {
@@ -84,7 +85,7 @@ struct TaskGen {
     x.out_idx = out_idx; x.out_val = out_val; x.ndep = 0; x.dur = dur; x.cls = cls;
     x.key[0] = k; x.key[1] = i; x.key[2] = j; x.key[3] = sl;
     x.group = -1;
-    x.np = 1; x.ocnt = 1;
+    x.np = 1; x.ocnt = 1; x.out2_idx = -1;
     t.push_back(x);
     return (int)t.size() - 1;
   }
@@ -127,6 +128,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
       for (int r = 0; r < nr; ++r) producer[pkey(r, x.out_idx, x.out_val)] = id;
     else
       for (int c = 0; c < x.ocnt; ++c) producer[pkey(x.rank, x.out_idx + c, x.out_val)] = id;
+    if (x.out2_idx >= 0) producer[pkey(x.rank, x.out2_idx, x.out_val)] = id;
   }
   std::vector<int> indeg(n, 0);
   std::vector<std::vector<int>> succ(n);
@@ -290,7 +292,8 @@ struct DurModel {
 // update of the steps whose default-granularity task count is below two waves (the tail).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
-                               int rwm = 128, double blq = 0.0, bool group = false, int np = 1, int fine = 0) {
+                               int rwm = 128, double blq = 0.0, bool group = false, int np = 1, int fine = 0,
+                               bool early = false) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -306,13 +309,15 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   // Panel progress of step k, per inner block l (a copy on every rank, R21):
   //   PF(k,l): factor parts done (GEQRT(k) then TSQRT(k,k+1), ...: value i-k+1 after TSQRT(k,i))
   //   PA(k,l): apply parts done, l >= 1 (left-looking update of block l's columns; owner only)
-  auto PF = [&](int k, int l) { return k * 2 * NPT + l; };
-  auto PA = [&](int k, int l) { return k * 2 * NPT + NPT + l; };
+  //   PR(k,l): R_kk's rows of block l final (a factor part's early release, owner only)
+  auto PF = [&](int k, int l) { return k * 3 * NPT + l; };
+  auto PA = [&](int k, int l) { return k * 3 * NPT + NPT + l; };
+  auto PR = [&](int k, int l) { return k * 3 * NPT + 2 * NPT + l; };
   auto COL = [&](int k, int64_t j, int sl) {
-    return K * 2 * NPT + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl);
+    return K * 3 * NPT + (int)(((int64_t)k * qloc(own(j)) + j / G) * nsl + sl);
   };
   out.nctr.assign(G, 0);
-  for (int r = 0; r < G; ++r) out.nctr[r] = K * 2 * NPT + (int)((int64_t)K * qloc(r) * nsl);
+  for (int r = 0; r < G; ++r) out.nctr[r] = K * 3 * NPT + (int)((int64_t)K * qloc(r) * nsl);
   // One panel task on tile (i,k) block l in two parts: A (apply this tile's blocks < l to
   // block l's columns: touches the rows of R_kk ABOVE the diagonal block) and F (factor: the
   // diagonal block).  A(k,i+1,l) may overlap F(k,i,l), which halves the TSQRT chain's step.
@@ -322,7 +327,8 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
       if (!split) {  // fused apply + factor per block (R21 without the A/F split)
         int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l, kind == K_G), cls);
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
-        if (v > 1) T.dep(id, PF(k, l), 1, v - 1);
+        if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
+        if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk block l: previous tile
         if (l > 0) T.dep(id, PF(k, l - 1), 1, v);
         else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
         continue;
@@ -335,7 +341,8 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
       }
       int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(kind == K_G), cls);
       T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
-      if (v > 1) T.dep(id, PF(k, l), 1, v - 1);        // R_kk diagonal block l: previous tile
+      if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
+      if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk diagonal block l: previous tile
       if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part
       else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);  // tile updated by step k-1
     }
@@ -466,6 +473,7 @@ struct tqr_plan {
   int orm_prio = PRIO_BLEVEL;  // list-schedule priority of apply-Q / form-Q
   double blq = 0.0;            // bottom-level quantum (ns) of the factorization schedule
   bool group = false;          // group the updates of one reflector panel (R22)
+  bool early = true;           // factor parts release R_kk's block rows early (R24)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -702,6 +710,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (const char* e = getenv("TQR_DEV_ORM_PRIO")) P->orm_prio = atoi(e);
   if (const char* e = getenv("TQR_DEV_BLQ")) P->blq = atof(e);
   if (const char* e = getenv("TQR_DEV_GROUP")) P->group = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_EARLY")) P->early = atoi(e) != 0;
   {
     const int w = exec_slice(p->b, p->s, P->rwm);  // one register pass
     P->nsl = (int)((p->b + w - 1) / w);
@@ -725,7 +734,8 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate)
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
-  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine);
+  build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine,
+                     P->early);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -1035,7 +1045,7 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   // inspected shapes
   build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1,
                      (p + q) % 2 == 0, s, p % 2 == 0 ? PRIO_BLEVEL : PRIO_CLASS, 4000.0, 128, 0.0, false,
-                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3));
+                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3), (p + 2 * q) % 3 != 0);
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;

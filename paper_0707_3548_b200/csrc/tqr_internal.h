@@ -25,7 +25,9 @@ enum Kind : int {
 //   [7] kc: STORAGE tile column of tile column k (A(k,k), A(i,k), T(., k))
 //   [8 + 2d], [9 + 2d], d = 0..2: dependency d = (index | count << 24, value):
 //       wait until ctr[index + x] >= base + value for x in [0, count); count 0 = none
-//   [14] flags: bit 0 = publish the out counter on every rank (panel progress, multi-GPU)
+//   [14] flags: bit 0 = publish the out counter on every rank (panel progress, multi-GPU),
+//        bit 1 / bit 2 = panel apply / factor part; bits 8..31 = 1 + an early-release
+//        counter that a panel factor part sets to [6] once R_kk's rows of its block are final
 //   [15] update tasks: np | ocnt << 8 -- register passes [slice, slice + np) (slice = [4], in
 //        units of SLICE columns), and ocnt consecutive out counters [5] .. [5] + ocnt - 1 set
 //        to [6] on completion (0 / panel tasks: one)

@@ -83,6 +83,9 @@ class RankSim:
                 self.held.remove(t)
                 for x in range(_out_count(rec)):  # update tasks: one counter per register pass
                     self.publish(int(rec[5]) + x, int(rec[6]))
+                pr = (int(rec[14]) >> 8) - 1  # panel factor parts: early-release counter (local)
+                if pr >= 0:
+                    self.publish(pr, int(rec[6]))
                 if rec[14] & 1:
                     self.published.append((int(rec[5]), int(rec[6])))
                 self.done += 1
@@ -108,7 +111,7 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
                 assert k % G == r and rec[7] == k // G  # panel parts on owner(k)
                 # factor parts (bit 2) and fused blocks publish their progress to every rank,
                 # apply parts (bit 1) stay local
-                assert rec[14] in (1, 2, 1 | 4)
+                assert rec[14] & 0xFF in (1, 2, 1 | 4)
             else:
                 assert _global_j(rec, G, r) % G == r and not rec[14] & 1  # update on owner(j), local
             keys.extend(_task_keys(rec, G, r))
@@ -134,8 +137,8 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
     for g, sim in enumerate(sims):
         # every rank ends with the complete panel progress of every step, received exactly once
         for k in range(K):
-            for l in range(NPT):  # PF(k, l) at k*2*NPT + l
-                assert sim.ctr[k * 2 * NPT + l] == max(1, p - k)
+            for l in range(NPT):  # PF(k, l) at k*3*NPT + l
+                assert sim.ctr[k * 3 * NPT + l] == max(1, p - k)
         assert all(v == 1 for v in seen[g].values())
 
 
@@ -173,7 +176,7 @@ def _gloo_rank(rank, world, port, p, q, nsl, workers, out):
             rounds += 1
             # nobody ran a task this round and some rank is unfinished: cross-rank deadlock
             assert rounds < 100000 and any(r for _, _, r in allp), "deadlock across ranks"
-        out.put((rank, sim.done, len(recs), [int(sim.ctr[k * 2 * NPT + l]) for k in range(min(p, q))
+        out.put((rank, sim.done, len(recs), [int(sim.ctr[k * 3 * NPT + l]) for k in range(min(p, q))
                                              for l in range(NPT)]))
     finally:
         dist.destroy_process_group()
