@@ -373,7 +373,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": e2e,
         "form_q": form_q,
-        "gpu_launches": (4 if world > 1 else 3) * args.steps,   # pack, [rank barrier,] executor, get_r
+        # pack, [rank barrier,] executor, [form_t: b*s > 8192, the executor's internal blocks
+        # are narrower than s], get_r
+        "gpu_launches": (3 + (world > 1) + (b * s > 8192)) * args.steps,
         "clocks": clk.summary(),
     }
     print(json.dumps(line), flush=True)
