@@ -694,14 +694,14 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   //    C5 12.5 s (80.7%) vs 232 ms / 13.7 s with RW = 128;
   //  * tall-skinny grids (p >= 4q) are bound by the TSQRT chain: the RW = 128 executor with
   //    32-column update tasks and the panel A/F split (C4: 60 ms vs 77 with RW = 256);
-  //  * b <= 128: RW = b, 1-pass tasks, A/F split (the GEQRT/TSQRT chain dominates C2);
+  //  * b <= 128: RW = b, 1-pass tasks, fused panel blocks (the GEQRT/TSQRT chain dominates C2);
   //  * dispatch order by bottom level (critical path) with a 4 us handoff per task, not by the
   //    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
   const bool tall = P->p >= 4 * P->q;
   P->rwm = (p->b >= 256 && !tall) ? 256 : 128;
   P->passes = p->b >= 256 ? (128 / exec_slice(p->b, p->s, P->rwm)) : 1;  // 128-column tasks
   if (tall && p->b <= 256) P->passes = 1;
-  P->split = tall || p->b <= 128;
+  P->split = tall;  // (square b <= 128 as well before the early R_kk release, R24: C2 7.15 -> 7.08 ms fused)
   if (const char* e = getenv("TQR_DEV_PASSES")) P->passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P->split = atoi(e) != 0;
   if (const char* e = getenv("TQR_DEV_RW")) P->rwm = atoi(e);
