@@ -52,8 +52,11 @@ struct Layout {
   static constexpr int Y0 = 0, T0 = YSZ, Y1 = YSZ + TSZ, T1 = 2 * YSZ + TSZ;
   static constexpr int LDP = B + 4;
   static_assert(LDP * S <= YSZ + TSZ, "P overlay");
-  static constexpr int XBUF = 2 * YSZ + 2 * TSZ;  // W partials, one per warp (RS > 1)
-  static constexpr int XSZ = C::RS > 1 ? C::NWARP * C::XW : 0;
+  // W partials (RS > 1): one per warp, double-buffered by block parity -- a warp rewrites a
+  // buffer two blocks later, after its partner has passed the next block's exchange barrier,
+  // so one named barrier per block suffices (group_apply BAR2 = false)
+  static constexpr int XBUF = 2 * YSZ + 2 * TSZ;
+  static constexpr int XSZ = C::RS > 1 ? 2 * C::NWARP * C::XW : 0;
   static constexpr int C1S = XBUF + XSZ;          // C1 blocks, 2 buffers x GPS groups
   static constexpr int C1SZ = C::GPS * C::C1W;
   // panel-only scratch (Rb, Z, tau; Rb reused for the plain T_l), aliased onto the partial /
@@ -162,9 +165,9 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
     if (li == 0) PH_MARK(0);
     if (threadIdx.x == 0) pf(li, nb);
     if (active)
-      group_apply<B, S, C::RW, C::RS, QT, true>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
+      group_apply<B, S, C::RW, C::RS, QT, false>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
                                                 buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
-                                                sm + L::XBUF + gi * C::RS * C::XW);
+                                                sm + L::XBUF + (li & 1) * (C::NWARP * C::XW) + gi * C::RS * C::XW);
     __syncwarp();
     if (lane == 0 && li + 2 < nb) {
       if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
