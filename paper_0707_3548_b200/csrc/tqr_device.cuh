@@ -436,30 +436,20 @@ __device__ __forceinline__ void c1_fetch(double* c1s, const double* tile, int ro
 //   TS = false (GEQRT): P holds the tile rows, block columns; column jj's
 //              alpha is P[c0+jj][jj], its x is P[c0+jj+1 :][jj].
 // P column c at P + c*LDP.  Column c belongs to warp c % NW and only that warp writes it.
-// No block-wide barrier inside the column loop: the owner of column jj publishes v_jj (in
-// place, P column jj is final once generated) and tau_jj, then ARRIVES (bar.arrive, no
-// wait) on hardware named barrier 1 + jj % 15; every other warp waits on it (bar.sync)
-// before applying reflector jj to its own columns.  The owner of column jj+1 updates that
-// column first and immediately generates the next reflector, so the critical path per
-// column is one dot/update plus one Householder generation; the other warps' columns are
-// updated off the critical path with their reductions interleaved.  (Measured with
-// tools/panel_bench.cu: a shared-memory flag handoff costs ~400 clk, a named barrier ~30.)
+// No block-wide barrier inside the column loop: the owner warp of column jj publishes v_jj
+// (in place, P column jj is final once generated), tau_jj and beta_jj, then ARRIVES (release,
+// no wait) on column jj's mbarrier pmb[jj]; every other warp waits on that mbarrier alone
+// (acquire) before applying reflector jj to its own columns.  A named barrier would complete
+// only when EVERY warp arrived, so each column would wait for the slowest warp's off-path
+// updates of the previous column (1407 -> 1229 clk per column, tools/panel_bench.cu).  The
+// owner of column jj+1 updates that column first and immediately generates the next
+// reflector, so the critical path per column is one dot/update plus one Householder
+// generation; the other warps' columns are updated off the critical path with their
+// reductions interleaved.
 // Householder generator = DESIGN.md R2-R4 (the oracle's), v = x * (1/(alpha-beta)).
 // Outputs: P holds V_l (below the diagonal for GEQRT), Rb / P's upper part the new R
-// entries, tau[S].  Uses named barriers 1..15 (all instances complete on return).
+// entries, tau[S].
 // ---------------------------------------------------------------------------------------
-__device__ __forceinline__ int ld_acquire_cta(const int* p) {
-  int v;
-  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_release_cta(int* p, int v) {
-  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
-}
-__device__ __forceinline__ void named_arrive(int id, int nthreads) {
-  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
 // pmb: S mbarriers (one arrival each), initialised once per launch (pmb_init); every call
 // completes each of them exactly once, so call number g of the CTA waits on parity g & 1.
 template <int B, int S, int NW, int LDP>

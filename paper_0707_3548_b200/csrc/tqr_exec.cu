@@ -409,6 +409,8 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         const int code = s_task[8 + 2 * d], cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
         if (cnt && (idx + cnt > a.nctr)) bad = true;
       }
+      const int pr = (s_task[14] >> 8) - 1;  // early-release counter of a panel factor part
+      if (pr >= a.nctr || (pr >= 0 && !(kind == K_G || kind == K_T))) bad = true;
       if (bad) {
         printf("tqr checked build: bad task record %d: kind %d k %d i %d j %d sl %d kc %d out %d\n", tk, kind, k, i,
                j, sl, kc, s_task[5]);
@@ -514,6 +516,21 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
       __threadfence();
       fence_proxy_async();
       const int oidx = s_task[5], oval = a.base + s_task[6];
+      if ((s_task[14] >> 8) != 0 && s_task[6] > 1) {
+        // Ordered publication of an early-releasing factor part (R24): the next
+        // tile's factor part of this block may have started on our early release and may
+        // finish first; PF(k,l) must still advance v-1 -> v -> v+1 (a consumer of PF >= v
+        // reads this task's Y_l / T_l), so wait for the previous tile's publication.  That
+        // task is past its own early release and waits on nothing: no deadlock.
+        const int* c = R.ctr + oidx;
+        if ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < oval - 1) {
+          const unsigned long long t0w = globaltimer();
+          while ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < oval - 1) {
+            __nanosleep(TQR_POLL_NS);
+            if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
+          }
+        }
+      }
       if ((s_task[14] & 1) && a.nranks > 1) {
         // panel progress: release on every rank (the V/T tiles it covers are already there)
         if (a.sys) {

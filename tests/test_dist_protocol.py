@@ -142,6 +142,122 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
         assert all(v == 1 for v in seen[g].values())
 
 
+class PhasedSim:
+    """All ranks of a job in one process, with the executor's TWO publication events per
+    early-releasing panel factor part (R24): the early release PR(k,l) mid-task and
+    the end-of-task PF(k,l) (+ the publication to every rank).  Events are taken in an
+    adversarial order: an early-released factor part finishes as LATE as possible (after
+    every other runnable event), so the next tile's factor part of the same block, which
+    starts on the early release, may reach its end first.  `ordered` models the executor's
+    end-of-task rule (tqr_exec.cu: wait for PF >= v - 1 before releasing PF = v); without it
+    PF(k,l) would jump.  Every publication asserts that the counter advances by exactly one,
+    and every consumer that starts on PF >= v must find the task that published v finished."""
+
+    def __init__(self, per_rank, G, workers, ordered=True, seed=0):
+        self.G, self.workers, self.ordered = G, workers, ordered
+        self.recs = [r for r, _ in per_rank]
+        self.ctr = [np.zeros(n, dtype=np.int64) for _, n in per_rank]
+        self.next = [0] * G
+        self.held = [[] for _ in range(G)]      # tickets taken, not started
+        self.running = [[] for _ in range(G)]   # [ticket, phase] (0: before PR, 1: after)
+        self.done = [0] * G
+        self.rng = np.random.default_rng(seed)
+
+    def _publish(self, r, idx, val):
+        assert val == self.ctr[r][idx] + 1, f"rank {r} counter {idx} jumps {self.ctr[r][idx]} -> {val}"
+        self.ctr[r][idx] = val
+
+    def _ready(self, r, rec):
+        for idx, cnt, val in _deps(rec):
+            if not np.all(self.ctr[r][idx:idx + cnt] >= val):
+                return False
+        return True
+
+    def _events(self):
+        ev = []
+        for r in range(self.G):
+            for t in self.held[r]:
+                if self._ready(r, self.recs[r][t]):
+                    ev.append((1, r, "start", t))
+            for t, ph in self.running[r]:
+                rec = self.recs[r][t]
+                pr = (int(rec[14]) >> 8) - 1
+                if pr >= 0 and ph == 0:
+                    ev.append((1, r, "mid", t))
+                else:
+                    can_end = True
+                    if self.ordered and pr >= 0 and int(rec[6]) > 1:
+                        can_end = self.ctr[r][int(rec[5])] >= int(rec[6]) - 1
+                    if can_end:   # early-released factor parts end last (adversarial)
+                        ev.append((2 if pr >= 0 else 1, r, "end", t))
+        return ev
+
+    def run(self):
+        G = self.G
+        for _ in range(10 ** 7):
+            for r in range(G):
+                while len(self.held[r]) + len(self.running[r]) < self.workers and self.next[r] < len(self.recs[r]):
+                    self.held[r].append(self.next[r])
+                    self.next[r] += 1
+            if all(self.done[r] == len(self.recs[r]) for r in range(G)):
+                return
+            ev = self._events()
+            assert ev, "deadlock: no event can fire"
+            best = min(e[0] for e in ev)
+            cand = [e for e in ev if e[0] == best]
+            _, r, what, t = cand[int(self.rng.integers(len(cand)))]
+            rec = self.recs[r][t]
+            if what == "start":
+                self.held[r].remove(t)
+                self.running[r].append([t, 0])
+            elif what == "mid":
+                pr = (int(rec[14]) >> 8) - 1
+                self._publish(r, pr, int(rec[6]))
+                next(x for x in self.running[r] if x[0] == t)[1] = 1
+            else:
+                self.running[r] = [x for x in self.running[r] if x[0] != t]
+                idx, val = int(rec[5]), int(rec[6])
+                if rec[14] & 1:   # panel progress: every rank's copy
+                    for g in range(G):
+                        self._publish(g, idx, val)
+                else:
+                    for x in range(_out_count(rec)):
+                        self._publish(r, idx + x, val)
+                self.done[r] += 1
+        raise AssertionError("replay did not finish")
+
+
+_PHASED = [(8, 7, 1, 1, 4), (12, 7, 2, 1, 8), (30, 4, 2, 1, 16), (14, 6, 2, 1, 6), (10, 9, 2, 3, 3), (24, 4, 1, 4, 6)]
+
+
+@pytest.mark.parametrize("p,q,nsl,G,workers", _PHASED)
+def test_phased_adversarial_replay(L, p, q, nsl, G, workers):
+    """The early release (PR mid-task) lets F(k,i+1,l) overtake F(k,i,l); with the executor's
+    ordered end-of-task publication every PF(k,l) still advances by one on every rank, and
+    the replay finishes (no deadlock from the extra wait)."""
+    per_rank = [L.schedule_records(p, q, nsl, workers, G, r) for r in range(G)]
+    if not any((int(rec[14]) >> 8) for recs, _ in per_rank for rec in recs):
+        pytest.skip("schedule without early release")
+    for seed in range(3):
+        sim = PhasedSim(per_rank, G, workers, ordered=True, seed=seed)
+        sim.run()
+        for r in range(G):
+            assert sim.done[r] == len(per_rank[r][0])
+            for k in range(min(p, q)):
+                for l_ in range(NPT):
+                    assert sim.ctr[r][k * 3 * NPT + l_] == max(1, p - k)
+
+
+def test_phased_replay_detects_unordered_publication(L):
+    """Negative check: without the ordered publication, the adversarial order makes PF(k,l)
+    jump (a consumer of PF >= v would read tile i's Y_l / T_l before they are stored)."""
+    per_rank = [L.schedule_records(30, 4, 2, 16, 1, 0)]
+    assert any((int(rec[14]) >> 8) for rec in per_rank[0][0])
+    with pytest.raises(AssertionError, match="jumps"):
+        for seed in range(5):
+            PhasedSim(per_rank, 1, 16, ordered=False, seed=seed).run()
+
+
 def _free_port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

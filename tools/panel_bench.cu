@@ -4,8 +4,17 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 #include "../paper_0707_3548_b200/csrc/tqr_device.cuh"
-#include "panel_factor_old.inc"
 using namespace tqr;
+
+// shared-memory flag handoff primitives (measured below against named barriers / mbarriers)
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared.s32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 
 __global__ void k_prims(long long* out, double x0) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -95,7 +104,7 @@ __global__ void k_prims(long long* out, double x0) {
 }
 
 // The product panel factorization (TS and GEQRT flavour) on a random 256 x 32 panel.
-template <int B, int S, int NW, bool TS, bool OLD = false>
+template <int B, int S, int NW, bool TS>
 __global__ void __launch_bounds__(NW * 32, 1) k_panel(const double* src, long long* out, int reps) {
   constexpr int LDP = B + 4;
   extern __shared__ double sm[];
@@ -114,8 +123,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel(const double* src, long lo
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     long long t0 = clock64();
-    if (OLD) panel_factor_old<B, S, NW, LDP>(P, 0, Rb, tau, TS);
-    else panel_factor<B, S, NW, LDP>(P, 0, Rb, tau, TS, pmb, rep & 1);
+    panel_factor<B, S, NW, LDP>(P, 0, Rb, tau, TS, pmb, rep & 1);
     long long t1 = clock64();
     tot += t1 - t0;
     __syncthreads();
@@ -151,11 +159,6 @@ int main() {
   k_panel<256, 32, 8, false><<<1, 256, smem>>>(src, d, 20);
   cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
   printf("panel_factor GE  b=256 s=32:  %lld clk (%.0f per column)  %s\n", h[0], h[0] / 32.0,
-         cudaGetErrorString(cudaGetLastError()));
-  cudaFuncSetAttribute(k_panel<256, 32, 8, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_panel<256, 32, 8, true, true><<<1, 256, smem>>>(src, d, 20);
-  cudaMemcpy(h, d, 8, cudaMemcpyDeviceToHost);
-  printf("OLD panel_factor TS b=256 s=32: %lld clk (%.0f per column)  %s\n", h[0], h[0] / 32.0,
          cudaGetErrorString(cudaGetLastError()));
   size_t smem2 = ((128 + 4) * 32 + 32 * 32 + 32 + 2 + 32) * 8;
   cudaFuncSetAttribute(k_panel<128, 32, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
