@@ -110,22 +110,31 @@ class ClockSampler:
                 "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.samples)}
 
 
-def cpu_baseline_sample(cfg, threads):
-    """The oracle as it stands, on a bounded sample of the workload: a smaller square matrix
-    with the same tiling (b, s), same distribution and seed recipe, factored by the oracle's
-    DAG executor on `threads` host threads.  Returns (GFLOP/s standard count, seconds, desc)."""
-    import oracle
-    b, s = cfg["b"], cfg["s"]
+FULL_ORACLE_MAX_FLOPS = 1.2e13   # C1-C4: the whole workload (C3 ~80 s on 16 host threads); C5 (3.8e14): a sample
+
+
+def sample_block(cfg, A=None):
+    """A bounded sample of the workload's OWN bytes: the leading principal submatrix (same
+    tiling, same seeded entries) -- 6144^2 for the square configs, 32 x 4 tiles for C4."""
+    b = cfg["b"]
     m = n = min(cfg["m"], cfg["n"], max(8 * b, 6144 // b * b))
     if cfg["m"] > 4 * cfg["n"]:  # tall-skinny: keep the aspect ratio class
         n = min(cfg["n"], 4 * b)
         m = min(cfg["m"], 32 * n)
-    A = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"])
+    if A is None:
+        A = tqr_inputs.make(cfg["m"], cfg["n"], cfg["dist"], cfg["seed"])
+    return np.asfortranarray(A[:m, :n])
+
+
+def time_oracle(A, cfg, threads):
+    """The oracle as it stands (oracle/, plain C DAG executor) on host matrix A.
+    Returns (GFLOP/s standard count, seconds, tiles At, T)."""
+    import oracle
+    m, n = A.shape
     t0 = time.perf_counter()
-    oracle.geqrf(A, b, s, nthreads=threads)
+    At, T = oracle.geqrf(A, cfg["b"], cfg["s"], nthreads=threads)
     dt = time.perf_counter() - t0
-    return oracle.flops_standard(m, n) / dt / 1e9, dt, f"oracle_geqrf_tiles {m}x{n} b={b} s={s} ({cfg['dist']}), " \
-                                                       f"{threads} threads, one factorization"
+    return oracle.flops_standard(m, n) / dt / 1e9, dt, At, T
 
 
 def run_reference(args, cfg, rank):
@@ -133,9 +142,12 @@ def run_reference(args, cfg, rank):
         return 0
     threads = len(os.sched_getaffinity(0))
     vals = []
-    desc = ""
+    S = sample_block(cfg)
+    desc = (f"oracle_geqrf_tiles on the leading {S.shape[0]}x{S.shape[1]} block of the {cfg['m']}x{cfg['n']} "
+            f"workload matrix (same seeded bytes, b={cfg['b']} s={cfg['s']}), {threads} threads, one "
+            f"factorization per step")
     for it in range(args.warmup + args.steps):
-        v, dt, desc = cpu_baseline_sample(cfg, threads)
+        v, dt, _, _ = time_oracle(S, cfg, threads)
         if it >= args.warmup:
             vals.append(v)
     value = statistics.median(vals)
@@ -200,7 +212,9 @@ def main():
         plan.get_r(At, R)
 
     flops = tqr.flops_standard(m, n)
-    flops_exec = tqr.flops_tiled(m, n, b, s)
+    # executed count at the executor's internal inner block (b = 512, s = 64 runs SI = 16 blocks,
+    # DESIGN.md R16; the off-diagonal T blocks of form_t are not counted)
+    flops_exec = tqr.flops_tiled(m, n, b, plan.info()["inner"])
     for _ in range(args.warmup):
         step()
     stream.synchronize()
@@ -332,11 +346,36 @@ def main():
             dist.destroy_process_group()
         return 0
 
-    cpu = None
+    cpu, parity = None, None
     if not args.no_cpu_baseline and world == 1:
+        # The oracle as it stands on the host cores.  Up to C4 it factors the WHOLE workload
+        # (the same A bytes the GPU factored) and the GPU's R of the last timed step is
+        # compared with it elementwise (BJ north_star: within 1e-10 * ||A||_F); C5 (3.8e14
+        # flops, hours on the host) times the oracle on a leading-block sample instead.
         threads = len(os.sched_getaffinity(0))
-        v, dt, desc = cpu_baseline_sample(cfg, threads)
-        cpu = {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc, "seconds": dt}
+        A_host = A_pin.numpy().T                          # m x n, Fortran order (no copy)
+        if flops <= FULL_ORACLE_MAX_FLOPS:
+            import oracle
+            v, dt, At_o, _ = time_oracle(A_host, cfg, threads)
+            desc = (f"oracle_geqrf_tiles on the full {m}x{n} workload (the same A bytes), b={b} s={s}, "
+                    f"{threads} threads, one factorization")
+            R_o = oracle.get_r(At_o, m, n, b)
+            del At_o
+            R_g = R.cpu().numpy().T
+            nA = float(np.linalg.norm(A_host))
+            err = float(np.max(np.abs(R_g - R_o)))
+            parity = {"R_max_abs_diff_vs_oracle": err, "tol": 1e-10 * nA, "ok": err <= 1e-10 * nA,
+                      "what": "GPU R of the last timed step vs the oracle's R on the same A, elementwise"}
+            del R_o, R_g
+            cpu = {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc, "seconds": dt,
+                   "same_config": True}
+        else:
+            S = sample_block(cfg, A_host)
+            v, dt, _, _ = time_oracle(S, cfg, threads)
+            desc = (f"oracle_geqrf_tiles on the leading {S.shape[0]}x{S.shape[1]} block of the workload matrix "
+                    f"(same bytes), b={b} s={s}, {threads} threads, one factorization")
+            cpu = {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": desc, "seconds": dt,
+                   "same_config": False}
 
     achieved = flops / world / (kern_ms * 1e-3) / 1e12   # this GPU's share of the job, per launch
     traffic = None
@@ -356,8 +395,8 @@ def main():
                    "seed": cfg["seed"],
                    "parallelism": (f"1D block-cyclic tile columns over {world} GPUs, V/T by NVLink peer stores"
                                    if world > 1 else ("1 GPU" if G == 1 else f"1 GPU, {G} emulated ranks")),
-                   "l2": "inputs 2 GiB > 126 MB L2; no flush between steps" if m * n * 8 > (1 << 28)
-                   else "inputs smaller than L2 (not flushed)",
+                   "l2": (f"inputs {m * n * 8 / 2**30:.1f} GiB > 126 MB L2; no flush between steps"
+                          if m * n * 8 > (1 << 28) else "inputs smaller than L2 (not flushed)"),
                    "step": "pack + geqrf (persistent DAG executor) + get_r"},
         "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
         "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
@@ -371,6 +410,7 @@ def main():
                      "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt); "
                                     "MEASURED_PEAKS.json has no fp64 entry"},
         "cpu_baseline": cpu,
+        "parity": parity,
         "e2e": e2e,
         "form_q": form_q,
         # pack, [rank barrier,] executor, [form_t: b*s > 8192, the executor's internal blocks

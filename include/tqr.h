@@ -176,6 +176,20 @@ tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t wo
 tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, int32_t rank,
                                 int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr);
 
+/* The factorization dispatch records THIS plan executes (same 16-int32 layout), for its
+ * local rank index `local` (0 .. ranks run by this process - 1; emulated plans run every
+ * rank): *n = task count, up to `cap` records copied to host `rec` (synchronous device copy).
+ * Lets tests check which task granularities (register passes per update task, record [15])
+ * a parity case actually exercises.  TQR_ERR_INVALID_ARG(2) for a bad local index. */
+tqr_status tqr_plan_records(tqr_plan* plan, int32_t local, int32_t* rec, int64_t cap, int64_t* n);
+/* Policy the plan chose (host): info[0] rows-per-warp variant (128 / 256), [1] register passes
+ * per default update task, [2] register passes (column slices) per tile, [3] panel A/F split,
+ * [4] early R_kk release, [5] executor CTAs, [6] priority (0 classes, 1 bottom level),
+ * [7] fine-granularity rule (R23), [8] internal inner block SI of the executor (== s
+ * except b*s > 8192, R16), [9] ranks of the job, [10] ranks run by this process,
+ * [11] columns per register pass. */
+tqr_status tqr_plan_info(const tqr_plan* plan, int32_t info[12]);
+
 /* Trace of the last tqr_geqrf with TQR_FLAG_TRACE: up to `cap` records of
  * {kind, k, i, j, slice, sm, start_ns, end_ns} as 8 int64 each (host memory);
  * returns the number of records written in *n. */

@@ -52,6 +52,8 @@ def lib():
         L.oracle_kernel_flops.restype = _d
         L.oracle_flops_eq4.argtypes = [_i64, _i64, _d]
         L.oracle_flops_eq4.restype = _d
+        L.oracle_dag_edges.argtypes = [_i64, _i64, ctypes.POINTER(_i64), _i64]
+        L.oracle_dag_edges.restype = _i64
         L.oracle_last_task_counts.argtypes = [ctypes.POINTER(_i64)]
         L.oracle_last_task_counts.restype = None
         _lib = L
@@ -163,6 +165,17 @@ def orgqr(At, T, m, n, b, s, k=None, nthreads=1):
     E = np.zeros((m, k), order="F")
     E[np.arange(min(m, k)), np.arange(min(m, k))] = 1.0
     return ormqr(At, T, m, n, b, s, E, 0, nthreads)
+
+
+def dag_edges(p, q):
+    """Edges of the oracle's DAG: list of ((kind, k, i, j), (kind, k, i, j)), kind 'G','T','L','S'."""
+    n = lib().oracle_dag_edges(p, q, None, 0)
+    buf = np.zeros(max(1, 8 * n), dtype=np.int64)
+    lib().oracle_dag_edges(p, q, buf.ctypes.data_as(ctypes.POINTER(_i64)), n)
+    names = "GTLS"
+    e = buf[: 8 * n].reshape(n, 8)
+    return [((names[r[0]], int(r[1]), int(r[2]), int(r[3])), (names[r[4]], int(r[5]), int(r[6]), int(r[7])))
+            for r in e]
 
 
 def task_counts():

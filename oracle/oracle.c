@@ -431,53 +431,85 @@ static void* dag_worker(void* arg) {
   }
 }
 
-static int geqrf_dag(const qr_ctx* X, int nthreads) {
-  int64_t p = X->p, q = X->q, K = p < q ? p : q;
-  dag_ctx D;
-  memset(&D, 0, sizeof(D));
-  D.X = *X;
+/* Nodes in Algorithm 1's loop order and the edges of the comment above (the SPEC dag
+ * module's rules).  Shared by the threaded executor and the oracle_dag_edges test hook. */
+static void dag_build(dag_ctx* D, int64_t p, int64_t q) {
+  int64_t K = p < q ? p : q;
   int64_t nt = 0;
   for (int64_t k = 0; k < K; ++k) nt += 1 + (q - k - 1) + (p - k - 1) + (p - k - 1) * (q - k - 1);
-  D.ntasks = nt;
-  D.tasks = (dag_task*)calloc(nt, sizeof(dag_task));
-  D.heap = (int64_t*)malloc(sizeof(int64_t) * nt);
-  D.idG = (int64_t*)malloc(sizeof(int64_t) * K);
-  D.idL = (int64_t*)malloc(sizeof(int64_t) * K * q);
-  D.idT = (int64_t*)malloc(sizeof(int64_t) * K * p);
-  D.idS = (int64_t*)malloc(sizeof(int64_t) * K * p * q);
-  D.efrom = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
-  D.eto = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
-#define IDL(k, j) D.idL[(k) * q + (j)]
-#define IDT(k, i) D.idT[(k) * p + (i)]
-#define IDS(k, i, j) D.idS[((k) * p + (i)) * q + (j)]
+  D->ntasks = nt;
+  D->tasks = (dag_task*)calloc(nt, sizeof(dag_task));
+  D->heap = (int64_t*)malloc(sizeof(int64_t) * nt);
+  D->idG = (int64_t*)malloc(sizeof(int64_t) * K);
+  D->idL = (int64_t*)malloc(sizeof(int64_t) * K * q);
+  D->idT = (int64_t*)malloc(sizeof(int64_t) * K * p);
+  D->idS = (int64_t*)malloc(sizeof(int64_t) * K * p * q);
+  D->efrom = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
+  D->eto = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
+#define IDL(k, j) D->idL[(k) * q + (j)]
+#define IDT(k, i) D->idT[(k) * p + (i)]
+#define IDS(k, i, j) D->idS[((k) * p + (i)) * q + (j)]
   int64_t id = 0;
   for (int64_t k = 0; k < K; ++k) {
-    D.tasks[id] = (dag_task){KG, k, k, k, 0}; D.idG[k] = id++;
-    for (int64_t j = k + 1; j < q; ++j) { D.tasks[id] = (dag_task){KL, k, k, j, 0}; IDL(k, j) = id++; }
+    D->tasks[id] = (dag_task){KG, k, k, k, 0}; D->idG[k] = id++;
+    for (int64_t j = k + 1; j < q; ++j) { D->tasks[id] = (dag_task){KL, k, k, j, 0}; IDL(k, j) = id++; }
     for (int64_t i = k + 1; i < p; ++i) {
-      D.tasks[id] = (dag_task){KT, k, i, k, 0}; IDT(k, i) = id++;
-      for (int64_t j = k + 1; j < q; ++j) { D.tasks[id] = (dag_task){KS, k, i, j, 0}; IDS(k, i, j) = id++; }
+      D->tasks[id] = (dag_task){KT, k, i, k, 0}; IDT(k, i) = id++;
+      for (int64_t j = k + 1; j < q; ++j) { D->tasks[id] = (dag_task){KS, k, i, j, 0}; IDS(k, i, j) = id++; }
     }
   }
   for (int64_t k = 0; k < K; ++k) {
-    if (k > 0) add_edge(&D, IDS(k - 1, k, k), D.idG[k]);
+    if (k > 0) add_edge(D, IDS(k - 1, k, k), D->idG[k]);
     for (int64_t j = k + 1; j < q; ++j) {
-      add_edge(&D, D.idG[k], IDL(k, j));
-      if (k > 0) add_edge(&D, IDS(k - 1, k, j), IDL(k, j));
+      add_edge(D, D->idG[k], IDL(k, j));
+      if (k > 0) add_edge(D, IDS(k - 1, k, j), IDL(k, j));
     }
     for (int64_t i = k + 1; i < p; ++i) {
-      add_edge(&D, i == k + 1 ? D.idG[k] : IDT(k, i - 1), IDT(k, i));
-      if (k > 0) add_edge(&D, IDS(k - 1, i, k), IDT(k, i));
+      add_edge(D, i == k + 1 ? D->idG[k] : IDT(k, i - 1), IDT(k, i));
+      if (k > 0) add_edge(D, IDS(k - 1, i, k), IDT(k, i));
       for (int64_t j = k + 1; j < q; ++j) {
-        add_edge(&D, IDT(k, i), IDS(k, i, j));
-        add_edge(&D, i == k + 1 ? IDL(k, j) : IDS(k, i - 1, j), IDS(k, i, j));
-        if (k > 0) add_edge(&D, IDS(k - 1, i, j), IDS(k, i, j));
+        add_edge(D, IDT(k, i), IDS(k, i, j));
+        add_edge(D, i == k + 1 ? IDL(k, j) : IDS(k, i - 1, j), IDS(k, i, j));
+        if (k > 0) add_edge(D, IDS(k - 1, i, j), IDS(k, i, j));
       }
     }
   }
 #undef IDL
 #undef IDT
 #undef IDS
+}
+
+static void dag_free(dag_ctx* D) {
+  free(D->tasks); free(D->heap); free(D->idG); free(D->idL); free(D->idT); free(D->idS);
+  free(D->efrom); free(D->eto); free(D->soff); free(D->succ);
+}
+
+/* Test hook: the DAG's edges for a p x q tile grid, 8 int64 per edge {kind, k, i, j} of the
+ * predecessor then of the successor (kind 0 G, 1 T, 2 L, 3 S; T(k,i) has j = k, G and L
+ * have i = k); returns the edge count, writes min(cap, count) edges. */
+int64_t oracle_dag_edges(int64_t p, int64_t q, int64_t* out, int64_t cap) {
+  if (p < 1 || q < 1) return -1;
+  dag_ctx D;
+  memset(&D, 0, sizeof(D));
+  dag_build(&D, p, q);
+  for (int64_t e = 0; e < D.nedge && e < cap; ++e) {
+    const dag_task* a = &D.tasks[D.efrom[e]];
+    const dag_task* b = &D.tasks[D.eto[e]];
+    int64_t* o = out + 8 * e;
+    o[0] = a->kind; o[1] = a->k; o[2] = a->i; o[3] = a->j;
+    o[4] = b->kind; o[5] = b->k; o[6] = b->i; o[7] = b->j;
+  }
+  int64_t n = D.nedge;
+  dag_free(&D);
+  return n;
+}
+
+static int geqrf_dag(const qr_ctx* X, int nthreads) {
+  dag_ctx D;
+  memset(&D, 0, sizeof(D));
+  D.X = *X;
+  dag_build(&D, X->p, X->q);
+  const int64_t nt = D.ntasks;
   D.soff = (int64_t*)calloc(nt + 1, sizeof(int64_t));
   D.succ = (int64_t*)malloc(sizeof(int64_t) * (D.nedge + 1));
   for (int64_t e = 0; e < D.nedge; ++e) D.soff[D.efrom[e] + 1]++;
@@ -498,8 +530,8 @@ static int geqrf_dag(const qr_ctx* X, int nthreads) {
   pthread_mutex_destroy(&D.mu);
   pthread_cond_destroy(&D.cv);
   int ok = (D.ndone == nt);
-  free(th); free(D.tasks); free(D.heap); free(D.idG); free(D.idL); free(D.idT); free(D.idS);
-  free(D.efrom); free(D.eto); free(D.soff); free(D.succ);
+  free(th);
+  dag_free(&D);
   return ok ? 0 : -99;
 }
 

@@ -68,6 +68,11 @@ double oracle_flops_standard(int64_t m, int64_t n);
 double oracle_kernel_flops(int kind, double b);
 double oracle_flops_eq4(int64_t p, int64_t q, double b);
 
+/* Test hook: the DAG edges of Algorithm 1 for a p x q grid (SPEC dag module rules), as 8 int64
+ * per edge {kind, k, i, j} of predecessor and successor (kind 0 G, 1 T, 2 L, 3 S).  Returns
+ * the edge count (-1 on bad p, q); writes at most cap edges. */
+int64_t oracle_dag_edges(int64_t p, int64_t q, int64_t* out, int64_t cap);
+
 /* Test hook: count of tasks executed by the last oracle_geqrf_tiles call, per kind. */
 void oracle_last_task_counts(int64_t counts[4]);
 

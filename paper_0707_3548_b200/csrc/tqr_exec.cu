@@ -569,12 +569,16 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
 template <int B, int S, int MODE, int RWM>
 static cudaError_t launch_mode(const ExecArgs& a, int grid, cudaStream_t st) {
   using L = Layout<B, Inner<B, S>::SI, RWM>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(exec_kernel<B, S, MODE, RWM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)L::BYTES);
+  // the shared-memory attribute is per device: cache it per device ordinal
+  constexpr int NDEV = 64;
+  static bool attr[NDEV] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= NDEV || !attr[dev]) {
+    e = cudaFuncSetAttribute(exec_kernel<B, S, MODE, RWM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L::BYTES);
     if (e != cudaSuccess) return e;
-    attr = true;
+    if (dev < NDEV) attr[dev] = true;
   }
   ExecArgs args = a;
   void* params[] = {&args};
@@ -649,54 +653,106 @@ int exec_max_ctas(int b, int s, int rwm, int device) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Layout kernels (Block Data Layout).  HBM-bound copies: one thread per
-// element, tile-row index fastest so both the column-major and the tile-major side are
-// contiguous runs of b doubles.
+// Layout kernels (Block Data Layout).  HBM-bound copies, organised by
+// RUNS: a run is column cc of tile (i, jl) -- B contiguous doubles in the tile-major array
+// and rows [i*B, i*B + B) of global column c = (coff + jl*cstride)*B + cc in the
+// column-major array.  Runs are numbered (jl*B + cc)*p + i, so consecutive runs continue one
+// column of the column-major side.  A warp moves a run (B >= 64) or 32/(B/2) runs (B < 64)
+// per iteration with 16-byte accesses, all of a lane's loads issued before its stores; the
+// index arithmetic (64-bit div/mod) is per run, not per element.  A run cropped at m / n,
+// or whose column-major start is not 16-byte aligned (odd leading dimension), goes scalar.
+// get_r skips the reads of runs wholly below the diagonal (zeros).
 // ---------------------------------------------------------------------------------------
-// tile-major element e of a (p x qloc tiles) storage array -> global (r, c); storage
-// column jl holds global tile column coff + jl*cstride
-__device__ __forceinline__ void tile_elem(int64_t e, int b, int64_t p, int cstride, int coff, int64_t& r, int64_t& c) {
-  const int64_t bb = (int64_t)b * b;
-  const int64_t tile = e / bb, in = e % bb;
-  const int64_t i = tile % p, jl = tile / p;
-  r = i * b + in % b;
-  c = ((int64_t)coff + jl * cstride) * b + in / b;
-}
-__global__ void pack_kernel(const double* __restrict__ A, int64_t lda, double* __restrict__ At, int64_t m, int64_t n,
-                            int b, int64_t p, int cstride, int coff, int64_t total) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r, c;
-    tile_elem(e, b, p, cstride, coff, r, c);
-    At[e] = (r < m && c < n) ? A[r + c * lda] : 0.0;
+enum RunOp { OP_PACK = 0, OP_UNPACK = 1, OP_GETR = 2, OP_EYE = 3 };
+
+template <int B, int OP>
+__global__ void __launch_bounds__(256) runs_kernel(const double* __restrict__ src, double* __restrict__ dst, int64_t ld,
+                                                   int64_t m, int64_t n, int64_t p, int cstride, int coff,
+                                                   int64_t nruns) {
+  constexpr int NV = B / 2;                     // double2 per run
+  constexpr int RPW = NV >= 32 ? 1 : 32 / NV;   // runs per warp iteration
+  constexpr int VPL = NV >= 32 ? NV / 32 : 1;   // double2 per lane per run
+  const int lane = threadIdx.x & 31;
+  const int sub = NV >= 32 ? 0 : lane / NV, x0 = NV >= 32 ? lane : lane % NV;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t kmin = m < n ? m : n;  // rows of R (GETR)
+  for (int64_t run = warp * RPW + sub; run < nruns; run += nw * RPW) {
+    const int64_t i = run % p, col = run / p;
+    const int64_t jl = col / B;
+    const int cc = (int)(col - jl * B);
+    const int64_t c = ((int64_t)coff + jl * cstride) * B + cc;  // global column
+    const int64_t r0 = i * B;                                   // global first row
+    const int64_t toff = ((i + jl * p) * B + cc) * B;           // run start, tile-major
+    if (OP == OP_EYE) {  // dst tile-major, columns < n (= k) and rows < m hold I
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) {
+        const int e = 2 * (x0 + 32 * v);
+        const double2 z = make_double2((r0 + e == c && c < n && r0 + e < m) ? 1.0 : 0.0,
+                                       (r0 + e + 1 == c && c < n && r0 + e + 1 < m) ? 1.0 : 0.0);
+        reinterpret_cast<double2*>(dst + toff)[x0 + 32 * v] = z;
+      }
+      continue;
+    }
+    const int64_t rows = OP == OP_GETR ? kmin : m;  // rows of the column-major side
+    const bool in_col = c < n;
+    const bool full = in_col && r0 + B <= rows;
+    const bool al = ((c * ld) & 1) == 0;            // 16-byte aligned column-major run start
+    const double* s_ = OP == OP_PACK ? src + c * ld + r0 : src + toff;
+    double* d_ = OP == OP_PACK ? dst + toff : dst + c * ld + r0;
+    if (OP != OP_PACK && !in_col) continue;         // nothing to write
+    if (OP == OP_GETR && r0 > c) {                  // wholly below the diagonal: zeros, no read
+      if (full && al) {
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) reinterpret_cast<double2*>(d_)[x0 + 32 * v] = make_double2(0.0, 0.0);
+      } else {
+        for (int e = x0; e < B; e += (NV >= 32 ? 32 : NV))
+          if (r0 + e < rows) d_[e] = 0.0;
+      }
+      continue;
+    }
+    if (OP == OP_PACK && !in_col) {                 // padding column
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) reinterpret_cast<double2*>(d_)[x0 + 32 * v] = make_double2(0.0, 0.0);
+      continue;
+    }
+    if (full && al) {
+      double2 t[VPL];
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) t[v] = __ldcs(reinterpret_cast<const double2*>(s_) + x0 + 32 * v);
+      if (OP == OP_GETR && r0 + B - 1 > c) {        // diagonal run: zeros below row c
+#pragma unroll
+        for (int v = 0; v < VPL; ++v) {
+          const int64_t r = r0 + 2 * (x0 + 32 * v);
+          if (r > c) t[v].x = 0.0;
+          if (r + 1 > c) t[v].y = 0.0;
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < VPL; ++v) reinterpret_cast<double2*>(d_)[x0 + 32 * v] = t[v];
+    } else {                                         // cropped or unaligned run: scalar
+      for (int e = x0; e < B; e += (NV >= 32 ? 32 : NV)) {
+        const int64_t r = r0 + e;
+        if (OP == OP_PACK) d_[e] = r < m ? s_[e] : 0.0;
+        else if (r < rows) d_[e] = (OP == OP_GETR && r > c) ? 0.0 : s_[e];
+      }
+    }
   }
 }
-__global__ void unpack_kernel(const double* __restrict__ At, double* __restrict__ A, int64_t lda, int64_t m, int64_t n,
-                              int b, int64_t p, int cstride, int coff, int64_t total) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r, c;
-    tile_elem(e, b, p, cstride, coff, r, c);
-    if (r < m && c < n) A[r + c * lda] = At[e];
-  }
-}
-// R = upper trapezoid (k = min(m,n) rows), zeros below the diagonal; only the tile columns
-// held by this storage array are written
-__global__ void get_r_kernel(const double* __restrict__ At, double* __restrict__ R, int64_t ldr, int64_t m, int64_t n,
-                             int b, int64_t p, int cstride, int coff, int64_t total) {
-  const int64_t k = m < n ? m : n;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r, c;
-    tile_elem(e, b, p, cstride, coff, r, c);
-    if (r < k && c < n) R[r + c * ldr] = (r <= c) ? At[e] : 0.0;
-  }
-}
-__global__ void eye_tiles_kernel(double* __restrict__ Qt, int64_t m, int64_t k, int b, int64_t p, int64_t total) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t bb = (int64_t)b * b;
-    const int64_t tile = e / bb, in = e % bb;
-    const int64_t i = tile % p, jt = tile / p;
-    const int64_t r = i * b + in % b, c = jt * b + in / b;
-    Qt[e] = (r == c && c < k && r < m) ? 1.0 : 0.0;
-  }
+
+template <int OP>
+static cudaError_t launch_runs(int b, const double* src, double* dst, int64_t ld, int64_t m, int64_t n, int64_t p,
+                               int64_t qloc, int cstride, int coff, cudaStream_t st) {
+  const int64_t nruns = p * qloc * (int64_t)b;
+  if (nruns == 0) return cudaSuccess;
+  const int rpw = b >= 64 ? 1 : 32 / (b / 2);
+  int64_t g = ((nruns + rpw - 1) / rpw + 7) / 8;   // 8 warps per block
+  if (g > 148 * 8) g = 148 * 8;                    // 8 resident 256-thread blocks per SM
+#define RUNS_B(BB) \
+  if (b == BB) { runs_kernel<BB, OP><<<(unsigned)g, 256, 0, st>>>(src, dst, ld, m, n, p, cstride, coff, nruns); return cudaGetLastError(); }
+  RUNS_B(16) RUNS_B(32) RUNS_B(64) RUNS_B(128) RUNS_B(256) RUNS_B(512)
+#undef RUNS_B
+  return cudaErrorInvalidValue;
 }
 
 // Packed reflector panels for apply-Q from the boundary factors (At, T): the same Yp/Tp
@@ -807,24 +863,15 @@ static int grid_for(int64_t total) {
 
 cudaError_t launch_pack(const double* A, int64_t lda, double* At, int64_t m, int64_t n, int b, int64_t p,
                         int64_t qloc, int cstride, int coff, cudaStream_t st) {
-  const int64_t total = p * qloc * (int64_t)b * b;
-  if (total == 0) return cudaSuccess;
-  pack_kernel<<<grid_for(total), 256, 0, st>>>(A, lda, At, m, n, b, p, cstride, coff, total);
-  return cudaGetLastError();
+  return launch_runs<OP_PACK>(b, A, At, lda, m, n, p, qloc, cstride, coff, st);
 }
 cudaError_t launch_unpack(const double* At, double* A, int64_t lda, int64_t m, int64_t n, int b, int64_t p,
                           int64_t qloc, int cstride, int coff, cudaStream_t st) {
-  const int64_t total = p * qloc * (int64_t)b * b;
-  if (total == 0) return cudaSuccess;
-  unpack_kernel<<<grid_for(total), 256, 0, st>>>(At, A, lda, m, n, b, p, cstride, coff, total);
-  return cudaGetLastError();
+  return launch_runs<OP_UNPACK>(b, At, A, lda, m, n, p, qloc, cstride, coff, st);
 }
 cudaError_t launch_get_r(const double* At, double* R, int64_t ldr, int64_t m, int64_t n, int b, int64_t p,
                          int64_t qloc, int cstride, int coff, cudaStream_t st) {
-  const int64_t total = p * qloc * (int64_t)b * b;
-  if (total == 0) return cudaSuccess;
-  get_r_kernel<<<grid_for(total), 256, 0, st>>>(At, R, ldr, m, n, b, p, cstride, coff, total);
-  return cudaGetLastError();
+  return launch_runs<OP_GETR>(b, At, R, ldr, m, n, p, qloc, cstride, coff, st);
 }
 
 // Cross-rank entry barrier (real multi-GPU): every rank publishes `gen` into arrive[me] of
@@ -902,9 +949,7 @@ cudaError_t launch_form_t(const double* A, double* T, int b, int s, int64_t p, i
 }
 
 cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qb, cudaStream_t st) {
-  const int64_t total = p * qb * (int64_t)b * b;
-  eye_tiles_kernel<<<grid_for(total), 256, 0, st>>>(Qt, m, k, b, p, total);
-  return cudaGetLastError();
+  return launch_runs<OP_EYE>(b, nullptr, Qt, 0, m, k, p, qb, 1, 0, st);
 }
 
 }  // namespace tqr

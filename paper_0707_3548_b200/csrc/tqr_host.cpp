@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -47,6 +48,30 @@ tqr_status cuda_fail(cudaError_t e, const char* where) {
   g_err = std::string(where) + ": " + cudaGetErrorString(e);
   return TQR_ERR_CUDA;
 }
+// The caller's current device is restored on return from every entry point that touches a
+// device (calls may come from a thread whose current device is another GPU).
+struct DevGuard {
+  int prev = -1;
+  cudaError_t err = cudaSuccess;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) err = cudaSetDevice(dev);
+    else prev = -1;
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+// include/tqr.h: every data pointer must be 16-byte aligned (TMA bulk copies and 16-byte
+// vector accesses); a misaligned pointer is an invalid argument, not a device fault
+static inline bool misaligned(const void* p) { return ((uintptr_t)p & 15u) != 0; }
+#define GUARD(P)                                                         \
+  DevGuard dg_((P)->prm.device);                                         \
+  if (dg_.err != cudaSuccess) return cuda_fail(dg_.err, "cudaSetDevice")
+#define ALIGNED(ptr, idx)                                                         \
+  do {                                                                            \
+    if (misaligned(ptr)) return bad_arg(idx, #ptr " is not 16-byte aligned");     \
+  } while (0)
 #define CU(call)                                            \
   do {                                                      \
     cudaError_t e_ = (call);                                \
@@ -677,7 +702,8 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || p->device < 0 || p->device >= ndev)
     return bad_arg(5, "device ordinal not available");
-  CU(cudaSetDevice(p->device));
+  DevGuard dg_(p->device);
+  if (dg_.err != cudaSuccess) return cuda_fail(dg_.err, "cudaSetDevice");
   tqr_plan* P = new tqr_plan();
   P->prm = *p;
   P->p = (p->m + p->b - 1) / p->b;
@@ -777,6 +803,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
 
 tqr_status tqr_plan_destroy(tqr_plan* P) {
   if (!P) return bad_arg(1, "plan is NULL");
+  GUARD(P);
   destroy_plan(P);
   return TQR_OK;
 }
@@ -806,6 +833,7 @@ tqr_status tqr_comm_export(tqr_plan* P, void* blob) {
   x.nranks = P->G;
   x.bytes = P->lay.bytes;
   x.m = P->prm.m; x.n = P->prm.n; x.b = P->prm.b; x.s = P->prm.s;
+  GUARD(P);
   CU(cudaIpcGetMemHandle(&x.h, P->sym_own[P->me]));
   std::memset(blob, 0, TQR_IPC_BLOB_BYTES);
   std::memcpy(blob, &x, sizeof(x));
@@ -820,7 +848,7 @@ tqr_status tqr_comm_connect(tqr_plan* P, const void* blobs) {
     return TQR_ERR_UNSUPPORTED;
   }
   if (P->connected) return TQR_OK;
-  CU(cudaSetDevice(P->prm.device));
+  GUARD(P);
   for (int g = 0; g < P->G; ++g) {
     IpcBlob x;
     std::memcpy(&x, (const char*)blobs + (size_t)g * TQR_IPC_BLOB_BYTES, sizeof(x));
@@ -850,6 +878,7 @@ tqr_status tqr_comm_ping(tqr_plan* P, int32_t magic) {
     g_err = "tqr_comm_ping: needs a connected real multi-rank plan";
     return TQR_ERR_UNSUPPORTED;
   }
+  GUARD(P);
   int* pings[MAX_RANKS] = {};
   for (int g = 0; g < P->G; ++g) pings[g] = ping_of(P->arrive[g]);
   CU(launch_ping(pings, P->G, P->me, magic, P->st));
@@ -897,6 +926,9 @@ tqr_status tqr_pack(tqr_plan* P, const double* A, int64_t lda, double* At) {
   if (!A) return bad_arg(2, "A is NULL");
   if (lda < P->prm.m) return bad_arg(3, "lda < m");
   if (!At) return bad_arg(4, "At is NULL");
+  ALIGNED(A, 2);
+  ALIGNED(At, 4);
+  GUARD(P);
   int cs, co;
   colmap(P, &cs, &co);
   CU(launch_pack(A, lda, At, P->prm.m, P->prm.n, P->prm.b, P->p, qloc_of(P, P->me), cs, co, P->st));
@@ -907,6 +939,9 @@ tqr_status tqr_unpack(tqr_plan* P, const double* At, double* A, int64_t lda) {
   if (!At) return bad_arg(2, "At is NULL");
   if (!A) return bad_arg(3, "A is NULL");
   if (lda < P->prm.m) return bad_arg(4, "lda < m");
+  ALIGNED(At, 2);
+  ALIGNED(A, 3);
+  GUARD(P);
   int cs, co;
   colmap(P, &cs, &co);
   CU(launch_unpack(At, A, lda, P->prm.m, P->prm.n, P->prm.b, P->p, qloc_of(P, P->me), cs, co, P->st));
@@ -917,6 +952,9 @@ tqr_status tqr_get_r(tqr_plan* P, const double* At, double* R, int64_t ldr) {
   if (!At) return bad_arg(2, "At is NULL");
   if (!R) return bad_arg(3, "R is NULL");
   if (ldr < std::min(P->prm.m, P->prm.n)) return bad_arg(4, "ldr < min(m, n)");
+  ALIGNED(At, 2);
+  ALIGNED(R, 3);
+  GUARD(P);
   int cs, co;
   colmap(P, &cs, &co);
   CU(launch_get_r(At, R, ldr, P->prm.m, P->prm.n, P->prm.b, P->p, qloc_of(P, P->me), cs, co, P->st));
@@ -928,6 +966,10 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   if (!At) return bad_arg(2, "At is NULL");
   if (!T) return bad_arg(3, "T is NULL");
   if (!work && P->G == 1) return bad_arg(4, "work is NULL (tqr_workspace_size bytes required)");
+  ALIGNED(At, 2);
+  ALIGNED(T, 3);
+  ALIGNED(work, 4);
+  GUARD(P);
   if (P->real && !P->connected) {
     g_err = "multi-rank plan not connected (tqr_comm_export / tqr_comm_connect)";
     return TQR_ERR_UNSUPPORTED;
@@ -993,6 +1035,11 @@ static tqr_status ormqr_impl(tqr_plan* P, char trans, const double* At, const do
   if (!Bt) return bad_arg(5, "Bt is NULL");
   if (nrhs < 1) return bad_arg(6, "nrhs < 1");
   if (!work) return bad_arg(7, "work is NULL (tqr_workspace_size bytes required)");
+  ALIGNED(At, 3);
+  ALIGNED(T, 4);
+  ALIGNED(Bt, 5);
+  ALIGNED(work, 7);
+  GUARD(P);
   if (P->G > 1) {
     g_err = "apply-Q is single-GPU in this version";
     return TQR_ERR_UNSUPPORTED;
@@ -1018,6 +1065,11 @@ tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, 
   if (k < 1 || k > P->prm.m) return bad_arg(4, "k outside [1, m]");
   if (!Qt) return bad_arg(5, "Qt is NULL");
   if (!work) return bad_arg(6, "work is NULL (tqr_workspace_size bytes required)");
+  ALIGNED(At, 2);
+  ALIGNED(T, 3);
+  ALIGNED(Qt, 5);
+  ALIGNED(work, 6);
+  GUARD(P);
   if (P->G > 1) {
     g_err = "form-Q is single-GPU in this version";
     return TQR_ERR_UNSUPPORTED;
@@ -1029,6 +1081,7 @@ tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, 
 
 tqr_status tqr_sync(tqr_plan* P) {
   if (!P) return bad_arg(1, "plan is NULL");
+  GUARD(P);
   CU(cudaStreamSynchronize(P->st));
   CU(cudaGetLastError());
   return TQR_OK;
@@ -1077,6 +1130,36 @@ tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t wo
   return TQR_OK;
 }
 
+tqr_status tqr_plan_records(tqr_plan* P, int32_t local, int32_t* rec, int64_t cap, int64_t* n) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (local < 0 || local >= (int32_t)P->fact.d_tasks.size()) return bad_arg(2, "local rank index out of range");
+  if (!rec && cap > 0) return bad_arg(3, "rec is NULL");
+  if (!n) return bad_arg(5, "n is NULL");
+  *n = P->fact.ntasks[local];
+  const int64_t c = std::min<int64_t>(cap, *n);
+  if (c > 0)
+    CU(cudaMemcpy(rec, P->fact.d_tasks[local], sizeof(int32_t) * (size_t)c * TASK_INTS, cudaMemcpyDeviceToHost));
+  return TQR_OK;
+}
+
+tqr_status tqr_plan_info(const tqr_plan* P, int32_t info[12]) {
+  if (!P) return bad_arg(1, "plan is NULL");
+  if (!info) return bad_arg(2, "info is NULL");
+  info[0] = P->rwm;
+  info[1] = P->passes;
+  info[2] = P->nsl;
+  info[3] = P->split ? 1 : 0;
+  info[4] = P->early ? 1 : 0;
+  info[5] = P->workers;
+  info[6] = P->prio;
+  info[7] = P->fine;
+  info[8] = exec_inner(P->prm.b, P->prm.s);
+  info[9] = P->G;
+  info[10] = P->nloc;
+  info[11] = exec_slice(P->prm.b, P->prm.s, P->rwm);
+  return TQR_OK;
+}
+
 tqr_status tqr_trace_fetch(tqr_plan* P, int64_t* rec, int64_t cap, int64_t* n) {
   if (!P) return bad_arg(1, "plan is NULL");
   if (!rec && cap > 0) return bad_arg(2, "rec is NULL");
@@ -1117,6 +1200,7 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
     g_err = "profiling needs a single-rank plan with p >= 2 and q >= 2";
     return TQR_ERR_UNSUPPORTED;
   }
+  GUARD(P);
   Sched s;
   s.rec.assign(1, std::vector<int>((size_t)count * TASK_INTS, 0));
   for (int64_t t = 0; t < count; ++t) {

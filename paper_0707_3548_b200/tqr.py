@@ -77,6 +77,8 @@ def lib():
         L.tqr_comm_flags.argtypes = [_vp, _vp]
         L.tqr_schedule_records.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _vp, _i64, ctypes.POINTER(_i64),
                                            ctypes.POINTER(_i32)]
+        L.tqr_plan_records.argtypes = [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]
+        L.tqr_plan_info.argtypes = [_vp, ctypes.POINTER(_i32)]
         _lib = L
     return _lib
 
@@ -253,6 +255,23 @@ class Plan:
     def phase_counters(self, d_counters):
         """Attach an int64 CUDA tensor of 16 phase-cycle totals (profiling builds only)."""
         _check(lib().tqr_phase_counters(self._h, None if d_counters is None else d_counters.data_ptr()))
+
+    def records(self, local: int = 0):
+        """The factorization dispatch records this plan executes (numpy int32 (ntasks, 16))."""
+        import numpy as np
+        n = _i64()
+        _check(lib().tqr_plan_records(self._h, local, None, 0, ctypes.byref(n)))
+        rec = np.zeros((max(1, n.value), TASK_INTS), dtype=np.int32)
+        _check(lib().tqr_plan_records(self._h, local, rec.ctypes.data, n.value, ctypes.byref(n)))
+        return rec[: n.value]
+
+    def info(self) -> dict:
+        """The plan's policy (include/tqr.h tqr_plan_info)."""
+        v = (_i32 * 12)()
+        _check(lib().tqr_plan_info(self._h, v))
+        keys = ("rwm", "passes", "nsl", "split", "early", "workers", "prio", "fine", "inner", "nranks", "nloc",
+                "slice")
+        return dict(zip(keys, list(v)))
 
     def trace(self, cap: int = 1 << 22):
         import numpy as np

@@ -63,8 +63,10 @@ def test_emulated_ranks_repeat_and_trace():
     plan.sync()
     assert np.array_equal(At.cpu().numpy(), g1["At"])
     rec = plan.trace()
-    assert len(rec) == sum(1 for _ in range(len(rec)))
+    # one trace record per executed task of the last call, over all four ranks' streams
+    assert len(rec) == sum(len(plan.records(li)) for li in range(4))
     assert set(np.unique(rec[:, 0])) == {0, 1, 2, 3}
+    assert np.all(rec[:, 7] >= rec[:, 6])  # end >= start
 
 
 @pytest.mark.parametrize("G", [2, 3])

@@ -41,7 +41,7 @@ def test_factor_parity(m, n, b, s, dist):
     nA = np.linalg.norm(A)
     err = np.max(np.abs(np.triu(g["R"]) - np.triu(R_o)))
     assert err <= 1e-10 * nA, f"R mismatch {err:.3e} > {1e-10 * nA:.3e}"
-    assert np.array_equal(np.tril(g["R"], -1), np.zeros_like(g["R"]) * 0) or np.all(np.tril(g["R"], -1) == 0)
+    assert np.all(np.tril(g["R"], -1) == 0), "get_r writes exact zeros below the diagonal"
     # V and T (diagnostic, same tolerance scale)
     assert np.max(np.abs(g["At"] - At_o)) <= 1e-9 * max(1.0, nA)
     assert np.max(np.abs(g["T"] - T_o)) <= 1e-9 * max(1.0, nA)
@@ -74,7 +74,10 @@ def test_ormqr_parity(m, n, b, s, nrhs, trans):
     plan.sync()
     got = oracle.unpack(Bt.cpu().numpy(), m, nrhs, b)
     want = oracle.ormqr(g["At"], g["T"], m, n, b, s, Bm, 1 if trans == "T" else 0, nthreads=4)
-    assert np.max(np.abs(got - want)) <= 1e-12 * max(1.0, np.linalg.norm(Bm)) * m
+    # an orthogonal transformation of each column: the GPU and the oracle differ only in
+    # rounding order, so every column agrees to a few ulps of its norm (10 m eps, relative)
+    col_err = np.linalg.norm(got - want, axis=0) / np.linalg.norm(Bm, axis=0)
+    assert np.max(col_err) <= 10 * m * EPS, np.max(col_err)
 
 
 @pytest.mark.parametrize("m,n,b,s", [(256, 256, 64, 16), (700, 600, 256, 32), (520, 300, 128, 32),
@@ -91,7 +94,7 @@ def test_orgqr_and_backward_error_on_gpu(m, n, b, s):
     plan.sync()
     Q = oracle.unpack(Qt.cpu().numpy(), m, k, b)
     Q_o = oracle.orgqr(g["At"], g["T"], m, n, b, s, k=k, nthreads=4)
-    assert np.max(np.abs(Q - Q_o)) <= 1e-12 * m
+    assert np.max(np.abs(Q - Q_o)) <= 10 * m * EPS  # unit-norm columns: 10 m eps absolute
     nA = np.linalg.norm(A)
     assert np.linalg.norm(A - Q @ g["R"]) / (nA * n * EPS) < 10
     assert np.linalg.norm(np.eye(k) - Q.T @ Q) / (n * EPS) < 10
@@ -119,3 +122,46 @@ def test_repeat_bitwise_stress(m, n, b, s, reps):
     for _ in range(reps - 1):
         g = run_factor(A, b, s)
         assert np.array_equal(g["At"], g0["At"]) and np.array_equal(g["T"], g0["T"])
+
+
+def test_misaligned_pointers_are_invalid_args():
+    """include/tqr.h: data pointers must be 16-byte aligned; a misaligned one is reported as
+    TQR_ERR_INVALID_ARG with its argument index (not a TMA fault), and the caller's current
+    device is left as it was."""
+    import torch
+    from paper_0707_3548_b200 import Plan
+    from paper_0707_3548_b200.tqr import TqrError
+    plan = Plan(64, 64, 16, 8)
+    At, T = plan.alloc()
+    A = torch.zeros(64 * 64 + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(TqrError) as e:
+        plan.pack(A[1:], At)              # 8-byte offset
+    assert e.value.status == 1 and e.value.bad_arg == 2
+    big = torch.zeros(At.numel() + 1, dtype=torch.float64, device="cuda")
+    with pytest.raises(TqrError) as e:
+        plan.geqrf(big[1:], T)
+    assert e.value.status == 1 and e.value.bad_arg == 2
+    assert torch.cuda.current_device() == 0
+    plan.pack(A[:-1], At)                 # aligned: fine
+    plan.sync()
+
+
+def test_layout_roundtrip_odd_leading_dimension():
+    """pack/unpack/get_r with an odd leading dimension (unaligned column starts take the
+    scalar path of the run kernels) and ragged tiles: bitwise round trip, exact R layout."""
+    import torch
+    from paper_0707_3548_b200 import Plan
+    for m, n, b, s in ((67, 41, 16, 8), (301, 257, 64, 16), (999, 130, 128, 32), (513, 700, 256, 32)):
+        A = tqr_inputs.uniform(m, n, 8 + m)
+        Ac = torch.from_numpy(np.ascontiguousarray(A.T)).cuda()
+        plan = Plan(m, n, b, s)
+        At, T = plan.alloc()
+        plan.pack(Ac, At)
+        back = torch.full_like(Ac, 7.0)
+        plan.unpack(At, back)
+        R = torch.full((n, min(m, n)), 7.0, dtype=torch.float64, device="cuda")
+        plan.get_r(At, R)
+        plan.sync()
+        assert torch.equal(back, Ac)
+        assert np.array_equal(At.cpu().numpy(), oracle.pack(A, b))
+        np.testing.assert_array_equal(R.cpu().numpy().T, np.triu(A[:min(m, n), :]))

@@ -434,6 +434,123 @@ def test_threaded_dag_bitwise_equals_sequential(nthreads):
     assert c1["S"] == sum((p - k - 1) * (q - k - 1) for k in range(K))
 
 
+# ---- the oracle's DAG edges -------------------------
+def _spec_edges(p, q):
+    """SPEC.md:334-337 restated 0-based (k = 0 .. min(p,q)-1): predecessor -> successor."""
+    E = set()
+    for k in range(min(p, q)):
+        G = ("G", k, k, k)
+        if k > 0:
+            E.add((("S", k - 1, k, k), G))
+        for j in range(k + 1, q):
+            E.add((G, ("L", k, k, j)))
+            if k > 0:
+                E.add((("S", k - 1, k, j), ("L", k, k, j)))
+        for i in range(k + 1, p):
+            E.add((G if i == k + 1 else ("T", k, i - 1, k), ("T", k, i, k)))
+            if k > 0:
+                E.add((("S", k - 1, i, k), ("T", k, i, k)))
+            for j in range(k + 1, q):
+                E.add((("T", k, i, k), ("S", k, i, j)))
+                E.add((("L", k, k, j) if i == k + 1 else ("S", k, i - 1, j), ("S", k, i, j)))
+                if k > 0:
+                    E.add((("S", k - 1, i, j), ("S", k, i, j)))
+    return E
+
+
+def _sequential_tasks(p, q):
+    """Algorithm 1's loop order."""
+    out = []
+    for k in range(min(p, q)):
+        out.append(("G", k, k, k))
+        out += [("L", k, k, j) for j in range(k + 1, q)]
+        for i in range(k + 1, p):
+            out.append(("T", k, i, k))
+            out += [("S", k, i, j) for j in range(k + 1, q)]
+    return out
+
+
+def _access(t):
+    """(reads, writes) of a task over data regions, from the kernels' definitions (SURVEY
+    8(c) c-3..c-6): A(k,k) is split into its upper triangle 'R' (R_kk) and strict lower part
+    'V' (V_kk) -- TSQRT touches only R_kk, LARFB reads only V_kk."""
+    kind, k, i, j = t
+    if kind == "G":
+        r, w = set(), {("R", k, k), ("V", k, k), ("T", k, k)}
+    elif kind == "L":
+        r, w = {("V", k, k), ("T", k, k)}, {("A", k, j)}
+    elif kind == "T":
+        r, w = set(), {("R", k, k), ("A", i, k), ("T", i, k)}
+    else:
+        r, w = {("A", i, k), ("T", i, k)}, {("A", k, j), ("A", i, j)}
+
+    def split(regs):  # a diagonal tile as a whole (update target) = its R and V parts
+        out = set()
+        for x in regs:
+            out |= {("R", x[1], x[1]), ("V", x[1], x[1])} if x[0] == "A" and x[1] == x[2] else {x}
+        return out
+    return split(r), split(w)
+
+
+def _verify_serialization(p, q, edges):
+    """Every pair of tasks that conflict (one writes a region the other reads or writes) must
+    be ordered by a DAG path in Algorithm 1's sequential order, and every edge must join two
+    conflicting tasks in that order.  Returns a list of violations."""
+    tasks = _sequential_tasks(p, q)
+    pos = {t: n for n, t in enumerate(tasks)}
+    succ = {t: set() for t in tasks}
+    for a, b in edges:
+        succ[a].add(b)
+    reach = {}
+    for t in reversed(tasks):   # reachability; a cycle shows up as an order violation below
+        r = set()
+        for u in succ[t]:
+            r.add(u)
+            r |= reach.get(u, set())
+        reach[t] = r
+    acc = {t: _access(t) for t in tasks}
+    bad = []
+    for a, b in edges:
+        (ra, wa), (rb, wb) = acc[a], acc[b]
+        if pos[a] >= pos[b] or not (wa & (rb | wb) or wb & ra):
+            bad.append(("edge", a, b))
+    for x in range(len(tasks)):
+        a = tasks[x]
+        ra, wa = acc[a]
+        for y in range(x + 1, len(tasks)):
+            b = tasks[y]
+            rb, wb = acc[b]
+            if (wa & (rb | wb) or wb & ra) and b not in reach[a]:
+                bad.append(("unordered", a, b))
+    return bad
+
+
+@pytest.mark.parametrize("p,q", [(1, 1), (2, 2), (3, 3), (4, 2), (2, 4), (5, 3), (3, 6)])
+def test_dag_edges_equal_spec_and_serialize(p, q):
+    """The oracle's edge set equals SPEC.md:334-337 exactly, every edge is a read/write
+    conflict of the kernels in Algorithm 1's order, and every conflicting pair is ordered."""
+    got = oracle.dag_edges(p, q)
+    assert len(got) == len(set(got))
+    assert set(got) == _spec_edges(p, q)
+    assert _verify_serialization(p, q, got) == []
+    if p == q == 2:   # SPEC.md:341 worked example: G(2)'s sole predecessor is S(1,2,2)
+        assert [a for a, b in got if b == ("G", 1, 1, 1)] == [("S", 0, 1, 1)]
+    if p == q == 1:
+        assert got == []
+
+
+def test_dag_edge_drop_or_flip_is_detected():
+    """Negative check of the pin: removing or reversing ANY single edge of the 3 x 3 DAG
+    (Fig. 3's instance) leaves a conflicting pair unordered or breaks the order."""
+    edges = oracle.dag_edges(3, 3)
+    for e in range(len(edges)):
+        dropped = edges[:e] + edges[e + 1:]
+        assert _verify_serialization(3, 3, dropped), f"dropping {edges[e]} went unnoticed"
+        a, b = edges[e]
+        flipped = edges[:e] + [(b, a)] + edges[e + 1:]
+        assert _verify_serialization(3, 3, flipped), f"flipping {edges[e]} went unnoticed"
+
+
 def test_dag_node_counts_golden():
     cases = json.load(open(os.path.join(GOLDEN, "dag_counts.json")))["cases"]
     for c in cases:
