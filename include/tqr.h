@@ -110,12 +110,19 @@ tqr_status tqr_get_r(tqr_plan* plan, const double* At, double* R, int64_t ldr);
 
 /* Apply Q^T (trans = 'T') or Q (trans = 'N') from the factors (At, T) to a tile-major
  * m x nrhs matrix Bt laid out like At (p row tiles, ceil(nrhs/b) tile columns),
- * in place.  (DORMQR analogue; reading R8.) */
+ * in place.  (DORMQR analogue; reading R8.)
+ * Multi-rank plans: COLLECTIVE (every rank calls it with the same trans, nrhs).  Bt is 1D
+ * block-cyclic like At (a real rank holds B's tile columns jb == rank mod nranks, storage
+ * column jb / nranks; emulated plans the global grid); each rank packs the reflector panels
+ * of its own columns of (At, T) into every rank's workspace over peer memory between two
+ * device-side rank barriers, then applies Q to its own columns of B with no further
+ * exchange.  `work` may be NULL (the plan owns the workspaces). */
 tqr_status tqr_ormqr(tqr_plan* plan, char trans, const double* At, const double* T,
                      double* Bt, int64_t nrhs, void* work);
 
 /* Form the first k columns of Q explicitly (Q [I_k; 0]) into tile-major Qt
- * (p row tiles, ceil(k/b) tile columns); 1 <= k <= m.  (DORGQR analogue.) */
+ * (p row tiles, ceil(k/b) tile columns); 1 <= k <= m.  (DORGQR analogue.)
+ * Multi-rank plans: collective, Qt block-cyclic as Bt of tqr_ormqr. */
 tqr_status tqr_orgqr(tqr_plan* plan, const double* At, const double* T, int64_t k,
                      double* Qt, void* work);
 
@@ -176,6 +183,14 @@ tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t wo
 tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, int32_t rank,
                                 int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr);
 
+/* Scaling MODEL (not a measurement; pure host): the list-schedule simulation the dispatch order
+ * comes from, run for an m x n factorization with the plan policy for (b, s) on `nranks`
+ * ranks of `workers` CTAs each (1D block-cyclic columns), task durations from the B200-fitted
+ * duration model, plus `remote_ns` on every dependency whose producer runs on another rank.
+ * *makespan_ns = modelled factorization time; *busy (may be NULL) = modelled utilisation. */
+tqr_status tqr_schedule_model(int64_t m, int64_t n, int32_t b, int32_t s, int32_t nranks, int32_t workers,
+                              double remote_ns, double* makespan_ns, double* busy);
+
 /* The factorization dispatch records THIS plan executes (same 16-int32 layout), for its
  * local rank index `local` (0 .. ranks run by this process - 1; emulated plans run every
  * rank): *n = task count, up to `cap` records copied to host `rec` (synchronous device copy).
@@ -195,8 +210,9 @@ tqr_status tqr_plan_info(const tqr_plan* plan, int32_t info[12]);
  * returns the number of records written in *n. */
 tqr_status tqr_trace_fetch(tqr_plan* plan, int64_t* rec, int64_t cap, int64_t* n);
 
-/* Profiling aid: run `count` mutually independent tasks of one kind (0 = GEQRT, 1 = TSQRT,
- * 2 = LARFB slice, 3 = SSRFB slice) through the same persistent executor on the plan's
+/* Profiling aid: run `count` mutually independent tasks of one kind (0 = GEQRT, 1 = TSQRT
+ * (whole tiles), 2 = LARFB slice, 3 = SSRFB slice, 4..7 the apply-Q kinds, 8 / 9 = the factor
+ * part alone of one inner block of a GEQRT / TSQRT, R21) through the same persistent executor on the plan's
  * tiles, with no DAG dependencies.  Results in At/T are meaningless afterwards (tasks race
  * on shared tiles); only the timing is.  Used to profile one kernel body in isolation with
  * ncu.  Requires p >= 2 and q >= 2. */

@@ -266,10 +266,13 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   } else {
     // meanwhile the other warps store the packed Y_l into every rank's workspace (the V
     // broadcast of SURVEY 8(e), fused into the panel task: peer stores over NVLink on a
-    // multi-GPU job, local stores otherwise)
-    for (int g = 0; g < a.nranks; ++g) {
-      double* dst = a.Yp[g] + yoff + (size_t)l * B * S;
-      for (int e = tid - 32 * NTW; e < B * S; e += C::NT - 32 * NTW) __stcg(dst + e, Ys[e]);
+    // multi-GPU job, local stores otherwise).  One flat loop over (rank, 16-byte chunk), so
+    // the stores to all G ranks are in flight together (not one rank after another).
+    constexpr int NV2 = B * S / 2;
+    const double2* ys2 = reinterpret_cast<const double2*>(Ys);
+    for (int e = tid - 32 * NTW; e < a.nranks * NV2; e += C::NT - 32 * NTW) {
+      const int g = e / NV2, x = e - g * NV2;
+      __stcg(reinterpret_cast<double2*>(a.Yp[g] + yoff + (size_t)l * B * S) + x, ys2[x]);
     }
   }
   __syncthreads();
@@ -280,9 +283,12 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   const int Lo = l / RB_, mo = (l % RB_) * S;
   for (int e = tid; e < S * S; e += C::NT) {
     const int r = e % S, c = e / S;
-    const double v = Tp[e];
-    __stcg(Tslot + ((size_t)Lo * SO + mo + c) * SO + mo + r, v);
-    for (int g = 0; g < a.nranks; ++g) __stcg(a.Tp[g] + toff + (size_t)l * S * S + swz<S>(r, c), v);
+    __stcg(Tslot + ((size_t)Lo * SO + mo + c) * SO + mo + r, Tp[e]);
+  }
+  for (int e = tid; e < a.nranks * S * S; e += C::NT) {  // packed T_l to every rank, flat
+    const int g = e / (S * S), x = e - g * (S * S);
+    const int r = x % S, c = x / S;
+    __stcg(a.Tp[g] + toff + (size_t)l * S * S + swz<S>(r, c), Tp[x]);
   }
   if (a.sys) __threadfence_system();  // peer stores ordered before the counter release
   // packed panels (generic stores) -> TMA reads of the next block of THIS task; a later task
@@ -380,11 +386,14 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
       for (int d = 0; d < TASK_NDEP; ++d) {
         const int code = s_task[8 + 2 * d], val = a.base + s_task[9 + 2 * d];
         const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+        // system scope only for a counter a peer GPU publishes (record [14] bit 3 + d); the
+        // rank-local chains (column counters, apply / early-release parts) stay at gpu scope
+        const bool sysd = a.sys && ((s_task[14] >> (3 + d)) & 1);
         for (int x = lane; x < cnt; x += 32) {
           const int* c = R.ctr + idx + x;
-          if ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) >= val) continue;
+          if ((sysd ? ld_acquire_sys(c) : ld_acquire(c)) >= val) continue;
           const unsigned long long t0w = globaltimer();
-          while ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < val) {
+          while ((sysd ? ld_acquire_sys(c) : ld_acquire(c)) < val) {
             __nanosleep(TQR_POLL_NS);
             // watchdog: a dependency that never resolves is a schedule bug; fail loudly
             if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
@@ -522,10 +531,10 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         // finish first; PF(k,l) must still advance v-1 -> v -> v+1 (a consumer of PF >= v
         // reads this task's Y_l / T_l), so wait for the previous tile's publication.  That
         // task is past its own early release and waits on nothing: no deadlock.
-        const int* c = R.ctr + oidx;
-        if ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < oval - 1) {
+        const int* c = R.ctr + oidx;  // (this rank's copy, published by this rank: gpu scope)
+        if (ld_acquire(c) < oval - 1) {
           const unsigned long long t0w = globaltimer();
-          while ((a.sys ? ld_acquire_sys(c) : ld_acquire(c)) < oval - 1) {
+          while (ld_acquire(c) < oval - 1) {
             __nanosleep(TQR_POLL_NS);
             if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
           }
@@ -757,18 +766,24 @@ static cudaError_t launch_runs(int b, const double* src, double* dst, int64_t ld
 
 // Packed reflector panels for apply-Q from the boundary factors (At, T): the same Yp/Tp
 // contents the factorization writes, one thread per element of the lower tile triangle.
-// The internal S x S blocks are the diagonal blocks of the output T_L (SO x SO).
+// The internal S x S blocks are the diagonal blocks of the output T_L (SO x SO).  The source
+// holds storage columns kc of global tile column k = coff + kc*cstride; every element goes to
+// all nd destination workspaces (multi-rank: this rank's panels into every rank's workspace).
+struct DPtrs {
+  double* p[MAX_RANKS];
+};
 template <int B, int SO>
-__global__ void pack_factors_kernel(const double* __restrict__ A, const double* __restrict__ T, double* __restrict__ Yp,
-                                    double* __restrict__ Tp, int p, int K) {
+__global__ void pack_factors_kernel(const double* __restrict__ A, const double* __restrict__ T, DPtrs Yd, DPtrs Td,
+                                    int nd, int p, int K, int64_t qloc, int cstride, int coff, int sys_fence) {
   constexpr int S = Inner<B, SO>::SI, RB_ = SO / S;
   const int64_t bb = (int64_t)B * B;
-  const int64_t total = (int64_t)p * K * bb;
+  const int64_t total = (int64_t)p * qloc * bb;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t tile = e / bb;
     const int in = (int)(e % bb);
-    const int i = (int)(tile % p), k = (int)(tile / p);
-    if (i < k) continue;
+    const int i = (int)(tile % p), kc = (int)(tile / p);
+    const int k = coff + kc * cstride;
+    if (k >= K || i < k) continue;
     // element `in` of the packed tile: panel l, swizzled position -> (r, c) of the panel
     const int l = in / (B * S), q = in % (B * S);
     const int blk = q >> 6, w = q & 63;
@@ -783,16 +798,18 @@ __global__ void pack_factors_kernel(const double* __restrict__ A, const double* 
     } else {
       y = r < gc ? 0.0 : (r == gc ? 1.0 : At[(size_t)gc * B + r]);
     }
-    Yp[tile * bb + in] = y;
+    const int64_t gtile = (int64_t)i + (int64_t)k * p;  // workspace index: global step k
+    for (int d = 0; d < nd; ++d) Yd.p[d][gtile * bb + in] = y;
     if (q < S * S) {  // internal T block l of slot (i, k) in swz<S>
       const int tb = q >> 6, tw = q & 63;
       const int tcb = tb / (S / 8), trb = tb % (S / 8);
       const int tc = tcb * 8 + (tw >> 3), tr = trb * 8 + ((tw & 7) ^ (tc & 6));
-      const int64_t slot = tile * (int64_t)SO * B;
       const int Lo = l / RB_, mo = (l % RB_) * S;
-      Tp[slot + (int64_t)l * S * S + q] = T[slot + ((int64_t)Lo * SO + mo + tc) * SO + mo + tr];
+      const double tv = T[tile * (int64_t)SO * B + ((int64_t)Lo * SO + mo + tc) * SO + mo + tr];
+      for (int d = 0; d < nd; ++d) Td.p[d][gtile * (int64_t)SO * B + (int64_t)l * S * S + q] = tv;
     }
   }
+  if (sys_fence) __threadfence_system();  // peer stores visible before the next rank barrier
 }
 
 // Output T_L blocks when the executor ran with SI < SO (b = 512, s = 64): the off-diagonal
@@ -908,11 +925,19 @@ cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int 
   rank_barrier_kernel<<<1, 32, 0, st>>>(arr, nranks, me, gen);
   return cudaGetLastError();
 }
-cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, double* Tp, int b, int s, int64_t p,
-                                int64_t K, cudaStream_t st) {
-  const int64_t total = p * K * (int64_t)b * b;
-#define X(BB, SS) \
-  if (b == BB && s == SS) { pack_factors_kernel<BB, SS><<<grid_for(total), 256, 0, st>>>(A, T, Yp, Tp, (int)p, (int)K); return cudaGetLastError(); }
+cudaError_t launch_pack_factors(const double* A, const double* T, double* const* Yp, double* const* Tp, int nd, int b,
+                                int s, int64_t p, int64_t K, int64_t qloc, int cstride, int coff, bool sys_fence,
+                                cudaStream_t st) {
+  const int64_t total = p * qloc * (int64_t)b * b;
+  if (total == 0) return cudaSuccess;
+  DPtrs Yd{}, Td{};
+  for (int d = 0; d < nd && d < MAX_RANKS; ++d) { Yd.p[d] = Yp[d]; Td.p[d] = Tp[d]; }
+#define X(BB, SS)                                                                                         \
+  if (b == BB && s == SS) {                                                                               \
+    pack_factors_kernel<BB, SS><<<grid_for(total), 256, 0, st>>>(A, T, Yd, Td, nd, (int)p, (int)K, qloc,   \
+                                                                 cstride, coff, sys_fence ? 1 : 0);      \
+    return cudaGetLastError();                                                                            \
+  }
   TQR_INSTANCES(X)
 #undef X
   return cudaErrorInvalidValue;
@@ -948,8 +973,9 @@ cudaError_t launch_form_t(const double* A, double* T, int b, int s, int64_t p, i
   return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qb, cudaStream_t st) {
-  return launch_runs<OP_EYE>(b, nullptr, Qt, 0, m, k, p, qb, 1, 0, st);
+cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qloc, int cstride, int coff,
+                             cudaStream_t st) {
+  return launch_runs<OP_EYE>(b, nullptr, Qt, 0, m, k, p, qloc, cstride, coff, st);
 }
 
 }  // namespace tqr

@@ -85,6 +85,8 @@ struct Sched {
   int64_t nedges = 0;
   int64_t counts[4] = {0, 0, 0, 0};
   bool topo_ok = true;
+  double makespan = 0.0;  // modelled (list-schedule simulation), ns
+  double busy = 0.0;      // modelled worker utilisation (sum of durations / (makespan x workers))
 };
 
 // ---- generic task list with counter deps -> list-schedule order --------------------------
@@ -140,8 +142,10 @@ static inline uint64_t ckey(int idx, int val) { return ((uint64_t)(uint32_t)idx 
 //    j at step k < j - 1 feed panel j's chain and outrank later-column work of earlier steps.
 enum Prio { PRIO_CLASS = 0, PRIO_BLEVEL = 1 };
 
+// lat_remote (ns): extra modelled delay of an edge whose producer runs on another rank (the
+// NVLink peer store + system-scope release / acquire); used by the scaling model.
 static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& out, int prio = PRIO_CLASS,
-                          double lat = 0.0, double blq = 0.0) {
+                          double lat = 0.0, double blq = 0.0, double lat_remote = 0.0) {
   const int n = (int)G.t.size();
   const int nr = (int)workers.size();
   std::unordered_map<uint64_t, int> producer;
@@ -224,7 +228,8 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
   std::vector<double> sim_start(n, 0.0);  // development aid: TQR_DEV_SIMDUMP=<file>
   std::vector<int> free_w(nr);
   for (int r = 0; r < nr; ++r) free_w[r] = std::max(1, workers[r]);
-  double now = 0.0;
+  std::priority_queue<Ev, std::vector<Ev>, std::greater<Ev>> arrivals;  // remote edges in flight
+  double now = 0.0, work = 0.0;
   int done = 0;
   while (done < n) {
     for (int r = 0; r < nr; ++r)
@@ -234,16 +239,34 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
         order.push_back(id);
         sim_start[id] = now;
         events.push({now + G.t[id].dur + lat, id});
+        work += G.t[id].dur;
         free_w[r]--;
       }
-    if (events.empty()) return false;  // cycle
+    if (events.empty() && arrivals.empty()) return false;  // cycle
+    if (!arrivals.empty() && (events.empty() || arrivals.top().first <= events.top().first)) {
+      const Ev a = arrivals.top();
+      arrivals.pop();
+      now = a.first;
+      if (--indeg[a.second] == 0) ready[G.t[a.second].rank].push(a.second);
+      continue;
+    }
     Ev e = events.top();
     events.pop();
     now = e.first;
     done++;
     free_w[G.t[e.second].rank]++;
-    for (int sidx : succ[e.second])
-      if (--indeg[sidx] == 0) ready[G.t[sidx].rank].push(sidx);
+    for (int sidx : succ[e.second]) {
+      if (lat_remote > 0.0 && G.t[sidx].rank != G.t[e.second].rank)
+        arrivals.push({now + lat_remote, sidx});
+      else if (--indeg[sidx] == 0)
+        ready[G.t[sidx].rank].push(sidx);
+    }
+  }
+  {
+    int64_t wt = 0;
+    for (int x : workers) wt += std::max(1, x);
+    out.makespan = now;
+    out.busy = now > 0.0 ? work / (now * (double)wt) : 0.0;
   }
   if (const char* f = getenv("TQR_DEV_SIMDUMP")) {  // modelled start/end per task (ns), dispatch order
     if (FILE* fp = fopen(f, "w")) {
@@ -318,7 +341,7 @@ struct DurModel {
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
                                int rwm = 128, double blq = 0.0, bool group = false, int np = 1, int fine = 0,
-                               bool early = false) {
+                               bool early = false, double lat_remote = 0.0) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -388,6 +411,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         T.t[id].np = n_; T.t[id].ocnt = n_;
         if (group && j > k + 1) T.t[id].group = (int64_t)k * p + k;
         T.dep(id, PF(k, NPT - 1), 1, 1);
+        if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
         if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, 2);
         out.counts[2] += n_;  // counted per register pass (column slice)
       }
@@ -406,13 +430,14 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
           T.t[id].np = n_; T.t[id].ocnt = n_;
           if (group && j > k + 1) T.t[id].group = (int64_t)k * p + i;
           T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
+          if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
           T.dep(id, COL(k, j, sl), n_, i - k);
           if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, i - k + 2);
           out.counts[3] += n_;
         }
     }
   }
-  if (!list_schedule(T, workers, out, prio, lat, blq)) out.topo_ok = false;
+  if (!list_schedule(T, workers, out, prio, lat, blq, lat_remote)) out.topo_ok = false;
 }
 
 // apply-Q^T (trans) or apply-Q to a tile-major B with qb tile columns.
@@ -424,28 +449,41 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
 // left of step k untouched (they are still unit vectors in rows >= k b), so the tasks
 // (k, jb < k) are skipped -- the DORGQR saving, half the work of a dense Q*B.
 // nslf: column slices (register passes) per tile; tasks cover np of them (counters per task slice).
-static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nslf, bool trans, int workers,
-                            Sched& out, bool form_q = false, int prio = PRIO_CLASS, double lat = 0.0,
-                            int rwm = 128, int np = 1) {
-  out.nctr.assign(1, 0);
+// Multi-rank (workers.size() = G > 1): B's tile columns are 1D block-cyclic like A's, column
+// jb is applied by rank jb mod G with the packed reflectors in that rank's own workspace (every
+// rank holds every panel), so the ranks never wait on each other; counters are per rank,
+// indexed by the local column jb / G; `real_layout`: B holds only the rank's own columns
+// (record [3] = storage column jb / G), otherwise the global grid.
+static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int nslf, bool trans,
+                            const std::vector<int>& workers, bool real_layout, Sched& out, bool form_q = false,
+                            int prio = PRIO_CLASS, double lat = 0.0, int rwm = 128, int np = 1) {
+  const int G = (int)workers.size();
   const int K = (int)std::min(p, q);
   if (np < 1 || nslf % np != 0) np = 1;
   const int nsl = nslf / np;
   const int w = (b + nsl - 1) / nsl;
   DurModel dm(b, s, w, rwm);
-  TaskGen G;
-  auto CNT = [&](int k, int jb, int sl) { return (int)(((int64_t)k * qb + jb) * nsl + sl); };
-  out.nctr[0] = (int)((int64_t)K * qb * nsl);
-  for (int jb = 0; jb < qb; ++jb)
+  TaskGen TG;
+  auto qbl = [&](int r) { return r < qb ? (int)((qb - r + G - 1) / G) : 0; };
+  auto CNT = [&](int k, int64_t jb, int sl) { return (int)(((int64_t)k * qbl((int)(jb % G)) + jb / G) * nsl + sl); };
+  out.nctr.assign(G, 0);
+  for (int r = 0; r < G; ++r) out.nctr[r] = (int)((int64_t)K * qbl(r) * nsl);
+  auto add = [&](int kind, int k, int i, int64_t jb, int sl, int val, double dur, int cls) {
+    int id = TG.add(kind, k, i, real_layout ? (int)(jb / G) : (int)jb, sl, CNT(k, jb, sl), val, dur, cls);
+    TG.t[id].rank = (int)(jb % G);
+    TG.t[id].key[2] = (int)jb;
+    return id;
+  };
+  for (int64_t jb = 0; jb < qb; ++jb)
     for (int sl = 0; sl < nsl; ++sl) {
       if (trans) {
         for (int k = 0; k < K; ++k) {
-          int id = G.add(K_LQT, k, k, jb, sl, CNT(k, jb, sl), 1, dm.l, 0);
-          if (k > 0) G.dep(id, CNT(k - 1, jb, sl), 1, 2);
+          int id = add(K_LQT, k, k, jb, sl, 1, dm.l, 0);
+          if (k > 0) TG.dep(id, CNT(k - 1, jb, sl), 1, 2);
           for (int i = k + 1; i < p; ++i) {
-            id = G.add(K_SQT, k, i, jb, sl, CNT(k, jb, sl), i - k + 1, dm.s, 1);
-            G.dep(id, CNT(k, jb, sl), 1, i - k);
-            if (k > 0) G.dep(id, CNT(k - 1, jb, sl), 1, i - k + 2);
+            id = add(K_SQT, k, i, jb, sl, i - k + 1, dm.s, 1);
+            TG.dep(id, CNT(k, jb, sl), 1, i - k);
+            if (k > 0) TG.dep(id, CNT(k - 1, jb, sl), 1, i - k + 2);
           }
         }
       } else {
@@ -453,29 +491,30 @@ static void build_orm_sched(int64_t p, int64_t q, int64_t qb, int b, int s, int 
           if (form_q && jb < k) continue;                       // untouched unit columns
           const bool prev = k + 1 < K && !(form_q && jb < k + 1);  // step k+1 had tasks here
           for (int i = (int)p - 1; i > k; --i) {
-            int id = G.add(K_SQ, k, i, jb, sl, CNT(k, jb, sl), (int)p - i, dm.s, 1);
-            G.t[id].key[0] = K - 1 - k;  // reverse order: later steps first
-            G.t[id].key[1] = (int)p - 1 - i;
-            if (i < p - 1) G.dep(id, CNT(k, jb, sl), 1, (int)p - i - 1);
-            if (prev) G.dep(id, CNT(k + 1, jb, sl), 1, (int)p - i);
+            int id = add(K_SQ, k, i, jb, sl, (int)p - i, dm.s, 1);
+            TG.t[id].key[0] = K - 1 - k;  // reverse order: later steps first
+            TG.t[id].key[1] = (int)p - 1 - i;
+            if (i < p - 1) TG.dep(id, CNT(k, jb, sl), 1, (int)p - i - 1);
+            if (prev) TG.dep(id, CNT(k + 1, jb, sl), 1, (int)p - i);
           }
-          int id = G.add(K_LQ, k, k, jb, sl, CNT(k, jb, sl), (int)p - k, dm.l, 0);
-          G.t[id].key[0] = K - 1 - k;
-          if (k + 1 < p) G.dep(id, CNT(k, jb, sl), 1, (int)p - k - 1);
+          int id = add(K_LQ, k, k, jb, sl, (int)p - k, dm.l, 0);
+          TG.t[id].key[0] = K - 1 - k;
+          if (k + 1 < p) TG.dep(id, CNT(k, jb, sl), 1, (int)p - k - 1);
         }
       }
     }
-  for (auto& x : G.t) {  // record: first register pass (column slice of width b / nslf), passes
+  for (auto& x : TG.t) {  // record: first register pass (column slice of width b / nslf), passes
     x.np = np;
     x.sl *= np;
   }
-  if (!list_schedule(G, std::vector<int>{workers}, out, prio, lat)) out.topo_ok = false;
+  if (!list_schedule(TG, workers, out, prio, lat)) out.topo_ok = false;
 }
 
 struct DevSched {
   std::vector<int*> d_tasks;  // per local rank
   std::vector<int> ntasks;
   int mode = 0;  // executor instance: 0 factorization, 1 apply Q^T, 2 apply Q
+  int nctr = 0;  // counters per rank (max over the local ranks)
 };
 
 }  // namespace
@@ -517,6 +556,8 @@ struct tqr_plan {
   SymLayout lay{};
   bool connected = false;
   int* d_ctr1 = nullptr;      // single-rank counters
+  int* d_octr = nullptr;      // multi-rank plans: rank-local apply-Q counters, nloc x octr_n
+  int octr_n = 0;
   int* d_ticket = nullptr;    // one per local rank
   int gen = 0;                // call generation (counter base = gen * (p + 2))
   unsigned long long* d_trace = nullptr;
@@ -525,6 +566,45 @@ struct tqr_plan {
   bool trace_valid = false;
   long long* d_phases = nullptr;  // set by tqr_phase_counters (profiling builds)
 };
+
+// Granularity policy (measured on B200, r01):
+//  * square grids, b >= 256: the RW = 256 executor (a warp holds all 256 rows of its column
+//    group: no row-partial exchange) with 128-column update tasks -- C3 224 ms (70.5%),
+//    C5 12.5 s (80.7%) vs 232 ms / 13.7 s with RW = 128;
+//  * tall-skinny grids (p >= 4q) are bound by the TSQRT chain: the RW = 128 executor with
+//    32-column update tasks and the panel A/F split (C4: 60 ms vs 77 with RW = 256);
+//  * b <= 128: RW = b, 1-pass tasks, fused panel blocks (the GEQRT/TSQRT chain dominates C2);
+//  * dispatch order by bottom level (critical path) with a 4 us handoff per task, not by the
+//    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
+struct Policy {
+  int rwm = 128, passes = 1, nsl = 1, fine = 2, prio = PRIO_BLEVEL, orm_prio = PRIO_BLEVEL;
+  bool split = true, early = true, group = false;
+  double lat = 4000.0, blq = 0.0;
+};
+static Policy make_policy(int64_t p, int64_t q, int b, int s) {
+  Policy P;
+  const bool tall = p >= 4 * q;
+  P.rwm = (b >= 256 && !tall) ? 256 : 128;
+  P.passes = b >= 256 ? (128 / exec_slice(b, s, P.rwm)) : 1;  // 128-column tasks
+  if (tall && b <= 256) P.passes = 1;
+  P.split = tall;  // (square b <= 128 as well before the early R_kk release, R24: C2 7.15 -> 7.08 ms fused)
+  if (const char* e = getenv("TQR_DEV_PASSES")) P.passes = std::max(1, atoi(e));   // development knobs
+  if (const char* e = getenv("TQR_DEV_SPLIT")) P.split = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_RW")) P.rwm = atoi(e);
+  if (const char* e = getenv("TQR_DEV_PRIO")) P.prio = atoi(e);
+  if (const char* e = getenv("TQR_DEV_LAT")) P.lat = atof(e);
+  if (const char* e = getenv("TQR_DEV_ORM_PRIO")) P.orm_prio = atoi(e);
+  if (const char* e = getenv("TQR_DEV_BLQ")) P.blq = atof(e);
+  if (const char* e = getenv("TQR_DEV_GROUP")) P.group = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_EARLY")) P.early = atoi(e) != 0;
+  {
+    const int w = exec_slice(b, s, P.rwm);  // one register pass
+    P.nsl = (int)((b + w - 1) / w);
+    if (P.nsl % P.passes != 0) P.passes = 1;
+  }
+  if (const char* e = getenv("TQR_DEV_FINE")) P.fine = atoi(e);
+  return P;
+}
 
 static int64_t qloc_of(const tqr_plan* P, int r) {
   return P->real ? (r < P->q ? (P->q - r + P->G - 1) / P->G : 0) : P->q;
@@ -569,6 +649,7 @@ static tqr_status next_base(tqr_plan* P, int* base) {
     for (int r = 0; r < MAX_RANKS; ++r)
       if (P->ctr[r] && (P->emulate || r == P->me))
         CU(cudaMemsetAsync(P->ctr[r], 0, sizeof(int) * (size_t)std::max(1, P->nctr_max), P->st));
+    if (P->d_octr) CU(cudaMemsetAsync(P->d_octr, 0, sizeof(int) * (size_t)P->nloc * P->octr_n, P->st));
     P->gen = 0;
   }
   P->gen++;
@@ -576,7 +657,10 @@ static tqr_status next_base(tqr_plan* P, int* base) {
   return TQR_OK;
 }
 
-static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, double* Bt, void* work, bool trace) {
+// ctr_local (multi-rank apply-Q): rank-local counter arrays replacing the symmetric ones,
+// one per local rank, indexed like local_ranks(P)
+static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, double* Bt, void* work, bool trace,
+                      int* const* ctr_local = nullptr) {
   int total = 0;
   for (int n : d.ntasks) total += n;
   if (total == 0) return TQR_OK;
@@ -618,6 +702,8 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
     P->trace_valid = true;
   }
   const std::vector<int> lr = local_ranks(P);
+  if (ctr_local)
+    for (int li = 0; li < nl; ++li) a.ctr[P->G == 1 ? 0 : lr[li]] = ctr_local[li];
   for (int li = 0; li < nl; ++li) {
     RankLocal& R = a.loc[li];
     R.tasks = d.d_tasks[li];
@@ -677,6 +763,7 @@ static void destroy_plan(tqr_plan* P) {
     if (P->sym_own[r]) cudaFree(P->sym_own[r]);
   }
   if (P->d_ctr1) cudaFree(P->d_ctr1);
+  if (P->d_octr) cudaFree(P->d_octr);
   if (P->d_ticket) cudaFree(P->d_ticket);
   if (P->d_trace) cudaFree(P->d_trace);
   delete P;
@@ -714,35 +801,12 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   P->emulate = emulate;
   P->real = P->G > 1 && !emulate;
   P->nloc = emulate ? P->G : 1;
-  // Granularity policy (measured on B200, r01):
-  //  * square grids, b >= 256: the RW = 256 executor (a warp holds all 256 rows of its column
-  //    group: no row-partial exchange) with 128-column update tasks -- C3 224 ms (70.5%),
-  //    C5 12.5 s (80.7%) vs 232 ms / 13.7 s with RW = 128;
-  //  * tall-skinny grids (p >= 4q) are bound by the TSQRT chain: the RW = 128 executor with
-  //    32-column update tasks and the panel A/F split (C4: 60 ms vs 77 with RW = 256);
-  //  * b <= 128: RW = b, 1-pass tasks, fused panel blocks (the GEQRT/TSQRT chain dominates C2);
-  //  * dispatch order by bottom level (critical path) with a 4 us handoff per task, not by the
-  //    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
-  const bool tall = P->p >= 4 * P->q;
-  P->rwm = (p->b >= 256 && !tall) ? 256 : 128;
-  P->passes = p->b >= 256 ? (128 / exec_slice(p->b, p->s, P->rwm)) : 1;  // 128-column tasks
-  if (tall && p->b <= 256) P->passes = 1;
-  P->split = tall;  // (square b <= 128 as well before the early R_kk release, R24: C2 7.15 -> 7.08 ms fused)
-  if (const char* e = getenv("TQR_DEV_PASSES")) P->passes = std::max(1, atoi(e));   // development knobs
-  if (const char* e = getenv("TQR_DEV_SPLIT")) P->split = atoi(e) != 0;
-  if (const char* e = getenv("TQR_DEV_RW")) P->rwm = atoi(e);
-  if (const char* e = getenv("TQR_DEV_PRIO")) P->prio = atoi(e);
-  if (const char* e = getenv("TQR_DEV_LAT")) P->lat = atof(e);
-  if (const char* e = getenv("TQR_DEV_ORM_PRIO")) P->orm_prio = atoi(e);
-  if (const char* e = getenv("TQR_DEV_BLQ")) P->blq = atof(e);
-  if (const char* e = getenv("TQR_DEV_GROUP")) P->group = atoi(e) != 0;
-  if (const char* e = getenv("TQR_DEV_EARLY")) P->early = atoi(e) != 0;
   {
-    const int w = exec_slice(p->b, p->s, P->rwm);  // one register pass
-    P->nsl = (int)((p->b + w - 1) / w);
-    if (P->nsl % P->passes != 0) P->passes = 1;
+    const Policy pol = make_policy(P->p, P->q, p->b, p->s);
+    P->rwm = pol.rwm; P->passes = pol.passes; P->nsl = pol.nsl; P->fine = pol.fine; P->split = pol.split;
+    P->early = pol.early; P->group = pol.group; P->prio = pol.prio; P->orm_prio = pol.orm_prio; P->lat = pol.lat;
+    P->blq = pol.blq;
   }
-  if (const char* e = getenv("TQR_DEV_FINE")) P->fine = atoi(e);
   P->st = (cudaStream_t)p->stream;
   P->workers = exec_max_ctas(p->b, p->s, P->rwm, p->device);
   if (P->workers < P->nloc) {
@@ -990,6 +1054,13 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   return TQR_OK;
 }
 
+// tile columns of an m x nrhs tile-major B held by this process (real multi-rank: its own)
+static int64_t qb_local(const tqr_plan* P, int64_t nrhs) {
+  const int64_t qb = (nrhs + P->prm.b - 1) / P->prm.b;
+  if (!P->real) return qb;
+  return P->me < qb ? (qb - P->me + P->G - 1) / P->G : 0;
+}
+
 static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** out, bool form_q = false) {
   auto key = std::make_pair(trans ? 1 : (form_q ? 2 : 0), nrhs);
   auto it = P->orm.find(key);
@@ -999,30 +1070,70 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
       g_err = "nrhs too large for 24-bit counter indices";
       return TQR_ERR_UNSUPPORTED;
     }
+    // worker pools as for the factorization (emulation splits this device's CTAs by rank)
+    std::vector<int> workers(P->G, P->workers);
+    if (P->emulate)
+      for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
     Sched s;
-    build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, P->workers, s, form_q, P->orm_prio, P->lat,
-                    P->rwm, P->passes);
+    build_orm_sched(P->p, P->q, qb, P->prm.b, P->prm.s, P->nsl, trans, workers, P->real, s, form_q, P->orm_prio,
+                    P->lat, P->rwm, P->passes);
     if (!s.topo_ok) {
       g_err = "internal: apply-Q schedule is not topological";
       return TQR_ERR_UNSUPPORTED;
     }
-    if (s.nctr[0] > P->nctr_max) {
+    DevSched d;
+    d.mode = trans ? 1 : 2;
+    for (int r : local_ranks(P)) d.nctr = std::max(d.nctr, s.nctr[r]);
+    if (P->G == 1 && d.nctr > P->nctr_max) {
       // grow the single-rank counter array (fresh zeros; the generation base stays valid)
       int* nc = nullptr;
-      CU(cudaMalloc(&nc, sizeof(int) * (size_t)s.nctr[0]));
-      CU(cudaMemset(nc, 0, sizeof(int) * (size_t)s.nctr[0]));
+      CU(cudaMalloc(&nc, sizeof(int) * (size_t)d.nctr));
+      CU(cudaMemset(nc, 0, sizeof(int) * (size_t)d.nctr));
       CU(cudaStreamSynchronize(P->st));
       cudaFree(P->d_ctr1);
       P->d_ctr1 = nc;
-      P->nctr_max = s.nctr[0];
+      P->nctr_max = d.nctr;
     }
-    DevSched d;
-    d.mode = trans ? 1 : 2;
-    tqr_status st = upload(s, std::vector<int>{0}, d);
+    if (P->G > 1 && d.nctr > P->octr_n) {  // rank-local apply-Q counters (never touched by peers)
+      int* nc = nullptr;
+      CU(cudaMalloc(&nc, sizeof(int) * (size_t)P->nloc * d.nctr));
+      CU(cudaMemset(nc, 0, sizeof(int) * (size_t)P->nloc * d.nctr));
+      CU(cudaStreamSynchronize(P->st));
+      if (P->d_octr) cudaFree(P->d_octr);
+      P->d_octr = nc;
+      P->octr_n = d.nctr;
+    }
+    tqr_status st = upload(s, local_ranks(P), d);
     if (st != TQR_OK) return st;
     it = P->orm.emplace(key, d).first;
   }
   *out = &it->second;
+  return TQR_OK;
+}
+
+// Packed reflector panels of the factors (At, T) into the workspace(s) the apply-Q tasks
+// stream from.  1 GPU: the caller's `work`.  Emulated ranks: every rank's workspace (global
+// At / T).  Real multi-rank: each rank packs the tile columns k it owns into EVERY rank's
+// workspace over NVLink peer stores -- the only exchange of apply-Q -- between two
+// device-side rank barriers (nobody still reads the old panels; nobody reads before all
+// ranks' panels have landed, the second barrier being run()'s entry barrier).
+static tqr_status stage_factors(tqr_plan* P, const double* At, const double* T, void* work) {
+  const int b = P->prm.b, s = P->prm.s;
+  if (P->G == 1) {
+    double* Yp = reinterpret_cast<double*>(work);
+    double* Tp = Yp + (size_t)P->p * P->q * b * b;
+    CU(launch_pack_factors(At, T, &Yp, &Tp, 1, b, s, P->p, P->K, P->q, 1, 0, false, P->st));
+    return TQR_OK;
+  }
+  if (P->emulate) {
+    CU(launch_pack_factors(At, T, P->Yp, P->Tp, P->G, b, s, P->p, P->K, P->q, 1, 0, false, P->st));
+    return TQR_OK;
+  }
+  int base = 0;
+  tqr_status st = next_base(P, &base);
+  if (st != TQR_OK) return st;
+  CU(launch_rank_barrier(P->arrive, P->G, P->me, P->gen, P->st));
+  CU(launch_pack_factors(At, T, P->Yp, P->Tp, P->G, b, s, P->p, P->K, qloc_of(P, P->me), P->G, P->me, true, P->st));
   return TQR_OK;
 }
 
@@ -1034,23 +1145,25 @@ static tqr_status ormqr_impl(tqr_plan* P, char trans, const double* At, const do
   if (!T) return bad_arg(4, "T is NULL");
   if (!Bt) return bad_arg(5, "Bt is NULL");
   if (nrhs < 1) return bad_arg(6, "nrhs < 1");
-  if (!work) return bad_arg(7, "work is NULL (tqr_workspace_size bytes required)");
+  if (!work && P->G == 1) return bad_arg(7, "work is NULL (tqr_workspace_size bytes required)");
   ALIGNED(At, 3);
   ALIGNED(T, 4);
   ALIGNED(Bt, 5);
   ALIGNED(work, 7);
   GUARD(P);
-  if (P->G > 1) {
-    g_err = "apply-Q is single-GPU in this version";
+  if (P->real && !P->connected) {
+    g_err = "multi-rank plan not connected (tqr_comm_export / tqr_comm_connect)";
     return TQR_ERR_UNSUPPORTED;
   }
   DevSched* d = nullptr;
   tqr_status st = orm_sched(P, trans == 'T' || trans == 't', nrhs, &d, form_q);
   if (st != TQR_OK) return st;
-  double* Yp = reinterpret_cast<double*>(work);
-  double* Tp = Yp + (size_t)P->p * P->q * P->prm.b * P->prm.b;
-  CU(launch_pack_factors(At, T, Yp, Tp, P->prm.b, P->prm.s, P->p, P->K, P->st));
-  return run(P, *d, const_cast<double*>(At), const_cast<double*>(T), Bt, work, false);
+  st = stage_factors(P, At, T, work);
+  if (st != TQR_OK) return st;
+  if (P->G == 1) return run(P, *d, const_cast<double*>(At), const_cast<double*>(T), Bt, work, false);
+  int* ctrs[MAX_RANKS] = {};
+  for (int li = 0; li < P->nloc; ++li) ctrs[li] = P->d_octr + (size_t)li * P->octr_n;
+  return run(P, *d, const_cast<double*>(At), const_cast<double*>(T), Bt, work, false, ctrs);
 }
 
 tqr_status tqr_ormqr(tqr_plan* P, char trans, const double* At, const double* T, double* Bt, int64_t nrhs,
@@ -1064,18 +1177,15 @@ tqr_status tqr_orgqr(tqr_plan* P, const double* At, const double* T, int64_t k, 
   if (!T) return bad_arg(3, "T is NULL");
   if (k < 1 || k > P->prm.m) return bad_arg(4, "k outside [1, m]");
   if (!Qt) return bad_arg(5, "Qt is NULL");
-  if (!work) return bad_arg(6, "work is NULL (tqr_workspace_size bytes required)");
+  if (!work && P->G == 1) return bad_arg(6, "work is NULL (tqr_workspace_size bytes required)");
   ALIGNED(At, 2);
   ALIGNED(T, 3);
   ALIGNED(Qt, 5);
   ALIGNED(work, 6);
   GUARD(P);
-  if (P->G > 1) {
-    g_err = "form-Q is single-GPU in this version";
-    return TQR_ERR_UNSUPPORTED;
-  }
-  const int64_t qb = (k + P->prm.b - 1) / P->prm.b;
-  CU(launch_eye_tiles(Qt, P->prm.m, k, P->prm.b, P->p, qb, P->st));
+  int cs, co;
+  colmap(P, &cs, &co);
+  CU(launch_eye_tiles(Qt, P->prm.m, k, P->prm.b, P->p, qb_local(P, k), cs, co, P->st));
   return ormqr_impl(P, 'N', At, T, Qt, k, work, true);
 }
 
@@ -1127,6 +1237,30 @@ tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t wo
   *n = (int64_t)(v.size() / TASK_INTS);
   if (nctr) *nctr = s.nctr[rank];
   if (rec) std::memcpy(rec, v.data(), sizeof(int32_t) * (size_t)std::min<int64_t>(cap, *n) * TASK_INTS);
+  return TQR_OK;
+}
+
+tqr_status tqr_schedule_model(int64_t m, int64_t n, int32_t b, int32_t s, int32_t nranks, int32_t workers,
+                              double remote_ns, double* makespan_ns, double* busy) {
+  g_badarg = 0;
+  if (m < 1) return bad_arg(1, "m < 1");
+  if (n < 1) return bad_arg(2, "n < 1");
+  if (!exec_supported(b, s)) return bad_arg(3, "no kernel instance for (b, s)");
+  if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
+  if (workers < 1) return bad_arg(6, "workers < 1");
+  if (remote_ns < 0.0) return bad_arg(7, "remote_ns < 0");
+  if (!makespan_ns) return bad_arg(8, "makespan_ns is NULL");
+  const int64_t p = (m + b - 1) / b, q = (n + b - 1) / b;
+  const Policy pol = make_policy(p, q, b, s);
+  Sched sc;
+  build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
+                     pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, remote_ns);
+  if (!sc.topo_ok) {
+    g_err = "schedule is not a topological order";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  *makespan_ns = sc.makespan;
+  if (busy) *busy = sc.busy;
   return TQR_OK;
 }
 
@@ -1191,7 +1325,7 @@ tqr_status tqr_trace_fetch(tqr_plan* P, int64_t* rec, int64_t cap, int64_t* n) {
 
 tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* At, double* T, void* work) {
   if (!P) return bad_arg(1, "plan is NULL");
-  if (kind < 0 || kind > 7) return bad_arg(2, "kind outside [0, 7]");
+  if (kind < 0 || kind > 9) return bad_arg(2, "kind outside [0, 9]");
   if (count < 1 || count > (1 << 24)) return bad_arg(3, "count outside [1, 2^24]");
   if (!At) return bad_arg(4, "At is NULL");
   if (!T) return bad_arg(5, "T is NULL");
@@ -1207,20 +1341,27 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
     int* q = &s.rec[0][(size_t)t * TASK_INTS];
     const int i = 1 + (int)(t % (P->p - 1));
     const int j = 1 + (int)((t / (P->p - 1)) % (P->q - 1));
+    // kinds 8 / 9: the factor part F(k,i,l) alone of a GEQRT / TSQRT (R21), block
+    // l = t mod (b/s): the panel column loop, Gram, T_l and the V/Y/T stores, no left-looking apply
+    const bool fpart = kind >= 8;
+    if (fpart) kind -= 8;
     q[0] = kind;
     q[1] = kind == 0 ? (int)(t % P->K) : 0;
     const bool lkind = kind == 2 || kind == 4 || kind == 6;
     q[2] = (kind == 0 || lkind) ? q[1] : i;
     q[3] = (kind == 0 || kind == 1) ? q[1] : j;
     // -1: a panel task over the whole tile; update tasks: first register pass, P->passes passes
-    q[4] = (kind == 0 || kind == 1) ? -1 : (int)(t % (P->nsl / P->passes)) * P->passes;
+    q[4] = (kind == 0 || kind == 1) ? (fpart ? (int)(t % (P->prm.b / P->prm.s)) : -1)
+                                    : (int)(t % (P->nsl / P->passes)) * P->passes;
+    q[14] = fpart ? 4 : 0;
     q[15] = P->passes | (1 << 8);
+    if (fpart) kind += 8;
     q[5] = 0;
     q[6] = 1;
     q[7] = q[1];
   }
   DevSched d;
-  d.mode = kind >= 6 ? 2 : (kind >= 4 ? 1 : 0);
+  d.mode = (kind >= 6 && kind <= 7) ? 2 : ((kind >= 4 && kind <= 7) ? 1 : 0);
   tqr_status st = upload(s, std::vector<int>{0}, d);
   if (st != TQR_OK) return st;
   st = run(P, d, At, T, At, work, false);

@@ -26,7 +26,9 @@ enum Kind : int {
 //   [8 + 2d], [9 + 2d], d = 0..2: dependency d = (index | count << 24, value):
 //       wait until ctr[index + x] >= base + value for x in [0, count); count 0 = none
 //   [14] flags: bit 0 = publish the out counter on every rank (panel progress, multi-GPU),
-//        bit 1 / bit 2 = panel apply / factor part; bits 8..31 = 1 + an early-release
+//        bit 1 / bit 2 = panel apply / factor part, bits 3..5 = dependency 0..2 is a counter a
+//        peer GPU publishes (system-scope acquire on a real multi-GPU job; gpu scope otherwise);
+//        bits 8..31 = 1 + an early-release
 //        counter that a panel factor part sets to [6] once R_kk's rows of its block are final
 //   [15] update tasks: np | ocnt << 8 -- register passes [slice, slice + np) (slice = [4], in
 //        units of SLICE columns), and ocnt consecutive out counters [5] .. [5] + ocnt - 1 set
@@ -92,9 +94,15 @@ cudaError_t launch_unpack(const double* At, double* A, int64_t lda, int64_t m, i
                           int64_t qloc, int cstride, int coff, cudaStream_t st);
 cudaError_t launch_get_r(const double* At, double* R, int64_t ldr, int64_t m, int64_t n, int b, int64_t p,
                          int64_t qloc, int cstride, int coff, cudaStream_t st);
-cudaError_t launch_pack_factors(const double* A, const double* T, double* Yp, double* Tp, int b, int s, int64_t p,
-                                int64_t K, cudaStream_t st);
-cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qb, cudaStream_t st);
+// Packed reflector panels of the factors (A, T) -- storage columns kc of global tile column
+// coff + kc*cstride, qloc of them -- into nd workspaces (Yp[d], Tp[d], indexed by the global
+// step k); sys_fence: the stores go to peer GPUs (system-scope fence at the end).
+cudaError_t launch_pack_factors(const double* A, const double* T, double* const* Yp, double* const* Tp, int nd, int b,
+                                int s, int64_t p, int64_t K, int64_t qloc, int cstride, int coff, bool sys_fence,
+                                cudaStream_t st);
+// Tile-major [I_k; 0] (m x k) in the storage columns jl of global tile column coff + jl*cstride.
+cudaError_t launch_eye_tiles(double* Qt, int64_t m, int64_t k, int b, int64_t p, int64_t qloc, int cstride, int coff,
+                             cudaStream_t st);
 // Cross-rank entry barrier of one call (real multi-GPU): publish `gen` into every rank's
 // arrive[me] (system scope), wait until arrive[g] >= gen for all g on this rank.
 cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int gen, cudaStream_t st);

@@ -77,6 +77,8 @@ def lib():
         L.tqr_comm_flags.argtypes = [_vp, _vp]
         L.tqr_schedule_records.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _vp, _i64, ctypes.POINTER(_i64),
                                            ctypes.POINTER(_i32)]
+        L.tqr_schedule_model.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, ctypes.c_double,
+                                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.tqr_plan_records.argtypes = [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]
         L.tqr_plan_info.argtypes = [_vp, ctypes.POINTER(_i32)]
         _lib = L
@@ -134,6 +136,14 @@ def schedule_records(p: int, q: int, nslice: int, workers: int, nranks: int, ran
     _check(lib().tqr_schedule_records(p, q, nslice, workers, nranks, rank, rec.ctypes.data, n.value, ctypes.byref(n),
                                       ctypes.byref(nc)))
     return rec[: n.value], nc.value
+
+
+def schedule_model(m: int, n: int, b: int, s: int, nranks: int = 1, workers: int = 148, remote_ns: float = 0.0):
+    """Modelled makespan (ms) and utilisation of the factorization schedule (a MODEL, pure host;
+    include/tqr.h tqr_schedule_model)."""
+    ms, busy = ctypes.c_double(), ctypes.c_double()
+    _check(lib().tqr_schedule_model(m, n, b, s, nranks, workers, remote_ns, ctypes.byref(ms), ctypes.byref(busy)))
+    return ms.value / 1e6, busy.value
 
 
 # ---- plan ----------------------------------------------------------------------------------

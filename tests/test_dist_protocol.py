@@ -114,6 +114,10 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
                 assert rec[14] & 0xFF in (1, 2, 1 | 4)
             else:
                 assert _global_j(rec, G, r) % G == r and not rec[14] & 1  # update on owner(j), local
+                # dep 0 (the panel counter PF(k, last)) is acquired at system scope exactly when
+                # a peer GPU publishes it; every other dependency is rank-local (gpu scope)
+                assert bool(rec[14] & 8) == (k % G != r) and not rec[14] & 0x30
+                assert _deps(rec)[0][0] == k * 3 * NPT + NPT - 1
             keys.extend(_task_keys(rec, G, r))
         sims.append(RankSim(recs, nctr, workers))
     assert sorted(keys) == ref, "the ranks' tasks are not exactly the single-GPU DAG"

@@ -149,3 +149,42 @@ def test_real_ranks_ipc_connect_and_peer_stores():
         p_.join(timeout=120)
         assert p_.exitcode == 0
     assert res[0] == [7000, 7001] and res[1] == [7000, 7001], res
+
+
+@pytest.mark.parametrize("m,n,b,s,G,nrhs", [(700, 600, 256, 32, 2, 300), (520, 300, 128, 32, 3, 260),
+                                            (1100, 1030, 512, 64, 2, 200), (2048, 2048, 128, 32, 4, 500),
+                                            (67, 41, 16, 8, 3, 20)])
+def test_emulated_ranks_ormqr_orgqr_bitwise_equal_single_gpu(m, n, b, s, G, nrhs):
+    """Multi-rank apply-Q / form-Q (include/tqr.h): B's tile columns block-cyclic over the
+    ranks, every rank's workspace filled with every rank's reflector panels, each rank
+    applying Q to its own columns -- bitwise equal to the single-GPU apply (same per-tile
+    operation sequence) and within the oracle's tolerance."""
+    import torch
+    from paper_0707_3548_b200 import Plan
+    A = tqr_inputs.uniform(m, n, 41 + m + G)
+    g1 = run_factor(A, b, s)
+    p1 = g1["plan"]
+    pe = Plan(m, n, b, s, nranks=G, rank=0, emulate=True)
+    At = torch.from_numpy(g1["At"]).cuda()
+    T = torch.from_numpy(g1["T"]).cuda()
+    Bm = tqr_inputs.uniform(m, nrhs, 7 + G)
+    for trans in ("T", "N"):
+        B1 = torch.from_numpy(oracle.pack(Bm, b)).cuda()
+        Be = B1.clone()
+        p1.ormqr(trans, g1["At_dev"], g1["T_dev"], B1, nrhs)
+        pe.ormqr(trans, At, T, Be, nrhs)
+        torch.cuda.synchronize()
+        assert torch.equal(B1, Be), f"apply-Q ({trans}) differs from the single-GPU result"
+        want = oracle.ormqr(g1["At"], g1["T"], m, n, b, s, Bm, 1 if trans == "T" else 0, nthreads=4)
+        got = oracle.unpack(Be.cpu().numpy(), m, nrhs, b)
+        col_err = np.linalg.norm(got - want, axis=0) / np.linalg.norm(Bm, axis=0)
+        assert np.max(col_err) <= 10 * m * np.finfo(np.float64).eps
+    k = min(m, n)
+    qb = -(-k // b)
+    Q1 = torch.empty(p1.p * qb * b * b, dtype=torch.float64, device="cuda")
+    Qe = torch.full_like(Q1, 3.0)
+    p1.orgqr(g1["At_dev"], g1["T_dev"], k, Q1)
+    pe.orgqr(At, T, k, Qe)
+    torch.cuda.synchronize()
+    assert torch.equal(Q1, Qe), "form-Q differs from the single-GPU result"
+    pe.close()

@@ -39,8 +39,10 @@ w = min(b, {64: 64, 128: 64, 256: 32, 512: 16}.get(b, 64))
 fl = {0: 4 / 3 * B ** 3 + 2 / 3 * S * B * B, 1: 2 * B ** 3 + 4 / 3 * S * B * B, 2: 2 * B * B * w + S * B * w,
       3: 4 * B * B * w + S * B * w}
 fl.update({4: fl[2], 5: fl[3], 6: fl[2], 7: fl[3]})
+# factor parts alone (one inner block): rank-1 panel updates + Gram, per block
+fl.update({8: (2 * B * S * S + B * S * S) / 2, 9: 2 * B * S * S + B * S * S})
 for kind in [int(x) for x in a.kinds.split(",")]:
-    count = a.count or (148 if kind in (0, 1) else 148 * 8)
+    count = a.count or (148 if kind in (0, 1, 8, 9) else 148 * 8)
     for r in range(a.reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(plan.stream)
@@ -56,6 +58,6 @@ for kind in [int(x) for x in a.kinds.split(",")]:
         names = PHASE_NAMES
         print("   phases (% of warp-0 cycles, all reps): " + ", ".join(f"{n} {100*x/tot:.1f}" for n, x in zip(names, v) if x))
     per_task_us = ms * 1e3 / waves
-    print(f"kind {['G','T','L','S','LQT','SQT','LQ','SQ'][kind]} b={b} s={s}: {count} tasks in {ms:.3f} ms -> {per_task_us:.1f} us/task/SM, "
+    print(f"kind {['G','T','L','S','LQT','SQT','LQ','SQ','G-factor-part','T-factor-part'][kind]} b={b} s={s}: {count} tasks in {ms:.3f} ms -> {per_task_us:.1f} us/task/SM, "
           f"{fl[kind] / (per_task_us * 1e3):.1f} GFLOP/s per SM ({100 * fl[kind] / (per_task_us * 1e3) / 251:.1f}% of 251)",
           flush=True)
