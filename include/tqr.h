@@ -206,7 +206,8 @@ tqr_status tqr_plan_records(tqr_plan* plan, int32_t local, int32_t* rec, int64_t
 tqr_status tqr_plan_info(const tqr_plan* plan, int32_t info[12]);
 
 /* Trace of the last tqr_geqrf with TQR_FLAG_TRACE: up to `cap` records of
- * {kind, k, i, j, slice, sm, start_ns, end_ns} as 8 int64 each (host memory);
+ * {kind, k, i, j, slice | flags << 16, sm, start_ns, end_ns} as 8 int64 each (host memory;
+ * flags = the low byte of task record [14]: 2 panel apply part, 4 panel factor part);
  * returns the number of records written in *n. */
 tqr_status tqr_trace_fetch(tqr_plan* plan, int64_t* rec, int64_t cap, int64_t* n);
 

@@ -660,530 +660,6 @@ __device__ __forceinline__ void panel_factor(double* P, int c0, double* Rb, doub
   __syncthreads();
 }
 
-// ---------------------------------------------------------------------------------------
-// Pipelined panel factorization (same contract as panel_factor; R26).  The owner of
-// column c publishes the UNSCALED updated column w_c (= alpha-free part of the next reflector,
-// v_c = scale_c * w_c, scale_c = 1/(alpha_c - beta_c)) the moment it has applied reflector c-1
-// to it -- mbarrier pmb[c] -- and only then computes the norm, beta, tau and scale, published
-// separately -- mbarrier pmb[S + c] with tau[c], scl[c].  Every consumer (the owner of c+1 on
-// the critical path, the other warps for their columns) starts its dot products with w_c as
-// soon as w_c lands and needs the scalars only for the final update
-//     u_c^T y = y_top(c) + scale_c * (w_c . y),   y -= tau_c (u_c^T y) u_c,
-// so the Householder generation of column c overlaps the next owner's reductions instead of
-// preceding them: the critical path per column is one publication + one 3-value reduction +
-// one update.  V = scale * w is written once after the loop.  Same reflectors as panel_factor
-// in exact arithmetic (rounding order differs).
-// pmb: 2S mbarriers (one arrival each), initialised once per launch; every call completes each
-// exactly once (call g waits on parity g & 1).  scl: S doubles of shared memory.
-// ---------------------------------------------------------------------------------------
-template <int B, int S, int NW, int LDP>
-__device__ __forceinline__ void panel_factor2(double* P, int c0, double* Rb, double* tau, double* scl, const bool TS,
-                                              unsigned long long* pmb, unsigned parity) {
-  static_assert(S <= 64, "top block rows: two per lane at most");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  constexpr int NR = (B + 31) / 32;       // x-part rows per lane: row r = lane + 32 q
-  constexpr int NC = (S + NW - 1) / NW;   // columns per warp: column c = warp + NW ci
-  constexpr int NTR = (S + 31) / 32;      // top-block rows per lane: block row L = lane + 32 h
-  const int lox = TS ? 0 : c0 + S;        // first x-part row
-  double x[NC][NR], tr[NC][NTR];
-#pragma unroll
-  for (int ci = 0; ci < NC; ++ci) {
-    const int c = warp + NW * ci;
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const int r = lane + 32 * q;
-      x[ci][q] = (c < S && r >= lox && r < B) ? P[r + c * LDP] : 0.0;
-    }
-#pragma unroll
-    for (int h = 0; h < NTR; ++h) {
-      const int L = lane + 32 * h;
-      tr[ci][h] = (c < S && L < S && (!TS || L <= c)) ? (TS ? Rb[L + c * S] : P[c0 + L + c * LDP]) : 0.0;
-    }
-  }
-  auto getT = [&](auto CI, int L) __attribute__((always_inline)) -> double {
-    constexpr int ci = decltype(CI)::value;
-    const double t = (NTR == 1 || L < 32) ? tr[ci][0] : tr[ci][NTR - 1];
-    return __shfl_sync(0xffffffffu, t, L & 31);
-  };
-  auto subT = [&](auto CI, int L, double w) __attribute__((always_inline)) {
-    constexpr int ci = decltype(CI)::value;
-    if (lane == (L & 31)) {
-      if (NTR == 1 || L < 32) tr[ci][0] -= w; else tr[ci][NTR - 1] -= w;
-    }
-  };
-  // publish the unscaled column c (x rows; GEQRT also the top-block rows below the pivot)
-  auto pub_w = [&](auto CI, int c) __attribute__((always_inline)) {
-    constexpr int ci = decltype(CI)::value;
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const int r = lane + 32 * q;
-      if (r >= lox && r < B) P[r + c * LDP] = x[ci][q];
-    }
-    if (!TS) {
-#pragma unroll
-      for (int h = 0; h < NTR; ++h) {
-        const int L = lane + 32 * h;
-        if (L > c && L < S) P[c0 + L + c * LDP] = tr[ci][h];
-      }
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(pmb + c);
-  };
-  // Householder scalars of column c (R2-R4, R17, R20) from alpha and sigma
-  auto house_pub = [&](auto CI, int c, double alpha, double sigma) __attribute__((always_inline)) {
-    double beta, tv, scale;
-    if (sigma == 0.0) {
-      beta = alpha; tv = 0.0; scale = 0.0;
-    } else {
-      const double nn = alpha * alpha + sigma;
-      const double rn = rsqrt(nn);                // 1/nu
-      const double nu = nn * rn;
-      beta = (alpha >= 0.0) ? -nu : nu;
-      tv = 1.0 + fabs(alpha) * rn;                 // (beta - alpha)/beta = 1 + |alpha|/nu
-      scale = __drcp_rn(alpha - beta);             // correctly rounded, == 1.0 / (alpha - beta)
-    }
-    if (lane == 0) {
-      if (TS) Rb[c + c * S] = beta; else P[c0 + c + c * LDP] = beta;
-      tau[c] = tv;
-      scl[c] = scale;
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(pmb + S + c);
-  };
-  auto norm_below = [&](auto CI, int j) __attribute__((always_inline)) -> double {
-    constexpr int ci = decltype(CI)::value;
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      if (q & 1) s1 += x[ci][q] * x[ci][q]; else s0 += x[ci][q] * x[ci][q];
-    }
-    if (!TS) {
-#pragma unroll
-      for (int h = 0; h < NTR; ++h) {
-        const int L = lane + 32 * h;
-        if (L > j && L < S) s0 += tr[ci][h] * tr[ci][h];
-      }
-    }
-    return warp_sum(s0 + s1);
-  };
-
-  if (warp == 0) {
-    const std::integral_constant<int, 0> C0;
-    const double sg = norm_below(C0, 0);
-    pub_w(C0, 0);
-    house_pub(C0, 0, getT(C0, 0), sg);
-  }
-  for (int jj = 0; jj + 1 < S; ++jj) {
-    mbar_wait(pmb + jj, parity);  // w_jj published (acquire)
-    double vr[NR], vt[NTR];
-#pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const int r = lane + 32 * q;
-      vr[q] = (r >= lox && r < B) ? P[r + jj * LDP] : 0.0;
-    }
-#pragma unroll
-    for (int h = 0; h < NTR; ++h) {  // w_jj inside the top block (GEQRT only; TSQRT: e_jj)
-      const int L = lane + 32 * h;
-      vt[h] = (!TS && L > jj && L < S) ? P[c0 + L + jj * LDP] : 0.0;
-    }
-    const int nxt = jj + 1;
-    bool have_b = false;
-    double tj = 0.0, sj = 0.0;
-    if (nxt % NW == warp) {
-      // critical path: reduce (x.w, x.x, w.w) for column jj+1 while reflector jj's scalars
-      // are still being generated, then update, publish w_{jj+1}, then its scalars
-      static_for<NC>([&](auto CI) __attribute__((always_inline)) {
-        constexpr int ci = decltype(CI)::value;
-        if (warp + NW * ci != nxt) return;
-        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          if (q & 1) { a1 += vr[q] * x[ci][q]; b1 += x[ci][q] * x[ci][q]; e1 += vr[q] * vr[q]; }
-          else { a0 += vr[q] * x[ci][q]; b0 += x[ci][q] * x[ci][q]; e0 += vr[q] * vr[q]; }
-        }
-        if (!TS) {
-#pragma unroll
-          for (int h = 0; h < NTR; ++h) {
-            const int L = lane + 32 * h;
-            const double tv_ = (L > jj && L < S) ? tr[ci][h] : 0.0;
-            a0 += vt[h] * tv_; b0 += tv_ * tv_; e0 += vt[h] * vt[h];
-          }
-        }
-        double sxw = a0 + a1, sxx = b0 + b1, sww = e0 + e1;
-        const double top = getT(CI, jj);
-        const double alpha_ts = TS ? getT(CI, nxt) : 0.0;  // TSQRT: unchanged by reflector jj
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          sxw += __shfl_xor_sync(0xffffffffu, sxw, o);
-          sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
-          sww += __shfl_xor_sync(0xffffffffu, sww, o);
-        }
-        mbar_wait(pmb + S + jj, parity);  // scalars of reflector jj
-        tj = tau[jj];
-        sj = scl[jj];
-        have_b = true;
-        const double tw = tj * (top + sj * sxw), f = tw * sj;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) x[ci][q] -= f * vr[q];
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) tr[ci][h] -= f * vt[h];
-        subT(CI, jj, tw);
-        pub_w(CI, nxt);
-        const double alpha = TS ? alpha_ts : getT(CI, nxt);
-        const double a2 = TS ? 0.0 : alpha * alpha;
-        double sigma = sxx - 2.0 * f * sxw + f * f * sww - a2;
-        const double mag = sxx + 2.0 * fabs(f * sxw) + f * f * sww + a2;
-        if (!(sigma >= 0.05 * mag)) sigma = norm_below(CI, nxt);  // possible cancellation / NaN
-        house_pub(CI, nxt, alpha, sigma);
-      });
-    }
-#ifdef TQR_PF_SKIP_NONCRIT  // tools/panel_bench.cu timing experiment only (wrong results)
-    continue;
-#endif
-    // the warp's other columns c > jj+1: dots with w_jj, one interleaved reduction, update
-    double dc[NC];
-#pragma unroll
-    for (int ci = 0; ci < NC; ++ci) {
-      const int c = warp + NW * ci;
-      double d0 = 0.0, d1 = 0.0;
-      if (c > nxt && c < S) {
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          if (q & 1) d1 += vr[q] * x[ci][q]; else d0 += vr[q] * x[ci][q];
-        }
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) d0 += vt[h] * tr[ci][h];
-      }
-      dc[ci] = d0 + d1;
-    }
-    warp_allreduce<NC>(dc);
-    if (!have_b) {
-      mbar_wait(pmb + S + jj, parity);
-      tj = tau[jj];
-      sj = scl[jj];
-    }
-    static_for<NC>([&](auto CI) __attribute__((always_inline)) {
-      constexpr int ci = decltype(CI)::value;
-      const int c = warp + NW * ci;
-      if (c > nxt && c < S) {
-        const double tw = tj * (getT(CI, jj) + sj * dc[ci]), f = tw * sj;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) x[ci][q] -= f * vr[q];
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) tr[ci][h] -= f * vt[h];
-        subT(CI, jj, tw);
-      }
-    });
-  }
-  __syncthreads();  // every warp has read every w from P: V = scale * w may overwrite it
-  // V = scale * w (x rows; GEQRT also the top-block rows below the pivot), R entries above the
-  // diagonal of the top block (the diagonal, beta, was stored by house_pub)
-#pragma unroll
-  for (int ci = 0; ci < NC; ++ci) {
-    const int c = warp + NW * ci;
-    if (c < S) {
-      const double sc = scl[c];
-#pragma unroll
-      for (int q = 0; q < NR; ++q) {
-        const int r = lane + 32 * q;
-        if (r >= lox && r < B) P[r + c * LDP] = x[ci][q] * sc;
-      }
-#pragma unroll
-      for (int h = 0; h < NTR; ++h) {
-        const int L = lane + 32 * h;
-        if (L < c) {
-          if (TS) Rb[L + c * S] = tr[ci][h]; else P[c0 + L + c * LDP] = tr[ci][h];
-        } else if (!TS && L > c && L < S) {
-          P[c0 + L + c * LDP] = tr[ci][h] * sc;
-        }
-      }
-    }
-  }
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------------------------------
-// Sub-panel panel factorization (R26; same contract as panel_factor).  The s-column
-// block is factored in sub-panels of SP = 8 columns (4 at b = 512), each by ONE warp holding
-// the SP columns in registers with every index compile-time (no inter-warp handoff, no
-// per-column branches); between sub-panels all warps apply the sub-panel's block reflector
-// (Y_g, T_g) to the columns to its right (a block update, as between the b/s blocks of a tile).
-// Inside a sub-panel, step j: the dot products of the UNSCALED pivot column w_j with the
-// columns to its right, the Gram entries u_t^T w_j (t < j) for T_g and the next column's norm
-// are reduced in ONE interleaved butterfly while the Householder scalars of column j are
-// generated from (alpha_j, sigma_j) (the two are independent), then
-//     u_j^T y = y(L_j) + scale_j (w_j . y),   y -= tau_j (u_j^T y) u_j,   v_j = scale_j w_j,
-// and the next column's sigma follows from ||x||^2, w.x, ||w||^2 (cancellation-guarded,
-// DESIGN.md R20).  Same reflectors as the column-by-column algorithm in exact arithmetic.
-// tgs: SP*SP doubles of shared memory (T_g).  Ends with __syncthreads.
-// ---------------------------------------------------------------------------------------
-template <int B, int S>
-struct PanelSP {
-  static constexpr int SP = (S < 8 ? S : 8) / ((B > 256 && S >= 8) ? 2 : 1);
-};
-
-template <int B, int S, int NW, int LDP>
-__device__ __forceinline__ void panel_factor3(double* P, int c0, double* Rb, double* tau, double* tgs, const bool TS) {
-  constexpr int SP = PanelSP<B, S>::SP;
-  constexpr int NSP = S / SP;
-  constexpr int NR = (B + 31) / 32;       // x-part rows per lane: row r = lane + 32 q
-  constexpr int NTR = (S + 31) / 32;      // top-block rows per lane: block row L = lane + 32 h
-  constexpr int NAR = SP < 2 ? 2 : SP;    // allreduce width (power of two >= SP)
-  static_assert(S % SP == 0 && (NAR & (NAR - 1)) == 0, "sub-panel width");
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int lox = TS ? 0 : c0 + S;        // first x-part row
-  // top-block element (block row L, panel column c)
-  auto topref = [&](int L, int c) __attribute__((always_inline)) -> double& {
-    return TS ? Rb[L + c * S] : P[c0 + L + c * LDP];
-  };
-  for (int g = 0; g < NSP; ++g) {
-    const int cs = g * SP;
-    if (warp == g % NW) {
-      // ---- factor sub-panel g in this warp's registers ----
-      double x[SP][NR], t[SP][NTR], tg[SP];
-#pragma unroll
-      for (int j = 0; j < SP; ++j) {
-        const int c = cs + j;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = lane + 32 * q;
-          x[j][q] = (r >= lox && r < B) ? P[r + c * LDP] : 0.0;
-        }
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) {
-          const int L = lane + 32 * h;
-          t[j][h] = (L < S && (!TS || L <= c)) ? topref(L, c) : 0.0;
-        }
-        tg[j] = 0.0;
-      }
-      auto bcast = [&](const double (&v)[NTR], int L) __attribute__((always_inline)) -> double {
-        const double y = (NTR == 1 || L < 32) ? v[0] : v[NTR - 1];
-        return __shfl_sync(0xffffffffu, y, L & 31);
-      };
-      // squared norm of column j below its pivot row L_j = cs + j (x rows; GEQRT: top rows > L_j)
-      auto norm_below = [&](int j) __attribute__((always_inline)) -> double {
-        double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          if (q & 1) s1 += x[j][q] * x[j][q]; else s0 += x[j][q] * x[j][q];
-        }
-        if (!TS) {
-#pragma unroll
-          for (int h = 0; h < NTR; ++h) {
-            const int L = lane + 32 * h;
-            if (L > cs + j && L < S) s0 += t[j][h] * t[j][h];
-          }
-        }
-        return warp_sum(s0 + s1);
-      };
-      double sigma = norm_below(0);
-      double alpha = bcast(t[0], cs);
-#pragma unroll
-      for (int j = 0; j < SP; ++j) {
-        const int L = cs + j;  // pivot block row
-        // (1) reductions with the unscaled w_j = column j below its pivot:
-        //     slot i > j: w_j . y_i;  slot t < j: v_t . w_j (Gram for T_g);  slot j: ||y_{j+1}||^2
-        //     below ITS pivot (the next sigma); every slot over x rows + top rows > L_j
-        double red[NAR];
-#pragma unroll
-        for (int i = 0; i < NAR; ++i) red[i] = 0.0;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-#pragma unroll
-          for (int i = 0; i < SP; ++i) {
-            if (i == j) {
-              if (j + 1 < SP) red[j] += x[j + 1][q] * x[j + 1][q];
-            } else {
-              red[i] += x[j][q] * x[i][q];  // i < j: x[i] holds v_i (scaled)
-            }
-          }
-        }
-        if (!TS) {
-#pragma unroll
-          for (int h = 0; h < NTR; ++h) {
-            const int Lh = lane + 32 * h;
-            const double wj = (Lh > L && Lh < S) ? t[j][h] : 0.0;
-#pragma unroll
-            for (int i = 0; i < SP; ++i) {
-              if (i == j) {
-                if (j + 1 < SP && Lh > L + 1 && Lh < S) red[j] += t[j + 1][h] * t[j + 1][h];
-              } else {
-                red[i] += wj * t[i][h];
-              }
-            }
-          }
-        }
-        // (2) Householder scalars of column j (independent of the reductions: overlaps them)
-        double beta, tv, scale;
-        if (sigma == 0.0) {
-          beta = alpha; tv = 0.0; scale = 0.0;
-        } else {
-          const double nn = alpha * alpha + sigma;
-          const double rn = rsqrt(nn);                // 1/nu
-          const double nu = nn * rn;
-          beta = (alpha >= 0.0) ? -nu : nu;
-          tv = 1.0 + fabs(alpha) * rn;                 // (beta - alpha)/beta = 1 + |alpha|/nu
-          scale = __drcp_rn(alpha - beta);             // == 1.0 / (alpha - beta)
-        }
-        const double wsq = sigma;                      // ||w_j||^2 below the pivot
-        const double wnext = (!TS && j + 1 < SP) ? bcast(t[j], L + 1) : 0.0;  // w_j at row L_{j+1}
-        warp_allreduce<NAR>(red);
-        // (3) v_j = scale * w_j in place; pivot row := beta; T_g column j
-#pragma unroll
-        for (int q = 0; q < NR; ++q) x[j][q] *= scale;
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) {
-          const int Lh = lane + 32 * h;
-          if (Lh == L) t[j][h] = beta;
-          else if (!TS && Lh > L && Lh < S) t[j][h] *= scale;
-        }
-        {
-          // z_t = u_t^T u_j = [GEQRT: v_t at row L_j] + scale_j (v_t . w_j over rows > L_j)
-          double acc = 0.0;
-#pragma unroll
-          for (int tt = 0; tt < j; ++tt) {
-            const double ztop = TS ? 0.0 : bcast(t[tt], L);
-            acc += tg[tt] * (ztop + scale * red[tt]);
-          }
-          tg[j] = (lane == j) ? tv : (lane < j ? -tv * acc : 0.0);
-        }
-        // (4) apply reflector j to the columns right of it (this sub-panel)
-#pragma unroll
-        for (int i = j + 1; i < SP; ++i) {
-          const double f = tv * (bcast(t[i], L) + scale * red[i]);
-#pragma unroll
-          for (int q = 0; q < NR; ++q) x[i][q] -= f * x[j][q];
-#pragma unroll
-          for (int h = 0; h < NTR; ++h) {
-            const int Lh = lane + 32 * h;
-            if (Lh == L) t[i][h] -= f;
-            else if (!TS && Lh > L && Lh < S) t[i][h] -= f * t[j][h];
-          }
-          if (i == j + 1) {
-            // next pivot: alpha = y(L_{j+1}) after the update; sigma from
-            // ||y||^2 - 2 f' (w.y) + f'^2 ||w||^2 over rows > L_{j+1}, f' = f scale
-            alpha = bcast(t[i], L + 1);
-            const double fp = f * scale;
-            // (w.y over rows > L_{j+1}) = red[i] - w(L_{j+1}) y_old(L_{j+1}); y_old = y_new + fp w
-            const double yold = TS ? 0.0 : alpha + fp * wnext;
-            const double wy2 = TS ? red[i] : red[i] - wnext * yold;
-            const double ww = wsq - wnext * wnext;
-            double sg = red[j] - 2.0 * fp * wy2 + fp * fp * ww;
-            const double mag = red[j] + 2.0 * fabs(fp * wy2) + fp * fp * ww;
-            if (!(sg >= 0.05 * mag)) sg = norm_below(i);  // possible cancellation / NaN
-            sigma = sg;
-          }
-        }
-        if (lane == 0) tau[cs + j] = tv;
-      }
-      // ---- write the sub-panel back: V (scaled), beta and R entries, T_g ----
-#pragma unroll
-      for (int j = 0; j < SP; ++j) {
-        const int c = cs + j;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = lane + 32 * q;
-          if (r >= lox && r < B) P[r + c * LDP] = x[j][q];
-        }
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) {
-          const int L = lane + 32 * h;
-          if (L < S && (!TS || L <= c)) topref(L, c) = t[j][h];
-        }
-        if (lane < SP) tgs[lane + j * SP] = tg[j];
-      }
-    }
-    __syncthreads();
-    if (g + 1 == NSP) break;
-    // ---- block update of the columns right of sub-panel g: y -= Y_g T_g^T Y_g^T y ----
-    // column c owned by warp c % NW; Y_g = [unit pivot rows; V] (TS: e tops, V in x rows);
-    // the warp's copy of V_g (x rows; GEQRT also the top rows below each pivot) in registers
-    if (cs + SP + warp < S) {
-      double vg[SP][NR], vgt[SP][NTR];
-#pragma unroll
-      for (int a = 0; a < SP; ++a) {
-        const int ca = cs + a;
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = lane + 32 * q;
-          vg[a][q] = (r >= lox && r < B) ? P[r + ca * LDP] : 0.0;
-        }
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) {
-          const int L = lane + 32 * h;
-          vgt[a][h] = (!TS && L > ca && L < S) ? P[c0 + L + ca * LDP] : 0.0;
-        }
-      }
-      for (int c = cs + SP + warp; c < S; c += NW) {
-        double y[NR], yt[NTR], w[NAR];
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = lane + 32 * q;
-          y[q] = (r >= lox && r < B) ? P[r + c * LDP] : 0.0;
-        }
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) {
-          const int L = lane + 32 * h;
-          yt[h] = (L < S && (!TS || L <= c)) ? topref(L, c) : 0.0;
-        }
-        // W_a = y(L_a) + v_a . y  (v_a: x rows; GEQRT also top rows > L_a)
-#pragma unroll
-        for (int a = 0; a < NAR; ++a) {
-          double d0 = 0.0, d1 = 0.0;
-          if (a < SP) {
-#pragma unroll
-            for (int q = 0; q < NR; ++q) {
-              if (q & 1) d1 += vg[a][q] * y[q]; else d0 += vg[a][q] * y[q];
-            }
-#pragma unroll
-            for (int h = 0; h < NTR; ++h) d0 += vgt[a][h] * yt[h];
-          }
-          w[a] = d0 + d1;
-        }
-        warp_allreduce<NAR>(w);
-        double wt[SP];
-#pragma unroll
-        for (int a = 0; a < SP; ++a) {
-          const int La = cs + a;
-          w[a] += __shfl_sync(0xffffffffu, (NTR == 1 || La < 32) ? yt[0] : yt[NTR - 1], La & 31);
-        }
-        // W <- T_g^T W (T_g upper: W'_a = sum_{b <= a} T[b][a] W_b)
-#pragma unroll
-        for (int a = 0; a < SP; ++a) {
-          double acc = 0.0;
-#pragma unroll
-          for (int b2 = 0; b2 <= a; ++b2) acc += tgs[b2 + a * SP] * w[b2];
-          wt[a] = acc;
-        }
-        // y -= Y_g W'
-#pragma unroll
-        for (int a = 0; a < SP; ++a) {
-          const int ca = cs + a;
-#pragma unroll
-          for (int q = 0; q < NR; ++q) y[q] -= vg[a][q] * wt[a];
-#pragma unroll
-          for (int h = 0; h < NTR; ++h) {
-            const int L = lane + 32 * h;
-            if (L == ca) yt[h] -= wt[a];
-            else yt[h] -= vgt[a][h] * wt[a];
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int r = lane + 32 * q;
-          if (r >= lox && r < B) P[r + c * LDP] = y[q];
-        }
-#pragma unroll
-        for (int h = 0; h < NTR; ++h) {
-          const int L = lane + 32 * h;
-          if (L < S && (!TS || L <= c)) topref(L, c) = yt[h];
-        }
-      }
-    }
-    __syncthreads();
-  }
-}
-
 // Gram matrix of the staged panel (DLARFT dot products): Z[a + b*S] = Y[:, a]^T Y[:, b]
 // for the upper block triangle, by DMMA on the swizzled Ys (GEQRT: Y = U_l with its unit
 // diagonal and zeros above; TSQRT: Y = V_l, identity tops orthogonal).
@@ -1195,18 +671,20 @@ __device__ void gram_upper(const double* __restrict__ Ys, double* Z) {
     int u1 = 0, rem = tile;
     while (rem >= NU - u1) { rem -= NU - u1; ++u1; }
     const int u2 = u1 + rem;
-    double g0[2] = {0.0, 0.0}, g1[2] = {0.0, 0.0};
+    // four independent accumulator chains (B/8 x 2 k-steps), summed in a fixed order
+    double g[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll 4
     for (int t = 0; t < B / 8; ++t)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const double a = Ys[swy<B>(8 * t + 2 * j + h, 8 * u1 + pn)];
         const double bb = Ys[swy<B>(8 * t + 2 * j + h, 8 * u2 + pn)];
-        if (t & 1) dmma(g1, a, bb); else dmma(g0, a, bb);
+        dmma(g[(t & 1) * 2 + h], a, bb);
       }
     // element (m = lane>>2, n = 2j+h): Z[8u1 + phi(m)][8u2 + phi(2j+h)], phi(2j+h) = 4h+j
 #pragma unroll
-    for (int h = 0; h < 2; ++h) Z[(8 * u1 + pn) + (8 * u2 + 4 * h + j) * S] = g0[h] + g1[h];
+    for (int h = 0; h < 2; ++h)
+      Z[(8 * u1 + pn) + (8 * u2 + 4 * h + j) * S] = (g[0][h] + g[1][h]) + (g[2][h] + g[3][h]);
   }
 }
 
@@ -1233,6 +711,68 @@ __device__ __forceinline__ void build_t(double* Tp, const double* tau, const dou
   if (t < S) {
 #pragma unroll
     for (int j = 0; j < S; ++j) Tp[t + j * S] = row[j];
+  }
+}
+
+// T_l by 8 x 8 blocks (the same forward column-wise T as build_t; R27): the
+// diagonal blocks T_bb by the row recurrence of build_t restricted to block b (warp b, one row
+// per lane), then block column by block column (Schreiber / Van Loan)
+//     T[0:8b, b] = -T[0:8b, 0:8b] (Z[0:8b, b] T_bb)
+// as 8 x 8 x 8 DMMA tile products (two m8n8k4 k-steps each).  Called by warps 0 .. S/8 - 1
+// (named barrier `bar` over them); Tp: S x S column-major (zeros below the diagonal), Z: the
+// Gram matrix (upper block triangle), M: (S - 8) x 8 doubles of scratch.
+// 8 x 8 tile product D (+)= X * Y, X and Y column-major in shared memory (leading dims lx, ly);
+// accumulator element (lane >> 2, 2 (lane & 3) + h) in d[h].
+__device__ __forceinline__ void tile_mma8(double (&d)[2], const double* X, int lx, const double* Y, int ly) {
+  const int lane = threadIdx.x & 31, m = lane >> 2, k = lane & 3;
+#pragma unroll
+  for (int kk = 0; kk < 8; kk += 4) dmma(d, X[m + (kk + k) * lx], Y[(kk + k) + m * ly]);
+}
+template <int S>
+__device__ __forceinline__ void build_t_blocked(double* Tp, const double* tau, const double* Z, double* M, int bar) {
+  constexpr int NB = S / 8;
+  static_assert(S % 8 == 0, "8 x 8 blocks");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m = lane >> 2, n0 = 2 * (lane & 3);
+  // zero the strictly lower blocks, then the diagonal blocks (warp b: block b)
+  for (int e = threadIdx.x; e < S * S; e += 32 * NB) {
+    const int r = e % S, c = e / S;
+    if (r / 8 > c / 8) Tp[e] = 0.0;
+  }
+  {
+    const int b = warp, t = lane & 7;
+    double row[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const double tj = tau[8 * b + j];
+      double acc = 0.0;
+#pragma unroll
+      for (int tp = 0; tp < j; ++tp) acc += row[tp] * Z[(8 * b + tp) + (8 * b + j) * S];
+      row[j] = (j == t) ? tj : (j > t ? -tj * acc : 0.0);
+    }
+    if (lane < 8) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) Tp[(8 * b + t) + (8 * b + j) * S] = row[j];
+    }
+  }
+  if (NB == 1) return;
+  named_bar(bar, 32 * NB);
+  for (int b = 1; b < NB; ++b) {
+    const double* Tbb = Tp + 8 * b + 8 * b * S;
+    if (warp < b) {  // M_c = Z_cb T_bb, c = warp
+      double d[2] = {0.0, 0.0};
+      tile_mma8(d, Z + 8 * warp + 8 * b * S, S, Tbb, S);
+      M[(8 * warp + m) + n0 * (S - 8)] = d[0];
+      M[(8 * warp + m) + (n0 + 1) * (S - 8)] = d[1];
+    }
+    named_bar(bar, 32 * NB);
+    if (warp < b) {  // T_ab = -sum_{c = a}^{b-1} T_ac M_c, a = warp
+      double d[2] = {0.0, 0.0};
+      for (int c = warp; c < b; ++c) tile_mma8(d, Tp + 8 * warp + 8 * c * S, S, M + 8 * c, S - 8);
+      Tp[(8 * warp + m) + (8 * b + n0) * S] = -d[0];
+      Tp[(8 * warp + m) + (8 * b + n0 + 1) * S] = -d[1];
+    }
+    named_bar(bar, 32 * NB);
   }
 }
 

@@ -187,6 +187,16 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
 // out and the packed Y_l / T_l are published for blocks l+1.. and for every update task.
 // TSQRT reads and writes only the upper triangle of A(k,k).
 // ---------------------------------------------------------------------------------------
+// The panel column loop as a called function, register-allocated on its own instead of inside
+// the whole executor: used by the tall-skinny b = 256 instance (RW = 128), whose inlined loop
+// measured 1880 clk per column vs 1440 called (tools/prof_tasks.py, r02 phase profiles); the
+// other instances keep it inlined (called: 3-9% slower there).
+template <int B, int S, int NW, int LDP, bool TS>
+__device__ __noinline__ void panel_factor_call(double* P, int c0, double* Rb, double* tau, unsigned long long* pmb,
+                                               unsigned parity) {
+  panel_factor<B, S, NW, LDP>(P, c0, Rb, tau, TS, pmb, parity);
+}
+
 template <int B, int S, int SO, int RWM, bool ts>
 __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<B, S, RWM>::RW / 8][2],
                                             double* Akk, double* Ab, double* Tslot, const ExecArgs& a, size_t yoff,
@@ -225,8 +235,12 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     }
   __syncthreads();
   PH_MARK(8);
-  panel_factor<B, S, C::NWARP, LDP>(P, c0, Rb, tau, ts, reinterpret_cast<unsigned long long*>(sm + L::PMB),
-                                    pf_gen & 1);
+  if constexpr (B == 256 && RWM == 128)
+    panel_factor_call<B, S, C::NWARP, LDP, ts>(P, c0, Rb, tau, reinterpret_cast<unsigned long long*>(sm + L::PMB),
+                                               pf_gen & 1);
+  else
+    panel_factor<B, S, C::NWARP, LDP>(P, c0, Rb, tau, ts, reinterpret_cast<unsigned long long*>(sm + L::PMB),
+                                      pf_gen & 1);
   ++pf_gen;  // every call completes each column mbarrier once
   PH_MARK(9);
   // V / R out, packed Y_l (Ys), Gram -> T_l, packed T_l
@@ -260,22 +274,26 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
   gram_upper<B, S, C::NWARP>(Ys, Z);
   __syncthreads();
   PH_MARK(11);
-  constexpr int NTW = (S + 31) / 32;  // warps building T_l
-  if (warp < NTW) {
-    build_t<S>(Tp, tau, Z);
-  } else {
-    // meanwhile the other warps store the packed Y_l into every rank's workspace (the V
-    // broadcast of SURVEY 8(e), fused into the panel task: peer stores over NVLink on a
-    // multi-GPU job, local stores otherwise).  One flat loop over (rank, 16-byte chunk), so
-    // the stores to all G ranks are in flight together (not one rank after another).
+  // T_l by 8 x 8 blocks on warps 0 .. S/8 - 1 (scratch: the P overlay, no longer read)
+  constexpr int NTW = S / 8 < C::NWARP ? S / 8 : C::NWARP;
+  // the packed Y_l into every rank's workspace (the V broadcast of SURVEY 8(e), fused into
+  // the panel task: peer stores over NVLink on a multi-GPU job, local stores otherwise).  One
+  // flat loop over (rank, 16-byte chunk), so the stores to all G ranks are in flight together.
+  auto store_y = [&](int t0, int nt) __attribute__((always_inline)) {
     constexpr int NV2 = B * S / 2;
     const double2* ys2 = reinterpret_cast<const double2*>(Ys);
-    for (int e = tid - 32 * NTW; e < a.nranks * NV2; e += C::NT - 32 * NTW) {
+    for (int e = tid - t0; e < a.nranks * NV2; e += nt) {
       const int g = e / NV2, x = e - g * NV2;
       __stcg(reinterpret_cast<double2*>(a.Yp[g] + yoff + (size_t)l * B * S) + x, ys2[x]);
     }
-  }
+  };
+  if (warp < NTW) build_t_blocked<S>(Tp, tau, Z, P, 14);
+  else store_y(32 * NTW, C::NT - 32 * NTW);  // meanwhile, on the other warps
   __syncthreads();
+  if constexpr (NTW == C::NWARP) {
+    store_y(0, C::NT);
+    __syncthreads();
+  }
   PH_MARK(12);
   // output slot: T_L (SO x SO) in columns [L*SO, L*SO+SO); this SI-block is its diagonal
   // block m (the off-diagonal blocks of SO > SI are formed after the factorization)

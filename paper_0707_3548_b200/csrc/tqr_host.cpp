@@ -1312,7 +1312,8 @@ tqr_status tqr_trace_fetch(tqr_plan* P, int64_t* rec, int64_t cap, int64_t* n) {
     for (int64_t r = 0; r < cnt; ++r) {
       const int* t = &tasks[(size_t)r * TASK_INTS];
       int64_t* o = rec + (w + r) * 8;
-      o[0] = t[0]; o[1] = t[1]; o[2] = t[2]; o[3] = t[3]; o[4] = t[4];
+      o[0] = t[0]; o[1] = t[1]; o[2] = t[2]; o[3] = t[3];
+      o[4] = (int64_t)(t[4] & 0xFFFF) | ((int64_t)(t[14] & 0xFF) << 16);  // slice | task flags << 16
       o[5] = (int64_t)(raw[r * 4] >> 32);
       o[6] = (int64_t)raw[r * 4 + 2];
       o[7] = (int64_t)raw[r * 4 + 3];

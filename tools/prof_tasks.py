@@ -28,7 +28,7 @@ plan = tqr.Plan(a.m or a.n, a.n, b, s)
 info = plan.info()
 import os  # noqa: E402
 PH = None
-if os.environ.get("TQR_LIB", "").endswith("libtqr_phases.so"):
+if os.environ.get("TQR_LIB", "").endswith("libtqr_phases.so") or os.environ.get("TQR_PH") == "1":
     PH = torch.zeros(16, dtype=torch.int64, device="cuda")
     plan.phase_counters(PH)
 At, T = plan.alloc()

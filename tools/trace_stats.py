@@ -7,7 +7,8 @@ import numpy as np
 
 d = json.load(open(sys.argv[1]))
 r = np.array(d["records"], dtype=np.int64)
-kind, k, i, j, sl, sm, st, en = r.T
+kind, k, i, j, slf, sm, st, en = r.T
+sl = slf & 0xFFFF  # slice | task flags << 16 (tqr_trace_fetch)
 t0 = st.min()
 st = (st - t0) / 1e3
 en = (en - t0) / 1e3
@@ -54,3 +55,15 @@ for kd, name in enumerate("GTLS"):
     if m.any():
         print(f"  gap before {name}: mean {gap[m].mean():7.1f} us, p90 {np.percentile(gap[m], 90):7.1f} us, "
               f"total {gap[m].sum() / 1e3:8.1f} SM-ms")
+# panel parts per inner block (R21): apply (flags 2) / factor (flags 4) / fused
+fl = (slf >> 16) & 0xFF
+blk = sl
+pm = (kind <= 1)
+if pm.any():
+    print("  panel parts per block l (median us): l: apply / factor / fused")
+    for l in sorted(set(blk[pm].tolist())):
+        mA = pm & (blk == l) & ((fl & 2) != 0)
+        mF = pm & (blk == l) & ((fl & 4) != 0)
+        mU = pm & (blk == l) & ((fl & 6) == 0)
+        f = lambda m: f"{np.median(dur[m]):6.1f}" if m.any() else "    - "
+        print(f"    l={l}: {f(mA)} / {f(mF)} / {f(mU)}")
