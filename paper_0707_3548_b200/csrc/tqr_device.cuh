@@ -98,9 +98,66 @@ __device__ __forceinline__ void dmma(double (&d)[2], double a, double b) {
       : "d"(a), "d"(b));
 }
 
+// L2 residency hints (locality): with TQR_L2HINT=1 the data an SM re-reads
+// soon from L2 -- the packed reflector panels Y/T (read by every update task of one (k, i))
+// and the C1 row tiles A(k, j) (read and written by the chain S(k, k+1.., j)) -- is loaded /
+// stored with an evict_last policy and the C2 tile slices (touched once per step) with
+// evict_first.  Measured at C3: DRAM reads 226 -> 207 GB but 0.5% slower (C4 1.1%), so the
+// product build leaves it off (plain .cg accesses).
+#ifndef TQR_L2HINT
+#define TQR_L2HINT 0
+#endif
+__device__ __forceinline__ unsigned long long pol_keep() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long pol_stream() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld_cg2(const double2* p, bool keep) {
+#if TQR_L2HINT
+  double2 v;
+  asm volatile("ld.global.cg.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+               : "=d"(v.x), "=d"(v.y)
+               : "l"(p), "l"(keep ? pol_keep() : pol_stream()));
+  return v;
+#else
+  return __ldcg(p);
+#endif
+}
+__device__ __forceinline__ void st_cg2(double2* p, double2 v, bool keep) {
+#if TQR_L2HINT
+  asm volatile("st.global.cg.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y),
+               "l"(keep ? pol_keep() : pol_stream())
+               : "memory");
+#else
+  __stcg(p, v);
+#endif
+}
+__device__ __forceinline__ void st_cg1(double* p, double v, bool keep) {
+#if TQR_L2HINT
+  asm volatile("st.global.cg.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(keep ? pol_keep() : pol_stream())
+               : "memory");
+#else
+  __stcg(p, v);
+#endif
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+// cp.async of 16 bytes kept in L2 (evict_last): the C1 row tiles
+__device__ __forceinline__ void cp_async16_keep(void* smem, const void* gmem) {
+#if TQR_L2HINT
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "l"(pol_keep())
+               : "memory");
+#else
+  cp_async16(smem, gmem);
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -128,19 +185,33 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 }
 // global -> shared bulk copy (bytes % 16 == 0, both addresses 16-byte aligned)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+#if TQR_L2HINT  // reflector panels: evict_last (re-read by every update task of the panel)
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol_keep())
+      : "memory");
+#else
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+#endif
 }
 // L2 prefetch of a contiguous global range (bytes % 16 == 0, 16-byte aligned); no SMEM, no
 // completion tracking -- a hint that turns the next task's HBM reads into L2 hits
-__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes) {
+__device__ __forceinline__ void prefetch_l2(const void* src, unsigned bytes, bool keep = false) {
   // issued in chunks of <= 64 KiB
   const char* p = static_cast<const char*>(src);
   for (unsigned off = 0; off < bytes; off += 65536u) {
     const unsigned n = bytes - off < 65536u ? bytes - off : 65536u;
+#if TQR_L2HINT
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(p + off), "r"(n),
+                 "l"(keep ? pol_keep() : pol_stream())
+                 : "memory");
+#else
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p + off), "r"(n) : "memory");
+#endif
   }
 }
 // order this thread's generic-proxy accesses before subsequent async-proxy (TMA) accesses
@@ -227,22 +298,24 @@ __device__ __forceinline__ double warp_sum(double x) {
 // ---------------------------------------------------------------------------------------
 // acc covers rows [8*t0, 8*t0 + RW) of the tile.
 template <int B, int RW>
-__device__ __forceinline__ void load_cols(double (&acc)[RW / 8][2], const double* tile, int col0, int t0) {
+__device__ __forceinline__ void load_cols(double (&acc)[RW / 8][2], const double* tile, int col0, int t0,
+                                          bool keep = false) {
   const int lane = threadIdx.x & 31;
   const double2* col = reinterpret_cast<const double2*>(tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + 2 * (lane & 3));
 #pragma unroll
   for (int t = 0; t < RW / 8; ++t) {
-    const double2 v = __ldcg(col + 4 * t);
+    const double2 v = ld_cg2(col + 4 * t, keep);
     acc[t][0] = v.x;
     acc[t][1] = v.y;
   }
 }
 template <int B, int RW>
-__device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], double* tile, int col0, int t0) {
+__device__ __forceinline__ void store_cols(const double (&acc)[RW / 8][2], double* tile, int col0, int t0,
+                                           bool keep = false) {
   const int lane = threadIdx.x & 31;
   double2* col = reinterpret_cast<double2*>(tile + (size_t)(col0 + (lane >> 2)) * B + 8 * t0 + 2 * (lane & 3));
 #pragma unroll
-  for (int t = 0; t < RW / 8; ++t) __stcg(col + 4 * t, make_double2(acc[t][0], acc[t][1]));
+  for (int t = 0; t < RW / 8; ++t) st_cg2(col + 4 * t, make_double2(acc[t][0], acc[t][1]), keep);
 }
 // w[u][h] <-> C1[row0 + 8u + 4h + (lane&3)][col0 + (lane>>2)]  (s rows of the "top" tile)
 template <int B, int S>
@@ -328,8 +401,8 @@ __device__ __forceinline__ void tmul_gemm2(double (&acc)[RW / 8][2], const doubl
   auto finish = [&](int u2) __attribute__((always_inline)) {  // C1 -= W (block u2), negate
     if (store_c1) {
       double* col = top + (size_t)(col0 + g) * B + row0 + j;
-      __stcg(col + 8 * u2, c1s[c1_idx<S>(u2, 0, lane)] - wn[u2][0]);
-      __stcg(col + 8 * u2 + 4, c1s[c1_idx<S>(u2, 1, lane)] - wn[u2][1]);
+      st_cg1(col + 8 * u2, c1s[c1_idx<S>(u2, 0, lane)] - wn[u2][0], true);      // C1: kept in L2
+      st_cg1(col + 8 * u2 + 4, c1s[c1_idx<S>(u2, 1, lane)] - wn[u2][1], true);
     }
     wn[u2][0] = -wn[u2][0];
     wn[u2][1] = -wn[u2][1];
@@ -421,7 +494,7 @@ __device__ __forceinline__ void c1_fetch(double* c1s, const double* tile, int ro
 #pragma unroll
   for (int q = lane; q < 8 * (S / 2); q += 32) {
     const int n = q / (S / 2), r2 = 2 * (q % (S / 2));
-    cp_async16(c1s + n * (S + 4) + r2, tile + (size_t)(col0 + n) * B + row0 + r2);
+    cp_async16_keep(c1s + n * (S + 4) + r2, tile + (size_t)(col0 + n) * B + row0 + r2);
   }
   cp_async_commit();
 }

@@ -115,7 +115,7 @@ __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const 
 template <int B, int S, int RWM, bool QT, bool DESC, class PF>
 __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S, RWM>::RW / 8][2], const double* Yp,
                                              const double* Tp, int lb0, int nbe, double* C1, const double* Ct,
-                                             int col0, int gact, PF&& pf) {
+                                             int col0, int gact, PF&& pf, bool keep = false) {
   // blocks lb0 .. nbe-1 (DESC: nbe-1 .. 0, lb0 must be 0)
   const int nb = nbe - lb0;
   using C = Cfg<B, S, RWM>;
@@ -140,7 +140,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
     if (nb > 1) issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
   }
   if (active) {
-    load_cols<B, C::RW>(acc, Ct, cg0, t0);
+    load_cols<B, C::RW>(acc, Ct, cg0, t0, keep);
   } else {
     // a def on every path: otherwise acc stays live (for the compiler) across the panel code
     // of a panel task, which then rematerialises its indices (RW = 256: +40% instructions
@@ -331,13 +331,13 @@ __device__ __forceinline__ void prefetch_task(const int* q, const RankLocal& R, 
   double* Bt = MODE == 0 ? R.A : R.Bt;
   const size_t off = (size_t)sl * C::SLICE * B;
   const unsigned bytes = (unsigned)(C::SLICE * B * 8);  // the first pass's columns
-  prefetch_l2(tile_ptr(Bt, lkind ? k : i, j, p, B) + off, bytes);
-  if (!lkind) prefetch_l2(tile_ptr(Bt, k, j, p, B) + off, bytes);
+  prefetch_l2(tile_ptr(Bt, lkind ? k : i, j, p, B) + off, bytes, lkind);       // C2 (LARFB: the C1 row tile)
+  if (!lkind) prefetch_l2(tile_ptr(Bt, k, j, p, B) + off, bytes, true);          // C1: kept in L2
   const int vrow = lkind ? k : i;
   const double* Y = Yme + ((size_t)vrow + (size_t)k * p) * (size_t)B * B;
   constexpr int NL = B / S;
   const int l0 = MODE == 2 ? (NL >= 2 ? NL - 2 : 0) : 0;
-  prefetch_l2(Y + (size_t)l0 * B * S, (unsigned)((NL >= 2 ? 2 : 1) * B * S * 8));
+  prefetch_l2(Y + (size_t)l0 * B * S, (unsigned)((NL >= 2 ? 2 : 1) * B * S * 8), true);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -494,8 +494,8 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         auto pf = [&](int li, int nbb) {
           if (!panel && sub + 1 < nsub && li == nbb / 2) {  // next register pass of this task
             const size_t nxt_off = (size_t)(col0 + Cfg<B, S, RWM>::SLICE) * B;
-            prefetch_l2(Ct + nxt_off, (unsigned)(Cfg<B, S, RWM>::SLICE * B * 8));
-            if (C1) prefetch_l2(C1 + nxt_off, (unsigned)(Cfg<B, S, RWM>::SLICE * B * 8));
+            prefetch_l2(Ct + nxt_off, (unsigned)(Cfg<B, S, RWM>::SLICE * B * 8), lkind);
+            if (C1) prefetch_l2(C1 + nxt_off, (unsigned)(Cfg<B, S, RWM>::SLICE * B * 8), true);
           }
           if (sub != nsub - 1 || nbb < 4) return;  // (nbb: blocks this pass applies)
           const int l0 = nbb / 2;
@@ -512,12 +512,15 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
             prefetch_task<B, S, SO, RWM, MODE>(s_next, R, Yme, p);
           }
         };
-        update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf);
+        // L2 policy of the target (R28): C1 row tiles (LARFB targets) and panel tiles are
+        // re-read soon (evict_last); SSRFB C2 slices stream (evict_first)
+        const bool keep = panel || lkind;
+        update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf, keep);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (a_part) {
           if (warp / Cfg<B, S, RWM>::RS < gact)
             store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
-                                         (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8));
+                                         (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8), true);
         } else if (panel) {
           // TS as a template argument: each flavour is register-allocated on its own
           const int rlo = f_part ? sub0 * S : 0;
@@ -532,7 +535,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
                                               prc, prv);
         } else if (warp / Cfg<B, S, RWM>::RS < gact) {
           store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
-                                       (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8));
+                                       (warp % Cfg<B, S, RWM>::RS) * (Cfg<B, S, RWM>::RW / 8), keep);
         }
         if (!panel) PH_MARK(5);
       }

@@ -145,7 +145,7 @@ enum Prio { PRIO_CLASS = 0, PRIO_BLEVEL = 1 };
 // lat_remote (ns): extra modelled delay of an edge whose producer runs on another rank (the
 // NVLink peer store + system-scope release / acquire); used by the scaling model.
 static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& out, int prio = PRIO_CLASS,
-                          double lat = 0.0, double blq = 0.0, double lat_remote = 0.0) {
+                          double lat = 0.0, double blq = 0.0, double lat_remote = 0.0, int gmode = 1) {
   const int n = (int)G.t.size();
   const int nr = (int)workers.size();
   std::unordered_map<uint64_t, int> producer;
@@ -190,16 +190,24 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
       for (int sidx : succ[id]) m = std::max(m, blevel[sidx] + lat);
       blevel[id] = G.t[id].dur + m;
     }
-    // grouped tasks (the updates that read one reflector panel, R22) take their
-    // group's highest bottom level, so they are dispatched together and share the panel in L2
-    std::unordered_map<int64_t, double> gmax;
+    // grouped tasks (the updates that read one reflector panel, R22) take one common
+    // bottom level -- the group's highest (gmode 1, 3) or its median (gmode 2) -- so they are
+    // dispatched together and share the panel in L2
+    std::unordered_map<int64_t, std::vector<double>> gval;
     for (int id = 0; id < n; ++id)
-      if (G.t[id].group >= 0) {
-        double& g = gmax[G.t[id].group];
-        g = std::max(g, blevel[id]);
+      if (G.t[id].group >= 0) gval[G.t[id].group].push_back(blevel[id]);
+    std::unordered_map<int64_t, double> gsel;
+    for (auto& kv : gval) {
+      auto& v = kv.second;
+      if (gmode == 2) {
+        std::nth_element(v.begin(), v.begin() + v.size() / 2, v.end());
+        gsel[kv.first] = v[v.size() / 2];
+      } else {
+        gsel[kv.first] = *std::max_element(v.begin(), v.end());
       }
+    }
     for (int id = 0; id < n; ++id)
-      if (G.t[id].group >= 0) blevel[id] = gmax[G.t[id].group];
+      if (G.t[id].group >= 0) blevel[id] = gsel[G.t[id].group];
     // quantised (blq > 0): tasks within one quantum keep the (k, i, j, slice) order, so the
     // updates sharing one reflector panel (k, i) run together and reuse it from L2
     if (blq > 0.0)
@@ -340,7 +348,7 @@ struct DurModel {
 // update of the steps whose default-granularity task count is below two waves (the tail).
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
-                               int rwm = 128, double blq = 0.0, bool group = false, int np = 1, int fine = 0,
+                               int rwm = 128, double blq = 0.0, int group = 0, int np = 1, int fine = 0,
                                bool early = false, double lat_remote = 0.0) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
@@ -409,7 +417,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         T.t[id].rank = own(j); T.t[id].kc = scol(k);
         T.t[id].key[2] = j;
         T.t[id].np = n_; T.t[id].ocnt = n_;
-        if (group && j > k + 1) T.t[id].group = (int64_t)k * p + k;
+        if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + k;
         T.dep(id, PF(k, NPT - 1), 1, 1);
         if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
         if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, 2);
@@ -428,7 +436,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
           T.t[id].np = n_; T.t[id].ocnt = n_;
-          if (group && j > k + 1) T.t[id].group = (int64_t)k * p + i;
+          if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + i;
           T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
           if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
           T.dep(id, COL(k, j, sl), n_, i - k);
@@ -437,7 +445,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         }
     }
   }
-  if (!list_schedule(T, workers, out, prio, lat, blq, lat_remote)) out.topo_ok = false;
+  if (!list_schedule(T, workers, out, prio, lat, blq, lat_remote, group == 2 ? 2 : 1)) out.topo_ok = false;
 }
 
 // apply-Q^T (trans) or apply-Q to a tile-major B with qb tile columns.
@@ -536,7 +544,7 @@ struct tqr_plan {
   double lat = 4000.0;     // modelled per-task handoff latency of the list schedule (ns)
   int orm_prio = PRIO_BLEVEL;  // list-schedule priority of apply-Q / form-Q
   double blq = 0.0;            // bottom-level quantum (ns) of the factorization schedule
-  bool group = false;          // group the updates of one reflector panel (R22)
+  int group = 0;               // group the updates of one reflector panel (R22)
   bool early = true;           // factor parts release R_kk's block rows early (R24)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
@@ -578,7 +586,8 @@ struct tqr_plan {
 //    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
 struct Policy {
   int rwm = 128, passes = 1, nsl = 1, fine = 2, prio = PRIO_BLEVEL, orm_prio = PRIO_BLEVEL;
-  bool split = true, early = true, group = false;
+  bool split = true, early = true;
+  int group = 0;
   double lat = 4000.0, blq = 0.0;
 };
 static Policy make_policy(int64_t p, int64_t q, int b, int s) {
@@ -595,7 +604,7 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s) {
   if (const char* e = getenv("TQR_DEV_LAT")) P.lat = atof(e);
   if (const char* e = getenv("TQR_DEV_ORM_PRIO")) P.orm_prio = atoi(e);
   if (const char* e = getenv("TQR_DEV_BLQ")) P.blq = atof(e);
-  if (const char* e = getenv("TQR_DEV_GROUP")) P.group = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_GROUP")) P.group = atoi(e);
   if (const char* e = getenv("TQR_DEV_EARLY")) P.early = atoi(e) != 0;
   {
     const int w = exec_slice(b, s, P.rwm);  // one register pass
