@@ -1360,6 +1360,13 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
     const bool lkind = kind == 2 || kind == 4 || kind == 6;
     q[2] = (kind == 0 || lkind) ? q[1] : i;
     q[3] = (kind == 0 || kind == 1) ? q[1] : j;
+    if (kind == 1) {  // TSQRT: distinct tiles (i, k), i > k, as long as there are enough of them
+      const int64_t np_ = std::max<int64_t>(1, (int64_t)P->K * P->p - P->K * (P->K + 1) / 2);
+      int64_t x = (fpart ? t / (P->prm.b / P->prm.s) : t) % np_;
+      int kk = 0;
+      while (x >= P->p - kk - 1) { x -= P->p - kk - 1; ++kk; }
+      q[1] = kk; q[2] = kk + 1 + (int)x; q[3] = kk;
+    }
     // -1: a panel task over the whole tile; update tasks: first register pass, P->passes passes
     q[4] = (kind == 0 || kind == 1) ? (fpart ? (int)(t % (P->prm.b / P->prm.s)) : -1)
                                     : (int)(t % (P->nsl / P->passes)) * P->passes;
