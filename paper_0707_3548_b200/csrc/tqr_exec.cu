@@ -16,6 +16,13 @@
 
 namespace tqr {
 
+// End-of-task publication: __syncthreads, then thread 0 releases the task's counter(s)
+// (st.release.gpu: cumulative over the CTA's stores ordered before it by the barrier).
+// TQR_RELEASE_FENCE=1 adds an explicit fence.sc.gpu before the release (experiment knob).
+#ifndef TQR_RELEASE_FENCE
+#define TQR_RELEASE_FENCE 1
+#endif
+
 #ifndef TQR_POLL_NS
 #define TQR_POLL_NS 200  // back-off between polls of an unresolved dependency counter
 #endif
@@ -112,10 +119,41 @@ __device__ __forceinline__ void issue_panel(double* sm, const double* Yp, const 
 // __syncthreads inside the block loop and every refill overlaps a whole block of math.
 // C1 is fetched one block ahead by the group's rpart-0 warp (cp.async).
 // `pf(li, nb)` is called by thread 0 once per block (cross-task prefetch hook).
+// Pipelined panel dependency (R31): `pp` (not null) points at the panel progress
+// counters PF(k, 0..) of the reflectors being applied; internal block l may only be staged
+// once PF(k, l / SPO) >= pp_val (SPO internal blocks per output T block); blocks < pp_ready
+// are known to be ready.  The thread that stages a block waits for it (acquire + proxy fence);
+// block 1, if not ready at phase start, is staged by the last reader of block 0.
+struct PanelDep {
+  const int* ctr = nullptr;  // PF(k, 0) on this rank (nullptr: every block ready)
+  int val = 0;
+  int ready = 1 << 30;       // internal blocks known ready
+  int spo = 1;               // internal blocks per output block
+  bool sys = false;          // a peer GPU publishes the counter
+};
+__device__ __forceinline__ bool panel_block_ready(const PanelDep& pd, int l) {
+  if (l < pd.ready) return true;
+  const int* c = pd.ctr + l / pd.spo;
+  return (pd.sys ? ld_acquire_sys(c) : ld_acquire(c)) >= pd.val;
+}
+__device__ __forceinline__ void panel_block_wait(const PanelDep& pd, int l) {
+  if (l < pd.ready) return;
+  const int* c = pd.ctr + l / pd.spo;
+  if ((pd.sys ? ld_acquire_sys(c) : ld_acquire(c)) < pd.val) {
+    const unsigned long long t0w = globaltimer();
+    while ((pd.sys ? ld_acquire_sys(c) : ld_acquire(c)) < pd.val) {
+      __nanosleep(TQR_POLL_NS);
+      if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
+    }
+  }
+  fence_proxy_async();  // the producer's generic stores -> our TMA reads
+}
+
 template <int B, int S, int RWM, bool QT, bool DESC, class PF>
 __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S, RWM>::RW / 8][2], const double* Yp,
                                              const double* Tp, int lb0, int nbe, double* C1, const double* Ct,
-                                             int col0, int gact, PF&& pf, bool keep = false) {
+                                             int col0, int gact, PF&& pf, bool keep = false,
+                                             const PanelDep& pd = PanelDep()) {
   // blocks lb0 .. nbe-1 (DESC: nbe-1 .. 0, lb0 must be 0)
   const int nb = nbe - lb0;
   using C = Cfg<B, S, RWM>;
@@ -126,7 +164,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
   const bool active = gi < gact;
   const bool top_owner = C1 != nullptr && active && rpart == 0;
   unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
-  int* done = reinterpret_cast<int*>(full + 2);
+  int* done = reinterpret_cast<int*>(full + 2);  // done[0], done[1]; done[2]: block 1 deferred
   double* c1s0 = sm + L::C1S + gi * C::C1W;           // C1 buffer for even li
   double* c1s1 = sm + L::C1S + L::C1SZ + gi * C::C1W;  // C1 buffer for odd li
   if (nb > 0 && threadIdx.x == 0) {  // staging first: nothing outstanding to wait for
@@ -134,10 +172,18 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
     mbar_init(full + 1, 1);
     done[0] = 0;
     done[1] = 0;
+    done[2] = 0;
     fence_mbar_init();
     fence_proxy_async();
-    issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);
-    if (nb > 1) issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
+    issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);  // (block 0: waited by the task)
+    if (nb > 1) {
+      if (DESC || panel_block_ready(pd, lb0 + 1)) {
+        fence_proxy_async();
+        issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
+      } else {
+        done[2] = 1;  // staged by the last reader of block 0
+      }
+    }
   }
   if (active) {
     load_cols<B, C::RW>(acc, Ct, cg0, t0, keep);
@@ -169,10 +215,18 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
                                                 buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
                                                 sm + L::XBUF + (li & 1) * (C::NWARP * C::XW) + gi * C::RS * C::XW);
     __syncwarp();
-    if (lane == 0 && li + 2 < nb) {
+    if (lane == 0 && (li + 2 < nb || (li == 0 && nb > 1))) {
       if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
         done[buf] = 0;
-        issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? l - 2 : l + 2, buf);
+        if (li == 0 && done[2]) {  // deferred block 1 (pipelined panel dependency)
+          done[2] = 0;
+          panel_block_wait(pd, l + 1);
+          issue_panel<B, S, RWM>(sm, Yp, Tp, l + 1, 1);
+        }
+        if (li + 2 < nb) {
+          if (!DESC) panel_block_wait(pd, l + 2);
+          issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? l - 2 : l + 2, buf);
+        }
       }
     }
   }
@@ -403,7 +457,11 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
 #pragma unroll
       for (int d = 0; d < TASK_NDEP; ++d) {
         const int code = s_task[8 + 2 * d], val = a.base + s_task[9 + 2 * d];
-        const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+        // pipelined panel dependency (record [14] bit 6, R31): dependency 0 names the
+        // LAST block's counter PF(k, NPT-1); the task starts on block 0's, PF(k, 0), and waits
+        // for each later block just before staging it (update_phase)
+        const int pipe = (d == 0 && (s_task[14] & 64)) ? B / SO - 1 : 0;
+        const int cnt = (int)((unsigned)code >> 24), idx = (code & 0xFFFFFF) - pipe;
         // system scope only for a counter a peer GPU publishes (record [14] bit 3 + d); the
         // rank-local chains (column counters, apply / early-release parts) stay at gpu scope
         const bool sysd = a.sys && ((s_task[14] >> (3 + d)) & 1);
@@ -512,10 +570,19 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
             prefetch_task<B, S, SO, RWM, MODE>(s_next, R, Yme, p);
           }
         };
-        // L2 policy of the target (R28): C1 row tiles (LARFB targets) and panel tiles are
-        // re-read soon (evict_last); SSRFB C2 slices stream (evict_first)
+        // L2 policy of the target (section 5): C1 row tiles (LARFB targets) and panel tiles are
+        // re-read soon (evict_last); SSRFB C2 slices stream (evict_first) -- TQR_L2HINT builds
         const bool keep = panel || lkind;
-        update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf, keep);
+        PanelDep pd;
+        if (MODE == 0 && !panel && (s_task[14] & 64) && sub == sub0) {
+          pd.ctr = R.ctr + (s_task[8] & 0xFFFFFF) - (B / SO - 1);
+          pd.val = a.base + s_task[9];
+          pd.spo = SO / S;
+          pd.sys = a.sys && (s_task[14] & 8);
+          pd.ready = pd.spo;  // output block 0: waited for above
+          if (panel_block_ready(pd, NL - 1)) pd.ready = NL;  // the whole panel is already done
+        }
+        update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf, keep, pd);
         if (panel) PH_MARK(7); else PH_MARK(4);
         if (a_part) {
           if (warp / Cfg<B, S, RWM>::RS < gact)
@@ -543,7 +610,9 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
     __syncthreads();
     PH_MARK(2);
     if (tid == 0) {
+#if TQR_RELEASE_FENCE
       __threadfence();
+#endif
       fence_proxy_async();
       const int oidx = s_task[5], oval = a.base + s_task[6];
       if ((s_task[14] >> 8) != 0 && s_task[6] > 1) {

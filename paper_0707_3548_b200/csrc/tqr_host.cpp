@@ -349,7 +349,7 @@ struct DurModel {
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
                                int rwm = 128, double blq = 0.0, int group = 0, int np = 1, int fine = 0,
-                               bool early = false, double lat_remote = 0.0) {
+                               bool early = false, double lat_remote = 0.0, bool pipe = false) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -420,6 +420,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + k;
         T.dep(id, PF(k, NPT - 1), 1, 1);
         if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
+        if (pipe) T.t[id].flags |= 64;             // pipelined panel dependency (R31)
         if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, 2);
         out.counts[2] += n_;  // counted per register pass (column slice)
       }
@@ -439,6 +440,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
           if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + i;
           T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
           if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
+          if (pipe) T.t[id].flags |= 64;             // pipelined panel dependency (R31)
           T.dep(id, COL(k, j, sl), n_, i - k);
           if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, i - k + 2);
           out.counts[3] += n_;
@@ -546,6 +548,7 @@ struct tqr_plan {
   double blq = 0.0;            // bottom-level quantum (ns) of the factorization schedule
   int group = 0;               // group the updates of one reflector panel (R22)
   bool early = true;           // factor parts release R_kk's block rows early (R24)
+  bool pipe = true;            // update tasks wait for the panel block by block (R31)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -586,7 +589,7 @@ struct tqr_plan {
 //    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
 struct Policy {
   int rwm = 128, passes = 1, nsl = 1, fine = 2, prio = PRIO_BLEVEL, orm_prio = PRIO_BLEVEL;
-  bool split = true, early = true;
+  bool split = true, early = true, pipe = true;
   int group = 0;
   double lat = 4000.0, blq = 0.0;
 };
@@ -606,6 +609,7 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s) {
   if (const char* e = getenv("TQR_DEV_BLQ")) P.blq = atof(e);
   if (const char* e = getenv("TQR_DEV_GROUP")) P.group = atoi(e);
   if (const char* e = getenv("TQR_DEV_EARLY")) P.early = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_PIPE")) P.pipe = atoi(e) != 0;
   {
     const int w = exec_slice(b, s, P.rwm);  // one register pass
     P.nsl = (int)((b + w - 1) / w);
@@ -815,6 +819,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     P->rwm = pol.rwm; P->passes = pol.passes; P->nsl = pol.nsl; P->fine = pol.fine; P->split = pol.split;
     P->early = pol.early; P->group = pol.group; P->prio = pol.prio; P->orm_prio = pol.orm_prio; P->lat = pol.lat;
     P->blq = pol.blq;
+    P->pipe = pol.pipe;
   }
   P->st = (cudaStream_t)p->stream;
   P->workers = exec_max_ctas(p->b, p->s, P->rwm, p->device);
@@ -834,7 +839,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
   build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine,
-                     P->early);
+                     P->early, 0.0, P->pipe);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -1217,7 +1222,7 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   // inspected shapes
   build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1,
                      (p + q) % 2 == 0, s, p % 2 == 0 ? PRIO_BLEVEL : PRIO_CLASS, 4000.0, 128, 0.0, false,
-                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3), (p + 2 * q) % 3 != 0);
+                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3), (p + 2 * q) % 3 != 0, 0.0, (p + q) % 3 != 1);
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
@@ -1263,7 +1268,7 @@ tqr_status tqr_schedule_model(int64_t m, int64_t n, int32_t b, int32_t s, int32_
   const Policy pol = make_policy(p, q, b, s);
   Sched sc;
   build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
-                     pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, remote_ns);
+                     pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, remote_ns, pol.pipe);
   if (!sc.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;

@@ -27,7 +27,9 @@ enum Kind : int {
 //       wait until ctr[index + x] >= base + value for x in [0, count); count 0 = none
 //   [14] flags: bit 0 = publish the out counter on every rank (panel progress, multi-GPU),
 //        bit 1 / bit 2 = panel apply / factor part, bits 3..5 = dependency 0..2 is a counter a
-//        peer GPU publishes (system-scope acquire on a real multi-GPU job; gpu scope otherwise);
+//        peer GPU publishes (system-scope acquire on a real multi-GPU job; gpu scope otherwise),
+//        bit 6 = pipelined panel dependency (update tasks: dependency 0 names PF(k, last block);
+//        the task starts on PF(k, 0) and waits for block l just before staging it);
 //        bits 8..31 = 1 + an early-release
 //        counter that a panel factor part sets to [6] once R_kk's rows of its block are final
 //   [15] update tasks: np | ocnt << 8 -- register passes [slice, slice + np) (slice = [4], in

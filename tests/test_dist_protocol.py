@@ -116,7 +116,7 @@ def test_partition_and_replay(L, p, q, nsl, G, workers):
                 assert _global_j(rec, G, r) % G == r and not rec[14] & 1  # update on owner(j), local
                 # dep 0 (the panel counter PF(k, last)) is acquired at system scope exactly when
                 # a peer GPU publishes it; every other dependency is rank-local (gpu scope)
-                assert bool(rec[14] & 8) == (k % G != r) and not rec[14] & 0x30
+                assert bool(rec[14] & 8) == (k % G != r) and not rec[14] & 0x30 and not rec[14] & 0x80
                 assert _deps(rec)[0][0] == k * 3 * NPT + NPT - 1
             keys.extend(_task_keys(rec, G, r))
         sims.append(RankSim(recs, nctr, workers))
@@ -171,8 +171,12 @@ class PhasedSim:
         assert val == self.ctr[r][idx] + 1, f"rank {r} counter {idx} jumps {self.ctr[r][idx]} -> {val}"
         self.ctr[r][idx] = val
 
-    def _ready(self, r, rec):
-        for idx, cnt, val in _deps(rec):
+    def _ready(self, r, rec, start=True):
+        """start: a pipelined update task (record [14] bit 6, R31) starts on block 0's
+        panel counter PF(k, 0) and can only FINISH once the last block's, PF(k, NPT-1), holds."""
+        for d, (idx, cnt, val) in enumerate(_deps(rec)):
+            if d == 0 and start and int(rec[14]) & 64:
+                idx -= NPT - 1
             if not np.all(self.ctr[r][idx:idx + cnt] >= val):
                 return False
         return True
@@ -189,9 +193,9 @@ class PhasedSim:
                 if pr >= 0 and ph == 0:
                     ev.append((1, r, "mid", t))
                 else:
-                    can_end = True
+                    can_end = self._ready(r, rec, start=False)  # pipelined: every panel block in
                     if self.ordered and pr >= 0 and int(rec[6]) > 1:
-                        can_end = self.ctr[r][int(rec[5])] >= int(rec[6]) - 1
+                        can_end = can_end and self.ctr[r][int(rec[5])] >= int(rec[6]) - 1
                     if can_end:   # early-released factor parts end last (adversarial)
                         ev.append((2 if pr >= 0 else 1, r, "end", t))
         return ev
@@ -231,7 +235,8 @@ class PhasedSim:
         raise AssertionError("replay did not finish")
 
 
-_PHASED = [(8, 7, 1, 1, 4), (12, 7, 2, 1, 8), (30, 4, 2, 1, 16), (14, 6, 2, 1, 6), (10, 9, 2, 3, 3), (24, 4, 1, 4, 6)]
+_PHASED = [(8, 7, 1, 1, 4), (12, 7, 2, 1, 8), (30, 4, 2, 1, 16), (14, 6, 2, 1, 6), (10, 9, 2, 3, 3), (24, 4, 1, 4, 6),
+           (10, 8, 2, 3, 3), (20, 7, 1, 2, 5)]
 
 
 @pytest.mark.parametrize("p,q,nsl,G,workers", _PHASED)
@@ -242,6 +247,7 @@ def test_phased_adversarial_replay(L, p, q, nsl, G, workers):
     per_rank = [L.schedule_records(p, q, nsl, workers, G, r) for r in range(G)]
     if not any((int(rec[14]) >> 8) for recs, _ in per_rank for rec in recs):
         pytest.skip("schedule without early release")
+    pipelined = sum(1 for recs, _ in per_rank for rec in recs if int(rec[14]) & 64)
     for seed in range(3):
         sim = PhasedSim(per_rank, G, workers, ordered=True, seed=seed)
         sim.run()

@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel(const double* src, double*
     if (V == 1) panel_factor<B, S, NW, LDP>(P, 0, Rb, tau, TS, pmb, rep & 1);
     else if (V == 2) panel_factor2<B, S, NW, LDP>(P, 0, Rb, tau, scl, TS, pmb, rep & 1);
     else if (V == 4) panel_factor4<B, S, NW, LDP>(P, 0, Rb, tau, TS, pmb, rep & 1);
+    else if (V == 5) panel_factor5<B, S, NW, LDP>(P, 0, Rb, tau, TS, pmb, rep & 1);
     else panel_factor3<B, S, NW, LDP>(P, 0, Rb, tau, tgs, TS);
     long long t1 = clock64();
     tot += t1 - t0;
@@ -71,7 +72,7 @@ __global__ void __launch_bounds__(NW * 32, 1) k_panel(const double* src, double*
   for (int e = threadIdx.x; e < S; e += blockDim.x) outT[e] = tau[e];
 }
 
-template <int B, int S, bool TS, int VB = 4>
+template <int B, int S, bool TS, int VB = 5>
 static void compare(const double* src, double* d, long long* dl) {
   constexpr int NW = 8;
   const size_t smem = ((B + 4) * S + S * S + 2 * S + 64) * 8 + 2 * S * 8 + 64;

@@ -737,4 +737,214 @@ __device__ __forceinline__ void panel_factor3(double* P, int c0, double* Rb, dou
   }
 }
 
+// panel_factor5: panel_factor with BLOCKED column ownership (warp w owns columns
+// [w NC, w NC + NC)): the critical chain stays inside one warp for NC consecutive columns.
+template <int B, int S, int NW, int LDP>
+__device__ __forceinline__ void panel_factor5(double* P, int c0, double* Rb, double* tau, const bool TS,
+                                             unsigned long long* pmb, unsigned parity) {
+  static_assert(S <= 64, "top block rows: two per lane at most");
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NR = (B + 31) / 32;       // x-part rows per lane: row r = lane + 32 q
+  constexpr int NC = (S + NW - 1) / NW;   // columns per warp: column c = warp NC + ci
+  constexpr int NTR = (S + 31) / 32;      // top-block rows per lane: block row L = lane + 32 h
+  // Column c of the panel = [top block (S rows); x part].  TSQRT: top = R_kk's diagonal block
+  // (Rb, upper triangle), x = the B rows of A(i,k); the reflector is [e_j; v_j].  GEQRT: top =
+  // tile rows [c0, c0+S), x = tile rows [c0+S, B); the reflector is [0; 1; v_j] with v_j's
+  // leading part inside the top block.  Every warp keeps its columns in registers (x and
+  // top), so no register row index is ever dynamic (row jj of the top block is a shuffle
+  // from lane jj) and no column step touches shared memory except v_j.
+  const int lox = TS ? 0 : c0 + S;  // first x-part row
+  double x[NC][NR], tr[NC][NTR];
+#pragma unroll
+  for (int ci = 0; ci < NC; ++ci) {
+    const int c = warp * NC + ci;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q;
+      x[ci][q] = (c < S && r >= lox && r < B) ? P[r + c * LDP] : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < NTR; ++h) {
+      const int L = lane + 32 * h;
+      tr[ci][h] = (c < S && L < S && (!TS || L <= c)) ? (TS ? Rb[L + c * S] : P[c0 + L + c * LDP]) : 0.0;
+    }
+  }
+  // block row L of column CI, broadcast to the warp
+  auto getT = [&](auto CI, int L) __attribute__((always_inline)) -> double {
+    constexpr int ci = decltype(CI)::value;
+    const double t = (NTR == 1 || L < 32) ? tr[ci][0] : tr[ci][NTR - 1];
+    return __shfl_sync(0xffffffffu, t, L & 31);
+  };
+  auto subT = [&](auto CI, int L, double w) __attribute__((always_inline)) {
+    constexpr int ci = decltype(CI)::value;
+    if (lane == (L & 31)) {
+      if (NTR == 1 || L < 32) tr[ci][0] -= w; else tr[ci][NTR - 1] -= w;
+    }
+  };
+
+  // Householder generation (R2-R4, R17, R20) for column jj (in CI) from alpha and
+  // sigma = ||x||^2 over its rows below the pivot; stores v into P, beta, tau; publishes.
+  auto house_pub = [&](auto CI, int jj, double alpha, double sigma) __attribute__((always_inline)) {
+    constexpr int ci = decltype(CI)::value;
+    double beta, tv, scale;
+    if (sigma == 0.0) {
+      beta = alpha; tv = 0.0; scale = 0.0;
+    } else {
+      const double nn = alpha * alpha + sigma;
+      const double rn = rsqrt(nn);                // 1/nu
+      const double nu = nn * rn;
+      beta = (alpha >= 0.0) ? -nu : nu;
+      tv = 1.0 + fabs(alpha) * rn;                 // (beta - alpha)/beta = 1 + |alpha|/nu
+      scale = __drcp_rn(alpha - beta);             // correctly rounded, == 1.0 / (alpha - beta)
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q;
+      if (r >= lox && r < B) P[r + jj * LDP] = x[ci][q] * scale;
+    }
+    if (!TS) {
+#pragma unroll
+      for (int h = 0; h < NTR; ++h) {
+        const int L = lane + 32 * h;
+        if (L > jj && L < S) P[c0 + L + jj * LDP] = tr[ci][h] * scale;
+      }
+    }
+    if (lane == 0) {
+      if (TS) Rb[jj + jj * S] = beta; else P[c0 + jj + jj * LDP] = beta;
+      tau[jj] = tv;
+    }
+    __syncwarp();                          // the warp's stores of v_jj, tau_jj, beta_jj ...
+    if (lane == 0) mbar_arrive(pmb + jj);  // ... published (release); the owner does not wait
+  };
+  // ||column CI below block row j||^2: x part, plus (GEQRT) top-block rows L > j
+  auto norm_below = [&](auto CI, int j) __attribute__((always_inline)) -> double {
+    constexpr int ci = decltype(CI)::value;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      if (q & 1) s1 += x[ci][q] * x[ci][q]; else s0 += x[ci][q] * x[ci][q];
+    }
+    if (!TS) {
+#pragma unroll
+      for (int h = 0; h < NTR; ++h) {
+        const int L = lane + 32 * h;
+        if (L > j && L < S) s0 += tr[ci][h] * tr[ci][h];
+      }
+    }
+    return warp_sum(s0 + s1);
+  };
+
+  if (warp == 0) {
+    const std::integral_constant<int, 0> C0;
+    const double sg = norm_below(C0, 0);
+    house_pub(C0, 0, getT(C0, 0), sg);
+  }
+  for (int jj = 0; jj + 1 < S; ++jj) {
+    if (warp != jj / NC) mbar_wait(pmb + jj, parity);  // v_jj published (acquire)
+    const double tj = tau[jj];
+    double vr[NR], vt[NTR];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int r = lane + 32 * q;
+      vr[q] = (r >= lox && r < B) ? P[r + jj * LDP] : 0.0;
+    }
+#pragma unroll
+    for (int h = 0; h < NTR; ++h) {  // v_jj inside the top block (GEQRT only; TSQRT: e_jj)
+      const int L = lane + 32 * h;
+      vt[h] = (!TS && L > jj && L < S) ? P[c0 + L + jj * LDP] : 0.0;
+    }
+    const int nxt = jj + 1;
+    if (nxt / NC == warp) {
+      // Critical path: update column jj+1 and generate reflector jj+1.  One interleaved
+      // reduction of (x.v, x.x, v.v) over the rows below the pivot jj gives the dot product
+      // AND the new norm by downdating, sigma' = x.x - 2 tw x.v + tw^2 v.v [- alpha'^2 for
+      // GEQRT, whose alpha' is one of those rows]; if it may have cancelled (below 5% of the
+      // magnitude of its terms) it is recomputed from the updated column (R20).
+      static_for<NC>([&](auto CI) __attribute__((always_inline)) {
+        constexpr int ci = decltype(CI)::value;
+        if (warp * NC + ci != nxt) return;
+        double a0 = 0.0, a1 = 0.0, b0 = 0.0, b1 = 0.0, e0 = 0.0, e1 = 0.0;
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          if (q & 1) { a1 += vr[q] * x[ci][q]; b1 += x[ci][q] * x[ci][q]; e1 += vr[q] * vr[q]; }
+          else { a0 += vr[q] * x[ci][q]; b0 += x[ci][q] * x[ci][q]; e0 += vr[q] * vr[q]; }
+        }
+        if (!TS) {
+#pragma unroll
+          for (int h = 0; h < NTR; ++h) {
+            const int L = lane + 32 * h;
+            const double tv_ = (L > jj && L < S) ? tr[ci][h] : 0.0;
+            a0 += vt[h] * tv_; b0 += tv_ * tv_; e0 += vt[h] * vt[h];
+          }
+        }
+        double sxv = a0 + a1, sxx = b0 + b1, svv = e0 + e1;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          sxv += __shfl_xor_sync(0xffffffffu, sxv, o);
+          sxx += __shfl_xor_sync(0xffffffffu, sxx, o);
+          svv += __shfl_xor_sync(0xffffffffu, svv, o);
+        }
+        const double tw = tj * (getT(CI, jj) + sxv);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];
+#pragma unroll
+        for (int h = 0; h < NTR; ++h) tr[ci][h] -= tw * vt[h];
+        subT(CI, jj, tw);
+        const double alpha = getT(CI, nxt);
+        const double a2 = TS ? 0.0 : alpha * alpha;
+        double sigma = sxx - 2.0 * tw * sxv + tw * tw * svv - a2;
+        const double mag = sxx + 2.0 * fabs(tw * sxv) + tw * tw * svv + a2;
+        if (!(sigma >= 0.05 * mag)) sigma = norm_below(CI, nxt);  // possible cancellation / NaN
+        house_pub(CI, nxt, alpha, sigma);
+      });
+    }
+    // the warp's other columns c > jj+1: dots, one interleaved butterfly, register updates
+#ifdef TQR_PF_SKIP_NONCRIT  // tools/panel_bench.cu timing experiment only (wrong results)
+    continue;
+#endif
+    double dc[NC];
+#pragma unroll
+    for (int ci = 0; ci < NC; ++ci) {
+      const int c = warp * NC + ci;
+      double d0 = 0.0, d1 = 0.0;
+      if (c > nxt && c < S) {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          if (q & 1) d1 += vr[q] * x[ci][q]; else d0 += vr[q] * x[ci][q];
+        }
+#pragma unroll
+        for (int h = 0; h < NTR; ++h) d0 += vt[h] * tr[ci][h];
+      }
+      dc[ci] = d0 + d1;
+    }
+    warp_allreduce<NC>(dc);
+    static_for<NC>([&](auto CI) __attribute__((always_inline)) {
+      constexpr int ci = decltype(CI)::value;
+      const int c = warp * NC + ci;
+      if (c > nxt && c < S) {
+        const double tw = tj * (getT(CI, jj) + dc[ci]);
+#pragma unroll
+        for (int q = 0; q < NR; ++q) x[ci][q] -= tw * vr[q];
+#pragma unroll
+        for (int h = 0; h < NTR; ++h) tr[ci][h] -= tw * vt[h];
+        subT(CI, jj, tw);
+      }
+    });
+  }
+  // R entries above the diagonal of the top block back to shared memory (the diagonal (beta)
+  // and V were stored by house_pub)
+#pragma unroll
+  for (int ci = 0; ci < NC; ++ci) {
+    const int c = warp * NC + ci;
+#pragma unroll
+    for (int h = 0; h < NTR; ++h) {
+      const int L = lane + 32 * h;
+      if (c < S && L < c) {
+        if (TS) Rb[L + c * S] = tr[ci][h]; else P[c0 + L + c * LDP] = tr[ci][h];
+      }
+    }
+  }
+  __syncthreads();
+}
+
 }  // namespace tqr
