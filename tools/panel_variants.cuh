@@ -6,7 +6,10 @@
 //                  is bound by its critical chain, not by control overhead;
 //   panel_factor2  early publication of the unscaled column (Householder scalars off the
 //                  chain): chain alone 709 vs 894 clk, but 1372 clk with the off-path work;
-//   panel_factor3  one warp per 8-column sub-panel + block updates: 1613 clk per column.
+//   panel_factor3  one warp per 8-column sub-panel + block updates: 1613 clk per column;
+//   panel_factor5  blocked column ownership (warp w owns columns [4w, 4w+4): the chain stays in
+//                  one warp for four columns): 1680 clk per column (the off-path work of the
+//                  late columns concentrates on fewer warps).
 #pragma once
 #include "../paper_0707_3548_b200/csrc/tqr_device.cuh"
 
