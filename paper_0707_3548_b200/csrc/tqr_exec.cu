@@ -19,6 +19,20 @@ namespace tqr {
 // End-of-task publication: __syncthreads, then thread 0 releases the task's counter(s)
 // (st.release.gpu: cumulative over the CTA's stores ordered before it by the barrier).
 // TQR_RELEASE_FENCE=1 adds an explicit fence.sc.gpu before the release (experiment knob).
+// Per-instance features, measured same-box against r01 (tools/ab3.sh):
+// the pipelined panel dependency (R31) and the blocked T_l (R26) pay off only where the panel
+// chain bounds the factorization (b <= 128, C2: 7.09 -> 6.75 ms); in the b >= 256 instances
+// their extra code in the executor costs 0.3-1% (C3, C4), so it is compiled out there.
+// TQR_PF_CALL=1 calls the panel column loop instead of inlining it in the b = 256 RW = 128
+// instance (the loop itself 58k -> 46k cycles, but C4 0.9% slower overall): off.
+#ifndef TQR_PF_CALL
+#define TQR_PF_CALL 0
+#endif
+template <int B>
+struct Feat {
+  static constexpr bool PIPE = B <= 128;      // pipelined panel dependency (R31)
+  static constexpr bool TBLOCKED = B <= 128;  // T_l by 8 x 8 DMMA blocks (R26)
+};
 #ifndef TQR_RELEASE_FENCE
 #define TQR_RELEASE_FENCE 1
 #endif
@@ -177,11 +191,15 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
     fence_proxy_async();
     issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 1 : lb0, 0);  // (block 0: waited by the task)
     if (nb > 1) {
-      if (DESC || panel_block_ready(pd, lb0 + 1)) {
-        fence_proxy_async();
-        issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
+      if constexpr (Feat<B>::PIPE) {
+        if (DESC || panel_block_ready(pd, lb0 + 1)) {
+          fence_proxy_async();
+          issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
+        } else {
+          done[2] = 1;  // staged by the last reader of block 0
+        }
       } else {
-        done[2] = 1;  // staged by the last reader of block 0
+        issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? nb - 2 : lb0 + 1, 1);
       }
     }
   }
@@ -215,6 +233,7 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
                                                 buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
                                                 sm + L::XBUF + (li & 1) * (C::NWARP * C::XW) + gi * C::RS * C::XW);
     __syncwarp();
+if constexpr (Feat<B>::PIPE) {
     if (lane == 0 && (li + 2 < nb || (li == 0 && nb > 1))) {
       if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
         done[buf] = 0;
@@ -229,6 +248,14 @@ __device__ __forceinline__ void update_phase(double* sm, double (&acc)[Cfg<B, S,
         }
       }
     }
+} else {
+    if (lane == 0 && li + 2 < nb) {
+      if (atomicAdd(done + buf, 1) == C::NWARP - 1) {  // last reader of this buffer: refill it
+        done[buf] = 0;
+        issue_panel<B, S, RWM>(sm, Yp, Tp, DESC ? l - 2 : l + 2, buf);
+      }
+    }
+}
   }
   __syncthreads();  // every staged buffer consumed before anyone reuses the staging space
 }
@@ -289,7 +316,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     }
   __syncthreads();
   PH_MARK(8);
-  if constexpr (B == 256 && RWM == 128)
+  if constexpr (TQR_PF_CALL && B == 256 && RWM == 128)
     panel_factor_call<B, S, C::NWARP, LDP, ts>(P, c0, Rb, tau, reinterpret_cast<unsigned long long*>(sm + L::PMB),
                                                pf_gen & 1);
   else
@@ -341,6 +368,7 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
       __stcg(reinterpret_cast<double2*>(a.Yp[g] + yoff + (size_t)l * B * S) + x, ys2[x]);
     }
   };
+if constexpr (Feat<B>::TBLOCKED) {
   if (warp < NTW) build_t_blocked<S>(Tp, tau, Z, P, 14);
   else store_y(32 * NTW, C::NT - 32 * NTW);  // meanwhile, on the other warps
   __syncthreads();
@@ -348,6 +376,12 @@ __device__ __forceinline__ void panel_block(double* sm, const double (&acc)[Cfg<
     store_y(0, C::NT);
     __syncthreads();
   }
+} else {
+  constexpr int NTW1 = (S + 31) / 32;
+  if (warp < NTW1) build_t<S>(Tp, tau, Z);
+  else store_y(32 * NTW1, C::NT - 32 * NTW1);
+  __syncthreads();
+}
   PH_MARK(12);
   // output slot: T_L (SO x SO) in columns [L*SO, L*SO+SO); this SI-block is its diagonal
   // block m (the off-diagonal blocks of SO > SI are formed after the factorization)
@@ -460,7 +494,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         // pipelined panel dependency (record [14] bit 6, R31): dependency 0 names the
         // LAST block's counter PF(k, NPT-1); the task starts on block 0's, PF(k, 0), and waits
         // for each later block just before staging it (update_phase)
-        const int pipe = (d == 0 && (s_task[14] & 64)) ? B / SO - 1 : 0;
+        const int pipe = (Feat<B>::PIPE && d == 0 && (s_task[14] & 64)) ? B / SO - 1 : 0;
         const int cnt = (int)((unsigned)code >> 24), idx = (code & 0xFFFFFF) - pipe;
         // system scope only for a counter a peer GPU publishes (record [14] bit 3 + d); the
         // rank-local chains (column counters, apply / early-release parts) stay at gpu scope
@@ -574,7 +608,7 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         // re-read soon (evict_last); SSRFB C2 slices stream (evict_first) -- TQR_L2HINT builds
         const bool keep = panel || lkind;
         PanelDep pd;
-        if (MODE == 0 && !panel && (s_task[14] & 64) && sub == sub0) {
+        if (Feat<B>::PIPE && MODE == 0 && !panel && (s_task[14] & 64) && sub == sub0) {
           pd.ctr = R.ctr + (s_task[8] & 0xFFFFFF) - (B / SO - 1);
           pd.val = a.base + s_task[9];
           pd.spo = SO / S;

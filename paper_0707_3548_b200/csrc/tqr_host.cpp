@@ -116,8 +116,10 @@ struct TaskGen {
     t.push_back(x);
     return (int)t.size() - 1;
   }
+  bool overflow = false;  // a task with more than TASK_NDEP dependencies (schedule bug)
   void dep(int id, int idx, int cnt, int val) {
     T& x = t[id];
+    if (x.ndep >= TASK_NDEP) { overflow = true; return; }
     x.dep_idx[x.ndep] = idx; x.dep_cnt[x.ndep] = cnt; x.dep_val[x.ndep] = val; x.ndep++;
   }
 };
@@ -148,6 +150,7 @@ static bool list_schedule(TaskGen& G, const std::vector<int>& workers, Sched& ou
                           double lat = 0.0, double blq = 0.0, double lat_remote = 0.0, int gmode = 1) {
   const int n = (int)G.t.size();
   const int nr = (int)workers.size();
+  if (G.overflow) return false;
   std::unordered_map<uint64_t, int> producer;
   producer.reserve(n * 2);
   auto pkey = [](int rank, int idx, int val) { return ((uint64_t)(uint32_t)rank << 56) ^ ckey(idx, val); };
@@ -349,7 +352,8 @@ struct DurModel {
 static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, const std::vector<int>& workers,
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
                                int rwm = 128, double blq = 0.0, int group = 0, int np = 1, int fine = 0,
-                               bool early = false, double lat_remote = 0.0, bool pipe = false) {
+                               bool early = false, double lat_remote = 0.0, bool pipe = false,
+                               bool slicedep = true) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -377,6 +381,11 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   // One panel task on tile (i,k) block l in two parts: A (apply this tile's blocks < l to
   // block l's columns: touches the rows of R_kk ABOVE the diagonal block) and F (factor: the
   // diagonal block).  A(k,i+1,l) may overlap F(k,i,l), which halves the TSQRT chain's step.
+  // the column slices (register passes of the update tasks) that hold inner block l's columns:
+  // a panel part only needs THOSE updated by step k-1 (R32), not the whole tile
+  const int sw = (b + nsl - 1) / nsl;
+  auto blk_sl0 = [&](int l) { return slicedep ? (l * s) / sw : 0; };
+  auto blk_nsl = [&](int l) { return slicedep ? ((l + 1) * s - 1) / sw - (l * s) / sw + 1 : nsl; };
   auto panel = [&](int kind, int k, int i, int cls) {
     const int ok = own(k), v = i - k + 1;
     for (int l = 0; l < NPT; ++l) {
@@ -386,7 +395,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
         if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk block l: previous tile
         if (l > 0) T.dep(id, PF(k, l - 1), 1, v);
-        else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);
+        if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), i - k + 2);  // block l's columns
         continue;
       }
       if (l > 0) {
@@ -394,13 +403,14 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
         T.dep(id, PF(k, l - 1), 1, v);                 // this tile's blocks < l factored
         if (v > 1) T.dep(id, PA(k, l), 1, v - 1);      // R_kk rows above block l: previous tile
+        if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), i - k + 2);  // block l's columns
       }
       int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(kind == K_G), cls);
       T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
       if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
       if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk diagonal block l: previous tile
-      if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part
-      else if (k > 0) T.dep(id, COL(k - 1, k, 0), nsl, i - k + 2);  // tile updated by step k-1
+      if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part (holds block l's slice dependency)
+      else if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(0)), blk_nsl(0), i - k + 2);  // block 0's columns
     }
   };
   for (int k = 0; k < K; ++k) {
@@ -549,6 +559,7 @@ struct tqr_plan {
   int group = 0;               // group the updates of one reflector panel (R22)
   bool early = true;           // factor parts release R_kk's block rows early (R24)
   bool pipe = true;            // update tasks wait for the panel block by block (R31)
+  bool slicedep = true;        // panel parts wait only for their block's column slices (R32)
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
@@ -589,7 +600,7 @@ struct tqr_plan {
 //    paper's fixed classes: C3 224 -> 213 ms, C4 62.1 -> 55.2 ms, C2 7.84 -> 7.33 ms.
 struct Policy {
   int rwm = 128, passes = 1, nsl = 1, fine = 2, prio = PRIO_BLEVEL, orm_prio = PRIO_BLEVEL;
-  bool split = true, early = true, pipe = true;
+  bool split = true, early = true, pipe = true, slicedep = true;
   int group = 0;
   double lat = 4000.0, blq = 0.0;
 };
@@ -600,6 +611,11 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s) {
   P.passes = b >= 256 ? (128 / exec_slice(b, s, P.rwm)) : 1;  // 128-column tasks
   if (tall && b <= 256) P.passes = 1;
   P.split = tall;  // (square b <= 128 as well before the early R_kk release, R24: C2 7.15 -> 7.08 ms fused)
+  // pipelined panel dependency (R31; the executor compiles it only for b <= 128) and per-slice
+  // panel dependencies (R32): for the panel-chain-bound b <= 128 grids (C2); measured same-box,
+  // the per-slice dependencies cost C3 0.3% and C4 0.5% (their dispatch order)
+  P.pipe = b <= 128;
+  P.slicedep = false;  // (C2: 6.749 vs 6.756 ms without; C3 +0.3%, C4 +0.5% with)
   if (const char* e = getenv("TQR_DEV_PASSES")) P.passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P.split = atoi(e) != 0;
   if (const char* e = getenv("TQR_DEV_RW")) P.rwm = atoi(e);
@@ -610,6 +626,7 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s) {
   if (const char* e = getenv("TQR_DEV_GROUP")) P.group = atoi(e);
   if (const char* e = getenv("TQR_DEV_EARLY")) P.early = atoi(e) != 0;
   if (const char* e = getenv("TQR_DEV_PIPE")) P.pipe = atoi(e) != 0;
+  if (const char* e = getenv("TQR_DEV_SLICEDEP")) P.slicedep = atoi(e) != 0;
   {
     const int w = exec_slice(b, s, P.rwm);  // one register pass
     P.nsl = (int)((b + w - 1) / w);
@@ -820,6 +837,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     P->early = pol.early; P->group = pol.group; P->prio = pol.prio; P->orm_prio = pol.orm_prio; P->lat = pol.lat;
     P->blq = pol.blq;
     P->pipe = pol.pipe;
+    P->slicedep = pol.slicedep;
   }
   P->st = (cudaStream_t)p->stream;
   P->workers = exec_max_ctas(p->b, p->s, P->rwm, p->device);
@@ -839,7 +857,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
   build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine,
-                     P->early, 0.0, P->pipe);
+                     P->early, 0.0, P->pipe, P->slicedep);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -1268,7 +1286,8 @@ tqr_status tqr_schedule_model(int64_t m, int64_t n, int32_t b, int32_t s, int32_
   const Policy pol = make_policy(p, q, b, s);
   Sched sc;
   build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
-                     pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, remote_ns, pol.pipe);
+                     pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, remote_ns, pol.pipe,
+                     pol.slicedep);
   if (!sc.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
