@@ -54,6 +54,14 @@ def lib():
         L.oracle_flops_eq4.restype = _d
         L.oracle_dag_edges.argtypes = [_i64, _i64, ctypes.POINTER(_i64), _i64]
         L.oracle_dag_edges.restype = _i64
+        L.oracle_dag_edges_h.argtypes = [_i64, _i64, _i, ctypes.POINTER(_i64), _i64]
+        L.oracle_dag_edges_h.restype = _i64
+        L.oracle_tsqrt_rows.argtypes = [_i, _i, _i, _pd, _pd, _pd]
+        L.oracle_ssrfb_rows.argtypes = [_i, _i, _i, _pd, _pd, _pd, _pd, _i]
+        L.oracle_geqrf_tiles_h.argtypes = [_i64, _i64, _i, _i, _i, _pd, _pd, _i]
+        L.oracle_ormqr_tiles_h.argtypes = [_i64, _i64, _i, _i, _i, _pd, _pd, _i, _i64, _pd, _i]
+        L.oracle_flops_eq4_h.argtypes = [_i64, _i64, _d, _i]
+        L.oracle_flops_eq4_h.restype = _d
         L.oracle_last_task_counts.argtypes = [ctypes.POINTER(_i64)]
         L.oracle_last_task_counts.restype = None
         _lib = L
@@ -106,6 +114,21 @@ def larfb(V, T, C, trans=1):
     return C
 
 
+def tsqrt_rows(R, B, s):
+    """TSQRT of [R (b x b upper); B (rows x b)] (R30: rows = h b, the 2b x b tiles)."""
+    R = tile(R); B = np.asfortranarray(np.array(B, dtype=np.float64)); b = R.shape[0]
+    T = np.zeros((s, b), order="F")
+    _chk(lib().oracle_tsqrt_rows(b, s, B.shape[0], _p(R), _p(B), _p(T)), "tsqrt_rows")
+    return R, B, T
+
+
+def ssrfb_rows(V, T, C1, C2, trans=1):
+    V = np.asfortranarray(np.array(V, dtype=np.float64)); T = tile(T); C1 = tile(C1)
+    C2 = np.asfortranarray(np.array(C2, dtype=np.float64)); b = C1.shape[0]; s = T.shape[0]
+    _chk(lib().oracle_ssrfb_rows(b, s, V.shape[0], _p(V), _p(T), _p(C1), _p(C2), trans), "ssrfb_rows")
+    return C1, C2
+
+
 def ssrfb(V, T, C1, C2, trans=1):
     V = tile(V); T = tile(T); C1 = tile(C1); C2 = tile(C2); b = V.shape[0]; s = T.shape[0]
     _chk(lib().oracle_ssrfb(b, s, _p(V), _p(T), _p(C1), _p(C2), trans), "ssrfb")
@@ -130,13 +153,17 @@ def unpack(At, m, n, b):
     return A
 
 
-def geqrf(A, b, s, nthreads=1):
-    """Factor column-major A; returns (At tiles after factorization, T slots)."""
+def geqrf(A, b, s, nthreads=1, h=1):
+    """Factor column-major A; returns (At tiles after factorization, T slots).  h > 1: the tile
+    rows below the diagonal in units of h (the paper's 2b x b tiles for h = 2; R30)."""
     A = np.asfortranarray(A, dtype=np.float64); m, n = A.shape
     p, q = dims(m, n, b)
     At = pack(A, b)
     T = np.zeros(p * q * s * b)
-    _chk(lib().oracle_geqrf_tiles(m, n, b, s, _p(At), _p(T), nthreads), "geqrf")
+    if h == 1:
+        _chk(lib().oracle_geqrf_tiles(m, n, b, s, _p(At), _p(T), nthreads), "geqrf")
+    else:
+        _chk(lib().oracle_geqrf_tiles_h(m, n, b, s, h, _p(At), _p(T), nthreads), "geqrf_h")
     return At, T
 
 
@@ -151,27 +178,32 @@ def get_r(At, m, n, b):
     return R
 
 
-def ormqr(At, T, m, n, b, s, B, trans, nthreads=1):
+def ormqr(At, T, m, n, b, s, B, trans, nthreads=1, h=1):
     """Apply Q^T (trans=1) or Q (trans=0) to column-major m x nrhs B; returns new B."""
     B = np.asfortranarray(B, dtype=np.float64); nrhs = B.shape[1]
     Bt = pack(B, b)
-    _chk(lib().oracle_ormqr_tiles(m, n, b, s, _p(np.ascontiguousarray(At)), _p(np.ascontiguousarray(T)),
-                                  trans, nrhs, _p(Bt), nthreads), "ormqr")
+    if h == 1:
+        _chk(lib().oracle_ormqr_tiles(m, n, b, s, _p(np.ascontiguousarray(At)), _p(np.ascontiguousarray(T)),
+                                      trans, nrhs, _p(Bt), nthreads), "ormqr")
+    else:
+        _chk(lib().oracle_ormqr_tiles_h(m, n, b, s, h, _p(np.ascontiguousarray(At)), _p(np.ascontiguousarray(T)),
+                                        trans, nrhs, _p(Bt), nthreads), "ormqr_h")
     return unpack(Bt, m, nrhs, b)
 
 
-def orgqr(At, T, m, n, b, s, k=None, nthreads=1):
+def orgqr(At, T, m, n, b, s, k=None, nthreads=1, h=1):
     k = n if k is None else k
     E = np.zeros((m, k), order="F")
     E[np.arange(min(m, k)), np.arange(min(m, k))] = 1.0
-    return ormqr(At, T, m, n, b, s, E, 0, nthreads)
+    return ormqr(At, T, m, n, b, s, E, 0, nthreads, h)
 
 
-def dag_edges(p, q):
-    """Edges of the oracle's DAG: list of ((kind, k, i, j), (kind, k, i, j)), kind 'G','T','L','S'."""
-    n = lib().oracle_dag_edges(p, q, None, 0)
+def dag_edges(p, q, h=1):
+    """Edges of the oracle's DAG: list of ((kind, k, i, j), (kind, k, i, j)), kind 'G','T','L','S'
+    (T / S tasks of units of h tile rows report the unit's first tile row)."""
+    n = lib().oracle_dag_edges_h(p, q, h, None, 0)
     buf = np.zeros(max(1, 8 * n), dtype=np.int64)
-    lib().oracle_dag_edges(p, q, buf.ctypes.data_as(ctypes.POINTER(_i64)), n)
+    lib().oracle_dag_edges_h(p, q, h, buf.ctypes.data_as(ctypes.POINTER(_i64)), n)
     names = "GTLS"
     e = buf[: 8 * n].reshape(n, 8)
     return [((names[r[0]], int(r[1]), int(r[2]), int(r[3])), (names[r[4]], int(r[5]), int(r[6]), int(r[7])))
@@ -190,6 +222,10 @@ def flops_standard(m, n):
 
 def kernel_flops(kind, b):
     return lib().oracle_kernel_flops({"GEQT2": 0, "LARFB": 1, "TSQT2": 2, "SSRFB": 3}[kind], float(b))
+
+
+def flops_eq4_h(p, q, b, h):
+    return lib().oracle_flops_eq4_h(p, q, float(b), h)
 
 
 def flops_eq4(p, q, b):

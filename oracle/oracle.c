@@ -141,36 +141,39 @@ int oracle_geqrt(int b, int s, double* A, double* T) {
 
 /* ---------------------------------------------------------------------------
  * TSQRT / DTSQT2: QR of [R_kk; A_ik]; reflectors [I; V_ik].
+ * `rows` rows in the lower block B (ld = rows): rows = b is the paper's square tile,
+ * rows = h b its non-square 2b x b tiles (reading R30).
  * R = upper triangle (incl. diagonal) of the diagonal tile; the strict lower
  * part (V_kk) is never read or written.  SURVEY 8(c) c-4.
  * ------------------------------------------------------------------------- */
-int oracle_tsqrt(int b, int s, double* R, double* B, double* T) {
+int oracle_tsqrt_rows(int b, int s, int rows, double* R, double* B, double* T) {
   int rc = check_bs(b, s);
   if (rc) return rc;
+  if (rows < 1) return -3;
   double* z = (double*)malloc(sizeof(double) * s);
   double* W = (double*)malloc(sizeof(double) * s);
   double* W2 = (double*)malloc(sizeof(double) * s);
 #define Rk(r, c) R[(int64_t)(r) + (int64_t)(c) * b]
-#define Bk(r, c) B[(int64_t)(r) + (int64_t)(c) * b]
+#define Bk(r, c) B[(int64_t)(r) + (int64_t)(c) * rows]
   for (int l = 0; l < b / s; ++l) {
     int c0 = l * s;
     double* Tl = T + (int64_t)l * s * s;
     for (int64_t e = 0; e < (int64_t)s * s; ++e) Tl[e] = 0.0;
     for (int c = c0; c < c0 + s; ++c) {
       double beta, tau;
-      oracle_house(Rk(c, c), &Bk(0, c), b, &beta, &tau, &Bk(0, c));
+      oracle_house(Rk(c, c), &Bk(0, c), rows, &beta, &tau, &Bk(0, c));
       Rk(c, c) = beta;
       for (int cp = c + 1; cp < c0 + s; ++cp) {
         double w = Rk(c, cp);
-        for (int r = 0; r < b; ++r) w += Bk(r, c) * Bk(r, cp);
+        for (int r = 0; r < rows; ++r) w += Bk(r, c) * Bk(r, cp);
         Rk(c, cp) -= tau * w;
-        for (int r = 0; r < b; ++r) Bk(r, cp) -= tau * w * Bk(r, c);
+        for (int r = 0; r < rows; ++r) Bk(r, cp) -= tau * w * Bk(r, c);
       }
       int j = c - c0;
       for (int t = 0; t < j; ++t) {
         /* identity tops are orthogonal (e_{c0+t} . e_c = 0) */
         double acc = 0.0;
-        for (int r = 0; r < b; ++r) acc += Bk(r, c0 + t) * Bk(r, c);
+        for (int r = 0; r < rows; ++r) acc += Bk(r, c0 + t) * Bk(r, c);
         z[t] = acc;
       }
       larft_column(Tl, s, j, tau, z);
@@ -178,12 +181,12 @@ int oracle_tsqrt(int b, int s, double* R, double* B, double* T) {
     for (int t = c0 + s; t < b; ++t) {
       for (int a = 0; a < s; ++a) {
         double acc = Rk(c0 + a, t);
-        for (int r = 0; r < b; ++r) acc += Bk(r, c0 + a) * Bk(r, t);
+        for (int r = 0; r < rows; ++r) acc += Bk(r, c0 + a) * Bk(r, t);
         W[a] = acc;
       }
       apply_tl(Tl, s, W, W2, 1);
       for (int a = 0; a < s; ++a) Rk(c0 + a, t) -= W2[a];
-      for (int r = 0; r < b; ++r) {
+      for (int r = 0; r < rows; ++r) {
         double acc = 0.0;
         for (int a = 0; a < s; ++a) acc += Bk(r, c0 + a) * W2[a];
         Bk(r, t) -= acc;
@@ -195,6 +198,9 @@ int oracle_tsqrt(int b, int s, double* R, double* B, double* T) {
   free(z); free(W); free(W2);
   return 0;
 }
+
+/* TSQRT of [R_kk; A_ik] with one b x b lower tile. */
+int oracle_tsqrt(int b, int s, double* R, double* B, double* T) { return oracle_tsqrt_rows(b, s, b, R, B, T); }
 
 /* ---------------------------------------------------------------------------
  * LARFB / DLARFB: A_kj <- Q_kk^T A_kj (trans=1, R1)
@@ -240,9 +246,10 @@ int oracle_larfb(int b, int s, const double* V, const double* T, double* C, int 
  * [A_kj; A_ij] <- (I - [I;V] T^T [I;V]^T) [A_kj; A_ij] per inner block l
  * (trans=1), or the Q form with T_l, l descending (trans=0).  SURVEY 8(c) c-6.
  * ------------------------------------------------------------------------- */
-int oracle_ssrfb(int b, int s, const double* V, const double* T, double* C1, double* C2, int trans) {
+int oracle_ssrfb_rows(int b, int s, int rows, const double* V, const double* T, double* C1, double* C2, int trans) {
   int rc = check_bs(b, s);
   if (rc) return rc;
+  if (rows < 1) return -3;
   double* W = (double*)malloc(sizeof(double) * s);
   double* W2 = (double*)malloc(sizeof(double) * s);
   int nl = b / s;
@@ -252,24 +259,29 @@ int oracle_ssrfb(int b, int s, const double* V, const double* T, double* C1, dou
     const double* Tl = T + (int64_t)l * s * s;
     for (int t = 0; t < b; ++t) {
       double* C1t = C1 + (int64_t)t * b;
-      double* C2t = C2 + (int64_t)t * b;
+      double* C2t = C2 + (int64_t)t * rows;
       for (int a = 0; a < s; ++a) {
         double acc = C1t[c0 + a];
-        const double* Va = V + (int64_t)(c0 + a) * b;
-        for (int r = 0; r < b; ++r) acc += Va[r] * C2t[r];
+        const double* Va = V + (int64_t)(c0 + a) * rows;
+        for (int r = 0; r < rows; ++r) acc += Va[r] * C2t[r];
         W[a] = acc;
       }
       apply_tl(Tl, s, W, W2, trans);
       for (int a = 0; a < s; ++a) C1t[c0 + a] -= W2[a];
-      for (int r = 0; r < b; ++r) {
+      for (int r = 0; r < rows; ++r) {
         double acc = 0.0;
-        for (int a = 0; a < s; ++a) acc += V[r + (int64_t)(c0 + a) * b] * W2[a];
+        for (int a = 0; a < s; ++a) acc += V[r + (int64_t)(c0 + a) * rows] * W2[a];
         C2t[r] -= acc;
       }
     }
   }
   free(W); free(W2);
   return 0;
+}
+
+/* SSRFB with one b x b lower tile. */
+int oracle_ssrfb(int b, int s, const double* V, const double* T, double* C1, double* C2, int trans) {
+  return oracle_ssrfb_rows(b, s, b, V, T, C1, C2, trans);
 }
 
 /* ---------------------------------------------------------------------------
@@ -327,20 +339,78 @@ typedef struct {
   int b, s;
   double* At;
   double* T;
+  int h;  /* tile rows per TSQRT/SSRFB unit (R30; 1 = the paper's square tiles) */
 } qr_ctx;
 
 static int64_t g_counts[4];
 
-static void run_task(const qr_ctx* X, int kind, int64_t k, int64_t i, int64_t j) {
+/* Units of step k (R30): the tile rows below the diagonal, k+1 .. p-1, in
+ * consecutive groups of h starting at k+1 (the last group may be shorter).  Unit g covers
+ * tile rows [unit_lo(k, g), unit_hi(k, g)); the tile row i lies in unit unit_of(k, i). */
+static int64_t unit_lo(int64_t k, int64_t g, int h) { return k + 1 + (int64_t)h * g; }
+static int64_t unit_hi(int64_t k, int64_t g, int h, int64_t p) {
+  int64_t e = k + 1 + (int64_t)h * (g + 1);
+  return e < p ? e : p;
+}
+static int64_t unit_of(int64_t k, int64_t i, int h) { return (i - k - 1) / h; }
+static int64_t unit_count(int64_t k, int64_t p, int h) { return (p - k - 1 + h - 1) / h; }
+
+/* The nt tiles (i0 .. i0+nt-1, j) stacked into a column-major (nt b) x b buffer, and back. */
+static void gather(const qr_ctx* X, int64_t i0, int64_t nt, int64_t j, double* buf) {
+  int b = X->b;
+  for (int64_t t = 0; t < nt; ++t) {
+    const double* tl = TILE(X->At, i0 + t, j, X->p, b);
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = 0; r < b; ++r) buf[t * b + r + c * nt * b] = tl[r + c * b];
+  }
+}
+static void scatter(const qr_ctx* X, int64_t i0, int64_t nt, int64_t j, const double* buf) {
+  int b = X->b;
+  for (int64_t t = 0; t < nt; ++t) {
+    double* tl = TILE(X->At, i0 + t, j, X->p, b);
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = 0; r < b; ++r) tl[r + c * b] = buf[t * b + r + c * nt * b];
+  }
+}
+
+/* Task (kind, k, g, j); for T and S, g is the unit index (h = 1: the tile row k+1+g).  The T
+ * factors of unit g live in the T slot of its first tile row. */
+static void run_task(const qr_ctx* X, int kind, int64_t k, int64_t g, int64_t j) {
   int64_t p = X->p;
   int b = X->b, s = X->s;
+  int64_t i0 = 0, nt = 0;
+  if (kind == KT || kind == KS) {
+    i0 = unit_lo(k, g, X->h);
+    nt = unit_hi(k, g, X->h, p) - i0;
+  }
   switch (kind) {
     case KG: oracle_geqrt(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b)); break;
     case KL: oracle_larfb(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b), TILE(X->At, k, j, p, b), 1); break;
-    case KT: oracle_tsqrt(b, s, TILE(X->At, k, k, p, b), TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b)); break;
+    case KT:
+      if (nt == 1) {
+        oracle_tsqrt(b, s, TILE(X->At, k, k, p, b), TILE(X->At, i0, k, p, b), TSLOT(X->T, i0, k, p, s, b));
+      } else {
+        double* V = (double*)malloc(sizeof(double) * nt * b * b);
+        gather(X, i0, nt, k, V);
+        oracle_tsqrt_rows(b, s, (int)(nt * b), TILE(X->At, k, k, p, b), V, TSLOT(X->T, i0, k, p, s, b));
+        scatter(X, i0, nt, k, V);
+        free(V);
+      }
+      break;
     case KS:
-      oracle_ssrfb(b, s, TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b), TILE(X->At, k, j, p, b),
-                   TILE(X->At, i, j, p, b), 1);
+      if (nt == 1) {
+        oracle_ssrfb(b, s, TILE(X->At, i0, k, p, b), TSLOT(X->T, i0, k, p, s, b), TILE(X->At, k, j, p, b),
+                     TILE(X->At, i0, j, p, b), 1);
+      } else {
+        double* V = (double*)malloc(sizeof(double) * nt * b * b);
+        double* C2 = (double*)malloc(sizeof(double) * nt * b * b);
+        gather(X, i0, nt, k, V);
+        gather(X, i0, nt, j, C2);
+        oracle_ssrfb_rows(b, s, (int)(nt * b), V, TSLOT(X->T, i0, k, p, s, b), TILE(X->At, k, j, p, b), C2, 1);
+        scatter(X, i0, nt, j, C2);
+        free(V);
+        free(C2);
+      }
       break;
   }
 }
@@ -351,7 +421,10 @@ static void run_task(const qr_ctx* X, int kind, int64_t k, int64_t i, int64_t j)
  *   L(k,j)   <- G(k), S(k-1,k,j)
  *   T(k,i)   <- G(k) if i == k+1 else T(k,i-1); S(k-1,i,k)
  *   S(k,i,j) <- T(k,i); L(k,j) if i == k+1 else S(k,i-1,j); S(k-1,i,j)
- * Priority G > T > L > S, ties by smaller k, then i, then j (R10).   */
+ * Priority G > T > L > S, ties by smaller k, then i, then j (R10).
+ * With units of h tile rows (R30) the T/S tasks are indexed by unit g; a task of step k that
+ * touches tile rows of step k-1's units depends on the LAST of those units (the step k-1
+ * tasks of one column form a chain over the units).                              */
 typedef struct {
   int kind;
   int64_t k, i, j;
@@ -433,10 +506,13 @@ static void* dag_worker(void* arg) {
 
 /* Nodes in Algorithm 1's loop order and the edges of the comment above (the SPEC dag
  * module's rules).  Shared by the threaded executor and the oracle_dag_edges test hook. */
-static void dag_build(dag_ctx* D, int64_t p, int64_t q) {
+static void dag_build(dag_ctx* D, int64_t p, int64_t q, int h) {
   int64_t K = p < q ? p : q;
   int64_t nt = 0;
-  for (int64_t k = 0; k < K; ++k) nt += 1 + (q - k - 1) + (p - k - 1) + (p - k - 1) * (q - k - 1);
+  for (int64_t k = 0; k < K; ++k) {
+    const int64_t ng = unit_count(k, p, h);
+    nt += 1 + (q - k - 1) + ng + ng * (q - k - 1);
+  }
   D->ntasks = nt;
   D->tasks = (dag_task*)calloc(nt, sizeof(dag_task));
   D->heap = (int64_t*)malloc(sizeof(int64_t) * nt);
@@ -447,30 +523,31 @@ static void dag_build(dag_ctx* D, int64_t p, int64_t q) {
   D->efrom = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
   D->eto = (int64_t*)malloc(sizeof(int64_t) * 3 * nt);
 #define IDL(k, j) D->idL[(k) * q + (j)]
-#define IDT(k, i) D->idT[(k) * p + (i)]
-#define IDS(k, i, j) D->idS[((k) * p + (i)) * q + (j)]
+#define IDT(k, g) D->idT[(k) * p + (g)]
+#define IDS(k, g, j) D->idS[((k) * p + (g)) * q + (j)]
   int64_t id = 0;
   for (int64_t k = 0; k < K; ++k) {
     D->tasks[id] = (dag_task){KG, k, k, k, 0}; D->idG[k] = id++;
     for (int64_t j = k + 1; j < q; ++j) { D->tasks[id] = (dag_task){KL, k, k, j, 0}; IDL(k, j) = id++; }
-    for (int64_t i = k + 1; i < p; ++i) {
-      D->tasks[id] = (dag_task){KT, k, i, k, 0}; IDT(k, i) = id++;
-      for (int64_t j = k + 1; j < q; ++j) { D->tasks[id] = (dag_task){KS, k, i, j, 0}; IDS(k, i, j) = id++; }
+    for (int64_t g = 0; g < unit_count(k, p, h); ++g) {
+      D->tasks[id] = (dag_task){KT, k, g, k, 0}; IDT(k, g) = id++;
+      for (int64_t j = k + 1; j < q; ++j) { D->tasks[id] = (dag_task){KS, k, g, j, 0}; IDS(k, g, j) = id++; }
     }
   }
   for (int64_t k = 0; k < K; ++k) {
-    if (k > 0) add_edge(D, IDS(k - 1, k, k), D->idG[k]);
+    if (k > 0) add_edge(D, IDS(k - 1, unit_of(k - 1, k, h), k), D->idG[k]);
     for (int64_t j = k + 1; j < q; ++j) {
       add_edge(D, D->idG[k], IDL(k, j));
-      if (k > 0) add_edge(D, IDS(k - 1, k, j), IDL(k, j));
+      if (k > 0) add_edge(D, IDS(k - 1, unit_of(k - 1, k, h), j), IDL(k, j));
     }
-    for (int64_t i = k + 1; i < p; ++i) {
-      add_edge(D, i == k + 1 ? D->idG[k] : IDT(k, i - 1), IDT(k, i));
-      if (k > 0) add_edge(D, IDS(k - 1, i, k), IDT(k, i));
+    for (int64_t g = 0; g < unit_count(k, p, h); ++g) {
+      const int64_t gp = k > 0 ? unit_of(k - 1, unit_hi(k, g, h, p) - 1, h) : 0;  /* last unit of step k-1 */
+      add_edge(D, g == 0 ? D->idG[k] : IDT(k, g - 1), IDT(k, g));
+      if (k > 0) add_edge(D, IDS(k - 1, gp, k), IDT(k, g));
       for (int64_t j = k + 1; j < q; ++j) {
-        add_edge(D, IDT(k, i), IDS(k, i, j));
-        add_edge(D, i == k + 1 ? IDL(k, j) : IDS(k, i - 1, j), IDS(k, i, j));
-        if (k > 0) add_edge(D, IDS(k - 1, i, j), IDS(k, i, j));
+        add_edge(D, IDT(k, g), IDS(k, g, j));
+        add_edge(D, g == 0 ? IDL(k, j) : IDS(k, g - 1, j), IDS(k, g, j));
+        if (k > 0) add_edge(D, IDS(k - 1, gp, j), IDS(k, g, j));
       }
     }
   }
@@ -487,28 +564,30 @@ static void dag_free(dag_ctx* D) {
 /* Test hook: the DAG's edges for a p x q tile grid, 8 int64 per edge {kind, k, i, j} of the
  * predecessor then of the successor (kind 0 G, 1 T, 2 L, 3 S; T(k,i) has j = k, G and L
  * have i = k); returns the edge count, writes min(cap, count) edges. */
-int64_t oracle_dag_edges(int64_t p, int64_t q, int64_t* out, int64_t cap) {
-  if (p < 1 || q < 1) return -1;
+int64_t oracle_dag_edges_h(int64_t p, int64_t q, int h, int64_t* out, int64_t cap) {
+  if (p < 1 || q < 1 || h < 1) return -1;
   dag_ctx D;
   memset(&D, 0, sizeof(D));
-  dag_build(&D, p, q);
+  dag_build(&D, p, q, h);
   for (int64_t e = 0; e < D.nedge && e < cap; ++e) {
     const dag_task* a = &D.tasks[D.efrom[e]];
     const dag_task* b = &D.tasks[D.eto[e]];
     int64_t* o = out + 8 * e;
-    o[0] = a->kind; o[1] = a->k; o[2] = a->i; o[3] = a->j;
-    o[4] = b->kind; o[5] = b->k; o[6] = b->i; o[7] = b->j;
+    /* T / S tasks report the FIRST tile row of their unit */
+    o[0] = a->kind; o[1] = a->k; o[2] = (a->kind == KT || a->kind == KS) ? unit_lo(a->k, a->i, h) : a->i; o[3] = a->j;
+    o[4] = b->kind; o[5] = b->k; o[6] = (b->kind == KT || b->kind == KS) ? unit_lo(b->k, b->i, h) : b->i; o[7] = b->j;
   }
   int64_t n = D.nedge;
   dag_free(&D);
   return n;
 }
+int64_t oracle_dag_edges(int64_t p, int64_t q, int64_t* out, int64_t cap) { return oracle_dag_edges_h(p, q, 1, out, cap); }
 
 static int geqrf_dag(const qr_ctx* X, int nthreads) {
   dag_ctx D;
   memset(&D, 0, sizeof(D));
   D.X = *X;
-  dag_build(&D, X->p, X->q);
+  dag_build(&D, X->p, X->q, X->h);
   const int64_t nt = D.ntasks;
   D.soff = (int64_t*)calloc(nt + 1, sizeof(int64_t));
   D.succ = (int64_t*)malloc(sizeof(int64_t) * (D.nedge + 1));
@@ -535,13 +614,14 @@ static int geqrf_dag(const qr_ctx* X, int nthreads) {
   return ok ? 0 : -99;
 }
 
-int oracle_geqrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double* T, int nthreads) {
+int oracle_geqrf_tiles_h(int64_t m, int64_t n, int b, int s, int h, double* At, double* T, int nthreads) {
   if (m < 1) return -1;
   if (n < 1) return -2;
   int rc = check_bs(b, s);
   if (rc) return rc - 2;
-  if (nthreads < 1) return -7;
-  qr_ctx X = {m, n, (m + b - 1) / b, (n + b - 1) / b, b, s, At, T};
+  if (h < 1) return -5;
+  if (nthreads < 1) return -8;
+  qr_ctx X = {m, n, (m + b - 1) / b, (n + b - 1) / b, b, s, At, T, h};
   int64_t p = X.p, q = X.q, K = p < q ? p : q;
   memset(g_counts, 0, sizeof(g_counts));
   for (int64_t e = 0; e < p * q * (int64_t)s * b; ++e) T[e] = 0.0;
@@ -549,12 +629,17 @@ int oracle_geqrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double* T
   for (int64_t k = 0; k < K; ++k) {
     run_task(&X, KG, k, k, k); g_counts[KG]++;
     for (int64_t j = k + 1; j < q; ++j) { run_task(&X, KL, k, k, j); g_counts[KL]++; }
-    for (int64_t i = k + 1; i < p; ++i) {
-      run_task(&X, KT, k, i, k); g_counts[KT]++;
-      for (int64_t j = k + 1; j < q; ++j) { run_task(&X, KS, k, i, j); g_counts[KS]++; }
+    for (int64_t g = 0; g < unit_count(k, p, h); ++g) {
+      run_task(&X, KT, k, g, k); g_counts[KT]++;
+      for (int64_t j = k + 1; j < q; ++j) { run_task(&X, KS, k, g, j); g_counts[KS]++; }
     }
   }
   return 0;
+}
+
+int oracle_geqrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double* T, int nthreads) {
+  int rc = oracle_geqrf_tiles_h(m, n, b, s, 1, At, T, nthreads);
+  return rc <= -5 ? rc + 1 : rc;  /* (argument numbering of the h-less signature) */
 }
 
 void oracle_last_task_counts(int64_t counts[4]) {
@@ -570,9 +655,35 @@ void oracle_last_task_counts(int64_t counts[4]) {
  * ------------------------------------------------------------------------- */
 typedef struct {
   int64_t m, n, p, q, qb, j0, j1;
-  int b, s, trans;
+  int b, s, trans, h;
   const double* At; const double* T; double* Bt;
 } orm_ctx;
+
+/* SSRFB-type application of unit g of step k (R30) to tile column j of B. */
+static void orm_unit(const orm_ctx* X, int64_t k, int64_t g, int64_t j, int trans) {
+  int64_t p = X->p;
+  int b = X->b, s = X->s;
+  const int64_t i0 = unit_lo(k, g, X->h), nt = unit_hi(k, g, X->h, p) - i0;
+  if (nt == 1) {
+    oracle_ssrfb(b, s, TILE(X->At, i0, k, p, b), TSLOT(X->T, i0, k, p, s, b), TILE(X->Bt, k, j, p, b),
+                 TILE(X->Bt, i0, j, p, b), trans);
+    return;
+  }
+  double* V = (double*)calloc(nt * b * b, sizeof(double));
+  double* C2 = (double*)calloc(nt * b * b, sizeof(double));
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = 0; r < b; ++r) {
+        V[t * b + r + c * nt * b] = TILE(X->At, i0 + t, k, p, b)[r + c * b];
+        C2[t * b + r + c * nt * b] = TILE(X->Bt, i0 + t, j, p, b)[r + c * b];
+      }
+  oracle_ssrfb_rows(b, s, (int)(nt * b), V, TSLOT(X->T, i0, k, p, s, b), TILE(X->Bt, k, j, p, b), C2, trans);
+  for (int64_t t = 0; t < nt; ++t)
+    for (int64_t c = 0; c < b; ++c)
+      for (int64_t r = 0; r < b; ++r) TILE(X->Bt, i0 + t, j, p, b)[r + c * b] = C2[t * b + r + c * nt * b];
+  free(V);
+  free(C2);
+}
 
 static void orm_columns(const orm_ctx* X) {
   int64_t p = X->p, K = X->p < X->q ? X->p : X->q;
@@ -581,15 +692,11 @@ static void orm_columns(const orm_ctx* X) {
     if (X->trans) {
       for (int64_t k = 0; k < K; ++k) {
         oracle_larfb(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b), TILE(X->Bt, k, j, p, b), 1);
-        for (int64_t i = k + 1; i < p; ++i)
-          oracle_ssrfb(b, s, TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b), TILE(X->Bt, k, j, p, b),
-                       TILE(X->Bt, i, j, p, b), 1);
+        for (int64_t g = 0; g < unit_count(k, p, X->h); ++g) orm_unit(X, k, g, j, 1);
       }
     } else {
       for (int64_t k = K - 1; k >= 0; --k) {
-        for (int64_t i = p - 1; i > k; --i)
-          oracle_ssrfb(b, s, TILE(X->At, i, k, p, b), TSLOT(X->T, i, k, p, s, b), TILE(X->Bt, k, j, p, b),
-                       TILE(X->Bt, i, j, p, b), 0);
+        for (int64_t g = unit_count(k, p, X->h) - 1; g >= 0; --g) orm_unit(X, k, g, j, 0);
         oracle_larfb(b, s, TILE(X->At, k, k, p, b), TSLOT(X->T, k, k, p, s, b), TILE(X->Bt, k, j, p, b), 0);
       }
     }
@@ -597,21 +704,22 @@ static void orm_columns(const orm_ctx* X) {
 }
 static void* orm_worker(void* a) { orm_columns((const orm_ctx*)a); return NULL; }
 
-int oracle_ormqr_tiles(int64_t m, int64_t n, int b, int s, const double* At, const double* T,
-                       int trans, int64_t nrhs, double* Bt, int nthreads) {
+int oracle_ormqr_tiles_h(int64_t m, int64_t n, int b, int s, int h, const double* At, const double* T,
+                         int trans, int64_t nrhs, double* Bt, int nthreads) {
   if (m < 1) return -1;
   if (n < 1) return -2;
   int rc = check_bs(b, s);
   if (rc) return rc - 2;
-  if (trans != 0 && trans != 1) return -7;
-  if (nrhs < 1) return -8;
-  if (nthreads < 1) return -10;
+  if (h < 1) return -5;
+  if (trans != 0 && trans != 1) return -8;
+  if (nrhs < 1) return -9;
+  if (nthreads < 1) return -11;
   int64_t p = (m + b - 1) / b, q = (n + b - 1) / b, qb = (nrhs + b - 1) / b;
   if (nthreads > qb) nthreads = (int)qb;
   orm_ctx* X = (orm_ctx*)malloc(sizeof(orm_ctx) * nthreads);
   pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * nthreads);
   for (int w = 0; w < nthreads; ++w) {
-    X[w] = (orm_ctx){m, n, p, q, qb, qb * w / nthreads, qb * (w + 1) / nthreads, b, s, trans, At, T, Bt};
+    X[w] = (orm_ctx){m, n, p, q, qb, qb * w / nthreads, qb * (w + 1) / nthreads, b, s, trans, h, At, T, Bt};
     if (nthreads == 1) orm_columns(&X[w]);
     else pthread_create(&th[w], NULL, orm_worker, &X[w]);
   }
@@ -619,6 +727,12 @@ int oracle_ormqr_tiles(int64_t m, int64_t n, int b, int s, const double* At, con
     for (int w = 0; w < nthreads; ++w) pthread_join(th[w], NULL);
   free(X); free(th);
   return 0;
+}
+
+int oracle_ormqr_tiles(int64_t m, int64_t n, int b, int s, const double* At, const double* T,
+                       int trans, int64_t nrhs, double* Bt, int nthreads) {
+  int rc = oracle_ormqr_tiles_h(m, n, b, s, 1, At, T, trans, nrhs, Bt, nthreads);
+  return rc <= -5 ? rc + 1 : rc;
 }
 
 /* ---------------------------------------------------------------------------
@@ -641,6 +755,21 @@ double oracle_kernel_flops(int kind, double b) {
     case 3: return 5.0 * b3;          /* DSSRFB */
   }
   return -1.0;
+}
+
+/* Eq. (4) with units of h tile rows (R30), s = b: per unit of nt tiles TSQRT (3 nt + 1/3) b^3
+ * (h = 1: 10/3 b^3) and SSRFB (4 nt + 1) b^3 (h = 1: 5 b^3). */
+double oracle_flops_eq4_h(int64_t p, int64_t q, double b, int h) {
+  double tot = 0.0, b3 = b * b * b;
+  int64_t K = p < q ? p : q;
+  for (int64_t k = 0; k < K; ++k) {
+    tot += 2.0 * b3 + (double)(q - k - 1) * 3.0 * b3;
+    for (int64_t g = 0; g < unit_count(k, p, h); ++g) {
+      const double nt = (double)(unit_hi(k, g, h, p) - unit_lo(k, g, h));
+      tot += (3.0 * nt + 1.0 / 3.0) * b3 + (double)(q - k - 1) * (4.0 * nt + 1.0) * b3;
+    }
+  }
+  return tot;
 }
 
 double oracle_flops_eq4(int64_t p, int64_t q, double b) {

@@ -41,6 +41,11 @@ int oracle_ssrfb(int b, int s, const double* V, const double* T, double* C1, dou
 /* trans = 1 applies Q^T (factorization, l ascending, T_l^T);
  * trans = 0 applies Q (l descending, T_l), used by apply-Q / form-Q. */
 
+/* TSQRT / SSRFB with `rows` rows in the lower block (ld = rows; rows = b: the functions above;
+ * rows = h b: the non-square 2b x b tiles of P:582-583, reading R30). */
+int oracle_tsqrt_rows(int b, int s, int rows, double* R, double* B, double* T);
+int oracle_ssrfb_rows(int b, int s, int rows, const double* V, const double* T, double* C1, double* C2, int trans);
+
 /* Block Data Layout pack/unpack, zero padding (R9). */
 int oracle_pack(int64_t m, int64_t n, int b, const double* A, int64_t lda, double* At);
 int oracle_unpack(int64_t m, int64_t n, int b, const double* At, double* A, int64_t lda);
@@ -51,6 +56,16 @@ int oracle_unpack(int64_t m, int64_t n, int b, const double* At, double* A, int6
  * bitwise identical either way (each tile's operation sequence is fixed by the
  * DAG edges). */
 int oracle_geqrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double* T, int nthreads);
+
+/* Algorithm 1 with the tile rows below the diagonal grouped in units of h (R30:
+ * units k+1.., k+1+h.., ...; the last may be shorter): TSQRT / SSRFB work on the (nt b) x b
+ * stack of a unit's tiles; its T factors are in the T slot of its first tile row (the other
+ * slots stay 0).  h = 1 is oracle_geqrf_tiles. */
+int oracle_geqrf_tiles_h(int64_t m, int64_t n, int b, int s, int h, double* At, double* T, int nthreads);
+int oracle_ormqr_tiles_h(int64_t m, int64_t n, int b, int s, int h, const double* At, const double* T,
+                         int trans, int64_t nrhs, double* Bt, int nthreads);
+int64_t oracle_dag_edges_h(int64_t p, int64_t q, int h, int64_t* out, int64_t cap);
+double oracle_flops_eq4_h(int64_t p, int64_t q, double b, int h);
 
 /* Apply Q^T (trans=1) or Q (trans=0) to a tile-major m x nrhs matrix Bt
  * (same row tiling p = ceil(m/b); ceil(nrhs/b) tile columns).
