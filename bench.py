@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", default="", help="write a per-task execution trace (JSON) of one extra step")
+    ap.add_argument("--tiles", default="square", choices=["square", "2bxb"],
+                    help="2bxb: the paper's non-square 2b x b tiles (TQR_FLAG_TALL_TILES, DESIGN.md R30)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
                     help="test mode: run the G-rank distributed schedule in one launch on one GPU")
     return ap.parse_args()
@@ -126,13 +128,13 @@ def sample_block(cfg, A=None):
     return np.asfortranarray(A[:m, :n])
 
 
-def time_oracle(A, cfg, threads):
-    """The oracle as it stands (oracle/, plain C DAG executor) on host matrix A.
-    Returns (GFLOP/s standard count, seconds, tiles At, T)."""
+def time_oracle(A, cfg, threads, h=1):
+    """The oracle as it stands (oracle/, plain C DAG executor) on host matrix A (h = 2: its
+    2b x b tile mode).  Returns (GFLOP/s standard count, seconds, tiles At, T)."""
     import oracle
     m, n = A.shape
     t0 = time.perf_counter()
-    At, T = oracle.geqrf(A, cfg["b"], cfg["s"], nthreads=threads)
+    At, T = oracle.geqrf(A, cfg["b"], cfg["s"], nthreads=threads, h=h)
     dt = time.perf_counter() - t0
     return oracle.flops_standard(m, n) / dt / 1e9, dt, At, T
 
@@ -190,8 +192,9 @@ def main():
     m, n, b, s = cfg["m"], cfg["n"], cfg["b"], cfg["s"]
     G = world if world > 1 else args.emulate_ranks
     stream = torch.cuda.Stream()
+    tall = args.tiles == "2bxb"
     plan = tqr.Plan(m, n, b, s, device=local, stream=stream, nranks=G, rank=rank if world > 1 else 0,
-                    emulate=world == 1 and G > 1)
+                    emulate=world == 1 and G > 1, tall=tall)
     if world > 1:
         tdist.connect(plan)   # one-time CUDA IPC blob exchange
     A_host = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"])                  # one matrix, every rank
@@ -310,7 +313,7 @@ def main():
 
     # ---- form Q explicitly (tqr_orgqr), once, after the timed region ----
     form_q = None
-    if world == 1 and not args.no_e2e:
+    if world == 1 and not args.no_e2e and not tall:
         qb = -(-n // b)
         free_b, _ = torch.cuda.mem_get_info(f"cuda:{local}")
         if free_b > 1.2 * plan.p * qb * b * b * 8:
@@ -356,9 +359,9 @@ def main():
         A_host = A_pin.numpy().T                          # m x n, Fortran order (no copy)
         if flops <= FULL_ORACLE_MAX_FLOPS:
             import oracle
-            v, dt, At_o, _ = time_oracle(A_host, cfg, threads)
-            desc = (f"oracle_geqrf_tiles on the full {m}x{n} workload (the same A bytes), b={b} s={s}, "
-                    f"{threads} threads, one factorization")
+            v, dt, At_o, _ = time_oracle(A_host, cfg, threads, h=2 if tall else 1)
+            desc = (f"oracle_geqrf_tiles on the full {m}x{n} workload (the same A bytes), b={b} s={s}"
+                    f"{', 2b x b tiles' if tall else ''}, {threads} threads, one factorization")
             R_o = oracle.get_r(At_o, m, n, b)
             del At_o
             R_g = R.cpu().numpy().T
@@ -397,7 +400,8 @@ def main():
                                    if world > 1 else ("1 GPU" if G == 1 else f"1 GPU, {G} emulated ranks")),
                    "l2": (f"inputs {m * n * 8 / 2**30:.1f} GiB > 126 MB L2; no flush between steps"
                           if m * n * 8 > (1 << 28) else "inputs smaller than L2 (not flushed)"),
-                   "step": "pack + geqrf (persistent DAG executor) + get_r"},
+                   "step": "pack + geqrf (persistent DAG executor) + get_r",
+                   "tiles": "2b x b (TQR_FLAG_TALL_TILES)" if tall else "b x b"},
         "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
         "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

@@ -66,6 +66,15 @@ typedef struct {
 #define TQR_FLAG_EMULATE_RANKS 2u  /* nranks > 1 on ONE device in ONE launch: every rank's task
                                       stream, counters and workspace, the same peer-store protocol
                                       (test mode for the multi-GPU path on a single GPU) */
+#define TQR_FLAG_TALL_TILES 4u     /* the paper's non-square 2b x b tiles (PAPER.md:582-583,
+                                      DESIGN.md R30): the tile rows below the diagonal in units of
+                                      two tiles (units start right below the diagonal tile; the last
+                                      may be one tile); TSQRT / SSRFB work on a unit's 2b x b stack,
+                                      its T factors in the T slot of its first tile row (the other
+                                      slots 0).  A different reflector sequence than square tiles:
+                                      R differs in row signs / rounding.  Built for b = 256, s = 32,
+                                      one rank, factorization (tqr_geqrf, tqr_get_r) only;
+                                      TQR_ERR_UNSUPPORTED otherwise. */
 
 /* ---- plan -------------------------------------------------------------------------- */
 /* Validates p (argument 2's fields: m=1, n=2, b=3, s=4, device=5, nranks=7, rank=8 are
@@ -202,8 +211,9 @@ tqr_status tqr_plan_records(tqr_plan* plan, int32_t local, int32_t* rec, int64_t
  * [4] early R_kk release, [5] executor CTAs, [6] priority (0 classes, 1 bottom level),
  * [7] fine-granularity rule (R23), [8] internal inner block SI of the executor (== s
  * except b*s > 8192, R16), [9] ranks of the job, [10] ranks run by this process,
- * [11] columns per register pass. */
-tqr_status tqr_plan_info(const tqr_plan* plan, int32_t info[12]);
+ * [11] columns per register pass, [12] tile rows per TSQRT / SSRFB unit (1, or 2 with
+ * TQR_FLAG_TALL_TILES), [13..15] 0. */
+tqr_status tqr_plan_info(const tqr_plan* plan, int32_t info[16]);
 
 /* Trace of the last tqr_geqrf with TQR_FLAG_TRACE: up to `cap` records of
  * {kind, k, i, j, slice | flags << 16, sm, start_ns, end_ns} as 8 int64 each (host memory;

@@ -380,7 +380,9 @@ __device__ __forceinline__ void gemm1(const double (&acc)[RW / 8][2], double (&w
 // needs w[u2..], so the order is u2 = NU-1, ..., 0.  Each block's T products are summed over
 // (u, h) ascending; GEMM2 (C^T += (-W)^T Y^T, accumulators chained per row block t) runs its
 // k-steps in the block order.
-template <int B, int S, int RW, bool QT>
+// LD: leading dimension of the C1 tile `top` (== B, the panel's rows, except for the tall
+// units of DESIGN.md R30, whose 2b-row panels update b-row C1 tiles)
+template <int B, int S, int RW, bool QT, int LD = B>
 __device__ __forceinline__ void tmul_gemm2(double (&acc)[RW / 8][2], const double (&w)[S / 8][2],
                                            const double* __restrict__ Ys, const double* __restrict__ Ts,
                                            const double* c1s, double* top, int row0, int col0, int t0,
@@ -400,7 +402,7 @@ __device__ __forceinline__ void tmul_gemm2(double (&acc)[RW / 8][2], const doubl
   };
   auto finish = [&](int u2) __attribute__((always_inline)) {  // C1 -= W (block u2), negate
     if (store_c1) {
-      double* col = top + (size_t)(col0 + g) * B + row0 + j;
+      double* col = top + (size_t)(col0 + g) * LD + row0 + j;
       st_cg1(col + 8 * u2, c1s[c1_idx<S>(u2, 0, lane)] - wn[u2][0], true);      // C1: kept in L2
       st_cg1(col + 8 * u2 + 4, c1s[c1_idx<S>(u2, 1, lane)] - wn[u2][1], true);
     }
@@ -455,7 +457,7 @@ __device__ __forceinline__ void store_top_minus_r(const double (&c1)[S / 8][2], 
 // c1: the group's C1 block in registers (fragment layout of w; used by rpart 0 only);
 // top/row0: where C1 - W is stored.  xg: the group's RS partial buffers.  BAR2 protects
 // xg when the caller reuses it before all warps of the group have read it.
-template <int B, int S, int RW, int RS, bool QT, bool BAR2>
+template <int B, int S, int RW, int RS, bool QT, bool BAR2, int LD = B>
 __device__ __forceinline__ void group_apply(double (&acc)[RW / 8][2], const double* __restrict__ Ys,
                                             const double* __restrict__ Ts, const double* c1s, double* top,
                                             int row0, int col0, int t0, int gi, int rpart, double* xg) {
@@ -483,7 +485,7 @@ __device__ __forceinline__ void group_apply(double (&acc)[RW / 8][2], const doub
       }
     if (BAR2) named_bar(1 + gi, 32 * RS);
   }
-  tmul_gemm2<B, S, RW, QT>(acc, w, Ys, Ts, c1s, top, row0, col0, t0, HAS_C1 && rpart == 0);
+  tmul_gemm2<B, S, RW, QT, LD>(acc, w, Ys, Ts, c1s, top, row0, col0, t0, HAS_C1 && rpart == 0);
 }
 
 // Warp-local cp.async of one group's C1 block (rows [row0, row0+S), 8 columns from col0)

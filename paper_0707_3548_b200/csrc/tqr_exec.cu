@@ -689,6 +689,421 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
 }
 
 // ---------------------------------------------------------------------------------------
+// Tall-unit executor (R30; "2b x b blocks"): the tile rows below
+// the diagonal are grouped in units of two b x b tiles (the last unit of a step may be one
+// tile); TSQRT / SSRFB work on the (2b) x b stack of a unit.  b = 256, s = 32 only: a unit is
+// 512 rows, so the executor runs the 512-row register configuration of the b = 512 instance
+// (RW = 256 rows per warp, two warps per column group, SI = 16 internal blocks: a 512 x 16
+// packed panel, double-buffered, fits shared memory) on 256-column tiles whose leading
+// dimension is 256: warp rpart of a column group holds tile i0 + rpart.  GEQRT / LARFB tasks
+// (the diagonal tile) are units whose second tile is absent (zero rows, not stored).
+// Records: [2] = the unit's first tile row i0, [14] bit 7 = the unit has a second tile.
+// Workspace: the packed panels of unit (i0, k) at (i0 + k p) * 2 b^2 doubles (TR x SI per
+// internal block), T blocks as for square tiles.
+// ---------------------------------------------------------------------------------------
+namespace tall {
+constexpr int TB = 256, TR = 512, SO = 32, S = Inner<TR, SO>::SI, RWM = 256;
+using C = Cfg<TR, S, RWM>;
+using L = Layout<TR, S, RWM>;
+static_assert(S == 16 && C::RS == 2 && C::RW == TB, "tall-unit configuration");
+constexpr int NL = TB / S;   // internal blocks per tile (16)
+constexpr int SPT = SO / S;  // internal blocks per output T block (2)
+
+__device__ __forceinline__ double* unit_panel(double* base, int i0, int k, int p) {
+  return base + ((size_t)i0 + (size_t)k * p) * 2 * (size_t)TB * TB;
+}
+
+// update phase on a unit: warp rpart of column group gi holds tile Ct[rpart] (nullptr: absent
+// rows -- zeros, still part of the group's W exchange)
+template <class PF>
+__device__ __forceinline__ void update_phase(double* sm, double (&acc)[C::RW / 8][2], const double* Yp,
+                                             const double* Tp, int lb0, int nbe, double* C1, double* const (&Ct)[2],
+                                             int col0, int gact, PF&& pf) {
+  const int nb = nbe - lb0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
+  const int cg0 = col0 + gi * 8;
+  const bool active = gi < gact;
+  const bool rows = active && Ct[rpart] != nullptr;
+  const bool top_owner = C1 != nullptr && active && rpart == 0;
+  unsigned long long* full = reinterpret_cast<unsigned long long*>(sm + L::MBAR);
+  int* done = reinterpret_cast<int*>(full + 2);
+  double* c1s0 = sm + L::C1S + gi * C::C1W;
+  double* c1s1 = sm + L::C1S + L::C1SZ + gi * C::C1W;
+  if (nb > 0 && threadIdx.x == 0) {
+    mbar_init(full, 1);
+    mbar_init(full + 1, 1);
+    done[0] = 0;
+    done[1] = 0;
+    fence_mbar_init();
+    fence_proxy_async();
+    issue_panel<TR, S, RWM>(sm, Yp, Tp, lb0, 0);
+    if (nb > 1) issue_panel<TR, S, RWM>(sm, Yp, Tp, lb0 + 1, 1);
+  }
+  if (rows) {
+    load_cols<TB, C::RW>(acc, Ct[rpart], cg0, 0);
+  } else {
+#pragma unroll
+    for (int t = 0; t < C::RW / 8; ++t) { acc[t][0] = 0.0; acc[t][1] = 0.0; }
+  }
+  if (nb <= 0) return;
+  if (top_owner) c1_fetch<TB, S>(c1s0, C1, lb0 * S, cg0);
+  __syncthreads();
+  for (int li = 0; li < nb; ++li) {
+    const int l = lb0 + li;
+    const int buf = li & 1;
+    if (top_owner) {
+      cp_async_wait<0>();
+      __syncwarp();
+      if (li + 1 < nb) c1_fetch<TB, S>(buf ? c1s0 : c1s1, C1, (l + 1) * S, cg0);
+    }
+    mbar_wait(full + buf, (li >> 1) & 1);
+    if (threadIdx.x == 0) pf(li, nb);
+    if (active)
+      group_apply<TR, S, C::RW, C::RS, true, false, TB>(acc, sm + (buf ? L::Y1 : L::Y0), sm + (buf ? L::T1 : L::T0),
+                                                        buf ? c1s1 : c1s0, C1, l * S, cg0, t0, gi, rpart,
+                                                        sm + L::XBUF + (li & 1) * (C::NWARP * C::XW) +
+                                                            gi * C::RS * C::XW);
+    __syncwarp();
+    if (lane == 0 && li + 2 < nb) {
+      if (atomicAdd(done + buf, 1) == C::NWARP - 1) {
+        done[buf] = 0;
+        issue_panel<TR, S, RWM>(sm, Yp, Tp, l + 2, buf);
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Panel block l of GEQRT(k) (ts = false; Ab = {A(k,k), nullptr}) or TSQRT(k, unit) (ts = true;
+// Ab = the unit's tiles): as ::panel_block on the 512-row staged block, V / R written back to
+// the unit's tiles, packed Y_l (512 x SI) / T_l to the workspace.
+template <bool ts>
+__device__ __forceinline__ void panel_block(double* sm, const double (&acc)[C::RW / 8][2], double* Akk,
+                                            double* const (&Ab)[2], double* Tslot, double* Yunit, double* Tunit,
+                                            int l, bool more, int rlo, unsigned& pf_gen, int* pr_ctr, int pr_val) {
+  constexpr int LDP = L::LDP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int gi = warp / C::RS, rpart = warp % C::RS, t0 = rpart * (C::RW / 8);
+  const int c0 = l * S;
+  double* P = sm + L::Y1;
+  double* Ys = sm + L::Y0;
+  double* Rb = sm + L::RB;
+  double* Tp = sm + L::RB;
+  double* Z = sm + L::ZZ;
+  double* tau = sm + L::TAU;
+  if (gi < S / 8) {
+    const int col = 8 * gi + (lane >> 2);
+#pragma unroll
+    for (int t = 0; t < C::RW / 8; ++t)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int r = 8 * (t0 + t) + 2 * (lane & 3) + h;  // unit row (rows >= TB: tile 2)
+        if (ts || r >= c0) P[r + col * LDP] = acc[t][h];
+        else if (r >= rlo) __stcg(Akk + (size_t)(c0 + col) * TB + r, acc[t][h]);  // (GEQRT: r < TB)
+      }
+  }
+  if (ts)
+    for (int e = tid; e < S * S; e += C::NT) {
+      const int r = e % S, c = e / S;
+      Rb[e] = (r <= c) ? __ldcg(Akk + (size_t)(c0 + c) * TB + c0 + r) : 0.0;
+    }
+  __syncthreads();
+  panel_factor<TR, S, C::NWARP, LDP>(P, c0, Rb, tau, ts, reinterpret_cast<unsigned long long*>(sm + L::PMB),
+                                     pf_gen & 1);
+  ++pf_gen;
+  for (int e = tid; e < TR * S; e += C::NT) {
+    const int r = e % TR, c = e / TR;
+    double y = 0.0;
+    if (ts) {
+      y = P[r + c * LDP];
+      double* t = Ab[r / TB];
+      if (t) __stcg(t + (size_t)(c0 + c) * TB + r % TB, y);
+    } else if (r >= c0 && r < TB) {
+      const double v = P[r + c * LDP];
+      __stcg(Akk + (size_t)(c0 + c) * TB + r, v);
+      y = (r - c0 == c) ? 1.0 : (r - c0 > c ? v : 0.0);
+    }
+    Ys[swy<TR>(r, c)] = y;
+  }
+  if (ts)
+    for (int e = tid; e < S * S; e += C::NT) {
+      const int r = e % S, c = e / S;
+      if (r <= c) __stcg(Akk + (size_t)(c0 + c) * TB + c0 + r, Rb[e]);
+    }
+  __syncthreads();
+  if (pr_ctr && !more && threadIdx.x == 0) {  // early release of R_kk's block rows (R24)
+    __threadfence();
+    st_release(pr_ctr, pr_val);
+  }
+  gram_upper<TR, S, C::NWARP>(Ys, Z);
+  __syncthreads();
+  if (warp == 0) {
+    build_t<S>(Tp, tau, Z);
+  } else {
+    const double2* ys2 = reinterpret_cast<const double2*>(Ys);
+    for (int e = tid - 32; e < TR * S / 2; e += C::NT - 32)
+      __stcg(reinterpret_cast<double2*>(Yunit + (size_t)l * TR * S) + e, ys2[e]);
+  }
+  __syncthreads();
+  const int Lo = l / SPT, mo = (l % SPT) * S;
+  for (int e = tid; e < S * S; e += C::NT) {
+    const int r = e % S, c = e / S;
+    __stcg(Tslot + ((size_t)Lo * SO + mo + c) * SO + mo + r, Tp[e]);
+    __stcg(Tunit + (size_t)l * S * S + swz<S>(r, c), Tp[e]);
+  }
+  if (more) fence_proxy_async();
+  __syncthreads();
+}
+
+// Persistent executor for tall-unit factorizations (one rank; same ticket / counter protocol
+// as ::exec_kernel, including the ordered end-of-task publication of R25).
+__global__ void __launch_bounds__(C::NT, 1) exec_kernel(const __grid_constant__ ExecArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_task[TASK_INTS];
+  __shared__ int s_ticket;
+  __shared__ __align__(16) int s_next[TASK_INTS];
+  __shared__ int s_have;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const RankLocal& R = a.loc[0];
+  double* const Yme = a.Yp[0];
+  double* const Tme = a.Tp[0];
+  unsigned pf_gen = 0;
+  if (tid < S) mbar_init(reinterpret_cast<unsigned long long*>(sm + L::PMB) + tid, 1);
+  fence_mbar_init();
+  __syncthreads();
+  int next_tk = -1, rec_for = -1;
+  const int p = a.p;
+  for (;;) {
+    if (tid == 0) {
+      if (next_tk < 0) next_tk = atomicAdd(R.ticket, 1);
+      cp_async_wait<0>();
+      s_ticket = next_tk;
+      s_have = rec_for == next_tk;
+      next_tk = -1;
+    }
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= R.ntasks) return;
+    if (tid < TASK_INTS) s_task[tid] = s_have ? s_next[tid] : R.tasks[(size_t)tk * TASK_INTS + tid];
+    __syncthreads();
+    unsigned long long t_grab = 0, t_start = 0;
+    if (R.trace && tid == 0) t_grab = globaltimer();
+    if (warp == 0) {
+#pragma unroll
+      for (int d = 0; d < TASK_NDEP; ++d) {
+        const int code = s_task[8 + 2 * d], val = a.base + s_task[9 + 2 * d];
+        const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+        for (int x = lane; x < cnt; x += 32) {
+          const int* c = R.ctr + idx + x;
+          if (ld_acquire(c) >= val) continue;
+          const unsigned long long t0w = globaltimer();
+          while (ld_acquire(c) < val) {
+            __nanosleep(TQR_POLL_NS);
+            if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
+          }
+        }
+      }
+      __syncwarp();
+      fence_proxy_async();
+    }
+    __syncthreads();
+    if (R.trace && tid == 0) t_start = globaltimer();
+    const int kind = s_task[0], k = s_task[1], i0 = s_task[2], j = s_task[3], sl = s_task[4];
+    const bool two = (s_task[14] & 128) != 0;
+    {
+      const bool panel = kind == K_G || kind == K_T;
+      const bool ts = kind == K_T;
+      const bool lkind = kind == K_L;
+      double* Akk = tile_ptr(R.A, k, k, p, TB);
+      const int urow = (panel && !ts) || lkind ? k : i0;  // the unit whose reflectors are applied
+      double* Tslot = tslot_ptr(R.T, urow, k, p, TB, SO);
+      double* Yunit = unit_panel(Yme, urow, k, p);
+      double* Tunit = Tme + ((size_t)urow + (size_t)k * p) * (size_t)SO * TB;
+      const int sub0 = panel ? sl * SPT : 0;
+      const int np = s_task[15] & 0xFF;
+      const int nsub = panel ? sub0 + SPT : np;
+      const bool a_part = panel && (s_task[14] & 2), f_part = panel && (s_task[14] & 4);
+      for (int sub = sub0; sub < nsub; ++sub) {
+        double acc[C::RW / 8][2];
+        double* C1;
+        double* Ct[2];
+        int col0, nb, gact, lb0 = 0;
+        if (panel) {
+          C1 = ts ? Akk : nullptr;
+          Ct[0] = ts ? tile_ptr(R.A, i0, k, p, TB) : Akk;
+          Ct[1] = ts && two ? tile_ptr(R.A, i0 + 1, k, p, TB) : nullptr;
+          col0 = sub * S;
+          nb = a_part ? sub0 : sub;
+          lb0 = f_part ? sub0 : 0;
+          gact = S / 8;
+        } else {
+          C1 = lkind ? nullptr : tile_ptr(R.A, k, j, p, TB);
+          Ct[0] = lkind ? tile_ptr(R.A, k, j, p, TB) : tile_ptr(R.A, i0, j, p, TB);
+          Ct[1] = !lkind && two ? tile_ptr(R.A, i0 + 1, j, p, TB) : nullptr;
+          col0 = (sl + sub) * C::SLICE;
+          nb = NL;
+          gact = (TB - col0) / 8 < C::GPS ? (TB - col0) / 8 : C::GPS;
+        }
+        auto pf = [&](int li, int nbb) {
+          if (sub != nsub - 1 || nbb < 4) return;
+          const int l0 = nbb / 2;
+          if (li == l0) next_tk = atomicAdd(R.ticket, 1);
+          if (li == l0 + 1 && next_tk < R.ntasks) {
+#pragma unroll
+            for (int x = 0; x < TASK_INTS; x += 4) cp_async16(s_next + x, R.tasks + (size_t)next_tk * TASK_INTS + x);
+            cp_async_commit();
+            rec_for = next_tk;
+          }
+          if (li == l0 + 2 && rec_for == next_tk && next_tk < R.ntasks) {
+            cp_async_wait<0>();
+            const int* q = s_next;
+            const int qk = q[1], qi = q[2], qj = q[3];
+            if (q[0] == K_S) {  // the next update's C2 / C1 column slices and first reflector blocks
+              const size_t off = (size_t)q[4] * C::SLICE * TB;
+              prefetch_l2(tile_ptr(R.A, qi, qj, p, TB) + off, (unsigned)(C::SLICE * TB * 8));
+              if (q[14] & 128) prefetch_l2(tile_ptr(R.A, qi + 1, qj, p, TB) + off, (unsigned)(C::SLICE * TB * 8));
+              prefetch_l2(tile_ptr(R.A, qk, qj, p, TB) + off, (unsigned)(C::SLICE * TB * 8));
+              prefetch_l2(unit_panel(Yme, qi, qk, p), (unsigned)(2 * TR * S * 8));
+            }
+          }
+        };
+        update_phase(sm, acc, Yunit, Tunit, lb0, nb, C1, Ct, col0, gact, pf);
+        if (a_part) {
+          const int gi = warp / C::RS, rp = warp % C::RS;
+          if (gi < gact && Ct[rp]) store_cols<TB, C::RW>(acc, Ct[rp], col0 + 8 * gi, 0);
+        } else if (panel) {
+          const int rlo = f_part ? sub0 * S : 0;
+          const int pr = (s_task[14] >> 8) - 1;
+          int* const prc = pr >= 0 ? R.ctr + pr : nullptr;
+          const int prv = a.base + s_task[6];
+          if (ts)
+            panel_block<true>(sm, acc, Akk, Ct, Tslot, Yunit, Tunit, sub, sub + 1 < nsub, rlo, pf_gen, prc, prv);
+          else
+            panel_block<false>(sm, acc, Akk, Ct, Tslot, Yunit, Tunit, sub, sub + 1 < nsub, rlo, pf_gen, prc, prv);
+        } else {
+          const int gi = warp / C::RS, rp = warp % C::RS;
+          if (gi < gact && Ct[rp]) store_cols<TB, C::RW>(acc, Ct[rp], col0 + 8 * gi, 0);
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      fence_proxy_async();
+      const int oidx = s_task[5], oval = a.base + s_task[6];
+      if ((s_task[14] >> 8) != 0 && s_task[6] > 1) {  // ordered publication (R25)
+        const int* c = R.ctr + oidx;
+        if (ld_acquire(c) < oval - 1) {
+          const unsigned long long t0w = globaltimer();
+          while (ld_acquire(c) < oval - 1) {
+            __nanosleep(TQR_POLL_NS);
+            if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();
+          }
+        }
+      }
+      const int ocnt = (s_task[15] >> 8) & 0xFF;
+      for (int x = 0; x < (ocnt > 0 ? ocnt : 1); ++x) st_release(R.ctr + oidx + x, oval);
+      if (R.trace) {
+        unsigned long long* tr = R.trace + (size_t)tk * 4;
+        tr[0] = ((unsigned long long)smid() << 32) | (unsigned)tk;
+        tr[1] = t_grab;
+        tr[2] = t_start;
+        tr[3] = globaltimer();
+      }
+    }
+  }
+}
+
+// Off-diagonal SI x SI blocks of the output T_L (SO x SO) of every unit (as ::form_t_kernel,
+// with the reflectors of a unit spanning its two tiles).  One CTA per (unit (i0, k), L).
+__global__ void __launch_bounds__(256) form_t_kernel(const double* __restrict__ A, double* __restrict__ T,
+                                                     const int* __restrict__ units, int nunits, int p) {
+  constexpr int NLO = TB / SO, RC = 64;
+  extern __shared__ double fsm[];
+  double(*U)[SO + 1] = reinterpret_cast<double(*)[SO + 1]>(fsm);
+  double* Z = fsm + RC * (SO + 1);
+  double* tau = Z + SO * SO;
+  double* Tf = fsm;
+  const int L = blockIdx.x % NLO, u = blockIdx.x / NLO;
+  if (u >= nunits) return;
+  const int i0 = units[3 * u], k = units[3 * u + 1], nt = units[3 * u + 2];
+  const bool diag = i0 == k;
+  double* Ts = T + ((size_t)i0 + (size_t)k * p) * (size_t)SO * TB + (size_t)L * SO * SO;
+  const int c0 = L * SO, tid = threadIdx.x;
+  const int a = tid % SO, bg = tid / SO, NBG = 256 / SO;
+  double acc[SO / (256 / SO)];
+#pragma unroll
+  for (int x = 0; x < SO / NBG; ++x) acc[x] = 0.0;
+  const int rows = nt * TB;
+  for (int r0 = diag ? c0 : 0; r0 < rows; r0 += RC) {
+    __syncthreads();
+    for (int e = tid; e < RC * SO; e += 256) {
+      const int rr = e % RC, c = e / RC, r = r0 + rr, gc = c0 + c;
+      double uv = 0.0;
+      if (r < rows) {
+        const double* At = A + ((size_t)(i0 + r / TB) + (size_t)k * p) * TB * TB;
+        const int rt = r % TB;
+        uv = diag ? (rt < gc ? 0.0 : (rt == gc ? 1.0 : At[(size_t)gc * TB + rt])) : At[(size_t)gc * TB + rt];
+      }
+      U[rr][c] = uv;
+    }
+    __syncthreads();
+    for (int rr = 0; rr < RC; ++rr) {
+      const double ua = U[rr][a];
+#pragma unroll
+      for (int x = 0; x < SO / NBG; ++x) acc[x] += ua * U[rr][bg + NBG * x];
+    }
+  }
+#pragma unroll
+  for (int x = 0; x < SO / NBG; ++x) Z[a + (bg + NBG * x) * SO] = acc[x];
+  if (tid < SO) tau[tid] = Ts[(size_t)tid * SO + tid];
+  __syncthreads();
+  if (tid < 32 * ((SO + 31) / 32)) build_t<SO>(Tf, tau, Z);
+  __syncthreads();
+  for (int e = tid; e < SO * SO; e += 256) {
+    const int r = e % SO, c = e / SO;
+    if (r / S < c / S) Ts[e] = Tf[e];
+  }
+}
+}  // namespace tall
+
+cudaError_t launch_exec_tall(const ExecArgs& a, int grid, cudaStream_t st) {
+  constexpr int NDEV = 64;
+  static bool attr[NDEV] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= NDEV || !attr[dev]) {
+    e = cudaFuncSetAttribute(tall::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tall::L::BYTES);
+    if (e != cudaSuccess) return e;
+    if (dev < NDEV) attr[dev] = true;
+  }
+  ExecArgs args = a;
+  void* params[] = {&args};
+  return cudaLaunchCooperativeKernel((const void*)tall::exec_kernel, dim3(grid), dim3(tall::C::NT), params,
+                                     tall::L::BYTES, st);
+}
+int exec_max_ctas_tall(int device) {
+  int per_sm = 0, sms = 0;
+  cudaFuncSetAttribute(tall::exec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tall::L::BYTES);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tall::exec_kernel, tall::C::NT, tall::L::BYTES) !=
+      cudaSuccess)
+    return 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  return per_sm * sms;
+}
+int exec_slice_tall() { return tall::C::SLICE; }
+cudaError_t launch_form_t_tall(const double* A, double* T, const int* d_units, int nunits, int p, cudaStream_t st) {
+  if (nunits == 0) return cudaSuccess;
+  constexpr size_t smem = (size_t)(64 * (tall::SO + 1) + tall::SO * tall::SO + tall::SO) * sizeof(double);
+  cudaError_t e = cudaFuncSetAttribute(tall::form_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  tall::form_t_kernel<<<(unsigned)(nunits * (tall::TB / tall::SO)), 256, smem, st>>>(A, T, d_units, nunits, p);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
 // Instances and dispatch.  (b, s) pairs built: the BASELINE.json configs (64,16),
 // (128,32), (256,32) plus small/test shapes and s == b (the paper's unblocked kernels).
 // ---------------------------------------------------------------------------------------

@@ -353,7 +353,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
                                int rwm = 128, double blq = 0.0, int group = 0, int np = 1, int fine = 0,
                                bool early = false, double lat_remote = 0.0, bool pipe = false,
-                               bool slicedep = true) {
+                               bool slicedep = true, int h = 1) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
@@ -386,8 +386,13 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   const int sw = (b + nsl - 1) / nsl;
   auto blk_sl0 = [&](int l) { return slicedep ? (l * s) / sw : 0; };
   auto blk_nsl = [&](int l) { return slicedep ? ((l + 1) * s - 1) / sw - (l * s) / sw + 1 : nsl; };
-  auto panel = [&](int kind, int k, int i, int cls) {
-    const int ok = own(k), v = i - k + 1;
+  // Units (R30): the tile rows below the diagonal in groups of h starting at k+1;
+  // unit g covers tile rows [k+1+hg, min(p, k+1+h(g+1))) and has chain value v = g + 2 (GEQRT:
+  // 1).  h = 1: the square-tile schedule (unit g = tile row k+1+g, v = i-k+1).  A step-k task
+  // on tile rows up to `il` waits for step k-1's chain on its column up to the unit holding il:
+  auto prevv = [&](int k, int il) { return (il - k) / h + 2; };
+  auto panel = [&](int kind, int k, int i, int il, int v, int cls) {
+    const int ok = own(k);
     for (int l = 0; l < NPT; ++l) {
       if (!split) {  // fused apply + factor per block (R21 without the A/F split)
         int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l, kind == K_G), cls);
@@ -395,7 +400,8 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
         if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk block l: previous tile
         if (l > 0) T.dep(id, PF(k, l - 1), 1, v);
-        if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), i - k + 2);  // block l's columns
+        if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), prevv(k, il));  // block l's columns
+        if (il > i) T.t[id].flags |= 128;
         continue;
       }
       if (l > 0) {
@@ -403,18 +409,20 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
         T.dep(id, PF(k, l - 1), 1, v);                 // this tile's blocks < l factored
         if (v > 1) T.dep(id, PA(k, l), 1, v - 1);      // R_kk rows above block l: previous tile
-        if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), i - k + 2);  // block l's columns
+        if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), prevv(k, il));  // block l's columns
+        if (il > i) T.t[id].flags |= 128;
       }
       int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(kind == K_G), cls);
       T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
       if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
       if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk diagonal block l: previous tile
       if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part (holds block l's slice dependency)
-      else if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(0)), blk_nsl(0), i - k + 2);  // block 0's columns
+      else if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(0)), blk_nsl(0), prevv(k, il));  // block 0's columns
+      if (il > i) T.t[id].flags |= 128;
     }
   };
   for (int k = 0; k < K; ++k) {
-    panel(K_G, k, k, 0);
+    panel(K_G, k, k, k, 1, 0);
     out.counts[0]++;
     // task granularity of step k's updates (R23)
     const bool tail = fine >= 2 && (int64_t)(q - k - 1) * (p - k) * (nsl / np) < 2 * wtot;
@@ -434,25 +442,27 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, 2);
         out.counts[2] += n_;  // counted per register pass (column slice)
       }
-    for (int i = k + 1; i < p; ++i) {
-      // TSQRT(k,i) block l touches only column block l of R_kk (and tile (i,k)): a wavefront
-      // over (i, l) (R21)
-      panel(K_T, k, i, 1);
+    for (int i = k + 1, v = 2; i < p; i += h, ++v) {
+      const int il = (int)std::min<int64_t>(p, (int64_t)i + h) - 1;  // the unit's last tile row
+      // TSQRT(k,unit) block l touches only column block l of R_kk (and the unit's tiles): a
+      // wavefront over (unit, l) (R21)
+      panel(K_T, k, i, il, v, 1);
       out.counts[1]++;
       for (int j = k + 1; j < q; ++j)
         for (int sl = 0; sl < nsl; sl += npj(j)) {
           const int n_ = npj(j);
-          int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), i - k + 1, (n_ == np ? dm : dmf).s,
+          int id = T.add(K_S, k, i, scol(j), sl, COL(k, j, sl), v, (n_ == np ? dm : dmf).s * (il - i + 1),
                          j == k + 1 ? 1 : 3);
+          if (il > i) T.t[id].flags |= 128;
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
           T.t[id].np = n_; T.t[id].ocnt = n_;
           if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + i;
-          T.dep(id, PF(k, NPT - 1), 1, i - k + 1);
+          T.dep(id, PF(k, NPT - 1), 1, v);
           if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
           if (pipe) T.t[id].flags |= 64;             // pipelined panel dependency (R31)
-          T.dep(id, COL(k, j, sl), n_, i - k);
-          if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, i - k + 2);
+          T.dep(id, COL(k, j, sl), n_, v - 1);
+          if (k > 0) T.dep(id, COL(k - 1, j, sl), n_, prevv(k, il));
           out.counts[3] += n_;
         }
     }
@@ -563,6 +573,9 @@ struct tqr_plan {
   cudaStream_t st;
   int G = 1, me = 0;          // job ranks, this process's rank
   bool emulate = false;       // all G ranks in this process, one launch on one device
+  int h = 1;                  // tile rows per TSQRT / SSRFB unit (2: TQR_FLAG_TALL_TILES, R30)
+  int* d_units = nullptr;     // h = 2: the units (i0, k, nt) whose output T blocks form_t completes
+  int nunits = 0;
   bool real = false;          // G > 1, one rank per process / GPU
   int nloc = 1;               // ranks run by this process
   int nctr_max = 0;
@@ -712,7 +725,7 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
   a.phases = P->d_phases;
   if (P->G == 1) {
     a.Yp[0] = reinterpret_cast<double*>(work);
-    a.Tp[0] = a.Yp[0] + (size_t)P->p * P->q * P->prm.b * P->prm.b;
+    a.Tp[0] = a.Yp[0] + (size_t)P->h * P->p * P->q * P->prm.b * P->prm.b;
     a.ctr[0] = P->d_ctr1;
   } else {
     for (int r = 0; r < P->G; ++r) {
@@ -748,7 +761,10 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
   }
   if (P->real) CU(launch_rank_barrier(P->arrive, P->G, P->me, P->gen, P->st));
   const int grid = std::max(nl, std::min(P->workers, std::max(1, total)));
-  CU(launch_exec(P->prm.b, P->prm.s, d.mode, P->rwm, a, grid, P->st));
+  if (P->h > 1)
+    CU(launch_exec_tall(a, grid, P->st));
+  else
+    CU(launch_exec(P->prm.b, P->prm.s, d.mode, P->rwm, a, grid, P->st));
   return TQR_OK;
 }
 
@@ -794,6 +810,7 @@ static void destroy_plan(tqr_plan* P) {
   }
   if (P->d_ctr1) cudaFree(P->d_ctr1);
   if (P->d_octr) cudaFree(P->d_octr);
+  if (P->d_units) cudaFree(P->d_units);
   if (P->d_ticket) cudaFree(P->d_ticket);
   if (P->d_trace) cudaFree(P->d_trace);
   delete P;
@@ -814,6 +831,11 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   if (emulate && p->rank != 0) return bad_arg(8, "emulated multi-rank plans run every rank: rank must be 0");
   if (!exec_supported(p->b, p->s)) {
     g_err = "no kernel instance for this (b, s)";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  const bool tall = (p->flags & TQR_FLAG_TALL_TILES) != 0;
+  if (tall && (p->b != 256 || p->s != 32 || p->nranks != 1)) {
+    g_err = "TQR_FLAG_TALL_TILES is built for b = 256, s = 32 on one rank";
     return TQR_ERR_UNSUPPORTED;
   }
   int ndev = 0;
@@ -839,8 +861,17 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     P->pipe = pol.pipe;
     P->slicedep = pol.slicedep;
   }
+  if (tall) {  // the tall-unit executor: 32-column update passes, A/F-split panels (R30)
+    P->h = 2;
+    P->nsl = p->b / exec_slice_tall();
+    P->passes = 1;
+    P->split = true;
+    P->early = true;
+    P->pipe = false;
+    P->slicedep = false;
+  }
   P->st = (cudaStream_t)p->stream;
-  P->workers = exec_max_ctas(p->b, p->s, P->rwm, p->device);
+  P->workers = tall ? exec_max_ctas_tall(p->device) : exec_max_ctas(p->b, p->s, P->rwm, p->device);
   if (P->workers < P->nloc) {
     destroy_plan(P);
     g_err = "executor does not fit on this device";
@@ -857,7 +888,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
   build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine,
-                     P->early, 0.0, P->pipe, P->slicedep);
+                     P->early, 0.0, P->pipe, P->slicedep, P->h);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -867,6 +898,17 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   tqr_status st = upload(s, local_ranks(P), P->fact);
   if (st != TQR_OK) { destroy_plan(P); return st; }
   if (cudaMalloc(&P->d_ticket, sizeof(int) * MAX_RANKS) != cudaSuccess) { destroy_plan(P); return TQR_ERR_OOM; }
+  if (P->h > 1) {  // units whose output T blocks form_t completes: (k, k, 1) and every TSQRT unit
+    std::vector<int> u;
+    for (int64_t k = 0; k < P->K; ++k) {
+      u.insert(u.end(), {(int)k, (int)k, 1});
+      for (int64_t i = k + 1; i < P->p; i += P->h)
+        u.insert(u.end(), {(int)i, (int)k, (int)(std::min<int64_t>(P->p, i + P->h) - i)});
+    }
+    P->nunits = (int)(u.size() / 3);
+    if (cudaMalloc(&P->d_units, sizeof(int) * u.size()) != cudaSuccess) { destroy_plan(P); return TQR_ERR_OOM; }
+    CU(cudaMemcpy(P->d_units, u.data(), sizeof(int) * u.size(), cudaMemcpyHostToDevice));
+  }
   if (P->G == 1) {
     if (cudaMalloc(&P->d_ctr1, sizeof(int) * (size_t)std::max(1, P->nctr_max)) != cudaSuccess) {
       destroy_plan(P);
@@ -1004,7 +1046,7 @@ tqr_status tqr_tiles_size(const tqr_plan* P, size_t* a, size_t* t) {
 static size_t work_bytes(const tqr_plan* P) {
   if (P->G > 1) return 0;  // multi-rank plans own their (peer-visible) workspace
   const size_t b = (size_t)P->prm.b, s = (size_t)P->prm.s;
-  return ((size_t)P->p * P->q * b * b + (size_t)P->p * P->q * s * b) * sizeof(double);
+  return ((size_t)P->h * P->p * P->q * b * b + (size_t)P->p * P->q * s * b) * sizeof(double);
 }
 tqr_status tqr_workspace_size(const tqr_plan* P, size_t* bytes) {
   if (!P) return bad_arg(1, "plan is NULL");
@@ -1075,7 +1117,9 @@ tqr_status tqr_geqrf(tqr_plan* P, double* At, double* T, void* work) {
   if (tsz) CU(cudaMemsetAsync(T, 0, tsz * sizeof(double), P->st));
   tqr_status st = run(P, P->fact, At, T, nullptr, work, (P->prm.flags & TQR_FLAG_TRACE) != 0);
   if (st != TQR_OK) return st;
-  if (exec_inner(P->prm.b, P->prm.s) != P->prm.s) {
+  if (P->h > 1) {  // the tall-unit executor factors with 16-column internal blocks (R16, R30)
+    CU(launch_form_t_tall(At, T, P->d_units, P->nunits, (int)P->p, P->st));
+  } else if (exec_inner(P->prm.b, P->prm.s) != P->prm.s) {
     int cs, co;
     colmap(P, &cs, &co);
     if (P->emulate || P->G == 1)
@@ -1132,6 +1176,7 @@ static tqr_status orm_sched(tqr_plan* P, bool trans, int64_t nrhs, DevSched** ou
       CU(cudaMemset(nc, 0, sizeof(int) * (size_t)P->nloc * d.nctr));
       CU(cudaStreamSynchronize(P->st));
       if (P->d_octr) cudaFree(P->d_octr);
+  if (P->d_units) cudaFree(P->d_units);
       P->d_octr = nc;
       P->octr_n = d.nctr;
     }
@@ -1185,6 +1230,10 @@ static tqr_status ormqr_impl(tqr_plan* P, char trans, const double* At, const do
   GUARD(P);
   if (P->real && !P->connected) {
     g_err = "multi-rank plan not connected (tqr_comm_export / tqr_comm_connect)";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  if (P->h > 1) {
+    g_err = "apply-Q / form-Q are not built for TQR_FLAG_TALL_TILES plans";
     return TQR_ERR_UNSUPPORTED;
   }
   DevSched* d = nullptr;
@@ -1309,7 +1358,7 @@ tqr_status tqr_plan_records(tqr_plan* P, int32_t local, int32_t* rec, int64_t ca
   return TQR_OK;
 }
 
-tqr_status tqr_plan_info(const tqr_plan* P, int32_t info[12]) {
+tqr_status tqr_plan_info(const tqr_plan* P, int32_t info[16]) {
   if (!P) return bad_arg(1, "plan is NULL");
   if (!info) return bad_arg(2, "info is NULL");
   info[0] = P->rwm;
@@ -1323,7 +1372,10 @@ tqr_status tqr_plan_info(const tqr_plan* P, int32_t info[12]) {
   info[8] = exec_inner(P->prm.b, P->prm.s);
   info[9] = P->G;
   info[10] = P->nloc;
-  info[11] = exec_slice(P->prm.b, P->prm.s, P->rwm);
+  info[11] = P->h > 1 ? exec_slice_tall() : exec_slice(P->prm.b, P->prm.s, P->rwm);
+  info[12] = P->h;
+  info[13] = info[14] = info[15] = 0;
+  if (P->h > 1) info[8] = 16;  // (the tall-unit executor's internal block)
   return TQR_OK;
 }
 
@@ -1364,8 +1416,8 @@ tqr_status tqr_profile_tasks(tqr_plan* P, int32_t kind, int64_t count, double* A
   if (!At) return bad_arg(4, "At is NULL");
   if (!T) return bad_arg(5, "T is NULL");
   if (!work) return bad_arg(6, "work is NULL");
-  if (P->p < 2 || P->q < 2 || P->G > 1) {
-    g_err = "profiling needs a single-rank plan with p >= 2 and q >= 2";
+  if (P->p < 2 || P->q < 2 || P->G > 1 || P->h > 1) {
+    g_err = "profiling needs a single-rank square-tile plan with p >= 2 and q >= 2";
     return TQR_ERR_UNSUPPORTED;
   }
   GUARD(P);

@@ -88,6 +88,16 @@ int exec_inner(int b, int s);
 cudaError_t launch_form_t(const double* A, double* T, int b, int s, int64_t p, int64_t qloc, int cstride, int coff,
                           cudaStream_t st);
 
+// Tall-unit executor (R30: the tile rows below the diagonal in units of two b x b
+// tiles; b = 256, s = 32 only, one rank, factorization only).  Records as for the square
+// executor with [2] = the unit's first tile row and [14] bit 7 = a second tile; the workspace
+// holds 2 b^2 doubles of packed panels per (tile row, step).
+cudaError_t launch_exec_tall(const ExecArgs& a, int grid, cudaStream_t st);
+int exec_max_ctas_tall(int device);
+int exec_slice_tall();  // columns per register pass of its update tasks
+// off-diagonal blocks of the output T_L of the units listed in d_units (3 ints each: i0, k, nt)
+cudaError_t launch_form_t_tall(const double* A, double* T, const int* d_units, int nunits, int p, cudaStream_t st);
+
 // Layout kernels.  Tile-major arrays hold the tile columns j = coff + jl*cstride of the
 // global p x q grid at storage column jl (single GPU / emulation: cstride 1, coff 0).
 cudaError_t launch_pack(const double* A, int64_t lda, double* At, int64_t m, int64_t n, int b, int64_t p,

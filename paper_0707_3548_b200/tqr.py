@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("TQR_LIB") or os.path.join(HERE, "libtqr.so")
 TQR_OK = 0
 TQR_FLAG_TRACE = 1
 TQR_FLAG_EMULATE_RANKS = 2
+TQR_FLAG_TALL_TILES = 4
 TQR_IPC_BLOB_BYTES = 256
 TASK_INTS = 16
 _STATUS = {0: "TQR_OK", 1: "TQR_ERR_INVALID_ARG", 2: "TQR_ERR_CUDA", 3: "TQR_ERR_NCCL", 4: "TQR_ERR_OOM",
@@ -157,10 +158,11 @@ class Plan:
     """
 
     def __init__(self, m: int, n: int, b: int, s: int, device: int = 0, stream=None, trace: bool = False,
-                 nranks: int = 1, rank: int = 0, emulate: bool = False):
+                 nranks: int = 1, rank: int = 0, emulate: bool = False, tall: bool = False):
         """nranks > 1: 1D block-cyclic multi-GPU plan for `rank` (connect it with
         paper_0707_3548_b200.dist.connect), or with emulate=True all nranks ranks in one
-        launch on this device (tile arrays then keep the global layout)."""
+        launch on this device (tile arrays then keep the global layout).  tall=True: the paper's
+        2b x b tiles (TQR_FLAG_TALL_TILES; b = 256, s = 32, one rank, factorization only)."""
         import torch
         self.m, self.n, self.b, self.s = m, n, b, s
         self.p, self.q = -(-m // b), -(-n // b)
@@ -168,7 +170,8 @@ class Plan:
         if stream is None:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
-        flags = (TQR_FLAG_TRACE if trace else 0) | (TQR_FLAG_EMULATE_RANKS if emulate else 0)
+        flags = (TQR_FLAG_TRACE if trace else 0) | (TQR_FLAG_EMULATE_RANKS if emulate else 0) | \
+            (TQR_FLAG_TALL_TILES if tall else 0)
         prm = _Params(m, n, b, s, device, ctypes.c_void_p(stream.cuda_stream), nranks, rank, flags)
         h = _vp()
         _check(lib().tqr_plan_create(ctypes.byref(h), ctypes.byref(prm)))
@@ -277,10 +280,10 @@ class Plan:
 
     def info(self) -> dict:
         """The plan's policy (include/tqr.h tqr_plan_info)."""
-        v = (_i32 * 12)()
+        v = (_i32 * 16)()
         _check(lib().tqr_plan_info(self._h, v))
         keys = ("rwm", "passes", "nsl", "split", "early", "workers", "prio", "fine", "inner", "nranks", "nloc",
-                "slice")
+                "slice", "h")
         return dict(zip(keys, list(v)))
 
     def trace(self, cap: int = 1 << 22):
