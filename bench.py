@@ -333,7 +333,7 @@ def main():
 
     # ---- optional trace of one extra step ----
     if args.trace and rank == 0 and world == 1:
-        tplan = tqr.Plan(m, n, b, s, device=local, stream=stream, trace=True, nranks=G, emulate=G > 1)
+        tplan = tqr.Plan(m, n, b, s, device=local, stream=stream, trace=True, nranks=G, emulate=G > 1, tall=tall)
         tplan.pack(A_dev, At)
         tplan.geqrf(At, T)
         tplan.sync()

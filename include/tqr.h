@@ -191,6 +191,10 @@ tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t wo
  * lets CPU tests replay the distributed protocol. */
 tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, int32_t rank,
                                 int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr);
+/* The same with the tile rows below the diagonal in units of h (1..4; TQR_FLAG_TALL_TILES
+ * uses h = 2): record [2] = a unit's first tile row, [14] bit 7 = a multi-tile unit. */
+tqr_status tqr_schedule_records_h(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks,
+                                  int32_t rank, int32_t h, int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr);
 
 /* Scaling MODEL (not a measurement; pure host): the list-schedule simulation the dispatch order
  * comes from, run for an m x n factorization with the plan policy for (b, s) on `nranks`

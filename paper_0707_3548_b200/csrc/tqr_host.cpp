@@ -1278,7 +1278,8 @@ tqr_status tqr_sync(tqr_plan* P) {
   return TQR_OK;
 }
 
-static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, Sched& s) {
+static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, Sched& s,
+                          int h = 1) {
   g_badarg = 0;
   if (p < 1) return bad_arg(1, "p < 1");
   if (q < 1) return bad_arg(2, "q < 1");
@@ -1289,7 +1290,7 @@ static tqr_status inspect(int64_t p, int64_t q, int32_t nslice, int32_t workers,
   // inspected shapes
   build_factor_sched(p, q, 64 * nslice, 32 * nslice, nslice, std::vector<int>(nranks, workers), nranks > 1,
                      (p + q) % 2 == 0, s, p % 2 == 0 ? PRIO_BLEVEL : PRIO_CLASS, 4000.0, 128, 0.0, false,
-                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3), (p + 2 * q) % 3 != 0, 0.0, (p + q) % 3 != 1);
+                     nslice % 2 == 0 ? 2 : 1, (int)(q % 3), (p + 2 * q) % 3 != 0, 0.0, (p + q) % 3 != 1, true, h);
   if (!s.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
@@ -1309,10 +1310,16 @@ tqr_status tqr_schedule_inspect(int64_t p, int64_t q, int32_t nslice, int32_t wo
 
 tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks, int32_t rank,
                                 int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr) {
+  return tqr_schedule_records_h(p, q, nslice, workers, nranks, rank, 1, rec, cap, n, nctr);
+}
+
+tqr_status tqr_schedule_records_h(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks,
+                                  int32_t rank, int32_t h, int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr) {
   if (rank < 0 || rank >= nranks) return bad_arg(6, "rank outside [0, nranks)");
-  if (!n) return bad_arg(9, "n is NULL");
+  if (h < 1 || h > 4) return bad_arg(7, "h outside [1, 4]");
+  if (!n) return bad_arg(10, "n is NULL");
   Sched s;
-  tqr_status st = inspect(p, q, nslice, workers, nranks, s);
+  tqr_status st = inspect(p, q, nslice, workers, nranks, s, h);
   if (st != TQR_OK) return st;
   const auto& v = s.rec[rank];
   *n = (int64_t)(v.size() / TASK_INTS);

@@ -78,6 +78,8 @@ def lib():
         L.tqr_comm_flags.argtypes = [_vp, _vp]
         L.tqr_schedule_records.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _vp, _i64, ctypes.POINTER(_i64),
                                            ctypes.POINTER(_i32)]
+        L.tqr_schedule_records_h.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64,
+                                             ctypes.POINTER(_i64), ctypes.POINTER(_i32)]
         L.tqr_schedule_model.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, ctypes.c_double,
                                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.tqr_plan_records.argtypes = [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]
@@ -127,15 +129,17 @@ def schedule_inspect(p: int, q: int, nslice: int, workers: int):
     return dict(G=c[0], T=c[1], L=c[2], S=c[3]), ne.value
 
 
-def schedule_records(p: int, q: int, nslice: int, workers: int, nranks: int, rank: int):
+def schedule_records(p: int, q: int, nslice: int, workers: int, nranks: int, rank: int, h: int = 1):
     """Dispatch records (numpy int32 (ntasks, 16)) of `rank` in the nranks-rank factorization
-    schedule, and that rank's counter count (pure host; include/tqr.h)."""
+    schedule, and that rank's counter count (pure host; include/tqr.h); h: tile rows per
+    TSQRT / SSRFB unit."""
     import numpy as np
     n, nc = _i64(), _i32()
-    _check(lib().tqr_schedule_records(p, q, nslice, workers, nranks, rank, None, 0, ctypes.byref(n), ctypes.byref(nc)))
+    _check(lib().tqr_schedule_records_h(p, q, nslice, workers, nranks, rank, h, None, 0, ctypes.byref(n),
+                                        ctypes.byref(nc)))
     rec = np.zeros((max(1, n.value), TASK_INTS), dtype=np.int32)
-    _check(lib().tqr_schedule_records(p, q, nslice, workers, nranks, rank, rec.ctypes.data, n.value, ctypes.byref(n),
-                                      ctypes.byref(nc)))
+    _check(lib().tqr_schedule_records_h(p, q, nslice, workers, nranks, rank, h, rec.ctypes.data, n.value,
+                                        ctypes.byref(n), ctypes.byref(nc)))
     return rec[: n.value], nc.value
 
 

@@ -258,6 +258,27 @@ def test_phased_adversarial_replay(L, p, q, nsl, G, workers):
                     assert sim.ctr[r][k * 3 * NPT + l_] == max(1, p - k)
 
 
+@pytest.mark.parametrize("p,q,nsl,G,workers,h", [(9, 4, 2, 1, 5, 2), (12, 5, 1, 1, 7, 2), (11, 6, 2, 2, 4, 2),
+                                                 (10, 3, 1, 1, 3, 3)])
+def test_phased_replay_tall_units(L, p, q, nsl, G, workers, h):
+    """Units of h tile rows (TQR_FLAG_TALL_TILES, DESIGN.md R30): the same adversarial replay;
+    every step's panel chain ends at 1 + (number of units), and the ranks' tasks are exactly
+    the single-rank unit DAG."""
+    per_rank = [L.schedule_records(p, q, nsl, workers, G, r, h=h) for r in range(G)]
+    single, _ = L.schedule_records(p, q, nsl, workers, 1, 0, h=h)
+    ref = sorted(key for rec in single for key in _task_keys(rec, 1, 0))
+    keys = sorted(key for r, (recs, _) in enumerate(per_rank) for rec in recs for key in _task_keys(rec, G, r))
+    assert keys == ref
+    assert any(int(rec[14]) & 128 for rec in single)  # two-tile units present
+    for seed in range(2):
+        sim = PhasedSim(per_rank, G, workers, ordered=True, seed=seed)
+        sim.run()
+        for r in range(G):
+            for k in range(min(p, q)):
+                for l_ in range(NPT):
+                    assert sim.ctr[r][k * 3 * NPT + l_] == 1 + -(-(p - k - 1) // h)
+
+
 def test_phased_replay_detects_unordered_publication(L):
     """Negative check: without the ordered publication, the adversarial order makes PF(k,l)
     jump (a consumer of PF >= v would read tile i's Y_l / T_l before they are stored)."""
