@@ -909,7 +909,8 @@ __global__ void __launch_bounds__(C::NT, 1) exec_kernel(const __grid_constant__ 
     }
     __syncthreads();
     if (R.trace && tid == 0) t_start = globaltimer();
-    const int kind = s_task[0], k = s_task[1], i0 = s_task[2], j = s_task[3], sl = s_task[4];
+    const int kind = s_task[0], k = s_task[1], i0 = s_task[2], j = s_task[3];
+    const int sl = s_task[4] & 0xFF, lsub = (s_task[4] >> 8) - 1;  // apply sub-task: output block lsub
     const bool two = (s_task[14] & 128) != 0;
     {
       const bool panel = kind == K_G || kind == K_T;
@@ -934,8 +935,8 @@ __global__ void __launch_bounds__(C::NT, 1) exec_kernel(const __grid_constant__ 
           Ct[0] = ts ? tile_ptr(R.A, i0, k, p, TB) : Akk;
           Ct[1] = ts && two ? tile_ptr(R.A, i0 + 1, k, p, TB) : nullptr;
           col0 = sub * S;
-          nb = a_part ? sub0 : sub;
-          lb0 = f_part ? sub0 : 0;
+          nb = a_part ? (lsub >= 0 ? (lsub + 1) * SPT : sub0) : sub;  // (apply sub-task: blocks of lsub)
+          lb0 = f_part ? sub0 : (lsub >= 0 ? lsub * SPT : 0);
           gact = S / 8;
         } else {
           C1 = lkind ? nullptr : tile_ptr(R.A, k, j, p, TB);

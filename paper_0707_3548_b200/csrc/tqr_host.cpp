@@ -378,6 +378,14 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   };
   out.nctr.assign(G, 0);
   for (int r = 0; r < G; ++r) out.nctr[r] = K * 3 * NPT + (int)((int64_t)K * qloc(r) * nsl);
+  // Split apply parts (units of h > 1 tile rows, R30): A(k,u,l) becomes one sub-task
+  // per earlier output block lp, A(k,u,l,lp); PA2(k,l,lp) counts them over the units (owner only)
+  const bool asplit = h > 1 && split;
+  auto PA2 = [&](int k, int l, int lp) {
+    return K * 3 * NPT + (int)((int64_t)K * qloc(own(k)) * nsl) + (k * NPT + l) * NPT + lp;
+  };
+  if (asplit)
+    for (int r = 0; r < G; ++r) out.nctr[r] += K * NPT * NPT;
   // One panel task on tile (i,k) block l in two parts: A (apply this tile's blocks < l to
   // block l's columns: touches the rows of R_kk ABOVE the diagonal block) and F (factor: the
   // diagonal block).  A(k,i+1,l) may overlap F(k,i,l), which halves the TSQRT chain's step.
@@ -404,7 +412,21 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         if (il > i) T.t[id].flags |= 128;
         continue;
       }
-      if (l > 0) {
+      if (l > 0 && asplit) {
+        // one apply sub-task per earlier output block lp (record [4] = l | (lp + 1) << 8):
+        // A(k,u,l,lp) <- F(k,u,lp), A(k,u,l,lp-1), A(k,u-1,l,lp) (R_kk rows of block lp in
+        // block l's columns) -- the unit chain of each stage is one block apply long
+        for (int lp = 0; lp < l; ++lp) {
+          int id = T.add(kind, k, i, scol(k), l | ((lp + 1) << 8), PA2(k, l, lp), v, dm.apply_part(1), cls);
+          T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
+          T.t[id].key[3] = l * NPT + lp;
+          T.dep(id, PF(k, lp), 1, v);                            // block lp of this unit factored
+          if (lp > 0) T.dep(id, PA2(k, l, lp - 1), 1, v);        // block l's columns: previous sub-apply
+          if (v > 1) T.dep(id, PA2(k, l, lp), 1, v - 1);         // R_kk rows of block lp: previous unit
+          if (lp == 0 && k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), prevv(k, il));
+          if (il > i) T.t[id].flags |= 128;
+        }
+      } else if (l > 0) {
         int id = T.add(kind, k, i, scol(k), l, PA(k, l), v, dm.apply_part(l), cls);
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
         T.dep(id, PF(k, l - 1), 1, v);                 // this tile's blocks < l factored
@@ -416,7 +438,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
       T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
       if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
       if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk diagonal block l: previous tile
-      if (l > 0) T.dep(id, PA(k, l), 1, v);            // own apply part (holds block l's slice dependency)
+      if (l > 0) T.dep(id, asplit ? PA2(k, l, l - 1) : PA(k, l), 1, v);  // own apply part(s)
       else if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(0)), blk_nsl(0), prevv(k, il));  // block 0's columns
       if (il > i) T.t[id].flags |= 128;
     }

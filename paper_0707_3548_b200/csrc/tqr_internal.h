@@ -90,7 +90,8 @@ cudaError_t launch_form_t(const double* A, double* T, int b, int s, int64_t p, i
 
 // Tall-unit executor (R30: the tile rows below the diagonal in units of two b x b
 // tiles; b = 256, s = 32 only, one rank, factorization only).  Records as for the square
-// executor with [2] = the unit's first tile row and [14] bit 7 = a second tile; the workspace
+// executor with [2] = the unit's first tile row, [14] bit 7 = a second tile and, for the split
+// apply parts, [4] = l | (lp + 1) << 8 (apply output block lp to block l's columns); the workspace
 // holds 2 b^2 doubles of packed panels per (tile row, step).
 cudaError_t launch_exec_tall(const ExecArgs& a, int grid, cudaStream_t st);
 int exec_max_ctas_tall(int device);

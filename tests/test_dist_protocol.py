@@ -259,7 +259,8 @@ def test_phased_adversarial_replay(L, p, q, nsl, G, workers):
 
 
 @pytest.mark.parametrize("p,q,nsl,G,workers,h", [(9, 4, 2, 1, 5, 2), (12, 5, 1, 1, 7, 2), (11, 6, 2, 2, 4, 2),
-                                                 (10, 3, 1, 1, 3, 3)])
+                                                 (10, 3, 1, 1, 3, 3), (10, 4, 2, 1, 6, 2), (12, 6, 2, 2, 4, 2),
+                                                 (13, 5, 1, 1, 3, 2)])
 def test_phased_replay_tall_units(L, p, q, nsl, G, workers, h):
     """Units of h tile rows (TQR_FLAG_TALL_TILES, DESIGN.md R30): the same adversarial replay;
     every step's panel chain ends at 1 + (number of units), and the ranks' tasks are exactly

@@ -8,7 +8,7 @@ import numpy as np
 d = json.load(open(sys.argv[1]))
 r = np.array(d["records"], dtype=np.int64)
 kind, k, i, j, slf, sm, st, en = r.T
-sl = slf & 0xFFFF  # slice | task flags << 16 (tqr_trace_fetch)
+sl = slf & 0xFF  # slice (low byte; tall apply sub-tasks carry lp + 1 in bits 8..15) | task flags << 16
 t0 = st.min()
 st = (st - t0) / 1e3
 en = (en - t0) / 1e3
