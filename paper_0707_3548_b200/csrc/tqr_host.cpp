@@ -767,8 +767,10 @@ static tqr_status run(tqr_plan* P, const DevSched& d, double* A, double* T, doub
     P->trace_valid = true;
   }
   const std::vector<int> lr = local_ranks(P);
-  if (ctr_local)
+  if (ctr_local) {
     for (int li = 0; li < nl; ++li) a.ctr[P->G == 1 ? 0 : lr[li]] = ctr_local[li];
+    a.nctr = P->octr_n;  // (TQR_CHECKS bounds: the rank-local apply-Q counter arrays)
+  }
   for (int li = 0; li < nl; ++li) {
     RankLocal& R = a.loc[li];
     R.tasks = d.d_tasks[li];
