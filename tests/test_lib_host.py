@@ -73,3 +73,22 @@ def test_invalid_args_without_gpu(L):
     assert lib.tqr_status_string(0) == b"TQR_OK"
     assert L.supported(256, 32) and L.supported(128, 32) and L.supported(64, 16)
     assert not L.supported(48, 16)
+
+
+def test_scaling_model_properties(L):
+    """tqr_schedule_model (a MODEL of the multi-GPU schedule): splitting a
+    grid over more GPUs never makes the modelled time longer than the 1-GPU time, efficiency
+    T1 / (G TG) stays <= 1, remote-edge latency only adds time, and the modelled utilisation is
+    a fraction."""
+    m = n = 4096
+    t1, busy1 = L.schedule_model(m, n, 128, 32, 1, 148, 0.0)
+    assert 0.0 < busy1 <= 1.0 and t1 > 0.0
+    for G in (2, 4):
+        tg, busy = L.schedule_model(m, n, 128, 32, G, 148, 3000.0)
+        assert tg <= t1 * 1.02 and t1 / (G * tg) <= 1.0 + 1e-9 and 0.0 < busy <= 1.0
+        slow, _ = L.schedule_model(m, n, 128, 32, G, 148, 50000.0)
+        assert slow >= tg
+    # a big square grid scales: 2 GPUs model at least 1.6x faster than 1
+    t1b, _ = L.schedule_model(8192, 8192, 128, 32, 1, 148, 3000.0)
+    t2b, _ = L.schedule_model(8192, 8192, 128, 32, 2, 148, 3000.0)
+    assert t1b / t2b > 1.6
