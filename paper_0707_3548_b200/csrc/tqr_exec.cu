@@ -33,6 +33,9 @@ struct Feat {
   static constexpr bool PIPE = B <= 128;      // pipelined panel dependency (R31)
   static constexpr bool TBLOCKED = B <= 128;  // T_l by 8 x 8 DMMA blocks (R26)
 };
+#ifndef TQR_PANEL_NEXT  // panel tasks take their successor ticket before factoring (section 5)
+#define TQR_PANEL_NEXT 1
+#endif
 #ifndef TQR_RELEASE_FENCE
 #define TQR_RELEASE_FENCE 1
 #endif
@@ -618,6 +621,18 @@ __global__ void __launch_bounds__(Cfg<B, Inner<B, SO>::SI, RWM>::NT, 1) exec_ker
         }
         update_phase<B, S, RWM, MODE != 2, MODE == 2>(sm, acc, Ypt, Tps, lb0, nb, C1, Ct, col0, gact, pf, keep, pd);
         if (panel) PH_MARK(7); else PH_MARK(4);
+        if (TQR_PANEL_NEXT && panel && sub == nsub - 1 && tid == 0 && next_tk < 0) {
+          // a panel task's last block: take the next ticket and fetch its record now, so both
+          // round trips overlap the factorization (update tasks do this half-way through their
+          // last pass); holding it early cannot deadlock (every wait is on a smaller ticket)
+          next_tk = atomicAdd(R.ticket, 1);
+          if (next_tk < R.ntasks) {
+#pragma unroll
+            for (int x = 0; x < TASK_INTS; x += 4) cp_async16(s_next + x, R.tasks + (size_t)next_tk * TASK_INTS + x);
+            cp_async_commit();
+            rec_for = next_tk;
+          }
+        }
         if (a_part) {
           if (warp / Cfg<B, S, RWM>::RS < gact)
             store_cols<B, Cfg<B, S, RWM>::RW>(acc, Ct, col0 + 8 * (warp / Cfg<B, S, RWM>::RS),
@@ -970,6 +985,15 @@ __global__ void __launch_bounds__(C::NT, 1) exec_kernel(const __grid_constant__ 
           }
         };
         update_phase(sm, acc, Yunit, Tunit, lb0, nb, C1, Ct, col0, gact, pf);
+        if (TQR_PANEL_NEXT && panel && sub == nsub - 1 && tid == 0 && next_tk < 0) {  // (as ::exec_kernel)
+          next_tk = atomicAdd(R.ticket, 1);
+          if (next_tk < R.ntasks) {
+#pragma unroll
+            for (int x = 0; x < TASK_INTS; x += 4) cp_async16(s_next + x, R.tasks + (size_t)next_tk * TASK_INTS + x);
+            cp_async_commit();
+            rec_for = next_tk;
+          }
+        }
         if (a_part) {
           const int gi = warp / C::RS, rp = warp % C::RS;
           if (gi < gact && Ct[rp]) store_cols<TB, C::RW>(acc, Ct[rp], col0 + 8 * gi, 0);
