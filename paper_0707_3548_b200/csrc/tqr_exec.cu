@@ -34,7 +34,7 @@ struct Feat {
   static constexpr bool TBLOCKED = B <= 128;  // T_l by 8 x 8 DMMA blocks (R26)
 };
 #ifndef TQR_PANEL_NEXT  // panel tasks take their successor ticket before factoring (section 5)
-#define TQR_PANEL_NEXT 1
+#define TQR_PANEL_NEXT 0  // (measured: C2 +1.4%, C4 -0.1%: off)
 #endif
 #ifndef TQR_RELEASE_FENCE
 #define TQR_RELEASE_FENCE 1
@@ -996,7 +996,21 @@ __global__ void __launch_bounds__(C::NT, 1) exec_kernel(const __grid_constant__ 
         }
         if (a_part) {
           const int gi = warp / C::RS, rp = warp % C::RS;
-          if (gi < gact && Ct[rp]) store_cols<TB, C::RW>(acc, Ct[rp], col0 + 8 * gi, 0);
+          if (gi < gact && Ct[rp]) {
+            if (!ts && lsub >= 0) {
+              // a GEQRT apply sub-task changes only rows >= lsub*SO of block l's columns (U is zero
+              // above): store only those -- the TSQRT sub-applies of unit 0 already update R_kk's
+              // rows of earlier blocks in these columns while this sub-task runs
+              const int rmin = lsub * SO;
+              double2* col = reinterpret_cast<double2*>(Ct[rp] + (size_t)(col0 + 8 * gi + (lane >> 2)) * TB +
+                                                        2 * (lane & 3));
+#pragma unroll
+              for (int t = 0; t < C::RW / 8; ++t)
+                if (8 * t >= rmin) __stcg(col + 4 * t, make_double2(acc[t][0], acc[t][1]));
+            } else {
+              store_cols<TB, C::RW>(acc, Ct[rp], col0 + 8 * gi, 0);
+            }
+          }
         } else if (panel) {
           const int rlo = f_part ? sub0 * S : 0;
           const int pr = (s_task[14] >> 8) - 1;
