@@ -195,6 +195,18 @@ tqr_status tqr_schedule_records(int64_t p, int64_t q, int32_t nslice, int32_t wo
  * uses h = 2): record [2] = a unit's first tile row, [14] bit 7 = a multi-tile unit. */
 tqr_status tqr_schedule_records_h(int64_t p, int64_t q, int32_t nslice, int32_t workers, int32_t nranks,
                                   int32_t rank, int32_t h, int32_t* rec, int64_t cap, int64_t* n, int32_t* nctr);
+/* The factorization records a plan for (m, n, b, s, nranks, flags) would execute on `rank`
+ * with `workers` CTAs per rank (the plan policy -- tile columns 1D block-cyclic for nranks > 1,
+ * TQR_FLAG_TALL_TILES selects the tall-unit executor's schedule; pure host, no device): for
+ * footprint / race checks of the production schedules (tests/test_race_model.py).  *ntask =
+ * task count, up to `cap` records copied to host `rec` (may be NULL); *nctr = the rank's
+ * counter count; info (may be NULL) = {panel blocks per tile b/s, columns per register pass,
+ * register passes per tile, tile rows per unit}.  TQR_ERR_INVALID_ARG: 1 m, 2 n, 3 (b, s)
+ * without a kernel instance, 5 nranks, 6 rank, 7 workers, 8 tall flag off its (256, 32, 1 rank)
+ * instance, 11 ntask NULL. */
+tqr_status tqr_schedule_records_policy(int64_t m, int64_t n, int32_t b, int32_t s, int32_t nranks, int32_t rank,
+                                       int32_t workers, uint32_t flags, int32_t* rec, int64_t cap, int64_t* ntask,
+                                       int32_t* nctr, int32_t info[4]);
 
 /* Scaling MODEL (not a measurement; pure host): the list-schedule simulation the dispatch order
  * comes from, run for an m x n factorization with the plan policy for (b, s) on `nranks`

@@ -638,9 +638,20 @@ struct Policy {
   bool split = true, early = true, pipe = true, slicedep = true;
   int group = 0;
   double lat = 4000.0, blq = 0.0;
+  int h = 1;  // tile rows per TSQRT / SSRFB unit
 };
-static Policy make_policy(int64_t p, int64_t q, int b, int s) {
+static Policy make_policy(int64_t p, int64_t q, int b, int s, bool tall_tiles = false) {
   Policy P;
+  if (tall_tiles) {  // the tall-unit executor: 32-column update passes, A/F-split panels (R30)
+    P.h = 2;
+    P.nsl = b / exec_slice_tall();
+    P.passes = 1;
+    P.split = true;
+    P.early = true;
+    P.pipe = false;
+    P.slicedep = false;
+    return P;
+  }
   const bool tall = p >= 4 * q;
   P.rwm = (b >= 256 && !tall) ? 256 : 128;
   P.passes = b >= 256 ? (128 / exec_slice(b, s, P.rwm)) : 1;  // 128-column tasks
@@ -878,21 +889,13 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   P->real = P->G > 1 && !emulate;
   P->nloc = emulate ? P->G : 1;
   {
-    const Policy pol = make_policy(P->p, P->q, p->b, p->s);
+    const Policy pol = make_policy(P->p, P->q, p->b, p->s, tall);
     P->rwm = pol.rwm; P->passes = pol.passes; P->nsl = pol.nsl; P->fine = pol.fine; P->split = pol.split;
     P->early = pol.early; P->group = pol.group; P->prio = pol.prio; P->orm_prio = pol.orm_prio; P->lat = pol.lat;
     P->blq = pol.blq;
     P->pipe = pol.pipe;
     P->slicedep = pol.slicedep;
-  }
-  if (tall) {  // the tall-unit executor: 32-column update passes, A/F-split panels (R30)
-    P->h = 2;
-    P->nsl = p->b / exec_slice_tall();
-    P->passes = 1;
-    P->split = true;
-    P->early = true;
-    P->pipe = false;
-    P->slicedep = false;
+    P->h = pol.h;
   }
   P->st = (cudaStream_t)p->stream;
   P->workers = tall ? exec_max_ctas_tall(p->device) : exec_max_ctas(p->b, p->s, P->rwm, p->device);
@@ -1349,6 +1352,42 @@ tqr_status tqr_schedule_records_h(int64_t p, int64_t q, int32_t nslice, int32_t 
   *n = (int64_t)(v.size() / TASK_INTS);
   if (nctr) *nctr = s.nctr[rank];
   if (rec) std::memcpy(rec, v.data(), sizeof(int32_t) * (size_t)std::min<int64_t>(cap, *n) * TASK_INTS);
+  return TQR_OK;
+}
+
+tqr_status tqr_schedule_records_policy(int64_t m, int64_t n, int32_t b, int32_t s, int32_t nranks, int32_t rank,
+                                       int32_t workers, uint32_t flags, int32_t* rec, int64_t cap, int64_t* ntask,
+                                       int32_t* nctr, int32_t info[4]) {
+  g_badarg = 0;
+  if (m < 1) return bad_arg(1, "m < 1");
+  if (n < 1) return bad_arg(2, "n < 1");
+  if (!exec_supported(b, s)) return bad_arg(3, "no kernel instance for (b, s)");
+  if (nranks < 1 || nranks > MAX_RANKS) return bad_arg(5, "nranks outside [1, 8]");
+  if (rank < 0 || rank >= nranks) return bad_arg(6, "rank outside [0, nranks)");
+  if (workers < 1) return bad_arg(7, "workers < 1");
+  const bool tall = (flags & TQR_FLAG_TALL_TILES) != 0;
+  if (tall && (b != 256 || s != 32 || nranks != 1)) return bad_arg(8, "TQR_FLAG_TALL_TILES: b = 256, s = 32, one rank");
+  if (!ntask) return bad_arg(11, "ntask is NULL");
+  const int64_t p = (m + b - 1) / b, q = (n + b - 1) / b;
+  const Policy pol = make_policy(p, q, b, s, tall);
+  Sched sc;
+  build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
+                     pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, 0.0, pol.pipe,
+                     pol.slicedep, pol.h);
+  if (!sc.topo_ok) {
+    g_err = "schedule is not a topological order";
+    return TQR_ERR_UNSUPPORTED;
+  }
+  const auto& v = sc.rec[rank];
+  *ntask = (int64_t)(v.size() / TASK_INTS);
+  if (nctr) *nctr = sc.nctr[rank];
+  if (info) {
+    info[0] = b / s;                                                  // panel blocks per tile
+    info[1] = tall ? exec_slice_tall() : exec_slice(b, s, pol.rwm);   // columns per register pass
+    info[2] = pol.nsl;
+    info[3] = pol.h;
+  }
+  if (rec) std::memcpy(rec, v.data(), sizeof(int32_t) * (size_t)std::min<int64_t>(cap, *ntask) * TASK_INTS);
   return TQR_OK;
 }
 

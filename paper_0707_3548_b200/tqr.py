@@ -80,6 +80,8 @@ def lib():
                                            ctypes.POINTER(_i32)]
         L.tqr_schedule_records_h.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _i32, _vp, _i64,
                                              ctypes.POINTER(_i64), ctypes.POINTER(_i32)]
+        L.tqr_schedule_records_policy.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, _i32, ctypes.c_uint32, _vp,
+                                                  _i64, ctypes.POINTER(_i64), ctypes.POINTER(_i32), _vp]
         L.tqr_schedule_model.argtypes = [_i64, _i64, _i32, _i32, _i32, _i32, ctypes.c_double,
                                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double)]
         L.tqr_plan_records.argtypes = [_vp, _i32, _vp, _i64, ctypes.POINTER(_i64)]
@@ -141,6 +143,23 @@ def schedule_records(p: int, q: int, nslice: int, workers: int, nranks: int, ran
     _check(lib().tqr_schedule_records_h(p, q, nslice, workers, nranks, rank, h, rec.ctypes.data, n.value,
                                         ctypes.byref(n), ctypes.byref(nc)))
     return rec[: n.value], nc.value
+
+
+def schedule_records_policy(m: int, n: int, b: int, s: int, nranks: int = 1, rank: int = 0, workers: int = 148,
+                            tall: bool = False):
+    """The records a plan for (m, n, b, s) would execute on `rank` (production policy; pure host;
+    include/tqr.h tqr_schedule_records_policy): (records (ntasks, 16) int32, counter count,
+    (panel blocks per tile, columns per register pass, passes per tile, tile rows per unit))."""
+    import numpy as np
+    n_, nc = _i64(), _i32()
+    info = (ctypes.c_int32 * 4)()
+    fl = TQR_FLAG_TALL_TILES if tall else 0
+    _check(lib().tqr_schedule_records_policy(m, n, b, s, nranks, rank, workers, fl, None, 0, ctypes.byref(n_),
+                                             ctypes.byref(nc), info))
+    rec = np.zeros((max(1, n_.value), TASK_INTS), dtype=np.int32)
+    _check(lib().tqr_schedule_records_policy(m, n, b, s, nranks, rank, workers, fl, rec.ctypes.data, n_.value,
+                                             ctypes.byref(n_), ctypes.byref(nc), None))
+    return rec[: n_.value], nc.value, tuple(info)
 
 
 def schedule_model(m: int, n: int, b: int, s: int, nranks: int = 1, workers: int = 148, remote_ns: float = 0.0):
