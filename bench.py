@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", default="", help="write a per-task execution trace (JSON) of one extra step")
+    ap.add_argument("--schedule", default="critical", choices=["critical", "locality"],
+                    help="locality: TQR_FLAG_LOCALITY dispatch order (DESIGN.md R22)")
     ap.add_argument("--tiles", default="square", choices=["square", "2bxb"],
                     help="2bxb: the paper's non-square 2b x b tiles (TQR_FLAG_TALL_TILES, DESIGN.md R30)")
     ap.add_argument("--emulate-ranks", type=int, default=1,
@@ -194,7 +196,7 @@ def main():
     stream = torch.cuda.Stream()
     tall = args.tiles == "2bxb"
     plan = tqr.Plan(m, n, b, s, device=local, stream=stream, nranks=G, rank=rank if world > 1 else 0,
-                    emulate=world == 1 and G > 1, tall=tall)
+                    emulate=world == 1 and G > 1, tall=tall, locality=args.schedule == "locality")
     if world > 1:
         tdist.connect(plan)   # one-time CUDA IPC blob exchange
     A_host = tqr_inputs.make(m, n, cfg["dist"], cfg["seed"])                  # one matrix, every rank
@@ -401,7 +403,8 @@ def main():
                    "l2": (f"inputs {m * n * 8 / 2**30:.1f} GiB > 126 MB L2; no flush between steps"
                           if m * n * 8 > (1 << 28) else "inputs smaller than L2 (not flushed)"),
                    "step": "pack + geqrf (persistent DAG executor) + get_r",
-                   "tiles": "2b x b (TQR_FLAG_TALL_TILES)" if tall else "b x b"},
+                   "tiles": "2b x b (TQR_FLAG_TALL_TILES)" if tall else "b x b",
+                   "schedule": "locality (TQR_FLAG_LOCALITY)" if args.schedule == "locality" else "critical path"},
         "pct_of_fp64_peak": 100.0 * value / (world * FP64_PEAK_TFLOPS * 1e3),
         "executed_gflops": flops_exec / (ms * 1e-3) / 1e9,
         "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",

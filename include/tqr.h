@@ -75,6 +75,13 @@ typedef struct {
                                       R differs in row signs / rounding.  Built for b = 256, s = 32,
                                       one rank, factorization (tqr_geqrf, tqr_get_r) only;
                                       TQR_ERR_UNSUPPORTED otherwise. */
+#define TQR_FLAG_LOCALITY 8u       /* locality-aware dispatch ("Enforcing data
+                                      locality"; R22): the update tasks that apply one
+                                      reflector panel (k, i) share one priority so they run together
+                                      and read the panel from L2 (about half the DRAM reads at C3),
+                                      except in the last quarter of the steps, where the critical
+                                      path decides.  Same results bit for bit (dispatch order only);
+                                      square tiles, factorization schedule. */
 
 /* ---- plan -------------------------------------------------------------------------- */
 /* Validates p (argument 2's fields: m=1, n=2, b=3, s=4, device=5, nranks=7, rank=8 are

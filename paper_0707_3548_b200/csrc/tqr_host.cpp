@@ -640,7 +640,7 @@ struct Policy {
   double lat = 4000.0, blq = 0.0;
   int h = 1;  // tile rows per TSQRT / SSRFB unit
 };
-static Policy make_policy(int64_t p, int64_t q, int b, int s, bool tall_tiles = false) {
+static Policy make_policy(int64_t p, int64_t q, int b, int s, bool tall_tiles = false, bool locality = false) {
   Policy P;
   if (tall_tiles) {  // the tall-unit executor: 32-column update passes, A/F-split panels (R30)
     P.h = 2;
@@ -662,6 +662,7 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s, bool tall_tiles = 
   // the per-slice dependencies cost C3 0.3% and C4 0.5% (their dispatch order)
   P.pipe = b <= 128;
   P.slicedep = false;  // (C2: 6.749 vs 6.756 ms without; C3 +0.3%, C4 +0.5% with)
+  if (locality) P.group = 3;  // TQR_FLAG_LOCALITY: panel groups, not in the last quarter (R22)
   if (const char* e = getenv("TQR_DEV_PASSES")) P.passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P.split = atoi(e) != 0;
   if (const char* e = getenv("TQR_DEV_RW")) P.rwm = atoi(e);
@@ -889,7 +890,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
   P->real = P->G > 1 && !emulate;
   P->nloc = emulate ? P->G : 1;
   {
-    const Policy pol = make_policy(P->p, P->q, p->b, p->s, tall);
+    const Policy pol = make_policy(P->p, P->q, p->b, p->s, tall, (p->flags & TQR_FLAG_LOCALITY) != 0);
     P->rwm = pol.rwm; P->passes = pol.passes; P->nsl = pol.nsl; P->fine = pol.fine; P->split = pol.split;
     P->early = pol.early; P->group = pol.group; P->prio = pol.prio; P->orm_prio = pol.orm_prio; P->lat = pol.lat;
     P->blq = pol.blq;
@@ -1369,7 +1370,7 @@ tqr_status tqr_schedule_records_policy(int64_t m, int64_t n, int32_t b, int32_t 
   if (tall && (b != 256 || s != 32 || nranks != 1)) return bad_arg(8, "TQR_FLAG_TALL_TILES: b = 256, s = 32, one rank");
   if (!ntask) return bad_arg(11, "ntask is NULL");
   const int64_t p = (m + b - 1) / b, q = (n + b - 1) / b;
-  const Policy pol = make_policy(p, q, b, s, tall);
+  const Policy pol = make_policy(p, q, b, s, tall, (flags & TQR_FLAG_LOCALITY) != 0);
   Sched sc;
   build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
                      pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, 0.0, pol.pipe,

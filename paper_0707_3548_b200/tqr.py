@@ -16,6 +16,7 @@ TQR_OK = 0
 TQR_FLAG_TRACE = 1
 TQR_FLAG_EMULATE_RANKS = 2
 TQR_FLAG_TALL_TILES = 4
+TQR_FLAG_LOCALITY = 8
 TQR_IPC_BLOB_BYTES = 256
 TASK_INTS = 16
 _STATUS = {0: "TQR_OK", 1: "TQR_ERR_INVALID_ARG", 2: "TQR_ERR_CUDA", 3: "TQR_ERR_NCCL", 4: "TQR_ERR_OOM",
@@ -146,14 +147,14 @@ def schedule_records(p: int, q: int, nslice: int, workers: int, nranks: int, ran
 
 
 def schedule_records_policy(m: int, n: int, b: int, s: int, nranks: int = 1, rank: int = 0, workers: int = 148,
-                            tall: bool = False):
+                            tall: bool = False, locality: bool = False):
     """The records a plan for (m, n, b, s) would execute on `rank` (production policy; pure host;
     include/tqr.h tqr_schedule_records_policy): (records (ntasks, 16) int32, counter count,
     (panel blocks per tile, columns per register pass, passes per tile, tile rows per unit))."""
     import numpy as np
     n_, nc = _i64(), _i32()
     info = (ctypes.c_int32 * 4)()
-    fl = TQR_FLAG_TALL_TILES if tall else 0
+    fl = (TQR_FLAG_TALL_TILES if tall else 0) | (TQR_FLAG_LOCALITY if locality else 0)
     _check(lib().tqr_schedule_records_policy(m, n, b, s, nranks, rank, workers, fl, None, 0, ctypes.byref(n_),
                                              ctypes.byref(nc), info))
     rec = np.zeros((max(1, n_.value), TASK_INTS), dtype=np.int32)
@@ -181,11 +182,13 @@ class Plan:
     """
 
     def __init__(self, m: int, n: int, b: int, s: int, device: int = 0, stream=None, trace: bool = False,
-                 nranks: int = 1, rank: int = 0, emulate: bool = False, tall: bool = False):
+                 nranks: int = 1, rank: int = 0, emulate: bool = False, tall: bool = False,
+                 locality: bool = False):
         """nranks > 1: 1D block-cyclic multi-GPU plan for `rank` (connect it with
         paper_0707_3548_b200.dist.connect), or with emulate=True all nranks ranks in one
         launch on this device (tile arrays then keep the global layout).  tall=True: the paper's
-        2b x b tiles (TQR_FLAG_TALL_TILES; b = 256, s = 32, one rank, factorization only)."""
+        2b x b tiles (TQR_FLAG_TALL_TILES; b = 256, s = 32, one rank, factorization only).
+        locality=True: the locality-aware dispatch order (TQR_FLAG_LOCALITY, R22)."""
         import torch
         self.m, self.n, self.b, self.s = m, n, b, s
         self.p, self.q = -(-m // b), -(-n // b)
@@ -194,7 +197,7 @@ class Plan:
             stream = torch.cuda.current_stream(device)
         self.stream = stream
         flags = (TQR_FLAG_TRACE if trace else 0) | (TQR_FLAG_EMULATE_RANKS if emulate else 0) | \
-            (TQR_FLAG_TALL_TILES if tall else 0)
+            (TQR_FLAG_TALL_TILES if tall else 0) | (TQR_FLAG_LOCALITY if locality else 0)
         prm = _Params(m, n, b, s, device, ctypes.c_void_p(stream.cuda_stream), nranks, rank, flags)
         h = _vp()
         _check(lib().tqr_plan_create(ctypes.byref(h), ctypes.byref(prm)))

@@ -2,12 +2,12 @@
 import numpy as np
 
 
-def run_factor(A, b, s, trace=False, return_plan=False):
+def run_factor(A, b, s, trace=False, return_plan=False, locality=False):
     """A: numpy (m, n) float64 (any order).  Returns dict with numpy At, T, R and the plan."""
     import torch
     from paper_0707_3548_b200 import Plan
     m, n = A.shape
-    plan = Plan(m, n, b, s, trace=trace)
+    plan = Plan(m, n, b, s, trace=trace, locality=locality)
     Ac = torch.from_numpy(np.ascontiguousarray(np.asfortranarray(A).T)).cuda()  # column-major storage
     At, T = plan.alloc()
     plan.pack(Ac, At)

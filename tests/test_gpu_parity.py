@@ -59,6 +59,18 @@ def test_factor_deterministic():
     assert np.array_equal(g1["At"], g2["At"]) and np.array_equal(g1["T"], g2["T"])
 
 
+@pytest.mark.parametrize("m,n,b,s", [(4096, 4096, 256, 32), (2048, 2048, 128, 32), (3000, 1500, 256, 32)])
+def test_locality_schedule_bitwise_equal(m, n, b, s):
+    """TQR_FLAG_LOCALITY changes only the dispatch order (R22): same bits as the
+    critical-path order, and the plan really runs a different order."""
+    A = tqr_inputs.uniform(m, n, 77 + m)
+    g0 = run_factor(A, b, s)
+    g1 = run_factor(A, b, s, locality=True)
+    assert np.array_equal(g0["At"], g1["At"]) and np.array_equal(g0["T"], g1["T"])
+    r0, r1 = g0["plan"].records(), g1["plan"].records()
+    assert r0.shape == r1.shape and not np.array_equal(r0, r1)
+
+
 @pytest.mark.parametrize("m,n,b,s,nrhs", [(256, 256, 64, 16, 100), (700, 600, 256, 32, 300), (67, 41, 16, 8, 20),
                                            (520, 300, 128, 32, 128), (1100, 700, 512, 64, 200)])
 @pytest.mark.parametrize("trans", ["T", "N"])

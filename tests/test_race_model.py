@@ -230,11 +230,12 @@ _PROD = [(1024, 1024, 128, 32, 1, 12, False), (1152, 896, 128, 32, 1, 9, False),
          (2048, 2048, 256, 32, 4, 8, False)]
 
 
-@pytest.mark.parametrize("m,n,b,s,G,workers,tall", _PROD)
-def test_production_schedules_race_free(L, m, n, b, s, G, workers, tall):
+@pytest.mark.parametrize("m,n,b,s,G,workers,tall,loc", [c + (False,) for c in _PROD] +
+                         [(2048, 2048, 256, 32, 1, 16, False, True), (2048, 2048, 128, 32, 2, 12, False, True)])
+def test_production_schedules_race_free(L, m, n, b, s, G, workers, tall, loc):
     per_rank, info = [], None
     for r in range(G):
-        recs, nctr, info = L.schedule_records_policy(m, n, b, s, G, r, workers, tall=tall)
+        recs, nctr, info = L.schedule_records_policy(m, n, b, s, G, r, workers, tall=tall, locality=loc)
         per_rank.append((recs, nctr))
     npt, sw, nsl, h = info
     assert npt == b // s and sw * nsl >= b
