@@ -230,3 +230,111 @@ def flops_eq4_h(p, q, b, h):
 
 def flops_eq4(p, q, b):
     return lib().oracle_flops_eq4(p, q, float(b))
+
+
+# ---- tiled LU (oracle_lu.c, LU1-LU7) ----------------------------
+
+_pi = ctypes.POINTER(ctypes.c_int32)
+
+
+def _lu_lib():
+    L = lib()
+    if not getattr(L, "_lu_ready", False):
+        L.oracle_lu_getrf.argtypes = [_i, _i, _pd, _pi]
+        L.oracle_lu_gessm.argtypes = [_i, _i, _pd, _pi, _pd]
+        L.oracle_lu_tstrf.argtypes = [_i, _i, _pd, _pd, _pd, _pi]
+        L.oracle_lu_ssssm.argtypes = [_i, _i, _pd, _pd, _pi, _pd, _pd]
+        L.oracle_lu_getrf_tiles.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _pi, _i]
+        L.oracle_lu_apply.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _pi, _i64, _pd, _i]
+        L.oracle_lu_solve.argtypes = [_i64, _i, _i, _pd, _pd, _pi, _i64, _pd, _i]
+        L.oracle_lu_flops_standard.argtypes = [_i64, _i64]
+        L.oracle_lu_flops_standard.restype = _d
+        L.oracle_lu_flops_tiled.argtypes = [_i64, _i64, _i, _i]
+        L.oracle_lu_flops_tiled.restype = _d
+        L._lu_ready = True
+    return L
+
+
+def _pp(a: np.ndarray):
+    assert a.dtype == np.int32 and a.flags.c_contiguous
+    return a.ctypes.data_as(_pi)
+
+
+def lu_getrf(A, s):
+    """GETRF of one tile: returns (tile after, piv int32[b])."""
+    A = tile(A); b = A.shape[0]
+    piv = np.zeros(b, dtype=np.int32)
+    _chk(_lu_lib().oracle_lu_getrf(b, s, _p(A), _pp(piv)), "lu_getrf")
+    return A, piv
+
+
+def lu_gessm(L, piv, C, s):
+    L = tile(L); C = tile(C); b = C.shape[0]
+    _chk(_lu_lib().oracle_lu_gessm(b, s, _p(L), _pp(np.ascontiguousarray(piv, dtype=np.int32)), _p(C)), "lu_gessm")
+    return C
+
+
+def lu_tstrf(U, A, s):
+    """TSTRF of [U; A]: returns (U after, A after, Lt (s x b, column-major slot), piv int32[b])."""
+    U = tile(U); A = tile(A); b = U.shape[0]
+    Lt = np.zeros((s, b), order="F")
+    piv = np.zeros(b, dtype=np.int32)
+    _chk(_lu_lib().oracle_lu_tstrf(b, s, _p(U), _p(A), _p(Lt), _pp(piv)), "lu_tstrf")
+    return U, A, Lt, piv
+
+
+def lu_ssssm(V, Lt, piv, C1, C2, s):
+    V = tile(V); Lt = np.asfortranarray(Lt, dtype=np.float64); C1 = tile(C1); C2 = tile(C2); b = C1.shape[0]
+    _chk(_lu_lib().oracle_lu_ssssm(b, s, _p(V), _p(Lt), _pp(np.ascontiguousarray(piv, dtype=np.int32)), _p(C1),
+                                   _p(C2)), "lu_ssssm")
+    return C1, C2
+
+
+def lu_getrf_tiles_inplace(m, n, b, s, At, Lt, piv, nthreads=1):
+    _chk(_lu_lib().oracle_lu_getrf_tiles(m, n, b, s, _p(At), _p(Lt), _pp(piv), nthreads), "lu_getrf_tiles")
+
+
+def lu_sizes(m, n, b, s):
+    """(tile doubles, Lt doubles, piv ints) of the tiled LU storage (oracle_lu.h)."""
+    p, q = dims(m, n, b)
+    K = min(p, q)
+    return p * q * b * b, p * K * s * b, p * K * b
+
+
+def lu_getrf_tiles(A, b, s, nthreads=1):
+    """Tiled LU of column-major A; returns (At tiles after, Lt slots, piv slots)."""
+    A = np.asfortranarray(A, dtype=np.float64); m, n = A.shape
+    _, nl, npv = lu_sizes(m, n, b, s)
+    At = pack(A, b)
+    Lt = np.zeros(nl)
+    piv = np.zeros(npv, dtype=np.int32)
+    lu_getrf_tiles_inplace(m, n, b, s, At, Lt, piv, nthreads)
+    return At, Lt, piv
+
+
+def lu_apply(At, Lt, piv, m, n, b, s, B, nthreads=1):
+    """B <- M B (every interchange and elimination of the factorization, in order); B m x nrhs."""
+    B = np.asfortranarray(B, dtype=np.float64); nrhs = B.shape[1]
+    qb = -(-nrhs // b)
+    Bt = pack(B, b)
+    _chk(_lu_lib().oracle_lu_apply(m, n, b, s, _p(np.ascontiguousarray(At)), _p(np.ascontiguousarray(Lt)),
+                                   _pp(np.ascontiguousarray(piv)), qb, _p(Bt), nthreads), "lu_apply")
+    return unpack(Bt, m, nrhs, b)
+
+
+def lu_solve(At, Lt, piv, n, b, s, B, nthreads=1):
+    """X = A^{-1} B for square A (n a multiple of b) from the tiled factors."""
+    B = np.asfortranarray(B, dtype=np.float64); nrhs = B.shape[1]
+    qb = -(-nrhs // b)
+    Bt = pack(B, b)
+    _chk(_lu_lib().oracle_lu_solve(n, b, s, _p(np.ascontiguousarray(At)), _p(np.ascontiguousarray(Lt)),
+                                   _pp(np.ascontiguousarray(piv)), qb, _p(Bt), nthreads), "lu_solve")
+    return unpack(Bt, n, nrhs, b)
+
+
+def lu_flops_standard(m, n):
+    return _lu_lib().oracle_lu_flops_standard(m, n)
+
+
+def lu_flops_tiled(m, n, b, s):
+    return _lu_lib().oracle_lu_flops_tiled(m, n, b, s)
