@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--trace", default="", help="write a per-task execution trace (JSON) of one extra step")
+    ap.add_argument("--method", default="qr", choices=["qr", "lu"],
+                    help="lu: the tiled LU (include/tlu.h, SURVEY NEXT-4) on the config's matrix, 1 GPU")
     ap.add_argument("--schedule", default="critical", choices=["critical", "locality"],
                     help="locality: TQR_FLAG_LOCALITY dispatch order (DESIGN.md R22)")
     ap.add_argument("--tiles", default="square", choices=["square", "2bxb"],
@@ -166,6 +168,169 @@ def run_reference(args, cfg, rank):
     return 0
 
 
+LU_METRIC = "fp64 tiled-LU GFLOP/s (mn\u00b2\u2212n\u00b3/3) and % of fp64 peak"
+LU_FULL_ORACLE_MAX_FLOPS = 2.0e11
+
+
+def run_lu(args, cfg, rank, world, local):
+    """The tiled LU (include/tlu.h) on the config's matrix: pack + getrf +
+    get_u per step, CUDA events on the plan stream; the oracle on the same A bytes (whole matrix
+    up to 2e11 flops, else its leading block); e2e through the public API with host buffers."""
+    import oracle
+    if world > 1:
+        if rank == 0:
+            print(json.dumps({"method": "lu", "unavailable": "the tiled LU runs on one GPU (replicas only)"}))
+        return 0
+    m, n, b, s = cfg["m"], cfg["n"], cfg["b"], cfg["s"]
+    threads = len(os.sched_getaffinity(0))
+    A_host = np.asfortranarray(tqr_inputs.make(m, n, cfg["dist"], cfg["seed"]))
+    flops = oracle.lu_flops_standard(m, n)
+    if args.impl == "reference":
+        S = A_host if flops <= LU_FULL_ORACLE_MAX_FLOPS else np.asfortranarray(
+            A_host[:min(m, 6144 // b * b), :min(n, 6144 // b * b)])
+        vals = []
+        for it in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oracle.lu_getrf_tiles(S, b, s, nthreads=threads)
+            dt = time.perf_counter() - t0
+            if it >= args.warmup:
+                vals.append(oracle.lu_flops_standard(*S.shape) / dt / 1e9)
+        v = statistics.median(vals)
+        desc = f"oracle_lu_getrf_tiles on {S.shape[0]}x{S.shape[1]} (leading block of the workload), {threads} threads"
+        print(json.dumps({"impl": "reference", "method": "lu", "metric": LU_METRIC, "value": v, "unit": "GFLOP/s",
+                          "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                          "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                          "config": {"workload": cfg["name"].replace(" QR ", " LU "), "sample": desc},
+                          "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": threads, "kind": "oracle",
+                                           "sample": desc},
+                          "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+        return 0
+    import torch
+    from paper_0707_3548_b200 import tlu
+    torch.cuda.set_device(local)
+    stream = torch.cuda.Stream()
+    plan = tlu.LUPlan(m, n, b, s, device=local, stream=stream)
+    A_pin = torch.from_numpy(np.ascontiguousarray(A_host.T)).pin_memory()
+    dev = f"cuda:{local}"
+    with torch.cuda.stream(stream):
+        A_dev = A_pin.to(dev, non_blocking=True)
+        At, W, piv = plan.alloc()
+        U = torch.zeros((n, min(m, n)), dtype=torch.float64, device=dev)
+    stream.synchronize()
+    for _ in range(args.warmup):
+        plan.pack(A_dev, At)
+        plan.getrf(At, W, piv)
+        plan.get_u(At, U)
+    stream.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)
+        e0.record(stream)
+        for kk in range(args.steps):
+            plan.pack(A_dev, At)
+            ev[kk][0].record(stream)
+            plan.getrf(At, W, piv)
+            ev[kk][1].record(stream)
+            plan.get_u(At, U)
+        e1.record(stream)
+        stream.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    kern_ms = statistics.mean(a.elapsed_time(b_) for a, b_ in ev)
+    value = flops / (ms * 1e-3) / 1e9
+    U_g = U.cpu().numpy().T
+    piv_g = piv.cpu().numpy()
+    # e2e: host A in (pinned), pack, getrf, get_u, U out -- every step, serial on the plan stream
+    e2e = None
+    if not args.no_e2e:
+        U_pin = torch.empty((n, min(m, n)), dtype=torch.float64).pin_memory()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                A_dev.copy_(A_pin, non_blocking=True)
+            plan.pack(A_dev, At)
+            plan.getrf(At, W, piv)
+            plan.get_u(At, U)
+            with torch.cuda.stream(stream):
+                U_pin.copy_(U, non_blocking=True)
+        f1.record(stream)
+        stream.synchronize()
+        ems = f0.elapsed_time(f1) / args.steps
+        e2e = {"value": flops / (ems * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": ems,
+               "h2d_bytes_per_step": m * n * 8, "d2h_bytes_per_step": n * min(m, n) * 8,
+               "note": "A in from pinned host memory, U out, every step, serial on the plan stream"}
+    cpu, parity = None, None
+    if not args.no_cpu_baseline:
+        full = flops <= LU_FULL_ORACLE_MAX_FLOPS
+        S = A_host if full else np.asfortranarray(A_host[:min(m, 6144 // b * b), :min(n, 6144 // b * b)])
+        t0 = time.perf_counter()
+        At_o, _, piv_o = oracle.lu_getrf_tiles(S, b, s, nthreads=threads)
+        dt = time.perf_counter() - t0
+        desc = (f"oracle_lu_getrf_tiles on {'the full' if full else 'the leading'} {S.shape[0]}x{S.shape[1]} "
+                f"{'workload (the same A bytes)' if full else 'block of the workload matrix (same bytes)'}, "
+                f"b={b} s={s}, {threads} threads")
+        cpu = {"value": oracle.lu_flops_standard(*S.shape) / dt / 1e9, "unit": "GFLOP/s", "cores": threads,
+               "kind": "oracle", "sample": desc, "seconds": dt, "same_config": full}
+        if full:
+            U_o = oracle.get_r(At_o, m, n, b)
+            rho = max(1.0, float(np.max(np.abs(U_o)) / np.max(np.abs(A_host))))
+            tol = 1e-10 * float(np.linalg.norm(A_host)) * rho
+            same = bool(np.array_equal(piv_g, piv_o))
+            parity = {"pivots_equal": same, "growth_rho": rho,
+                      "what": "GPU factors of the last timed step vs the oracle on the same A (DESIGN.md LU10)"}
+            if same:
+                err = float(np.max(np.abs(U_g - U_o)))
+                parity.update({"U_max_abs_diff_vs_oracle": err, "tol": tol, "ok": err <= tol})
+            else:
+                # pivots decided by rounding (the oracle itself moves thousands of pivots under a
+                # one-ulp perturbation of A here): check what is unique -- a partial-pivoting
+                # elimination (|multipliers| <= 1) whose recorded transformation maps A to U
+                At_g = At.cpu().numpy()
+                p_, q_ = -(-m // b), -(-n // b)
+                K_ = min(p_, q_)
+                T_g = At_g.reshape(q_, p_, b, b)
+                mx = max(max(float(np.max(np.abs(np.tril(T_g[k, k].T, -1)))) for k in range(K_)),
+                         max((float(np.max(np.abs(T_g[k, k + 1:]))) for k in range(K_) if k + 1 < p_), default=0.0))
+                Wg = W.cpu().numpy()
+                Lt_g = np.zeros_like(Wg)
+                for k in range(K_):
+                    for i in range(k + 1, p_):
+                        sl_ = (i + k * p_) * s * b
+                        for c0 in range(0, b, s):
+                            Wl = Wg[sl_ + c0 * s: sl_ + (c0 + s) * s].reshape(s, s, order="F")
+                            Lt_g[sl_ + c0 * s: sl_ + (c0 + s) * s] = (np.linalg.inv(Wl) - np.eye(s)).reshape(-1, order="F")
+                MA = oracle.lu_apply(At_g, Lt_g, piv_g, m, n, b, s, A_host, nthreads=threads)
+                kk = min(m, n)
+                res = float(np.max(np.abs(MA[:kk] - U_g)))
+                be = res / (max(m, n) * 2.0 ** -53 * float(np.max(np.abs(A_host))) * rho)
+                parity.update({"max_abs_multiplier": mx, "max_abs_ltilde": float(np.max(np.abs(Lt_g))),
+                               "backward_error_n_u_rho": be,
+                               "ok": mx <= 1.0 and float(np.max(np.abs(Lt_g))) <= 1.0 + 1e-12 and be < 1.0})
+    achieved = flops / (kern_ms * 1e-3) / 1e12
+    line = {"metric": LU_METRIC, "method": "lu", "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg["name"].replace(" QR ", " LU "), "m": m, "n": n, "b": b, "s": s,
+                       "dist": cfg["dist"], "seed": cfg["seed"], "parallelism": "1 GPU",
+                       "l2": (f"inputs {m * n * 8 / 2**30:.1f} GiB > 126 MB L2; no flush between steps"
+                              if m * n * 8 > (1 << 28) else "inputs smaller than L2 (not flushed)"),
+                       "step": "pack + getrf (persistent DAG executor, pairwise pivoting) + get_u"},
+            "pct_of_fp64_peak": 100.0 * value / (FP64_PEAK_TFLOPS * 1e3),
+            "executed_gflops": tlu.flops_tiled(m, n, b, s) / (ms * 1e-3) / 1e9,
+            "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "kernel": f"lu_exec_kernel<{b},{s}> (tlu_getrf)", "kernel_ms": kern_ms,
+                         "flops_per_launch": flops,
+                         "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt)"},
+            "cpu_baseline": cpu, "parity": parity, "e2e": e2e,
+            "gpu_launches": 3 * args.steps,   # pack, executor, get_u (+ a cudaMemsetAsync of the counters)
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -175,6 +340,8 @@ def main():
                    "C3": "C3 square QR m=n=16384 b=256 s=32 U[-0.5,0.5)",
                    "C4": "C4 tall-skinny QR m=131072 n=2048 b=256 s=32 N(0,1)",
                    "C5": "C5 square QR m=n=65536 b=512 s=64 U[-0.5,0.5)"}[args.config]
+    if args.method == "lu":
+        return run_lu(args, cfg, rank, world, local)
     if args.impl == "reference":
         return run_reference(args, cfg, rank)
 

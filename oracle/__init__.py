@@ -245,6 +245,8 @@ def _lu_lib():
         L.oracle_lu_tstrf.argtypes = [_i, _i, _pd, _pd, _pd, _pi]
         L.oracle_lu_ssssm.argtypes = [_i, _i, _pd, _pd, _pi, _pd, _pd]
         L.oracle_lu_getrf_tiles.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _pi, _i]
+        L.oracle_lu_getrf_tiles_forced.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _pi, _pi, _d, ctypes.POINTER(_i64),
+                                                    ctypes.POINTER(_i64), _i]
         L.oracle_lu_apply.argtypes = [_i64, _i64, _i, _i, _pd, _pd, _pi, _i64, _pd, _i]
         L.oracle_lu_solve.argtypes = [_i64, _i, _i, _pd, _pd, _pi, _i64, _pd, _i]
         L.oracle_lu_flops_standard.argtypes = [_i64, _i64]
@@ -310,6 +312,22 @@ def lu_getrf_tiles(A, b, s, nthreads=1):
     piv = np.zeros(npv, dtype=np.int32)
     lu_getrf_tiles_inplace(m, n, b, s, At, Lt, piv, nthreads)
     return At, Lt, piv
+
+
+def lu_getrf_tiles_forced(A, b, s, forced, rel=1e-8, nthreads=1):
+    """The oracle's tiled LU with every pivot forced to `forced` (LU10).  Returns
+    (At, Lt, piv, nearties, invalid): decisions where the forced pivot differs from the search's
+    and is within `rel` of the largest candidate / is not."""
+    A = np.asfortranarray(A, dtype=np.float64); m, n = A.shape
+    _, nl, npv = lu_sizes(m, n, b, s)
+    At = pack(A, b)
+    Lt = np.zeros(nl)
+    piv = np.zeros(npv, dtype=np.int32)
+    f = np.ascontiguousarray(forced, dtype=np.int32)
+    nt, ni = _i64(), _i64()
+    _chk(_lu_lib().oracle_lu_getrf_tiles_forced(m, n, b, s, _p(At), _p(Lt), _pp(piv), _pp(f), rel, ctypes.byref(nt),
+                                                ctypes.byref(ni), nthreads), "lu_getrf_tiles_forced")
+    return At, Lt, piv, nt.value, ni.value
 
 
 def lu_apply(At, Lt, piv, m, n, b, s, B, nthreads=1):

@@ -80,9 +80,26 @@ static void ssssm_block(int b, int s, int l, const double* V, const double* Lt, 
  * A[r][c] /= A[c][c] (r > c; skipped if the pivot is 0 -- then the whole column is 0); the
  * rank-1 update of the block's later columns; after the block, the trailing columns get the
  * block's interchanges and eliminations (gessm_block). */
+/* Forced-pivot mode (LU10; test infrastructure for pivots decided by rounding):
+ * when g_forced is set, the pivot of every column is taken from it instead of the search;
+ * a forced pivot that differs from the search's counts as a near-tie if its |candidate| is
+ * within g_rel (relative) of the largest, as invalid otherwise. */
+static const int32_t* g_forced = NULL;
+static double g_rel = 0.0;
+static int64_t g_nearties = 0, g_invalid = 0;
+
+static int take_forced(int pr, int fp, double best, double fv) {
+  if (fp != pr) {
+    if (fv >= best * (1.0 - g_rel)) g_nearties++;
+    else g_invalid++;
+  }
+  return fp;
+}
+
 int oracle_lu_getrf(int b, int s, double* A, int32_t* piv) {
   int rc = check_bs(b, s);
   if (rc) return rc;
+  const int32_t* forced = g_forced;
   for (int l = 0; l < b / s; ++l) {
     const int c0 = l * s;
     for (int c = c0; c < c0 + s; ++c) {
@@ -90,6 +107,7 @@ int oracle_lu_getrf(int b, int s, double* A, int32_t* piv) {
       double best = fabs(E(A, c, c, b));
       for (int r = c + 1; r < b; ++r)
         if (fabs(E(A, r, c, b)) > best) { best = fabs(E(A, r, c, b)); pr = r; }
+      if (forced) pr = take_forced(pr, forced[c], best, fabs(E(A, forced[c], c, b)));
       piv[c] = pr;
       if (pr != c) swap_rows(A, b, c, A, b, pr, c0, c0 + s);
       const double d = E(A, c, c, b);
@@ -123,6 +141,7 @@ int oracle_lu_gessm(int b, int s, const double* L, const int32_t* piv, double* C
 int oracle_lu_tstrf(int b, int s, double* U, double* A, double* Lt, int32_t* piv) {
   int rc = check_bs(b, s);
   if (rc) return rc;
+  const int32_t* forced = g_forced;
   for (int64_t e = 0; e < (int64_t)s * b; ++e) Lt[e] = 0.0;
   for (int l = 0; l < b / s; ++l) {
     const int c0 = l * s;
@@ -133,6 +152,10 @@ int oracle_lu_tstrf(int b, int s, double* U, double* A, double* Lt, int32_t* piv
       double best = fabs(E(U, c, c, b));
       for (int r = 0; r < b; ++r)
         if (fabs(E(A, r, c, b)) > best) { best = fabs(E(A, r, c, b)); pr = r; }
+      if (forced) {
+        const int fp = forced[c];
+        pr = take_forced(pr, fp, best, fp < 0 ? fabs(E(U, c, c, b)) : fabs(E(A, fp, c, b)));
+      }
       piv[c] = pr;
       if (pr >= 0) {
         for (int c2 = c0; c2 < c; ++c2) { /* L part: A's multipliers up, zeros down */
@@ -214,17 +237,36 @@ int oracle_lu_getrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double
   for (int64_t e = 0; e < p * K * (int64_t)s * b; ++e) Lt[e] = 0.0;
   for (int64_t e = 0; e < p * K * (int64_t)b; ++e) piv[e] = 0;
   lu_ctx X = {p, q, 0, b, s, At, At, Lt, piv, NULL, 0, 0, 0};
+  const int32_t* forced_all = g_forced;
   for (int64_t k = 0; k < K; ++k) {
+    if (forced_all) g_forced = PSLOT(forced_all, k, k, p, b);
     oracle_lu_getrf(b, s, TILE(At, k, k, p, b), PSLOT(piv, k, k, p, b));
     /* TSTRF(k, i) reads only U_kk and A_ik: all of them first (i ascending: the flat chain on
      * U_kk), then the tile columns' GESSM + SSSSM chains, in parallel over j */
-    for (int64_t i = k + 1; i < p; ++i)
+    for (int64_t i = k + 1; i < p; ++i) {
+      if (forced_all) g_forced = PSLOT(forced_all, i, k, p, b);
       oracle_lu_tstrf(b, s, TILE(At, k, k, p, b), TILE(At, i, k, p, b), LSLOT(Lt, i, k, p, s, b),
                       PSLOT(piv, i, k, p, b));
+    }
+    g_forced = forced_all;
     X.k = k;
     for_columns(&X, k + 1, q, nthreads, step_columns, step_worker);
   }
   return 0;
+}
+
+int oracle_lu_getrf_tiles_forced(int64_t m, int64_t n, int b, int s, double* At, double* Lt, int32_t* piv,
+                                  const int32_t* forced, double rel, int64_t* nearties, int64_t* invalid,
+                                  int nthreads) {
+  if (!forced) return -8;
+  g_forced = forced;
+  g_rel = rel;
+  g_nearties = g_invalid = 0;
+  int rc = oracle_lu_getrf_tiles(m, n, b, s, At, Lt, piv, nthreads);
+  g_forced = NULL;
+  if (nearties) *nearties = g_nearties;
+  if (invalid) *invalid = g_invalid;
+  return rc;
 }
 
 /* apply M to B: the same step sequence with the factors read-only, on B's tile columns */

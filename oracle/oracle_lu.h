@@ -53,6 +53,15 @@ int oracle_lu_ssssm(int b, int s, const double* V, const double* Lt, const int32
  * of operations is the same, so the result is bitwise identical to nthreads = 1). */
 int oracle_lu_getrf_tiles(int64_t m, int64_t n, int b, int s, double* At, double* Lt, int32_t* piv, int nthreads);
 
+/* The same factorization with every pivot FORCED to forced[] (same layout as piv; DESIGN.md
+ * LU10: where rounding decides a pivot, several pivot sequences are correct).  *nearties =
+ * decisions where the forced pivot differs from the search's but its |candidate| is within
+ * `rel` (relative) of the largest; *invalid = decisions where it is not (a wrong pivot).
+ * Not thread-safe across concurrent calls (one forced sequence at a time). */
+int oracle_lu_getrf_tiles_forced(int64_t m, int64_t n, int b, int s, double* At, double* Lt, int32_t* piv,
+                                  const int32_t* forced, double rel, int64_t* nearties, int64_t* invalid,
+                                  int nthreads);
+
 /* Forward application of the factorization's transformation M (= every interchange and
  * elimination of the factorization, in its order) to a tile-major B with p tile rows and
  * qb tile columns (same b): B <- M B.  With M A = U: the forward half of a solve. */

@@ -12,8 +12,8 @@ PHASES = os.environ.get("TQR_PHASES", "0") == "1"   # profiling variant with pha
 VARIANT_DEFS = os.environ.get("TQR_VARIANT_DEFS", "").split()
 VARIANT = os.environ.get("TQR_VARIANT", "")
 LIB = os.path.join(HERE, f"libtqr_{VARIANT}.so" if VARIANT else ("libtqr_phases.so" if PHASES else "libtqr.so"))
-SOURCES = ["tqr_exec.cu", "tqr_host.cpp"]
-HEADERS = ["tqr_device.cuh", "tqr_internal.h", os.path.join("..", "..", "include", "tqr.h")]
+SOURCES = ["tqr_exec.cu", "tqr_host.cpp", "tlu_exec.cu", "tlu_host.cpp"]
+HEADERS = ["tqr_device.cuh", "tqr_internal.h", "tqr_sched.h", "tlu_internal.h", os.path.join("..", "..", "include", "tlu.h"), os.path.join("..", "..", "include", "tqr.h")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O2"] + (["-DTQR_PROFILE_PHASES"] if PHASES else []) + VARIANT_DEFS

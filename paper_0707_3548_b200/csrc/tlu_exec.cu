@@ -1,0 +1,548 @@
+// tlu_exec.cu -- B200 executor of the tiled LU factorization ("an algorithm
+// that is analogous to the QR one"; kernels = DESIGN.md readings LU1-LU9).
+//
+// One persistent launch per factorization, one 8-warp CTA per SM, tickets in the host's
+// list-schedule order and "progress counter >= value" dependencies (the tiled-QR executor's
+// protocol, tqr_exec.cu).  Task kinds:
+//   G  GETRF(k)        panel: in-tile LU with partial pivoting, block by block (LU1)
+//   T  TSTRF(k,i)      panel: LU with pairwise pivoting of [U_kk; A_ik] (LU3)
+//   L  GESSM(k,j,sl)   update of a 64-column slice of A_kj (LU2)
+//   S  SSSSM(k,i,j,sl) update of a 64-column slice of [A_kj; A_ij] (LU4)
+// Update blocks (apply_block, per inner block l): the target slice Y lives in shared memory
+// (column-major, ld b + 4: conflict-free 8x8 accumulator fragments); the block's interchanges
+// are one gather/scatter of at most 2s rows (the net permutation the panel precomputed, so no
+// serial swap chain in the update); X_l = W_l X_l by DMMA (W_l = the inverse of the block's
+// unit-lower factor, computed once by the panel, LU8); Y -= L_l X_l by DMMA.8x8x4 with the
+// multipliers streamed from L2 straight into A fragments.  Bound: the fp64 DMMA pipe
+// (2 b s w flops per block against (b + s) w x 16 bytes of shared-memory traffic).
+// Panels: row-per-thread (thread r holds row r of the block's s columns in registers), one
+// block-wide argmax (warp shuffles + 8 partials) and one interchange per column.
+#include <cuda_runtime.h>
+
+#include "tlu_internal.h"
+#include "tqr_device.cuh"
+#include "tqr_internal.h"
+
+namespace tqr {
+namespace lu {
+
+constexpr int NT = 256;
+constexpr int W = 64;  // update slice width (columns)
+
+template <int B, int S>
+struct LCfg {
+  static_assert(B % 64 == 0 || B == 64, "b: 64, 128, 256");
+  static_assert(S % 8 == 0 && B % S == 0 && S <= 32, "s: 8 | s, s | b, s <= 32");
+  static constexpr int NB = B / S;
+  static constexpr int LDY = B + 4;          // Y slice, column-major
+  static constexpr int LDX = S + 4;          // X_l, column-major
+  static constexpr int LUT = S + 1;          // panel top block, row-major
+  static constexpr int PL = 2 + 4 * S;       // perm ints per block
+  static constexpr int RPW = B / 8;          // GEMM rows per warp
+  static constexpr int MT = RPW / 8;         // 8-row m-tiles per warp
+  // shared memory (doubles)
+  static constexpr int OFF_Y = 0;
+  static constexpr int OFF_X = OFF_Y + W * LDY;
+  static constexpr int OFF_X2 = OFF_X + W * LDX;
+  static constexpr int OFF_TMP = OFF_X2 + W * LDX;
+  static constexpr int OFF_UT = OFF_TMP + 2 * S * W;
+  static constexpr int OFF_BUF = OFF_UT + S * LUT;   // 2 x S (GETRF row interchange)
+  static constexpr int OFF_RED = OFF_BUF + 2 * S;    // 8 warp maxima
+  static constexpr int NDBL = OFF_RED + 8;
+  // ints after the doubles
+  static constexpr int IOFF_RIDX = 0;                // 8 warp argmax rows
+  static constexpr int IOFF_PIV = 8;                 // S pivots of the current block
+  static constexpr int IOFF_CUR = IOFF_PIV + S;      // B (GETRF net-permutation simulation)
+  static constexpr int IOFF_CNT = IOFF_CUR + B;      // 1
+  static constexpr int NINT = IOFF_CNT + 4;
+  static constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4;
+};
+
+__device__ __forceinline__ double* wslot_ptr(double* W_, int i, int k, int p, int B, int S) {
+  return W_ + ((size_t)i + (size_t)k * p) * (size_t)S * B;
+}
+
+// ---- one inner block of GESSM (SS = false) / SSSSM (SS = true) on the slice in shared memory ----
+// Ys: rows [0, B) x columns [cl, cl + nc) of the target tile (GESSM: A_kj; SSSSM: A_ij).
+// L: the tile holding block l's multipliers (GESSM: A_kk, rows >= c0 + S; SSSSM: A_ik, all rows).
+// Wl: W_l (S x S, column-major).  pl: the block's net interchange (count, -, dst, src, ...):
+// index < B = a Y row, B + r = row r of X_l.  C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l.
+template <int B, int S, bool SS>
+__device__ __forceinline__ void apply_block(double* sm, int l, const double* __restrict__ L,
+                                            const double* __restrict__ Wl, const int* __restrict__ pl, double* C1,
+                                            int cl, int nc) {
+  using C = LCfg<B, S>;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int c0 = l * S;
+  double* Ys = sm + C::OFF_Y;
+  double* Xs = sm + C::OFF_X;
+  double* X2 = sm + C::OFF_X2;
+  double* Tm = sm + C::OFF_TMP;
+  if (SS) {  // X_l = C1 rows [c0, c0 + S) of the slice
+    for (int e = tid; e < S * W; e += NT) {
+      const int r = e % S, c = e / S;
+      Xs[c * C::LDX + r] = c < nc ? __ldcg(C1 + (c0 + r) + (size_t)(cl + c) * B) : 0.0;
+    }
+  }
+  const int np = __ldcg(pl);
+  __syncthreads();
+  // the block's interchanges: gather the sources, then scatter to the destinations
+  for (int e = tid; e < np * W; e += NT) {
+    const int pe = e / W, c = e % W, src = __ldcg(pl + 3 + 2 * pe);
+    Tm[pe * W + c] = src < B ? Ys[c * C::LDY + src] : Xs[c * C::LDX + src - B];
+  }
+  __syncthreads();
+  for (int e = tid; e < np * W; e += NT) {
+    const int pe = e / W, c = e % W, dst = __ldcg(pl + 2 + 2 * pe);
+    (dst < B ? Ys[c * C::LDY + dst] : Xs[c * C::LDX + dst - B]) = Tm[pe * W + c];
+  }
+  if (!SS) {
+    __syncthreads();
+    for (int e = tid; e < S * W; e += NT) {
+      const int r = e % S, c = e / S;
+      Xs[c * C::LDX + r] = Ys[c * C::LDY + c0 + r];
+    }
+  }
+  __syncthreads();
+  // X2 = W_l Xs  (M = S, N = W, K = S)
+  {
+    constexpr int SMT = S / 8, NNT = W / 8;
+    for (int f = warp; f < SMT * NNT; f += 8) {
+      const int mt = f % SMT, nt = f / SMT;
+      double d[2] = {0.0, 0.0};
+#pragma unroll
+      for (int ks = 0; ks < S / 4; ++ks)
+        dmma(d, __ldcg(Wl + (4 * ks + t4) * S + 8 * mt + g), Xs[(8 * nt + g) * C::LDX + 4 * ks + t4]);
+      X2[(8 * nt + 2 * t4) * C::LDX + 8 * mt + g] = d[0];
+      X2[(8 * nt + 2 * t4 + 1) * C::LDX + 8 * mt + g] = d[1];
+    }
+  }
+  __syncthreads();
+  // Y -= L[:, c0:c0+S] X2; a warp owns rows [r0, r0 + RPW) (GESSM: rows < c0 + S are not
+  // updated -- with RPW | S a warp is wholly above or below)
+  const int r0 = warp * C::RPW;
+  if (SS || r0 >= c0 + S) {
+    double acc[C::MT][W / 8][2];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < W / 8; ++nt) {
+        acc[mt][nt][0] = Ys[(8 * nt + 2 * t4) * C::LDY + r0 + 8 * mt + g];
+        acc[mt][nt][1] = Ys[(8 * nt + 2 * t4 + 1) * C::LDY + r0 + 8 * mt + g];
+      }
+    // multipliers from L2, one k-step ahead (MT fragments in flight)
+    const double* Lr = L + r0 + g + (size_t)(c0 + t4) * B;
+    double an[C::MT];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt) an[mt] = __ldcg(Lr + 8 * mt);
+#pragma unroll
+    for (int ks = 0; ks < S / 4; ++ks) {
+      double a[C::MT];
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt) a[mt] = -an[mt];
+      if (ks + 1 < S / 4) {
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) an[mt] = __ldcg(Lr + 8 * mt + (size_t)(4 * (ks + 1)) * B);
+      }
+#pragma unroll
+      for (int nt = 0; nt < W / 8; ++nt) {
+        const double bb = X2[(8 * nt + g) * C::LDX + 4 * ks + t4];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) dmma(acc[mt][nt], a[mt], bb);
+      }
+    }
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < W / 8; ++nt) {
+        Ys[(8 * nt + 2 * t4) * C::LDY + r0 + 8 * mt + g] = acc[mt][nt][0];
+        Ys[(8 * nt + 2 * t4 + 1) * C::LDY + r0 + 8 * mt + g] = acc[mt][nt][1];
+      }
+  }
+  __syncthreads();
+  for (int e = tid; e < S * W; e += NT) {  // X_l back
+    const int r = e % S, c = e / S;
+    if (c < nc) {
+      if (SS)
+        C1[(c0 + r) + (size_t)(cl + c) * B] = X2[c * C::LDX + r];
+      else
+        Ys[c * C::LDY + c0 + r] = X2[c * C::LDX + r];
+    }
+  }
+}
+
+template <int B, int S>
+__device__ __forceinline__ void load_slice(double* Ys, const double* tile, int cl, int nc) {
+  using C = LCfg<B, S>;
+  for (int e = threadIdx.x; e < (B / 2) * W; e += NT) {
+    const int r2 = e % (B / 2), c = e / (B / 2);
+    double2 v = make_double2(0.0, 0.0);
+    if (c < nc) v = __ldcg(reinterpret_cast<const double2*>(tile + (size_t)(cl + c) * B) + r2);
+    *reinterpret_cast<double2*>(Ys + c * C::LDY + 2 * r2) = v;
+  }
+}
+template <int B, int S>
+__device__ __forceinline__ void store_slice(const double* Ys, double* tile, int cl, int nc) {
+  using C = LCfg<B, S>;
+  for (int e = threadIdx.x; e < (B / 2) * nc; e += NT) {
+    const int r2 = e % (B / 2), c = e / (B / 2);
+    reinterpret_cast<double2*>(tile + (size_t)(cl + c) * B)[r2] =
+        *reinterpret_cast<const double2*>(Ys + c * C::LDY + 2 * r2);
+  }
+}
+
+// block-wide argmax of v (ties: the smaller index); every thread gets (value, index)
+template <int B, int S>
+__device__ __forceinline__ void block_argmax(double* sm, int* ism, double v, int idx, double& bv, int& bi) {
+  using C = LCfg<B, S>;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) { v = ov; idx = oi; }
+  }
+  if (lane == 0) { sm[C::OFF_RED + warp] = v; ism[C::IOFF_RIDX + warp] = idx; }
+  __syncthreads();
+  bv = sm[C::OFF_RED];
+  bi = ism[C::IOFF_RIDX];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) {  // warps hold increasing row ranges: strict > keeps the smaller row
+    const double x = sm[C::OFF_RED + w];
+    if (x > bv) { bv = x; bi = ism[C::IOFF_RIDX + w]; }
+  }
+}
+
+// W_l = (I + strict lower of Ut)^{-1} (unit lower; LU8), column c = thread c, stored column-major
+template <int B, int S>
+__device__ __forceinline__ void build_w(const double* Ut, double* Wl) {
+  using C = LCfg<B, S>;
+  const int tid = threadIdx.x;
+  if (tid < S) {
+    double w[S];
+#pragma unroll
+    for (int r = 0; r < S; ++r) w[r] = r == tid ? 1.0 : 0.0;
+#pragma unroll
+    for (int r = 1; r < S; ++r) {
+      if (r > tid) {
+        double acc = 0.0;
+#pragma unroll
+        for (int t = 0; t < r; ++t) acc = fma(Ut[r * C::LUT + t], w[t], acc);
+        w[r] = -acc;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < S; ++r) Wl[tid * S + r] = w[r];
+  }
+}
+
+// GETRF(k) on tile Akk (LU1)
+template <int B, int S>
+__device__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* pivs, int* perms) {
+  using C = LCfg<B, S>;
+  const int tid = threadIdx.x;
+  double* Ut = sm + C::OFF_UT;
+  double* bufA = sm + C::OFF_BUF;
+  double* bufB = bufA + S;
+  int* spiv = ism + C::IOFF_PIV;
+  int* cur = ism + C::IOFF_CUR;
+  for (int l = 0; l < C::NB; ++l) {
+    const int c0 = l * S;
+    double x[S];
+    __syncthreads();  // the previous block's trailing stores
+#pragma unroll
+    for (int c = 0; c < S; ++c) x[c] = (tid < B) ? __ldcg(Akk + tid + (size_t)(c0 + c) * B) : 0.0;
+#pragma unroll
+    for (int jj = 0; jj < S; ++jj) {
+      const int c = c0 + jj;
+      double bv;
+      int pr;
+      block_argmax<B, S>(sm, ism, (tid >= c && tid < B) ? fabs(x[jj]) : -1.0, tid, bv, pr);
+      if (tid == c) {
+#pragma unroll
+        for (int cc = 0; cc < S; ++cc) bufA[cc] = x[cc];
+      }
+      if (tid == pr) {
+#pragma unroll
+        for (int cc = 0; cc < S; ++cc) bufB[cc] = x[cc];
+      }
+      if (tid == 0) spiv[jj] = pr;
+      __syncthreads();
+      if (pr != c) {
+        if (tid == c) {
+#pragma unroll
+          for (int cc = 0; cc < S; ++cc) x[cc] = bufB[cc];
+        } else if (tid == pr) {
+#pragma unroll
+          for (int cc = 0; cc < S; ++cc) x[cc] = bufA[cc];
+        }
+      }
+      if (tid > c && tid < B) {  // multipliers and the rank-1 update of the block's later columns
+        const double d = bufB[jj];
+        if (d != 0.0) x[jj] = x[jj] / d;
+#pragma unroll
+        for (int cc = jj + 1; cc < S; ++cc) x[cc] = fma(-x[jj], bufB[cc], x[cc]);
+      }
+    }
+    if (tid >= c0 && tid < B) {
+#pragma unroll
+      for (int c = 0; c < S; ++c) Akk[tid + (size_t)(c0 + c) * B] = x[c];
+    }
+    if (tid >= c0 && tid < c0 + S) {  // L11 of the block
+#pragma unroll
+      for (int c = 0; c < S; ++c) Ut[(tid - c0) * C::LUT + c] = c < tid - c0 ? x[c] : 0.0;
+    }
+    for (int e = tid; e < B; e += NT) cur[e] = e;
+    if (tid == 0) ism[C::IOFF_CNT] = 0;
+    __syncthreads();
+    double* Wl = Wsl + (size_t)l * S * S;
+    int* pl = perms + l * C::PL;
+    build_w<B, S>(Ut, Wl);
+    if (tid < S) pivs[c0 + tid] = spiv[tid];
+    if (tid == 0) {  // net permutation of the block's interchanges (at most 2S rows move)
+      for (int jj = 0; jj < S; ++jj) {
+        const int a = c0 + jj, bb = spiv[jj];
+        const int t = cur[a];
+        cur[a] = cur[bb];
+        cur[bb] = t;
+      }
+    }
+    __syncthreads();
+    if (tid < B && cur[tid] != tid) {
+      const int e = atomicAdd(ism + C::IOFF_CNT, 1);
+      pl[2 + 2 * e] = tid;
+      pl[3 + 2 * e] = cur[tid];
+    }
+    __syncthreads();
+    if (tid == 0) pl[0] = ism[C::IOFF_CNT];
+    __syncthreads();
+    for (int cl = c0 + S; cl < B; cl += W) {
+      const int nc = min(W, B - cl);
+      load_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
+      apply_block<B, S, false>(sm, l, Akk, Wl, pl, nullptr, cl, nc);
+      __syncthreads();
+      store_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
+      __syncthreads();
+    }
+  }
+}
+
+// TSTRF(k,i) on [U_kk; A_ik] (LU3)
+template <int B, int S>
+__device__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Wsl, int* pivs, int* perms) {
+  using C = LCfg<B, S>;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double* Ut = sm + C::OFF_UT;
+  int* spiv = ism + C::IOFF_PIV;
+  for (int l = 0; l < C::NB; ++l) {
+    const int c0 = l * S;
+    double x[S];
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < S; ++c) x[c] = (tid < B) ? __ldcg(Aik + tid + (size_t)(c0 + c) * B) : 0.0;
+    for (int e = tid; e < S * S; e += NT) {
+      const int r = e % S, c = e / S;
+      Ut[r * C::LUT + c] = c >= r ? __ldcg(Ukk + (c0 + r) + (size_t)(c0 + c) * B) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < S; ++jj) {
+      double bv;
+      int br;
+      block_argmax<B, S>(sm, ism, tid < B ? fabs(x[jj]) : -1.0, tid, bv, br);
+      const int pr = bv > fabs(Ut[jj * C::LUT + jj]) ? br : -1;  // ties: U_kk's row (LU5)
+      if (tid == 0) spiv[jj] = pr;
+      if (tid == pr) {  // interchange with U's row jj in the block's columns; L part -> Ltilde
+#pragma unroll
+        for (int cc = 0; cc < S; ++cc) {
+          if (cc < jj) {
+            Ut[jj * C::LUT + cc] = x[cc];
+            x[cc] = 0.0;
+          } else {
+            const double t = Ut[jj * C::LUT + cc];
+            Ut[jj * C::LUT + cc] = x[cc];
+            x[cc] = t;
+          }
+        }
+      }
+      __syncthreads();
+      if (tid < B) {
+        const double d = Ut[jj * C::LUT + jj];
+        if (d != 0.0) x[jj] = x[jj] / d;
+#pragma unroll
+        for (int cc = jj + 1; cc < S; ++cc) x[cc] = fma(-x[jj], Ut[jj * C::LUT + cc], x[cc]);
+      }
+    }
+    if (tid < B) {
+#pragma unroll
+      for (int c = 0; c < S; ++c) Aik[tid + (size_t)(c0 + c) * B] = x[c];
+    }
+    for (int e = tid; e < S * S; e += NT) {  // U's block (upper part only: A_kk's strict lower holds GETRF's L)
+      const int r = e % S, c = e / S;
+      if (c >= r) Ukk[(c0 + r) + (size_t)(c0 + c) * B] = Ut[r * C::LUT + c];
+    }
+    double* Wl = Wsl + (size_t)l * S * S;
+    int* pl = perms + l * C::PL;
+    build_w<B, S>(Ut, Wl);
+    if (tid < S) pivs[c0 + tid] = spiv[tid];
+    if (warp == 0) {  // net permutation: X row j <- (previous X row with the same A row) or A row; A row <- last X row
+      const int r = lane < S ? spiv[lane] : -1;
+      const bool act = r >= 0;
+      const unsigned same = __match_any_sync(0xffffffffu, act ? r : -1 - lane);
+      const unsigned below = same & ((1u << lane) - 1u);
+      const int prev = below ? 31 - __clz(below) : -1;
+      const int last = 31 - __clz(same);
+      const int n1 = act ? 1 : 0, n2 = (act && lane == last) ? 1 : 0;
+      const unsigned m1 = __ballot_sync(0xffffffffu, n1), m2 = __ballot_sync(0xffffffffu, n2);
+      const unsigned lt = (1u << lane) - 1u;
+      int pos = __popc(m1 & lt) + __popc(m2 & lt);
+      if (n1) {
+        pl[2 + 2 * pos] = B + lane;
+        pl[3 + 2 * pos] = prev >= 0 ? B + prev : r;
+        ++pos;
+      }
+      if (n2) {
+        pl[2 + 2 * pos] = r;
+        pl[3 + 2 * pos] = B + lane;
+      }
+      if (lane == 0) pl[0] = __popc(m1) + __popc(m2);
+    }
+    __syncthreads();
+    for (int cl = c0 + S; cl < B; cl += W) {
+      const int nc = min(W, B - cl);
+      load_slice<B, S>(sm + C::OFF_Y, Aik, cl, nc);
+      apply_block<B, S, true>(sm, l, Aik, Wl, pl, Ukk, cl, nc);
+      __syncthreads();
+      store_slice<B, S>(sm + C::OFF_Y, Aik, cl, nc);
+      __syncthreads();
+    }
+  }
+}
+
+template <int B, int S>
+__global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ LuArgs a) {
+  using C = LCfg<B, S>;
+  extern __shared__ __align__(16) double sm[];
+  int* ism = reinterpret_cast<int*>(sm + C::NDBL);
+  __shared__ int s_task[TASK_INTS];
+  __shared__ int s_ticket;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int p = a.p;
+  for (;;) {
+    if (tid == 0) s_ticket = atomicAdd(a.ticket, 1);
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= a.ntasks) return;
+    if (tid < TASK_INTS) s_task[tid] = a.tasks[(size_t)tk * TASK_INTS + tid];
+    __syncthreads();
+    unsigned long long t_grab = 0, t_start = 0;
+    if (a.trace && tid == 0) t_grab = globaltimer();
+    if (warp == 0) {
+#pragma unroll
+      for (int d = 0; d < TASK_NDEP; ++d) {
+        const int code = s_task[8 + 2 * d], val = s_task[9 + 2 * d];
+        const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+        for (int x = lane; x < cnt; x += 32) {
+          const int* c = a.ctr + idx + x;
+          if (ld_acquire(c) >= val) continue;
+          const unsigned long long t0w = globaltimer();
+          while (ld_acquire(c) < val) {
+            __nanosleep(64);
+            if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();  // schedule bug: fail loudly
+          }
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    if (a.trace && tid == 0) t_start = globaltimer();
+    const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
+    double* Akk = a.A + ((size_t)k + (size_t)k * p) * B * B;
+    if (kind == LK_G) {
+      getrf_task<B, S>(sm, ism, Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
+                       a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PL);
+    } else if (kind == LK_T) {
+      double* Aik = a.A + ((size_t)i + (size_t)k * p) * B * B;
+      tstrf_task<B, S>(sm, ism, Akk, Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
+                       a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PL);
+    } else {
+      const bool ss = kind == LK_S;
+      const int vr = ss ? i : k;  // tile row of the multipliers / W / perm applied
+      double* Y = a.A + ((size_t)(ss ? i : k) + (size_t)j * p) * B * B;
+      const double* L = a.A + ((size_t)vr + (size_t)k * p) * B * B;
+      const double* Wsl = wslot_ptr(a.W, vr, k, p, B, S);
+      const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PL;
+      double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
+      const int cl = sl * W, nc = min(W, B - cl);
+      load_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
+      for (int l = 0; l < C::NB; ++l) {
+        if (ss)
+          apply_block<B, S, true>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, C1, cl, nc);
+        else
+          apply_block<B, S, false>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, nullptr, cl, nc);
+      }
+      __syncthreads();
+      store_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
+    }
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      st_release(a.ctr + s_task[5], s_task[6]);
+      if (a.trace) {
+        unsigned long long* tr = a.trace + (size_t)tk * 4;
+        tr[0] = smid();
+        tr[1] = t_grab;
+        tr[2] = t_start;
+        tr[3] = globaltimer();
+      }
+    }
+  }
+}
+
+template <int B, int S>
+static cudaError_t launch_inst(const LuArgs& a, int grid, cudaStream_t st) {
+  using C = LCfg<B, S>;
+  static_assert(C::SMEM <= 227 * 1024, "shared memory");
+  cudaError_t e = cudaFuncSetAttribute(lu_exec_kernel<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  if (e != cudaSuccess) return e;
+  void* args[] = {(void*)&a};
+  return cudaLaunchCooperativeKernel((void*)lu_exec_kernel<B, S>, dim3(grid), dim3(NT), args, C::SMEM, st);
+}
+
+template <int B, int S>
+static int max_ctas_inst(int device) {
+  using C = LCfg<B, S>;
+  int nsm = 0, per = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
+  if (cudaFuncSetAttribute(lu_exec_kernel<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
+      cudaSuccess)
+    return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lu_exec_kernel<B, S>, NT, C::SMEM) != cudaSuccess) return 0;
+  return nsm * per;
+}
+
+#define LU_INSTANCES(X) X(256, 32) X(128, 32) X(64, 16)
+
+bool lu_supported(int b, int s) {
+#define SUP(BB, SS) if (b == BB && s == SS) return true;
+  LU_INSTANCES(SUP)
+#undef SUP
+  return false;
+}
+int lu_slice(int b, int s) { return lu_supported(b, s) ? (b < W ? b : W) : 0; }
+int lu_perm_ints(int b, int s) { return (b / s) * (2 + 4 * s); }
+int lu_max_ctas(int b, int s, int device) {
+#define MC(BB, SS) if (b == BB && s == SS) return max_ctas_inst<BB, SS>(device);
+  LU_INSTANCES(MC)
+#undef MC
+  return 0;
+}
+cudaError_t launch_lu_exec(int b, int s, const LuArgs& a, int grid, cudaStream_t st) {
+#define LI(BB, SS) if (b == BB && s == SS) return launch_inst<BB, SS>(a, grid, st);
+  LU_INSTANCES(LI)
+#undef LI
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace lu
+}  // namespace tqr

@@ -122,4 +122,7 @@ cudaError_t launch_rank_barrier(int* const* arrive_all, int nranks, int me, int 
 // Store magic + me into slot me of every rank's ping array (tqr_comm_ping).
 cudaError_t launch_ping(int* const* ping_all, int nranks, int me, int magic, cudaStream_t st);
 
+// Sets the thread's tqr_last_error() message and tqr_last_bad_arg() index (tqr_host.cpp).
+void set_last_error(const char* what, int bad_arg_idx);
+
 }  // namespace tqr

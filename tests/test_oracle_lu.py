@@ -257,3 +257,26 @@ def test_flop_counts():
     b = 64
     exact = sum((b - c - 1) + 2 * (b - c - 1) ** 2 for c in range(b))
     assert oracle.lu_flops_tiled(b, b, b, b) == exact
+
+
+def test_forced_pivot_mode():
+    """DESIGN.md LU10: forcing the oracle's own pivots reproduces it bit for bit; an exact tie
+    forced the other way is a near-tie (valid), a non-maximal pivot is invalid."""
+    A = _rand(96, 96, 123)
+    At, Lt, piv = oracle.lu_getrf_tiles(A, 32, 8)
+    At2, Lt2, piv2, nt, ni = oracle.lu_getrf_tiles_forced(A, 32, 8, piv)
+    assert np.array_equal(At, At2) and np.array_equal(Lt, Lt2) and np.array_equal(piv, piv2) and nt == ni == 0
+    T = np.array(A)
+    amax = int(np.argmax(np.abs(T[:32, 0])))
+    other = 5 if amax != 5 else 6
+    T[other, 0] = -T[amax, 0]                          # an exact tie in the first column of tile 0
+    _, _, pt = oracle.lu_getrf_tiles(T, 32, 8)
+    assert pt[0] == min(amax, other)
+    f = pt.copy()
+    f[0] = max(amax, other)
+    _, _, _, nt, ni = oracle.lu_getrf_tiles_forced(T, 32, 8, f)
+    assert nt >= 1
+    bad = piv.copy()
+    bad[1] = (bad[1] + 3) % 32 if (bad[1] + 3) % 32 >= 1 else 2
+    _, _, _, nt, ni = oracle.lu_getrf_tiles_forced(A, 32, 8, bad)
+    assert ni >= 1
