@@ -37,24 +37,28 @@ struct LCfg {
   static constexpr int LDY = B + 4;          // Y slice, column-major
   static constexpr int LDX = S + 4;          // X_l, column-major
   static constexpr int LUT = S + 1;          // panel top block, row-major
-  static constexpr int PL = 2 + 4 * S;       // perm ints per block
+  static constexpr int PL = 4 + 4 * S;       // perm ints per block (count, -, -, -, pairs; 16-byte multiple)
   static constexpr int RPW = B / 8;          // GEMM rows per warp
   static constexpr int MT = RPW / 8;         // 8-row m-tiles per warp
+  static constexpr int LDL = B + 8;          // staged multiplier block L_l, column-major
+  static constexpr int MAXE = 2 * S * W / 256;  // interchange elements per thread (<= 2S rows x W)
   // shared memory (doubles)
   static constexpr int OFF_Y = 0;
   static constexpr int OFF_X = OFF_Y + W * LDY;
-  static constexpr int OFF_X2 = OFF_X + W * LDX;
-  static constexpr int OFF_TMP = OFF_X2 + W * LDX;
-  static constexpr int OFF_UT = OFF_TMP + 2 * S * W;
-  static constexpr int OFF_BUF = OFF_UT + S * LUT;   // 2 x S (GETRF row interchange)
+  static constexpr int OFF_L = OFF_X + W * LDX;      // L_l (apply_block) / the panel's top block Ut
+  static constexpr int OFF_UT = OFF_L;
+  static constexpr int OFF_W = OFF_L + S * LDL;      // W_l (S x S, column-major)
+  static constexpr int OFF_BUF = OFF_W + S * S;      // 2 x S (GETRF row interchange)
   static constexpr int OFF_RED = OFF_BUF + 2 * S;    // 8 warp maxima
   static constexpr int NDBL = OFF_RED + 8;
+  static_assert(S * LUT <= S * LDL, "Ut fits the L_l area");
   // ints after the doubles
   static constexpr int IOFF_RIDX = 0;                // 8 warp argmax rows
   static constexpr int IOFF_PIV = 8;                 // S pivots of the current block
   static constexpr int IOFF_CUR = IOFF_PIV + S;      // B (GETRF net-permutation simulation)
   static constexpr int IOFF_CNT = IOFF_CUR + B;      // 1
-  static constexpr int NINT = IOFF_CNT + 4;
+  static constexpr int IOFF_PL = IOFF_CNT + 4;       // the block's interchange list (PL ints)
+  static constexpr int NINT = IOFF_PL + ((PL + 3) & ~3);
   static constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4;
 };
 
@@ -68,7 +72,7 @@ __device__ __forceinline__ double* wslot_ptr(double* W_, int i, int k, int p, in
 // Wl: W_l (S x S, column-major).  pl: the block's net interchange (count, -, dst, src, ...):
 // index < B = a Y row, B + r = row r of X_l.  C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l.
 template <int B, int S, bool SS>
-__device__ __forceinline__ void apply_block(double* sm, int l, const double* __restrict__ L,
+__device__ __noinline__ void apply_block(double* sm, int l, const double* __restrict__ L,
                                             const double* __restrict__ Wl, const int* __restrict__ pl, double* C1,
                                             int cl, int nc) {
   using C = LCfg<B, S>;
@@ -76,25 +80,52 @@ __device__ __forceinline__ void apply_block(double* sm, int l, const double* __r
   const int c0 = l * S;
   double* Ys = sm + C::OFF_Y;
   double* Xs = sm + C::OFF_X;
-  double* X2 = sm + C::OFF_X2;
-  double* Tm = sm + C::OFF_TMP;
-  if (SS) {  // X_l = C1 rows [c0, c0 + S) of the slice
-    for (int e = tid; e < S * W; e += NT) {
-      const int r = e % S, c = e / S;
-      Xs[c * C::LDX + r] = c < nc ? __ldcg(C1 + (c0 + r) + (size_t)(cl + c) * B) : 0.0;
+  double* Ls = sm + C::OFF_L;
+  double* Ws = sm + C::OFF_W;
+  int* pls = reinterpret_cast<int*>(sm + C::NDBL) + C::IOFF_PL;
+  // every input of the block in one round of cp.async: L_l (the block's multiplier columns;
+  // GESSM: only rows >= c0 + S are used), W_l, the interchange list and (SSSSM) X_l = C1's rows
+  // [c0, c0 + S) of the slice -- one L2 round trip per block instead of one per phase
+  {
+    const int r_lo = SS ? 0 : c0 + S;
+    const int nv = (B - r_lo) / 2;  // 16-byte granules per column
+    for (int e = tid; e < nv * S; e += NT) {
+      const int v = e % nv, c = e / nv;
+      cp_async16(Ls + c * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + c) * B);
     }
+    for (int e = tid; e < S * S / 2; e += NT) cp_async16(Ws + 2 * e, Wl + 2 * e);
+    for (int e = tid; e < C::PL / 4; e += NT) cp_async16(pls + 4 * e, pl + 4 * e);
+    if (SS) {
+      for (int e = tid; e < (S / 2) * W; e += NT) {
+        const int v = e % (S / 2), c = e / (S / 2);
+        if (c < nc) cp_async16(Xs + c * C::LDX + 2 * v, C1 + c0 + 2 * v + (size_t)(cl + c) * B);
+      }
+    }
+    cp_async_commit();
   }
-  const int np = __ldcg(pl);
+  cp_async_wait<0>();
   __syncthreads();
-  // the block's interchanges: gather the sources, then scatter to the destinations
-  for (int e = tid; e < np * W; e += NT) {
-    const int pe = e / W, c = e % W, src = __ldcg(pl + 3 + 2 * pe);
-    Tm[pe * W + c] = src < B ? Ys[c * C::LDY + src] : Xs[c * C::LDX + src - B];
-  }
-  __syncthreads();
-  for (int e = tid; e < np * W; e += NT) {
-    const int pe = e / W, c = e % W, dst = __ldcg(pl + 2 + 2 * pe);
-    (dst < B ? Ys[c * C::LDY + dst] : Xs[c * C::LDX + dst - B]) = Tm[pe * W + c];
+  const int np = pls[0];
+  // the block's interchanges: every source element into registers, then to its destination
+  {
+    double v[C::MAXE];
+#pragma unroll
+    for (int x = 0; x < C::MAXE; ++x) {
+      const int e = tid + x * NT, pe = e / W, c = e % W;
+      if (pe < np) {
+        const int src = pls[3 + 2 * pe];
+        v[x] = src < B ? Ys[c * C::LDY + src] : Xs[c * C::LDX + src - B];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < C::MAXE; ++x) {
+      const int e = tid + x * NT, pe = e / W, c = e % W;
+      if (pe < np) {
+        const int dst = pls[2 + 2 * pe];
+        (dst < B ? Ys[c * C::LDY + dst] : Xs[c * C::LDX + dst - B]) = v[x];
+      }
+    }
   }
   if (!SS) {
     __syncthreads();
@@ -104,22 +135,29 @@ __device__ __forceinline__ void apply_block(double* sm, int l, const double* __r
     }
   }
   __syncthreads();
-  // X2 = W_l Xs  (M = S, N = W, K = S)
+  // Xs <- W_l Xs  (M = S, N = W, K = S; results in registers until every warp has read Xs)
   {
-    constexpr int SMT = S / 8, NNT = W / 8;
-    for (int f = warp; f < SMT * NNT; f += 8) {
-      const int mt = f % SMT, nt = f / SMT;
-      double d[2] = {0.0, 0.0};
+    constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
+    double d[PER][2];
+#pragma unroll
+    for (int x = 0; x < PER; ++x) {
+      const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
+      d[x][0] = d[x][1] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < S / 4; ++ks)
-        dmma(d, __ldcg(Wl + (4 * ks + t4) * S + 8 * mt + g), Xs[(8 * nt + g) * C::LDX + 4 * ks + t4]);
-      X2[(8 * nt + 2 * t4) * C::LDX + 8 * mt + g] = d[0];
-      X2[(8 * nt + 2 * t4 + 1) * C::LDX + 8 * mt + g] = d[1];
+        dmma(d[x], Ws[(4 * ks + t4) * S + 8 * mt + g], Xs[(8 * nt + g) * C::LDX + 4 * ks + t4]);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < PER; ++x) {
+      const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
+      Xs[(8 * nt + 2 * t4) * C::LDX + 8 * mt + g] = d[x][0];
+      Xs[(8 * nt + 2 * t4 + 1) * C::LDX + 8 * mt + g] = d[x][1];
     }
   }
   __syncthreads();
-  // Y -= L[:, c0:c0+S] X2; a warp owns rows [r0, r0 + RPW) (GESSM: rows < c0 + S are not
-  // updated -- with RPW | S a warp is wholly above or below)
+  // Y -= L_l Xs; a warp owns rows [r0, r0 + RPW) (GESSM: rows < c0 + S are not updated -- with
+  // RPW | S a warp is wholly above or below)
   const int r0 = warp * C::RPW;
   if (SS || r0 >= c0 + S) {
     double acc[C::MT][W / 8][2];
@@ -130,23 +168,14 @@ __device__ __forceinline__ void apply_block(double* sm, int l, const double* __r
         acc[mt][nt][0] = Ys[(8 * nt + 2 * t4) * C::LDY + r0 + 8 * mt + g];
         acc[mt][nt][1] = Ys[(8 * nt + 2 * t4 + 1) * C::LDY + r0 + 8 * mt + g];
       }
-    // multipliers from L2, one k-step ahead (MT fragments in flight)
-    const double* Lr = L + r0 + g + (size_t)(c0 + t4) * B;
-    double an[C::MT];
-#pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt) an[mt] = __ldcg(Lr + 8 * mt);
-#pragma unroll
+#pragma unroll 2
     for (int ks = 0; ks < S / 4; ++ks) {
       double a[C::MT];
 #pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt) a[mt] = -an[mt];
-      if (ks + 1 < S / 4) {
-#pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) an[mt] = __ldcg(Lr + 8 * mt + (size_t)(4 * (ks + 1)) * B);
-      }
+      for (int mt = 0; mt < C::MT; ++mt) a[mt] = -Ls[(4 * ks + t4) * C::LDL + r0 + 8 * mt + g];
 #pragma unroll
       for (int nt = 0; nt < W / 8; ++nt) {
-        const double bb = X2[(8 * nt + g) * C::LDX + 4 * ks + t4];
+        const double bb = Xs[(8 * nt + g) * C::LDX + 4 * ks + t4];
 #pragma unroll
         for (int mt = 0; mt < C::MT; ++mt) dmma(acc[mt][nt], a[mt], bb);
       }
@@ -164,9 +193,9 @@ __device__ __forceinline__ void apply_block(double* sm, int l, const double* __r
     const int r = e % S, c = e / S;
     if (c < nc) {
       if (SS)
-        C1[(c0 + r) + (size_t)(cl + c) * B] = X2[c * C::LDX + r];
+        C1[(c0 + r) + (size_t)(cl + c) * B] = Xs[c * C::LDX + r];
       else
-        Ys[c * C::LDY + c0 + r] = X2[c * C::LDX + r];
+        Ys[c * C::LDY + c0 + r] = Xs[c * C::LDX + r];
     }
   }
 }
@@ -238,7 +267,7 @@ __device__ __forceinline__ void build_w(const double* Ut, double* Wl) {
 
 // GETRF(k) on tile Akk (LU1)
 template <int B, int S>
-__device__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* pivs, int* perms) {
+__device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* pivs, int* perms) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x;
   double* Ut = sm + C::OFF_UT;
@@ -329,7 +358,7 @@ __device__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* 
 
 // TSTRF(k,i) on [U_kk; A_ik] (LU3)
 template <int B, int S>
-__device__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Wsl, int* pivs, int* perms) {
+__device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Wsl, int* pivs, int* perms) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* Ut = sm + C::OFF_UT;
@@ -419,6 +448,26 @@ __device__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, doubl
   }
 }
 
+// GESSM(k,j,sl) (SS = false) / SSSSM(k,i,j,sl) (SS = true): one 64-column slice, every block
+template <int B, int S, bool SS>
+__device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int i, int j, int sl) {
+  using C = LCfg<B, S>;
+  const int p = a.p;
+  const int vr = SS ? i : k;  // tile row of the multipliers / W / perm applied
+  double* Y = a.A + ((size_t)(SS ? i : k) + (size_t)j * p) * B * B;
+  const double* L = a.A + ((size_t)vr + (size_t)k * p) * B * B;
+  const double* Wsl = wslot_ptr(a.W, vr, k, p, B, S);
+  const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PL;
+  double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
+  const int cl = sl * W, nc = min(W, B - cl);
+  load_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
+#pragma unroll 1
+  for (int l = 0; l < C::NB; ++l)
+    apply_block<B, S, SS>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, SS ? C1 : nullptr, cl, nc);
+  __syncthreads();
+  store_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
+}
+
 template <int B, int S>
 __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ LuArgs a) {
   using C = LCfg<B, S>;
@@ -465,24 +514,10 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
       double* Aik = a.A + ((size_t)i + (size_t)k * p) * B * B;
       tstrf_task<B, S>(sm, ism, Akk, Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
                        a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PL);
+    } else if (kind == LK_S) {
+      update_task<B, S, true>(sm, a, k, i, j, sl);
     } else {
-      const bool ss = kind == LK_S;
-      const int vr = ss ? i : k;  // tile row of the multipliers / W / perm applied
-      double* Y = a.A + ((size_t)(ss ? i : k) + (size_t)j * p) * B * B;
-      const double* L = a.A + ((size_t)vr + (size_t)k * p) * B * B;
-      const double* Wsl = wslot_ptr(a.W, vr, k, p, B, S);
-      const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PL;
-      double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
-      const int cl = sl * W, nc = min(W, B - cl);
-      load_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
-      for (int l = 0; l < C::NB; ++l) {
-        if (ss)
-          apply_block<B, S, true>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, C1, cl, nc);
-        else
-          apply_block<B, S, false>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, nullptr, cl, nc);
-      }
-      __syncthreads();
-      store_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
+      update_task<B, S, false>(sm, a, k, i, j, sl);
     }
     __syncthreads();
     if (tid == 0) {
@@ -530,7 +565,7 @@ bool lu_supported(int b, int s) {
   return false;
 }
 int lu_slice(int b, int s) { return lu_supported(b, s) ? (b < W ? b : W) : 0; }
-int lu_perm_ints(int b, int s) { return (b / s) * (2 + 4 * s); }
+int lu_perm_ints(int b, int s) { return (b / s) * (4 + 4 * s); }
 int lu_max_ctas(int b, int s, int device) {
 #define MC(BB, SS) if (b == BB && s == SS) return max_ctas_inst<BB, SS>(device);
   LU_INSTANCES(MC)

