@@ -34,31 +34,35 @@ struct LCfg {
   static_assert(B % 64 == 0 || B == 64, "b: 64, 128, 256");
   static_assert(S % 8 == 0 && B % S == 0 && S <= 32, "s: 8 | s, s | b, s <= 32");
   static constexpr int NB = B / S;
-  static constexpr int LDY = B + 4;          // Y slice, column-major
-  static constexpr int LDX = S + 4;          // X_l, column-major
+  // Row-major slices: 8x8 accumulator fragments (16-byte accesses, rows at 528-byte stride),
+  // 16-row x 4-column I/O tiles and whole-row interchanges take the minimum number of shared
+  // wavefronts.  L_l column-major at ld B + 4 (A fragments: 2 wavefronts per 256 bytes).
+  static constexpr int LDY = W + 2;          // Y slice: B rows x W
+  static constexpr int LDX = W + 4;          // X_l: S rows x W
+  static constexpr int LDW = S + 4;          // W_l: S x S column-major
+  static constexpr int LDL = B + 4;          // L_l: B x S column-major
   static constexpr int LUT = S + 1;          // panel top block, row-major
   static constexpr int PL = 4 + 4 * S;       // perm ints per block (count, -, -, -, pairs; 16-byte multiple)
   static constexpr int RPW = B / 8;          // GEMM rows per warp
   static constexpr int MT = RPW / 8;         // 8-row m-tiles per warp
-  static constexpr int LDL = B + 8;          // staged multiplier block L_l, column-major
-  static constexpr int MAXE = 2 * S * W / 256;  // interchange elements per thread (<= 2S rows x W)
+  static constexpr int MAXV = (2 * S * W / 2 + NT - 1) / NT;  // 16-byte interchange moves per thread
   // shared memory (doubles)
   static constexpr int OFF_Y = 0;
-  static constexpr int OFF_X = OFF_Y + W * LDY;
-  static constexpr int OFF_L = OFF_X + W * LDX;      // L_l (apply_block) / the panel's top block Ut
-  static constexpr int OFF_UT = OFF_L;
-  static constexpr int OFF_W = OFF_L + S * LDL;      // W_l (S x S, column-major)
-  static constexpr int OFF_BUF = OFF_W + S * S;      // 2 x S (GETRF row interchange)
+  static constexpr int OFF_X = OFF_Y + B * LDY;
+  static constexpr int OFF_W = OFF_X + S * LDX;
+  static constexpr int OFF_L = OFF_W + S * LDW;
+  static constexpr int OFF_UT = OFF_L;               // the panel's top block (never live with L_l)
+  static constexpr int OFF_BUF = OFF_L + S * LDL;    // 2 x S (GETRF row interchange)
   static constexpr int OFF_RED = OFF_BUF + 2 * S;    // 8 warp maxima
-  static constexpr int NDBL = OFF_RED + 8;
+  static constexpr int NDBL = (OFF_RED + 8 + 1) & ~1;
   static_assert(S * LUT <= S * LDL, "Ut fits the L_l area");
   // ints after the doubles
   static constexpr int IOFF_RIDX = 0;                // 8 warp argmax rows
   static constexpr int IOFF_PIV = 8;                 // S pivots of the current block
   static constexpr int IOFF_CUR = IOFF_PIV + S;      // B (GETRF net-permutation simulation)
   static constexpr int IOFF_CNT = IOFF_CUR + B;      // 1
-  static constexpr int IOFF_PL = IOFF_CNT + 4;       // the block's interchange list (PL ints)
-  static constexpr int NINT = IOFF_PL + ((PL + 3) & ~3);
+  static constexpr int IOFF_PL = (IOFF_CNT + 4 + 3) & ~3;  // the block's interchange list (PL ints)
+  static constexpr int NINT = IOFF_PL + PL;
   static constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4;
 };
 
@@ -66,72 +70,97 @@ __device__ __forceinline__ double* wslot_ptr(double* W_, int i, int k, int p, in
   return W_ + ((size_t)i + (size_t)k * p) * (size_t)S * B;
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+
+// 16-row x 4-column I/O tiles of an R x W region: element e of this thread's sweep -> (row pair
+// start r, column c): the thread moves rows r, r + 1 of column c (one 16-byte global access;
+// a warp covers 4 columns x 128 contiguous bytes)
+__device__ __forceinline__ void io_rc2(int e, int& r, int& c) {
+  const int lane = e & 31, t = e >> 5;
+  constexpr int CT = W / 4;
+  const int tc = t % CT, tr = t / CT;
+  r = 16 * tr + 2 * (lane >> 2);
+  c = 4 * tc + (lane & 3);
+}
+
 // ---- one inner block of GESSM (SS = false) / SSSSM (SS = true) on the slice in shared memory ----
-// Ys: rows [0, B) x columns [cl, cl + nc) of the target tile (GESSM: A_kj; SSSSM: A_ij).
+// Ys: rows [0, B) x columns [cl, cl + nc) of the target tile (GESSM: A_kj; SSSSM: A_ij), row-major.
 // L: the tile holding block l's multipliers (GESSM: A_kk, rows >= c0 + S; SSSSM: A_ik, all rows).
-// Wl: W_l (S x S, column-major).  pl: the block's net interchange (count, -, dst, src, ...):
-// index < B = a Y row, B + r = row r of X_l.  C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l.
+// Wl / pl: block l's W_l (S x S, column-major) and net interchange (count, -, -, -, dst, src,
+// ...: index < B = a Y row, B + r = row r of X_l).  C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l.
 template <int B, int S, bool SS>
 __device__ __noinline__ void apply_block(double* sm, int l, const double* __restrict__ L,
-                                            const double* __restrict__ Wl, const int* __restrict__ pl, double* C1,
-                                            int cl, int nc) {
+                                         const double* __restrict__ Wl, const int* __restrict__ pl, double* C1,
+                                         int cl, int nc) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int c0 = l * S;
   double* Ys = sm + C::OFF_Y;
   double* Xs = sm + C::OFF_X;
-  double* Ls = sm + C::OFF_L;
   double* Ws = sm + C::OFF_W;
+  double* Ls = sm + C::OFF_L;
   int* pls = reinterpret_cast<int*>(sm + C::NDBL) + C::IOFF_PL;
-  // every input of the block in one round of cp.async: L_l (the block's multiplier columns;
-  // GESSM: only rows >= c0 + S are used), W_l, the interchange list and (SSSSM) X_l = C1's rows
-  // [c0, c0 + S) of the slice -- one L2 round trip per block instead of one per phase
+  // cp.async group 1: the small inputs (W_l, the interchange list, SSSSM: X_l = C1's rows
+  // [c0, c0 + S)); group 2: L_l (GESSM: only rows >= c0 + S are used), waited for only before
+  // the GEMM, so its L2 latency hides behind the interchanges and the W_l product
+  for (int e = tid; e < S * S / 2; e += NT) {
+    const int r2 = e % (S / 2), cc = e / (S / 2);
+    cp_async16(Ws + cc * C::LDW + 2 * r2, Wl + cc * S + 2 * r2);
+  }
+  for (int e = tid; e < C::PL / 4; e += NT) cp_async16(pls + 4 * e, pl + 4 * e);
+  if (SS) {
+    for (int e = tid; e < S * W / 2; e += NT) {
+      int r, cc;
+      io_rc2(e, r, cc);
+      if (cc < nc) {
+        cp_async8(Xs + r * C::LDX + cc, C1 + (c0 + r) + (size_t)(cl + cc) * B);
+        cp_async8(Xs + (r + 1) * C::LDX + cc, C1 + (c0 + r + 1) + (size_t)(cl + cc) * B);
+      }
+    }
+  }
+  cp_async_commit();
   {
     const int r_lo = SS ? 0 : c0 + S;
     const int nv = (B - r_lo) / 2;  // 16-byte granules per column
     for (int e = tid; e < nv * S; e += NT) {
-      const int v = e % nv, c = e / nv;
-      cp_async16(Ls + c * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + c) * B);
+      const int v = e % nv, cc = e / nv;
+      cp_async16(Ls + cc * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + cc) * B);
     }
-    for (int e = tid; e < S * S / 2; e += NT) cp_async16(Ws + 2 * e, Wl + 2 * e);
-    for (int e = tid; e < C::PL / 4; e += NT) cp_async16(pls + 4 * e, pl + 4 * e);
-    if (SS) {
-      for (int e = tid; e < (S / 2) * W; e += NT) {
-        const int v = e % (S / 2), c = e / (S / 2);
-        if (c < nc) cp_async16(Xs + c * C::LDX + 2 * v, C1 + c0 + 2 * v + (size_t)(cl + c) * B);
-      }
-    }
-    cp_async_commit();
   }
-  cp_async_wait<0>();
+  cp_async_commit();
+  cp_async_wait<1>();
   __syncthreads();
   const int np = pls[0];
-  // the block's interchanges: every source element into registers, then to its destination
+  // the block's interchanges: whole rows, 16 bytes per move, into registers, then to the destinations
   {
-    double v[C::MAXE];
+    double2 v[C::MAXV];
 #pragma unroll
-    for (int x = 0; x < C::MAXE; ++x) {
-      const int e = tid + x * NT, pe = e / W, c = e % W;
+    for (int x = 0; x < C::MAXV; ++x) {
+      const int e = tid + x * NT, pe = e / (W / 2), c2 = e % (W / 2);
       if (pe < np) {
-        const int src = pls[3 + 2 * pe];
-        v[x] = src < B ? Ys[c * C::LDY + src] : Xs[c * C::LDX + src - B];
+        const int src = pls[5 + 2 * pe];
+        v[x] = *reinterpret_cast<const double2*>(src < B ? Ys + src * C::LDY + 2 * c2 : Xs + (src - B) * C::LDX + 2 * c2);
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int x = 0; x < C::MAXE; ++x) {
-      const int e = tid + x * NT, pe = e / W, c = e % W;
+    for (int x = 0; x < C::MAXV; ++x) {
+      const int e = tid + x * NT, pe = e / (W / 2), c2 = e % (W / 2);
       if (pe < np) {
-        const int dst = pls[2 + 2 * pe];
-        (dst < B ? Ys[c * C::LDY + dst] : Xs[c * C::LDX + dst - B]) = v[x];
+        const int dst = pls[4 + 2 * pe];
+        *reinterpret_cast<double2*>(dst < B ? Ys + dst * C::LDY + 2 * c2 : Xs + (dst - B) * C::LDX + 2 * c2) = v[x];
       }
     }
   }
-  if (!SS) {
+  if (!SS) {  // X_l = Y's rows [c0, c0 + S) after the interchanges
     __syncthreads();
-    for (int e = tid; e < S * W; e += NT) {
-      const int r = e % S, c = e / S;
-      Xs[c * C::LDX + r] = Ys[c * C::LDY + c0 + r];
+    for (int e = tid; e < S * W / 2; e += NT) {
+      const int r = e / (W / 2), c2 = e % (W / 2);
+      *reinterpret_cast<double2*>(Xs + r * C::LDX + 2 * c2) =
+          *reinterpret_cast<const double2*>(Ys + (c0 + r) * C::LDY + 2 * c2);
     }
   }
   __syncthreads();
@@ -145,29 +174,27 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
       d[x][0] = d[x][1] = 0.0;
 #pragma unroll
       for (int ks = 0; ks < S / 4; ++ks)
-        dmma(d[x], Ws[(4 * ks + t4) * S + 8 * mt + g], Xs[(8 * nt + g) * C::LDX + 4 * ks + t4]);
+        dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], Xs[(4 * ks + t4) * C::LDX + 8 * nt + g]);
     }
+    cp_async_wait<0>();  // L_l landed (this thread's part; the barrier publishes everyone's)
     __syncthreads();
 #pragma unroll
     for (int x = 0; x < PER; ++x) {
       const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
-      Xs[(8 * nt + 2 * t4) * C::LDX + 8 * mt + g] = d[x][0];
-      Xs[(8 * nt + 2 * t4 + 1) * C::LDX + 8 * mt + g] = d[x][1];
+      *reinterpret_cast<double2*>(Xs + (8 * mt + g) * C::LDX + 8 * nt + 2 * t4) = make_double2(d[x][0], d[x][1]);
     }
   }
   __syncthreads();
-  // Y -= L_l Xs; a warp owns rows [r0, r0 + RPW) (GESSM: rows < c0 + S are not updated -- with
-  // RPW | S a warp is wholly above or below)
+  // Y -= L_l Xs (a warp owns rows [r0, r0 + RPW); GESSM: rows < c0 + S are not updated, and
+  // with RPW | S a warp is wholly above or below)
   const int r0 = warp * C::RPW;
   if (SS || r0 >= c0 + S) {
-    double acc[C::MT][W / 8][2];
+    double2 acc[C::MT][W / 8];
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < W / 8; ++nt) {
-        acc[mt][nt][0] = Ys[(8 * nt + 2 * t4) * C::LDY + r0 + 8 * mt + g];
-        acc[mt][nt][1] = Ys[(8 * nt + 2 * t4 + 1) * C::LDY + r0 + 8 * mt + g];
-      }
+      for (int nt = 0; nt < W / 8; ++nt)
+        acc[mt][nt] = *reinterpret_cast<const double2*>(Ys + (r0 + 8 * mt + g) * C::LDY + 8 * nt + 2 * t4);
 #pragma unroll 2
     for (int ks = 0; ks < S / 4; ++ks) {
       double a[C::MT];
@@ -175,48 +202,70 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
       for (int mt = 0; mt < C::MT; ++mt) a[mt] = -Ls[(4 * ks + t4) * C::LDL + r0 + 8 * mt + g];
 #pragma unroll
       for (int nt = 0; nt < W / 8; ++nt) {
-        const double bb = Xs[(8 * nt + g) * C::LDX + 4 * ks + t4];
+        const double bb = Xs[(4 * ks + t4) * C::LDX + 8 * nt + g];
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) dmma(acc[mt][nt], a[mt], bb);
+        for (int mt = 0; mt < C::MT; ++mt) {
+          double d2[2] = {acc[mt][nt].x, acc[mt][nt].y};
+          dmma(d2, a[mt], bb);
+          acc[mt][nt] = make_double2(d2[0], d2[1]);
+        }
       }
     }
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt)
 #pragma unroll
-      for (int nt = 0; nt < W / 8; ++nt) {
-        Ys[(8 * nt + 2 * t4) * C::LDY + r0 + 8 * mt + g] = acc[mt][nt][0];
-        Ys[(8 * nt + 2 * t4 + 1) * C::LDY + r0 + 8 * mt + g] = acc[mt][nt][1];
-      }
+      for (int nt = 0; nt < W / 8; ++nt)
+        *reinterpret_cast<double2*>(Ys + (r0 + 8 * mt + g) * C::LDY + 8 * nt + 2 * t4) = acc[mt][nt];
   }
-  __syncthreads();
-  for (int e = tid; e < S * W; e += NT) {  // X_l back
-    const int r = e % S, c = e / S;
-    if (c < nc) {
-      if (SS)
-        C1[(c0 + r) + (size_t)(cl + c) * B] = Xs[c * C::LDX + r];
-      else
-        Ys[c * C::LDY + c0 + r] = Xs[c * C::LDX + r];
+  if (SS) {  // X_l back to C1 (Xs is final since the previous barrier)
+    for (int e = tid; e < S * W / 2; e += NT) {
+      int r, cc;
+      io_rc2(e, r, cc);
+      if (cc < nc)
+        *reinterpret_cast<double2*>(C1 + (c0 + r) + (size_t)(cl + cc) * B) =
+            make_double2(Xs[r * C::LDX + cc], Xs[(r + 1) * C::LDX + cc]);
     }
+    __syncthreads();
+  } else {
+    __syncthreads();
+    for (int e = tid; e < S * W / 2; e += NT) {
+      const int r = e / (W / 2), c2 = e % (W / 2);
+      *reinterpret_cast<double2*>(Ys + (c0 + r) * C::LDY + 2 * c2) =
+          *reinterpret_cast<const double2*>(Xs + r * C::LDX + 2 * c2);
+    }
+    __syncthreads();
   }
 }
 
 template <int B, int S>
-__device__ __forceinline__ void load_slice(double* Ys, const double* tile, int cl, int nc) {
+__device__ __noinline__ void load_slice(double* Ys, const double* tile, int cl, int nc) {
   using C = LCfg<B, S>;
-  for (int e = threadIdx.x; e < (B / 2) * W; e += NT) {
-    const int r2 = e % (B / 2), c = e / (B / 2);
-    double2 v = make_double2(0.0, 0.0);
-    if (c < nc) v = __ldcg(reinterpret_cast<const double2*>(tile + (size_t)(cl + c) * B) + r2);
-    *reinterpret_cast<double2*>(Ys + c * C::LDY + 2 * r2) = v;
+  constexpr int PER = B * W / 2 / NT;
+  double2 v[PER];
+#pragma unroll
+  for (int x = 0; x < PER; ++x) {
+    int r, c;
+    io_rc2(threadIdx.x + x * NT, r, c);
+    v[x] = c < nc ? __ldcg(reinterpret_cast<const double2*>(tile + r + (size_t)(cl + c) * B)) : make_double2(0.0, 0.0);
   }
+#pragma unroll
+  for (int x = 0; x < PER; ++x) {
+    int r, c;
+    io_rc2(threadIdx.x + x * NT, r, c);
+    Ys[r * C::LDY + c] = v[x].x;
+    Ys[(r + 1) * C::LDY + c] = v[x].y;
+  }
+  __syncthreads();
 }
 template <int B, int S>
-__device__ __forceinline__ void store_slice(const double* Ys, double* tile, int cl, int nc) {
+__device__ __noinline__ void store_slice(const double* Ys, double* tile, int cl, int nc) {
   using C = LCfg<B, S>;
-  for (int e = threadIdx.x; e < (B / 2) * nc; e += NT) {
-    const int r2 = e % (B / 2), c = e / (B / 2);
-    reinterpret_cast<double2*>(tile + (size_t)(cl + c) * B)[r2] =
-        *reinterpret_cast<const double2*>(Ys + c * C::LDY + 2 * r2);
+  for (int e = threadIdx.x; e < B * W / 2; e += NT) {
+    int r, c;
+    io_rc2(e, r, c);
+    if (c < nc)
+      *reinterpret_cast<double2*>(tile + r + (size_t)(cl + c) * B) =
+          make_double2(Ys[r * C::LDY + c], Ys[(r + 1) * C::LDY + c]);
   }
 }
 
@@ -339,8 +388,8 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
     __syncthreads();
     if (tid < B && cur[tid] != tid) {
       const int e = atomicAdd(ism + C::IOFF_CNT, 1);
-      pl[2 + 2 * e] = tid;
-      pl[3 + 2 * e] = cur[tid];
+      pl[4 + 2 * e] = tid;
+      pl[5 + 2 * e] = cur[tid];
     }
     __syncthreads();
     if (tid == 0) pl[0] = ism[C::IOFF_CNT];
@@ -349,7 +398,6 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
       const int nc = min(W, B - cl);
       load_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
       apply_block<B, S, false>(sm, l, Akk, Wl, pl, nullptr, cl, nc);
-      __syncthreads();
       store_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
       __syncthreads();
     }
@@ -426,13 +474,13 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
       const unsigned lt = (1u << lane) - 1u;
       int pos = __popc(m1 & lt) + __popc(m2 & lt);
       if (n1) {
-        pl[2 + 2 * pos] = B + lane;
-        pl[3 + 2 * pos] = prev >= 0 ? B + prev : r;
+        pl[4 + 2 * pos] = B + lane;
+        pl[5 + 2 * pos] = prev >= 0 ? B + prev : r;
         ++pos;
       }
       if (n2) {
-        pl[2 + 2 * pos] = r;
-        pl[3 + 2 * pos] = B + lane;
+        pl[4 + 2 * pos] = r;
+        pl[5 + 2 * pos] = B + lane;
       }
       if (lane == 0) pl[0] = __popc(m1) + __popc(m2);
     }
@@ -441,7 +489,6 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
       const int nc = min(W, B - cl);
       load_slice<B, S>(sm + C::OFF_Y, Aik, cl, nc);
       apply_block<B, S, true>(sm, l, Aik, Wl, pl, Ukk, cl, nc);
-      __syncthreads();
       store_slice<B, S>(sm + C::OFF_Y, Aik, cl, nc);
       __syncthreads();
     }
@@ -464,7 +511,6 @@ __device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int
 #pragma unroll 1
   for (int l = 0; l < C::NB; ++l)
     apply_block<B, S, SS>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, SS ? C1 : nullptr, cl, nc);
-  __syncthreads();
   store_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
 }
 
