@@ -103,24 +103,26 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
   double* Ws = sm + C::OFF_W;
   double* Ls = sm + C::OFF_L;
   int* pls = reinterpret_cast<int*>(sm + C::NDBL) + C::IOFF_PL;
-  // cp.async group 1: the small inputs (W_l, the interchange list, SSSSM: X_l = C1's rows
-  // [c0, c0 + S)); group 2: L_l (GESSM: only rows >= c0 + S are used), waited for only before
-  // the GEMM, so its L2 latency hides behind the interchanges and the W_l product
+  // SSSSM: X_l = C1's rows [c0, c0 + S) by 16-byte loads into registers (stored to shared memory
+  // below); cp.async group 1: W_l and the interchange list; group 2: L_l (GESSM: only rows
+  // >= c0 + S are used), waited for only before the GEMM, so its L2 latency hides behind the
+  // interchanges and the W_l product
+  constexpr int XPER = S * W / 2 / NT;
+  double2 xv[SS ? XPER : 1];
+  if (SS) {
+#pragma unroll
+    for (int x = 0; x < XPER; ++x) {
+      int r, cc;
+      io_rc2(tid + x * NT, r, cc);
+      xv[x] = cc < nc ? __ldcg(reinterpret_cast<const double2*>(C1 + (c0 + r) + (size_t)(cl + cc) * B))
+                      : make_double2(0.0, 0.0);
+    }
+  }
   for (int e = tid; e < S * S / 2; e += NT) {
     const int r2 = e % (S / 2), cc = e / (S / 2);
     cp_async16(Ws + cc * C::LDW + 2 * r2, Wl + cc * S + 2 * r2);
   }
   for (int e = tid; e < C::PL / 4; e += NT) cp_async16(pls + 4 * e, pl + 4 * e);
-  if (SS) {
-    for (int e = tid; e < S * W / 2; e += NT) {
-      int r, cc;
-      io_rc2(e, r, cc);
-      if (cc < nc) {
-        cp_async8(Xs + r * C::LDX + cc, C1 + (c0 + r) + (size_t)(cl + cc) * B);
-        cp_async8(Xs + (r + 1) * C::LDX + cc, C1 + (c0 + r + 1) + (size_t)(cl + cc) * B);
-      }
-    }
-  }
   cp_async_commit();
   {
     const int r_lo = SS ? 0 : c0 + S;
@@ -131,6 +133,15 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
     }
   }
   cp_async_commit();
+  if (SS) {
+#pragma unroll
+    for (int x = 0; x < XPER; ++x) {
+      int r, cc;
+      io_rc2(tid + x * NT, r, cc);
+      Xs[r * C::LDX + cc] = xv[x].x;
+      Xs[(r + 1) * C::LDX + cc] = xv[x].y;
+    }
+  }
   cp_async_wait<1>();
   __syncthreads();
   const int np = pls[0];
