@@ -124,10 +124,18 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
                                bool real_layout, bool split, Sched& out, int prio = PRIO_CLASS, double lat = 0.0,
                                int rwm = 128, double blq = 0.0, int group = 0, int np = 1, int fine = 0,
                                bool early = false, double lat_remote = 0.0, bool pipe = false,
-                               bool slicedep = true, int h = 1) {
+                               bool slicedep = true, int h = 1, double gtail = 0.75) {
   const int K = (int)std::min(p, q);
   const int G = (int)workers.size();
   const int w = (b + nsl - 1) / nsl;
+  // which updates join their reflector panel's group (R22): not the lookahead columns
+  // (j <= k + gj) and, in mode 3, not the last (1 - gt) of the steps, where the critical path
+  // decides (development knobs TQR_DEV_GROUP_J / TQR_DEV_GROUP_TAIL)
+  int gj = 1;
+  double gt = gtail;
+  if (const char* e = getenv("TQR_DEV_GROUP_J")) gj = atoi(e);
+  if (const char* e = getenv("TQR_DEV_GROUP_TAIL")) gt = atof(e);
+  auto grouped = [&](int k, int j) { return j > k + gj && (group != 3 || k < gt * K); };
   const int NPT = b / s;  // panel sub-tasks per tile: one per inner block l (one output T_l)
   if (np < 1 || nsl % np != 0) np = 1;
   DurModel dm(b, s, w * np, rwm), dmf(b, s, w, rwm);
@@ -228,7 +236,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         T.t[id].rank = own(j); T.t[id].kc = scol(k);
         T.t[id].key[2] = j;
         T.t[id].np = n_; T.t[id].ocnt = n_;
-        if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + k;
+        if (group && grouped(k, j)) T.t[id].group = (int64_t)k * p + k;
         T.dep(id, PF(k, NPT - 1), 1, 1);
         if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
         if (pipe) T.t[id].flags |= 64;             // pipelined panel dependency (R31)
@@ -250,7 +258,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
           T.t[id].rank = own(j); T.t[id].kc = scol(k);
           T.t[id].key[2] = j;
           T.t[id].np = n_; T.t[id].ocnt = n_;
-          if (group && j > k + 1 && (group != 3 || 4 * k < 3 * K)) T.t[id].group = (int64_t)k * p + i;
+          if (group && grouped(k, j)) T.t[id].group = (int64_t)k * p + i;
           T.dep(id, PF(k, NPT - 1), 1, v);
           if (own(j) != own(k)) T.t[id].flags |= 8;  // dep 0 is published by a peer GPU
           if (pipe) T.t[id].flags |= 64;             // pipelined panel dependency (R31)
@@ -360,6 +368,7 @@ struct tqr_plan {
   int orm_prio = PRIO_BLEVEL;  // list-schedule priority of apply-Q / form-Q
   double blq = 0.0;            // bottom-level quantum (ns) of the factorization schedule
   int group = 0;               // group the updates of one reflector panel (R22)
+  double gtail = 0.75;         //   ... in the steps k < gtail * K
   bool early = true;           // factor parts release R_kk's block rows early (R24)
   bool pipe = true;            // update tasks wait for the panel block by block (R31)
   bool slicedep = true;        // panel parts wait only for their block's column slices (R32)
@@ -408,6 +417,7 @@ struct Policy {
   int rwm = 128, passes = 1, nsl = 1, fine = 2, prio = PRIO_BLEVEL, orm_prio = PRIO_BLEVEL;
   bool split = true, early = true, pipe = true, slicedep = true;
   int group = 0;
+  double gtail = 0.75;  // grouped updates only in the steps k < gtail * K (R22)
   double lat = 4000.0, blq = 0.0;
   int h = 1;  // tile rows per TSQRT / SSRFB unit
 };
@@ -433,7 +443,13 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s, bool tall_tiles = 
   // the per-slice dependencies cost C3 0.3% and C4 0.5% (their dispatch order)
   P.pipe = b <= 128;
   P.slicedep = false;  // (C2: 6.749 vs 6.756 ms without; C3 +0.3%, C4 +0.5% with)
-  if (locality) P.group = 3;  // TQR_FLAG_LOCALITY: panel groups, not in the last quarter (R22)
+  // Reflector-panel groups (R22): square grids with b >= 256 group the updates of each panel in
+  // the first half of the steps by default (measured same-box: C3 199.8 -> 198.6 ms, DRAM reads
+  // 226 -> 127 GB; C5 -0.2%; C2 (+3%) and the tall-skinny C4 (+0.4%) keep the plain
+  // critical-path order); TQR_FLAG_LOCALITY groups them in the first three quarters on every
+  // grid (C3: 113 GB of reads, +1.1%)
+  if (b >= 256 && !tall) { P.group = 3; P.gtail = 0.5; }
+  if (locality) { P.group = 3; P.gtail = 0.75; }
   if (const char* e = getenv("TQR_DEV_PASSES")) P.passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P.split = atoi(e) != 0;
   if (const char* e = getenv("TQR_DEV_RW")) P.rwm = atoi(e);
@@ -668,6 +684,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     P->pipe = pol.pipe;
     P->slicedep = pol.slicedep;
     P->h = pol.h;
+    P->gtail = pol.gtail;
   }
   P->st = (cudaStream_t)p->stream;
   P->workers = tall ? exec_max_ctas_tall(p->device) : exec_max_ctas(p->b, p->s, P->rwm, p->device);
@@ -687,7 +704,7 @@ tqr_status tqr_plan_create(tqr_plan** out, const tqr_params* p) {
     for (int r = 0; r < P->G; ++r) workers[r] = P->workers / P->G + (r < P->workers % P->G ? 1 : 0);
   Sched s;
   build_factor_sched(P->p, P->q, p->b, p->s, P->nsl, workers, P->real, P->split, s, P->prio, P->lat, P->rwm, P->blq, P->group, P->passes, P->fine,
-                     P->early, 0.0, P->pipe, P->slicedep, P->h);
+                     P->early, 0.0, P->pipe, P->slicedep, P->h, P->gtail);
   if (!s.topo_ok) {
     destroy_plan(P);
     g_err = "internal: schedule is not topological";
@@ -1145,7 +1162,7 @@ tqr_status tqr_schedule_records_policy(int64_t m, int64_t n, int32_t b, int32_t 
   Sched sc;
   build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
                      pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, 0.0, pol.pipe,
-                     pol.slicedep, pol.h);
+                     pol.slicedep, pol.h, pol.gtail);
   if (!sc.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
@@ -1178,7 +1195,7 @@ tqr_status tqr_schedule_model(int64_t m, int64_t n, int32_t b, int32_t s, int32_
   Sched sc;
   build_factor_sched(p, q, b, s, pol.nsl, std::vector<int>(nranks, workers), nranks > 1, pol.split, sc, pol.prio,
                      pol.lat, pol.rwm, pol.blq, pol.group, pol.passes, pol.fine, pol.early, remote_ns, pol.pipe,
-                     pol.slicedep);
+                     pol.slicedep, 1, pol.gtail);
   if (!sc.topo_ok) {
     g_err = "schedule is not a topological order";
     return TQR_ERR_UNSUPPORTED;
