@@ -42,9 +42,10 @@ struct LCfg {
   static constexpr int LDW = S + 4;          // W_l: S x S column-major
   static constexpr int LDL = B + 4;          // L_l: B x S column-major
   static constexpr int LUT = S + 1;          // panel top block, row-major
-  static constexpr int PL = B + S;           // source map ints per block (rows [0, B) of Y, [B, B + S) of X_l)
+  static constexpr int PL = 4 + 4 * S;       // perm ints per block (count, -, -, -, pairs; 16-byte multiple)
   static constexpr int RPW = B / 8;          // GEMM rows per warp
   static constexpr int MT = RPW / 8;         // 8-row m-tiles per warp
+  static constexpr int MAXV = (2 * S * W / 2 + NT - 1) / NT;  // 16-byte interchange moves per thread
   // shared memory (doubles)
   static constexpr int OFF_Y = 0;
   static constexpr int OFF_X = OFF_Y + B * LDY;
@@ -60,7 +61,7 @@ struct LCfg {
   static constexpr int IOFF_PIV = 8;                 // S pivots of the current block
   static constexpr int IOFF_CUR = IOFF_PIV + S;      // B (GETRF net-permutation simulation)
   static constexpr int IOFF_CNT = IOFF_CUR + B;      // 1
-  static constexpr int IOFF_PL = (IOFF_CNT + 4 + 3) & ~3;  // the block's source map (PL ints)
+  static constexpr int IOFF_PL = (IOFF_CNT + 4 + 3) & ~3;  // the block's interchange list (PL ints)
   static constexpr int NINT = IOFF_PL + PL;
   static constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4;
 };
@@ -88,14 +89,11 @@ __device__ __forceinline__ void io_rc2(int e, int& r, int& c) {
 // ---- one inner block of GESSM (SS = false) / SSSSM (SS = true) on the slice in shared memory ----
 // Ys: rows [0, B) x columns [cl, cl + nc) of the target tile (GESSM: A_kj; SSSSM: A_ij), row-major.
 // L: the tile holding block l's multipliers (GESSM: A_kk, rows >= c0 + S; SSSSM: A_ik, all rows).
-// Wl / sp: block l's W_l (S x S, column-major) and source map: after the block's interchanges,
-// row d (< B: a Y row, B + r: row r of X_l) holds what was in row sp[d] before them (the panel
-// precomputed the net permutation).  No pass moves rows: the W_l product reads X_l's rows and
-// the GEMM reads its accumulators THROUGH the map, and everything is written back in place.
-// C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l; GESSM: X_l = Y's rows [c0, c0 + S).
+// Wl / pl: block l's W_l (S x S, column-major) and net interchange (count, -, -, -, dst, src,
+// ...: index < B = a Y row, B + r = row r of X_l).  C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l.
 template <int B, int S, bool SS>
 __device__ __noinline__ void apply_block(double* sm, int l, const double* __restrict__ L,
-                                         const double* __restrict__ Wl, const int* __restrict__ sp, double* C1,
+                                         const double* __restrict__ Wl, const int* __restrict__ pl, double* C1,
                                          int cl, int nc) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
@@ -104,10 +102,11 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
   double* Xs = sm + C::OFF_X;
   double* Ws = sm + C::OFF_W;
   double* Ls = sm + C::OFF_L;
-  int* sms = reinterpret_cast<int*>(sm + C::NDBL) + C::IOFF_PL;
+  int* pls = reinterpret_cast<int*>(sm + C::NDBL) + C::IOFF_PL;
   // SSSSM: X_l = C1's rows [c0, c0 + S) by 16-byte loads into registers (stored to shared memory
-  // below); cp.async group 1: W_l and the source map; group 2: L_l (GESSM: only rows >= c0 + S
-  // are used), waited for only before the GEMM
+  // below); cp.async group 1: W_l and the interchange list; group 2: L_l (GESSM: only rows
+  // >= c0 + S are used), waited for only before the GEMM, so its L2 latency hides behind the
+  // interchanges and the W_l product
   constexpr int XPER = S * W / 2 / NT;
   double2 xv[SS ? XPER : 1];
   if (SS) {
@@ -123,7 +122,7 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
     const int r2 = e % (S / 2), cc = e / (S / 2);
     cp_async16(Ws + cc * C::LDW + 2 * r2, Wl + cc * S + 2 * r2);
   }
-  for (int e = tid; e < C::PL / 4; e += NT) cp_async16(sms + 4 * e, sp + 4 * e);
+  for (int e = tid; e < C::PL / 4; e += NT) cp_async16(pls + 4 * e, pl + 4 * e);
   cp_async_commit();
   {
     const int r_lo = SS ? 0 : c0 + S;
@@ -145,37 +144,48 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
   }
   cp_async_wait<1>();
   __syncthreads();
-  // row d of the post-interchange slice (d < B: Y, B + r: X_l row r) lives at src(d) now
-  auto row_off = [&](int d) __attribute__((always_inline)) -> int {  // offset in sm (doubles)
-    const int s_ = sms[d];
-    return s_ < B ? C::OFF_Y + s_ * C::LDY : C::OFF_X + (s_ - B) * C::LDX;
-  };
-  const int r0 = warp * C::RPW;
-  const bool gemm = SS || r0 >= c0 + S;  // GESSM: rows < c0 + S are not updated (RPW | S)
-  double2 acc[C::MT][W / 8];
-  // X_l <- W_l X_l  (M = S, N = W, K = S; X_l's rows through the map; results in registers
-  // until every warp has read the old rows)
+  const int np = pls[0];
+  // the block's interchanges: whole rows, 16 bytes per move, into registers, then to the destinations
+  {
+    double2 v[C::MAXV];
+#pragma unroll
+    for (int x = 0; x < C::MAXV; ++x) {
+      const int e = tid + x * NT, pe = e / (W / 2), c2 = e % (W / 2);
+      if (pe < np) {
+        const int src = pls[5 + 2 * pe];
+        v[x] = *reinterpret_cast<const double2*>(src < B ? Ys + src * C::LDY + 2 * c2 : Xs + (src - B) * C::LDX + 2 * c2);
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int x = 0; x < C::MAXV; ++x) {
+      const int e = tid + x * NT, pe = e / (W / 2), c2 = e % (W / 2);
+      if (pe < np) {
+        const int dst = pls[4 + 2 * pe];
+        *reinterpret_cast<double2*>(dst < B ? Ys + dst * C::LDY + 2 * c2 : Xs + (dst - B) * C::LDX + 2 * c2) = v[x];
+      }
+    }
+  }
+  if (!SS) {  // X_l = Y's rows [c0, c0 + S) after the interchanges
+    __syncthreads();
+    for (int e = tid; e < S * W / 2; e += NT) {
+      const int r = e / (W / 2), c2 = e % (W / 2);
+      *reinterpret_cast<double2*>(Xs + r * C::LDX + 2 * c2) =
+          *reinterpret_cast<const double2*>(Ys + (c0 + r) * C::LDY + 2 * c2);
+    }
+  }
+  __syncthreads();
+  // Xs <- W_l Xs  (M = S, N = W, K = S; results in registers until every warp has read Xs)
   {
     constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
     double d[PER][2];
-    int xr[S / 4];
-#pragma unroll
-    for (int ks = 0; ks < S / 4; ++ks) xr[ks] = row_off(SS ? B + 4 * ks + t4 : c0 + 4 * ks + t4) + g;
 #pragma unroll
     for (int x = 0; x < PER; ++x) {
       const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
       d[x][0] = d[x][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < S / 4; ++ks) dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], sm[xr[ks] + 8 * nt]);
-    }
-    // accumulators of this warp's rows, read through the map
-    if (gemm) {
-#pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt) {
-        const int ro = row_off(r0 + 8 * mt + g) + 2 * t4;
-#pragma unroll
-        for (int nt = 0; nt < W / 8; ++nt) acc[mt][nt] = *reinterpret_cast<const double2*>(sm + ro + 8 * nt);
-      }
+      for (int ks = 0; ks < S / 4; ++ks)
+        dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], Xs[(4 * ks + t4) * C::LDX + 8 * nt + g]);
     }
     cp_async_wait<0>();  // L_l landed (this thread's part; the barrier publishes everyone's)
     __syncthreads();
@@ -186,8 +196,16 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
     }
   }
   __syncthreads();
-  // Y -= L_l Xs (a warp owns rows [r0, r0 + RPW)), stored to the rows' own positions
-  if (gemm) {
+  // Y -= L_l Xs (a warp owns rows [r0, r0 + RPW); GESSM: rows < c0 + S are not updated, and
+  // with RPW | S a warp is wholly above or below)
+  const int r0 = warp * C::RPW;
+  if (SS || r0 >= c0 + S) {
+    double2 acc[C::MT][W / 8];
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < W / 8; ++nt)
+        acc[mt][nt] = *reinterpret_cast<const double2*>(Ys + (r0 + 8 * mt + g) * C::LDY + 8 * nt + 2 * t4);
 #pragma unroll 2
     for (int ks = 0; ks < S / 4; ++ks) {
       double a[C::MT];
@@ -219,7 +237,8 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
             make_double2(Xs[r * C::LDX + cc], Xs[(r + 1) * C::LDX + cc]);
     }
     __syncthreads();
-  } else {  // X_l back to Y's rows [c0, c0 + S) (their old contents were read before the barrier)
+  } else {
+    __syncthreads();
     for (int e = tid; e < S * W / 2; e += NT) {
       const int r = e / (W / 2), c2 = e % (W / 2);
       *reinterpret_cast<double2*>(Ys + (c0 + r) * C::LDY + 2 * c2) =
@@ -363,6 +382,7 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
       for (int c = 0; c < S; ++c) Ut[(tid - c0) * C::LUT + c] = c < tid - c0 ? x[c] : 0.0;
     }
     for (int e = tid; e < B; e += NT) cur[e] = e;
+    if (tid == 0) ism[C::IOFF_CNT] = 0;
     __syncthreads();
     double* Wl = Wsl + (size_t)l * S * S;
     int* pl = perms + l * C::PL;
@@ -377,7 +397,13 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
       }
     }
     __syncthreads();
-    for (int e = tid; e < C::PL; e += NT) pl[e] = e < B ? cur[e] : e;  // source map (X rows unused)
+    if (tid < B && cur[tid] != tid) {
+      const int e = atomicAdd(ism + C::IOFF_CNT, 1);
+      pl[4 + 2 * e] = tid;
+      pl[5 + 2 * e] = cur[tid];
+    }
+    __syncthreads();
+    if (tid == 0) pl[0] = ism[C::IOFF_CNT];
     __syncthreads();
     for (int cl = c0 + S; cl < B; cl += W) {
       const int nc = min(W, B - cl);
@@ -447,8 +473,6 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
     int* pl = perms + l * C::PL;
     build_w<B, S>(Ut, Wl);
     if (tid < S) pivs[c0 + tid] = spiv[tid];
-    for (int e = tid; e < C::PL; e += NT) pl[e] = e;  // source map: identity, then the moved rows
-    __syncthreads();
     if (warp == 0) {  // net permutation: X row j <- (previous X row with the same A row) or A row; A row <- last X row
       const int r = lane < S ? spiv[lane] : -1;
       const bool act = r >= 0;
@@ -456,8 +480,20 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
       const unsigned below = same & ((1u << lane) - 1u);
       const int prev = below ? 31 - __clz(below) : -1;
       const int last = 31 - __clz(same);
-      if (act) pl[B + lane] = prev >= 0 ? B + prev : r;
-      if (act && lane == last) pl[r] = B + lane;
+      const int n1 = act ? 1 : 0, n2 = (act && lane == last) ? 1 : 0;
+      const unsigned m1 = __ballot_sync(0xffffffffu, n1), m2 = __ballot_sync(0xffffffffu, n2);
+      const unsigned lt = (1u << lane) - 1u;
+      int pos = __popc(m1 & lt) + __popc(m2 & lt);
+      if (n1) {
+        pl[4 + 2 * pos] = B + lane;
+        pl[5 + 2 * pos] = prev >= 0 ? B + prev : r;
+        ++pos;
+      }
+      if (n2) {
+        pl[4 + 2 * pos] = r;
+        pl[5 + 2 * pos] = B + lane;
+      }
+      if (lane == 0) pl[0] = __popc(m1) + __popc(m2);
     }
     __syncthreads();
     for (int cl = c0 + S; cl < B; cl += W) {
@@ -586,7 +622,7 @@ bool lu_supported(int b, int s) {
   return false;
 }
 int lu_slice(int b, int s) { return lu_supported(b, s) ? (b < W ? b : W) : 0; }
-int lu_perm_ints(int b, int s) { return (b / s) * (b + s); }
+int lu_perm_ints(int b, int s) { return (b / s) * (4 + 4 * s); }
 int lu_max_ctas(int b, int s, int device) {
 #define MC(BB, SS) if (b == BB && s == SS) return max_ctas_inst<BB, SS>(device);
   LU_INSTANCES(MC)
