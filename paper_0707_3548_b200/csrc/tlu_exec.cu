@@ -180,13 +180,14 @@ __device__ __noinline__ void apply_block(double* sm, int l, const double* __rest
     constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
     double d[PER][2];
 #pragma unroll
-    for (int x = 0; x < PER; ++x) {
-      const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
-      d[x][0] = d[x][1] = 0.0;
+    for (int x = 0; x < PER; ++x) d[x][0] = d[x][1] = 0.0;
 #pragma unroll
-      for (int ks = 0; ks < S / 4; ++ks)
+    for (int ks = 0; ks < S / 4; ++ks)  // k-step outer: the PER accumulator chains interleave
+#pragma unroll
+      for (int x = 0; x < PER; ++x) {
+        const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
         dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], Xs[(4 * ks + t4) * C::LDX + 8 * nt + g]);
-    }
+      }
     cp_async_wait<0>();  // L_l landed (this thread's part; the barrier publishes everyone's)
     __syncthreads();
 #pragma unroll
