@@ -269,13 +269,15 @@ __device__ __noinline__ void load_slice(double* Ys, const double* tile, int cl, 
   }
   __syncthreads();
 }
+// rows [r_lo, B) only (GETRF's trailing update: the rows above block l hold U rows that the
+// concurrent TSTRF tasks of earlier blocks update in these columns, LU11)
 template <int B, int S>
-__device__ __noinline__ void store_slice(const double* Ys, double* tile, int cl, int nc) {
+__device__ __noinline__ void store_slice(const double* Ys, double* tile, int cl, int nc, int r_lo = 0) {
   using C = LCfg<B, S>;
   for (int e = threadIdx.x; e < B * W / 2; e += NT) {
     int r, c;
     io_rc2(e, r, c);
-    if (c < nc)
+    if (c < nc && r >= r_lo)
       *reinterpret_cast<double2*>(tile + r + (size_t)(cl + c) * B) =
           make_double2(Ys[r * C::LDY + c], Ys[(r + 1) * C::LDY + c]);
   }
@@ -328,7 +330,8 @@ __device__ __forceinline__ void build_w(const double* Ut, double* Wl) {
 
 // GETRF(k) on tile Akk (LU1)
 template <int B, int S>
-__device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* pivs, int* perms) {
+__device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* pivs, int* perms,
+                                        int l0, int l1) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x;
   double* Ut = sm + C::OFF_UT;
@@ -336,7 +339,7 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
   double* bufB = bufA + S;
   int* spiv = ism + C::IOFF_PIV;
   int* cur = ism + C::IOFF_CUR;
-  for (int l = 0; l < C::NB; ++l) {
+  for (int l = l0; l < l1; ++l) {
     const int c0 = l * S;
     double x[S];
     __syncthreads();  // the previous block's trailing stores
@@ -410,7 +413,7 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
       const int nc = min(W, B - cl);
       load_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
       apply_block<B, S, false>(sm, l, Akk, Wl, pl, nullptr, cl, nc);
-      store_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
+      store_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc, c0);
       __syncthreads();
     }
   }
@@ -418,12 +421,13 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
 
 // TSTRF(k,i) on [U_kk; A_ik] (LU3)
 template <int B, int S>
-__device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Wsl, int* pivs, int* perms) {
+__device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Wsl, int* pivs, int* perms,
+                                        int l0, int l1) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* Ut = sm + C::OFF_UT;
   int* spiv = ism + C::IOFF_PIV;
-  for (int l = 0; l < C::NB; ++l) {
+  for (int l = l0; l < l1; ++l) {
     const int c0 = l * S;
     double x[S];
     __syncthreads();
@@ -565,13 +569,15 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
     if (a.trace && tid == 0) t_start = globaltimer();
     const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
     double* Akk = a.A + ((size_t)k + (size_t)k * p) * B * B;
+    // panel tasks: inner block sl (record [4]; -1: the whole tile)
+    const int l0 = sl < 0 ? 0 : sl, l1 = sl < 0 ? C::NB : sl + 1;
     if (kind == LK_G) {
       getrf_task<B, S>(sm, ism, Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
-                       a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PL);
+                       a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PL, l0, l1);
     } else if (kind == LK_T) {
       double* Aik = a.A + ((size_t)i + (size_t)k * p) * B * B;
       tstrf_task<B, S>(sm, ism, Akk, Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
-                       a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PL);
+                       a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PL, l0, l1);
     } else if (kind == LK_S) {
       update_task<B, S, true>(sm, a, k, i, j, sl);
     } else {

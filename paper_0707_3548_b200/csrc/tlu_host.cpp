@@ -2,12 +2,13 @@
 // list-schedule order, and the C ABI.  The DAG is the tiled QR's with the
 // kernels renamed (LU7); every dependency is a chain, expressed on the device as
 // "progress counter >= value":
-//   panel[k]      counts GETRF(k) (1), TSTRF(k,i) (i - k + 1)            -- the chain on U_kk
+//   PF[k][l]      counts GETRF(k) block l (1), TSTRF(k,i) block l (i - k + 1) -- block lane l of
+//                 the chain on U_kk (panel tasks per inner block, LU11)
 //   col[k][j][sl] counts GESSM(k,j,sl) (1), SSSSM(k,i,j,sl) (i - k + 1)  -- the chain on A_kj
-//   G(k)         <- col[k-1][k][*] >= 2                 (A_kk after step k-1)
-//   L(k,j,sl)    <- panel[k] >= 1;  col[k-1][j][sl] >= 2
-//   T(k,i)       <- panel[k] >= i - k;  col[k-1][k][*] >= i - k + 2
-//   S(k,i,j,sl)  <- panel[k] >= i - k + 1;  col[k][j][sl] >= i - k;  col[k-1][j][sl] >= i - k + 2
+//   G(k,l)       <- PF[k][l-1] >= 1 (l > 0) | col[k-1][k][*] >= 2 (l = 0; A_kk after step k-1)
+//   L(k,j,sl)    <- PF[k][last] >= 1;  col[k-1][j][sl] >= 2
+//   T(k,i,l)     <- PF[k][l] >= i - k;  PF[k][l-1] >= i - k + 1 (l > 0) | col[k-1][k][*] >= i - k + 2
+//   S(k,i,j,sl)  <- PF[k][last] >= i - k + 1;  col[k][j][sl] >= i - k;  col[k-1][j][sl] >= i - k + 2
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -84,30 +85,43 @@ struct LuDur {
   }
 };
 
-void build_lu_sched(int64_t p, int64_t q, int b, int s, int nsl, int w, int workers, Sched& out, int& nctr) {
+void build_lu_sched(int64_t p, int64_t q, int b, int s, int nsl, int w, int workers, Sched& out, int& nctr,
+                    bool split = true) {
+  // split (LU11): GETRF / TSTRF tasks per inner block l -- the flat TSTRF chain on
+  // U_kk becomes a wavefront over (i, l), as for the QR panels (R21).  Block l of a tile touches
+  // U_kk's rows of block l only (its column loop and the trailing update of those rows), so
+  // block lane l is a chain G(k,l) -> T(k,k+1,l) -> T(k,k+2,l) -> ..., and inside a tile
+  // T(k,i,l-1) -> T(k,i,l) (the trailing update of block l-1 feeds block l's columns).
   const int K = (int)std::min(p, q);
-  auto panel = [](int k) { return k; };
-  auto col = [&](int k, int j, int sl) { return K + ((k * (int)q) + j) * nsl + sl; };
-  nctr = K + K * (int)q * nsl;
+  const int NB = split ? b / s : 1;
+  auto PF = [&](int k, int l) { return k * NB + l; };
+  auto col = [&](int k, int j, int sl) { return K * NB + ((k * (int)q) + j) * nsl + sl; };
+  nctr = K * NB + K * (int)q * nsl;
   const LuDur D(b, s, w);
   TaskGen T;
   for (int k = 0; k < K; ++k) {
-    int id = T.add(LK_G, k, k, k, -1, panel(k), 1, D.g, 0);
-    if (k > 0) T.dep(id, col(k - 1, k, 0), nsl, 2);
+    for (int l = 0; l < NB; ++l) {
+      int id = T.add(LK_G, k, k, k, split ? l : -1, PF(k, l), 1, D.g / NB, 0);
+      if (l > 0) T.dep(id, PF(k, l - 1), 1, 1);
+      else if (k > 0) T.dep(id, col(k - 1, k, 0), nsl, 2);
+    }
     for (int j = k + 1; j < q; ++j)
       for (int sl = 0; sl < nsl; ++sl) {
-        id = T.add(LK_L, k, k, j, sl, col(k, j, sl), 1, D.l, 2);
-        T.dep(id, panel(k), 1, 1);
+        int id = T.add(LK_L, k, k, j, sl, col(k, j, sl), 1, D.l, 2);
+        T.dep(id, PF(k, NB - 1), 1, 1);
         if (k > 0) T.dep(id, col(k - 1, j, sl), 1, 2);
       }
     for (int i = k + 1; i < p; ++i) {
-      id = T.add(LK_T, k, i, k, -1, panel(k), i - k + 1, D.t, 1);
-      T.dep(id, panel(k), 1, i - k);
-      if (k > 0) T.dep(id, col(k - 1, k, 0), nsl, i - k + 2);
+      for (int l = 0; l < NB; ++l) {
+        int id = T.add(LK_T, k, i, k, split ? l : -1, PF(k, l), i - k + 1, D.t / NB, 1);
+        T.dep(id, PF(k, l), 1, i - k);
+        if (l > 0) T.dep(id, PF(k, l - 1), 1, i - k + 1);
+        else if (k > 0) T.dep(id, col(k - 1, k, 0), nsl, i - k + 2);
+      }
       for (int j = k + 1; j < q; ++j)
         for (int sl = 0; sl < nsl; ++sl) {
-          id = T.add(LK_S, k, i, j, sl, col(k, j, sl), i - k + 1, D.s, 3);
-          T.dep(id, panel(k), 1, i - k + 1);
+          int id = T.add(LK_S, k, i, j, sl, col(k, j, sl), i - k + 1, D.s, 3);
+          T.dep(id, PF(k, NB - 1), 1, i - k + 1);
           T.dep(id, col(k, j, sl), 1, i - k);
           if (k > 0) T.dep(id, col(k - 1, j, sl), 1, i - k + 2);
         }

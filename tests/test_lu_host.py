@@ -52,27 +52,32 @@ def test_invalid_args_and_support(L):
     assert lib.tlu_plan_create(ctypes.byref(h), ctypes.byref(P)) == 5   # valid, not built
 
 
-def _footprint(rec):
-    """(reads, writes) of one task as region keys; tile (k,k) is split into its U part (upper
-    incl. diagonal: GETRF, TSTRF) and its L part (strict lower: GETRF writes, GESSM reads),
-    update tasks touch one 64-column slice of their tiles (LU7)."""
+def _footprint(rec, nb):
+    """(reads, writes) of one task as region keys (LU7, LU11): ("A", i, j, slice) a
+    64-column slice of tile (i, j) ("all" = the whole tile); ("U", k, l) U_kk's rows of inner block
+    l; ("L", k) A_kk's strict lower part with GETRF's W / interchange slots.  GETRF block l writes
+    the rows of blocks >= l; TSTRF block l touches U_kk's block-l rows only."""
     kind, k, i, j, sl = (int(x) for x in rec[:5])
     if kind == 0:
-        return set(), {("U", k, k), ("L", k, k), ("T", k, k, "all")}
+        ls = range(nb) if sl < 0 else range(sl, nb)
+        return set(), {("A", k, k, "all"), ("L", k)} | {("U", k, l) for l in ls}
     if kind == 1:
-        return {("U", k, k)}, {("U", k, k), ("T", i, k, "all")}
+        ls = range(nb) if sl < 0 else [sl]
+        rw = {("A", i, k, "all")} | {("U", k, l) for l in ls}
+        return set(rw), set(rw)
     if kind == 2:
-        return {("L", k, k), ("T", k, k, "all")}, {("T", k, j, sl)}
-    return {("T", i, k, "all")}, {("T", k, j, sl), ("T", i, j, sl)}
+        return {("L", k)}, {("A", k, j, sl)}
+    return {("A", i, k, "all")}, {("A", k, j, sl), ("A", i, j, sl)}
 
 
-def _sequential_order(p, q, nsl):
-    """oracle_lu.c's order: step k: GETRF, TSTRF(k, i) for all i, then per column j: GESSM, SSSSM chain"""
+def _sequential_order(p, q, nsl, nb):
+    """oracle_lu.c's order, panels by inner block: step k: GETRF(k) blocks, TSTRF(k, i) blocks
+    for all i, then per column j: GESSM, SSSSM chain"""
     K = min(p, q)
     seq = []
     for k in range(K):
-        seq.append((0, k, k, k, -1))
-        seq += [(1, k, i, k, -1) for i in range(k + 1, p)]
+        seq += [(0, k, k, k, l) for l in range(nb)]
+        seq += [(1, k, i, k, l) for i in range(k + 1, p) for l in range(nb)]
         for j in range(k + 1, q):
             for sl in range(nsl):
                 seq.append((2, k, k, j, sl))
@@ -80,59 +85,85 @@ def _sequential_order(p, q, nsl):
     return seq
 
 
-def _conflicts(a, b):
-    ra, wa = _footprint(a)
-    rb, wb = _footprint(b)
+def _key(reg):
+    return reg[:3] if reg[0] == "A" else reg
+
+
+def _conflicts(a, b, nb):
+    ra, wa = _footprint(a, nb)
+    rb, wb = _footprint(b, nb)
     def hit(x, y):  # "all" slices of a tile overlap every slice of it
         for u in x:
             for v in y:
-                if u[:3] == v[:3] and (u[0] != "T" or u[3] == "all" or v[3] == "all" or u[3] == v[3]):
+                if _key(u) == _key(v) and (u[0] != "A" or u[3] == "all" or v[3] == "all" or u[3] == v[3]):
                     return True
         return False
     return hit(wa, rb | wb) or hit(wb, ra)
+
+
+def _replay(rec, nctr, p, q, nsl, nb, workers, seed):
+    """Replay the tickets on `workers` simulated CTAs that finish in random order; a task starts
+    only when its counter dependencies hold.  Returns the first (task, earlier conflicting task
+    not yet done) violation, or None; raises on deadlock."""
+    seq = _sequential_order(p, q, nsl, nb)
+    pos = {t: x for x, t in enumerate(seq)}
+    by_region = {}
+    for t in seq:
+        r_, w_ = _footprint(t, nb)
+        for reg in r_ | w_:
+            by_region.setdefault(_key(reg), []).append(t)
+    rng = random.Random(seed)
+    ctr = [0] * nctr
+    done, running, nxt = set(), [], 0
+    while nxt < len(rec) or running:
+        while nxt < len(rec) and len(running) < workers:
+            running.append(nxt)
+            nxt += 1
+        ready = [t for t in running
+                 if all(ctr[(rec[t][8 + 2 * d] & 0xFFFFFF) + x] >= rec[t][9 + 2 * d]
+                        for d in range(3) for x in range(int(rec[t][8 + 2 * d]) >> 24))]
+        if not ready:
+            raise RuntimeError("deadlock")
+        t = rng.choice(ready)
+        key = tuple(int(v) for v in rec[t][:5])
+        for reg in (lambda rw: rw[0] | rw[1])(_footprint(key, nb)):
+            for other in by_region[_key(reg)]:
+                if pos[other] < pos[key] and _conflicts(other, key, nb) and other not in done:
+                    return key, other
+        running.remove(t)
+        done.add(key)
+        ctr[rec[t][5]] = max(ctr[rec[t][5]], int(rec[t][6]))
+    return None
 
 
 @pytest.mark.parametrize("m,n,b,s,workers", [(256, 256, 64, 16, 3), (320, 192, 64, 16, 5), (192, 320, 64, 16, 4),
                                               (1024, 1024, 256, 32, 7), (640, 384, 128, 32, 6),
                                               (2048, 512, 256, 32, 9)])
 def test_dispatch_order_respects_every_data_dependence(L, m, n, b, s, workers):
-    """Replay the tickets on `workers` simulated CTAs that finish in random order; a task starts
-    only when its counter dependencies hold.  Every pair of tasks that conflict on a region must
-    run in the oracle's sequential order (the earlier one finished before the later starts), and
-    every ticket must eventually run (no deadlock)."""
+    """Every pair of tasks that conflict on a region runs in the oracle's sequential order (the
+    earlier one finished before the later starts), and every ticket eventually runs."""
     rec, nctr = L.schedule_records(m, n, b, s, workers)
     p, q = -(-m // b), -(-n // b)
-    nsl = b // min(64, b)
-    seq = _sequential_order(p, q, nsl)
-    pos = {t: x for x, t in enumerate(seq)}
+    nsl, nb = b // min(64, b), b // s
+    seq = _sequential_order(p, q, nsl, nb)
     assert len(rec) == len(seq) and sorted(tuple(int(v) for v in r[:5]) for r in rec) == sorted(seq)
-    by_region = {}
-    for t in seq:
-        r_, w_ = _footprint(t)
-        for reg in r_ | w_:
-            by_region.setdefault(reg[:3], []).append(t)
     for seed in range(3):
-        rng = random.Random(seed)
-        ctr = [0] * nctr
-        done, running, nxt = set(), [], 0
-        while nxt < len(rec) or running:
-            while nxt < len(rec) and len(running) < workers:
-                running.append(nxt)
-                nxt += 1
-            ready = []
-            for t in running:
-                r = rec[t]
-                ok = all(ctr[(r[8 + 2 * d] & 0xFFFFFF) + x] >= r[9 + 2 * d]
-                         for d in range(3) for x in range(int(r[8 + 2 * d]) >> 24))
-                if ok:
-                    ready.append(t)
-            assert ready, "deadlock"
-            t = rng.choice(ready)
-            key = tuple(int(v) for v in rec[t][:5])
-            for reg in (lambda rw: rw[0] | rw[1])(_footprint(key)):
-                for other in by_region[reg[:3]]:
-                    if pos[other] < pos[key] and _conflicts(other, key):
-                        assert other in done, (key, other)
-            running.remove(t)
-            done.add(key)
-            ctr[rec[t][5]] = max(ctr[rec[t][5]], int(rec[t][6]))
+        assert _replay(rec, nctr, p, q, nsl, nb, workers, seed) is None
+
+
+def test_replay_detects_a_dropped_dependency(L):
+    """Negative control: drop TSTRF(k,i,l)'s dependency on its tile's previous block (or a
+    chain dependency of an SSSSM) and the replay finds the race."""
+    m = n = 512
+    b, s, workers = 128, 32, 6
+    rec, nctr = L.schedule_records(m, n, b, s, workers)
+    p = q = m // b
+    nsl, nb = 2, 4
+    for kind, slot in [(1, 1), (3, 1)]:
+        bad = rec.copy()
+        hits = [t for t in range(len(bad)) if bad[t][0] == kind and (kind != 1 or bad[t][4] > 0)
+                and (bad[t][8 + 2 * slot] >> 24) > 0]
+        for t in hits:
+            bad[t][8 + 2 * slot] = 0
+        found = any(_replay(bad, nctr, p, q, nsl, nb, workers, seed) is not None for seed in range(6))
+        assert found, kind
