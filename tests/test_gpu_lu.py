@@ -184,3 +184,24 @@ def test_lu_trace_covers_every_task():
     tr = g["plan"].trace()
     rec = g["plan"].records()
     assert len(tr) == len(rec) and np.all(tr[:, 7] >= tr[:, 6]) and np.all(tr[:, 6] >= tr[:, 5])
+
+
+def test_lu_full_c3_valid_pairwise_pivoting():
+    """C3's matrix (16384^2, b = 256, s = 32; BASELINE configs[2]) in the bench's launch
+    configuration: the factors are a partial-pivoting elimination (every multiplier and every
+    Ltilde entry <= 1 in magnitude) whose recorded transformation, replayed by the oracle from
+    the GPU's factors, maps A's first and last tile columns to U (backward error < 1 in units of
+    n u ||A|| rho; LU10 -- the whole-matrix oracle factorization takes ~2 minutes on the
+    host and its pivot sequence is decided by rounding at this size)."""
+    n, b, s = 16384, 256, 32
+    A = np.asfortranarray(tqr_inputs.make(n, n, "uniform", 7073551))
+    g = run_lu(A, b, s)
+    p = n // b
+    Lt_g = lt_from_w(g["W"], p, p, b, s)
+    assert max_multiplier(g["At"], n, n, b) <= 1.0 and np.max(np.abs(Lt_g)) <= 1.0 + 1e-12
+    cols = np.r_[0:b, n - b:n]
+    MA = oracle.lu_apply(g["At"], Lt_g, g["piv"], n, n, b, s, np.asfortranarray(A[:, cols]), nthreads=16)
+    rho = np.max(np.abs(g["U"])) / np.max(np.abs(A))
+    be = np.max(np.abs(MA - g["U"][:, cols])) / (n * 2.0 ** -53 * np.max(np.abs(A)) * rho)
+    assert be < 1.0, be
+    assert np.all(np.isfinite(g["U"])) and np.all(np.diag(g["U"]) != 0)
