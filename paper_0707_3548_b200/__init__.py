@@ -6,6 +6,7 @@ is missing raises.
 """
 from .tqr import (Plan, TqrError, colmajor, flops_standard, flops_tiled, from_colmajor, lib, schedule_inspect,
                   supported)
+from .tlu import LUPlan  # the tiled LU (include/tlu.h)
 
-__all__ = ["Plan", "TqrError", "colmajor", "flops_standard", "flops_tiled", "from_colmajor", "lib",
+__all__ = ["LUPlan", "Plan", "TqrError", "colmajor", "flops_standard", "flops_tiled", "from_colmajor", "lib",
            "schedule_inspect", "supported"]
