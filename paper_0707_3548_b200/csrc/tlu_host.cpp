@@ -133,7 +133,9 @@ void build_lu_sched(int64_t p, int64_t q, int b, int s, int nsl, int w, int work
     else if (x.kind == LK_L) out.counts[2]++;
     else out.counts[3]++;
   }
-  if (!list_schedule(T, std::vector<int>{workers}, out, PRIO_BLEVEL, 4000.0)) out.topo_ok = false;
+  double lat = 4000.0;  // per-edge handoff term of the bottom-level priority (development knob)
+  if (const char* e = getenv("TLU_DEV_LAT")) lat = atof(e);
+  if (!list_schedule(T, std::vector<int>{workers}, out, PRIO_BLEVEL, lat)) out.topo_ok = false;
 }
 
 }  // namespace

@@ -449,6 +449,11 @@ static Policy make_policy(int64_t p, int64_t q, int b, int s, bool tall_tiles = 
   // critical-path order); TQR_FLAG_LOCALITY groups them in the first three quarters on every
   // grid (C3: 113 GB of reads, +1.1%)
   if (b >= 256 && !tall) { P.group = 3; P.gtail = 0.5; }
+  // Per-edge handoff term of the bottom-level priority (R10): 4 us fits the b >= 256 grids; on
+  // the panel-chain-bound b <= 128 grids a large term (the bottom level then counts chain hops)
+  // raises the panel chain's priority: C2 6.85 -> 6.46 ms same-box (C3 / C4 unchanged or worse
+  // with large terms, profiles/r02_lat_sweep.txt)
+  if (b <= 128) P.lat = 200000.0;
   if (locality) { P.group = 3; P.gtail = 0.75; }
   if (const char* e = getenv("TQR_DEV_PASSES")) P.passes = std::max(1, atoi(e));   // development knobs
   if (const char* e = getenv("TQR_DEV_SPLIT")) P.split = atoi(e) != 0;
