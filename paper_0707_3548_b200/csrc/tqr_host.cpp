@@ -178,8 +178,14 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   // 1).  h = 1: the square-tile schedule (unit g = tile row k+1+g, v = i-k+1).  A step-k task
   // on tile rows up to `il` waits for step k-1's chain on its column up to the unit holding il:
   auto prevv = [&](int k, int il) { return (il - k) / h + 2; };
+  // modelled durations of a two-tile unit's panel parts (R30; trace fit: factor part 45.8 vs
+  // 34 us, one-block apply sub-task 21 vs 10 us) -- development knobs TQR_DEV_TALLF / _TALLA
+  double tallf = 1.35, talla = 2.1;
+  if (const char* e = getenv("TQR_DEV_TALLF")) tallf = atof(e);
+  if (const char* e = getenv("TQR_DEV_TALLA")) talla = atof(e);
   auto panel = [&](int kind, int k, int i, int il, int v, int cls) {
     const int ok = own(k);
+    const double uf = il > i ? tallf : 1.0, ua = il > i ? talla : 1.0;
     for (int l = 0; l < NPT; ++l) {
       if (!split) {  // fused apply + factor per block (R21 without the A/F split)
         int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l, kind == K_G), cls);
@@ -196,7 +202,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         // A(k,u,l,lp) <- F(k,u,lp), A(k,u,l,lp-1), A(k,u-1,l,lp) (R_kk rows of block lp in
         // block l's columns) -- the unit chain of each stage is one block apply long
         for (int lp = 0; lp < l; ++lp) {
-          int id = T.add(kind, k, i, scol(k), l | ((lp + 1) << 8), PA2(k, l, lp), v, dm.apply_part(1), cls);
+          int id = T.add(kind, k, i, scol(k), l | ((lp + 1) << 8), PA2(k, l, lp), v, ua * dm.apply_part(1), cls);
           T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
           T.t[id].key[3] = l * NPT + lp;
           T.dep(id, PF(k, lp), 1, v);                            // block lp of this unit factored
@@ -213,7 +219,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
         if (k > 0) T.dep(id, COL(k - 1, k, blk_sl0(l)), blk_nsl(l), prevv(k, il));  // block l's columns
         if (il > i) T.t[id].flags |= 128;
       }
-      int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.factor_part(kind == K_G), cls);
+      int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, uf * dm.factor_part(kind == K_G), cls);
       T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1 | 4;
       if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
       if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk diagonal block l: previous tile
