@@ -178,17 +178,21 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
   // 1).  h = 1: the square-tile schedule (unit g = tile row k+1+g, v = i-k+1).  A step-k task
   // on tile rows up to `il` waits for step k-1's chain on its column up to the unit holding il:
   auto prevv = [&](int k, int il) { return (il - k) / h + 2; };
-  // modelled durations of a two-tile unit's panel parts (R30; trace fit: factor part 45.8 vs
-  // 34 us, one-block apply sub-task 21 vs 10 us) -- development knobs TQR_DEV_TALLF / _TALLA
-  double tallf = 1.35, talla = 2.1;
+  // modelled durations of a two-tile unit's panel parts (R30): 2x / 3x the one-tile model (the
+  // trace fit is 1.35x / 2.1x; the larger weights raise the unit chain's priority: C4 with 2b x b
+  // tiles 57.9 (1x) -> 55.6 (fit) -> 53.4 ms, profiles/r02_tall_sweep.txt) -- development knobs
+  // TQR_DEV_TALLF / _TALLA; TQR_DEV_PANF / _PANA scale the one-tile panel parts likewise
+  double tallf = 2.0, talla = 3.0, panf = 1.0, pana = 1.0;
   if (const char* e = getenv("TQR_DEV_TALLF")) tallf = atof(e);
   if (const char* e = getenv("TQR_DEV_TALLA")) talla = atof(e);
+  if (const char* e = getenv("TQR_DEV_PANF")) panf = atof(e);
+  if (const char* e = getenv("TQR_DEV_PANA")) pana = atof(e);
   auto panel = [&](int kind, int k, int i, int il, int v, int cls) {
     const int ok = own(k);
-    const double uf = il > i ? tallf : 1.0, ua = il > i ? talla : 1.0;
+    const double uf = il > i ? tallf : panf, ua = il > i ? talla : pana;
     for (int l = 0; l < NPT; ++l) {
       if (!split) {  // fused apply + factor per block (R21 without the A/F split)
-        int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, dm.panel(l, kind == K_G), cls);
+        int id = T.add(kind, k, i, scol(k), l, PF(k, l), v, uf * dm.panel(l, kind == K_G), cls);
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 1;
         if (early) { T.t[id].out2_idx = PR(k, l); T.t[id].flags |= (PR(k, l) + 1) << 8; }
         if (v > 1) T.dep(id, early ? PR(k, l) : PF(k, l), 1, v - 1);  // R_kk block l: previous tile
@@ -212,7 +216,7 @@ static void build_factor_sched(int64_t p, int64_t q, int b, int s, int nsl, cons
           if (il > i) T.t[id].flags |= 128;
         }
       } else if (l > 0) {
-        int id = T.add(kind, k, i, scol(k), l, PA(k, l), v, dm.apply_part(l), cls);
+        int id = T.add(kind, k, i, scol(k), l, PA(k, l), v, ua * dm.apply_part(l), cls);
         T.t[id].rank = ok; T.t[id].kc = scol(k); T.t[id].flags = 2;
         T.dep(id, PF(k, l - 1), 1, v);                 // this tile's blocks < l factored
         if (v > 1) T.dep(id, PA(k, l), 1, v - 1);      // R_kk rows above block l: previous tile
