@@ -205,3 +205,25 @@ def test_lu_full_c3_valid_pairwise_pivoting():
     be = np.max(np.abs(MA - g["U"][:, cols])) / (n * 2.0 ** -53 * np.max(np.abs(A)) * rho)
     assert be < 1.0, be
     assert np.all(np.isfinite(g["U"])) and np.all(np.diag(g["U"]) != 0)
+
+
+def test_lu_ties_and_rank_deficiency():
+    """Exact ties (small-integer entries: many equal |candidates|, LU5 picks the first on both
+    sides) and rank deficiency (duplicate columns: a zero pivot column, LU6) -- pivots exact and
+    the factors within tolerance, no NaN."""
+    rng = np.random.RandomState(3)
+    A = rng.randint(-2, 3, size=(384, 320)).astype(np.float64)
+    g = run_lu(A, 64, 16)
+    At_o, Lt_o, piv_o = oracle.lu_getrf_tiles(A, 64, 16)
+    assert np.array_equal(g["piv"], piv_o)
+    U_o = oracle.get_r(At_o, 384, 320, 64)
+    assert np.max(np.abs(g["At"] - At_o)) <= _tol(A, U_o)
+    B = tqr_inputs.make(300, 200, "uniform", 8)
+    B[:, 7] = B[:, 3]            # duplicate column
+    B[:, 150] = 0.0              # zero column
+    g = run_lu(B, 64, 16)
+    At_o, Lt_o, piv_o = oracle.lu_getrf_tiles(B, 64, 16)
+    assert np.all(np.isfinite(g["At"])) and np.all(np.isfinite(g["W"]))
+    assert np.array_equal(g["piv"], piv_o)
+    U_o = oracle.get_r(At_o, 300, 200, 64)
+    assert np.max(np.abs(g["At"] - At_o)) <= _tol(B, U_o)
