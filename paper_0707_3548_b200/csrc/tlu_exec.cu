@@ -34,35 +34,33 @@ struct LCfg {
   static_assert(B % 64 == 0 || B == 64, "b: 64, 128, 256");
   static_assert(S % 8 == 0 && B % S == 0 && S <= 32, "s: 8 | s, s | b, s <= 32");
   static constexpr int NB = B / S;
-  // Row-major slices: 8x8 accumulator fragments (16-byte accesses, rows at 528-byte stride),
-  // 16-row x 4-column I/O tiles and whole-row interchanges take the minimum number of shared
-  // wavefronts.  L_l column-major at ld B + 4 (A fragments: 2 wavefronts per 256 bytes).
-  static constexpr int LDY = W + 2;          // Y slice: B rows x W
-  static constexpr int LDX = W + 4;          // X_l: S rows x W
-  static constexpr int LDW = S + 4;          // W_l: S x S column-major
-  static constexpr int LDL = B + 4;          // L_l: B x S column-major
+  static constexpr int LDX = W + 4;          // X_l: S rows x W, row-major (two buffers)
+  static constexpr int LDW = S + 4;          // W_l: S x S column-major (two buffers)
+  static constexpr int LDL = B + 4;          // L_l: B x S column-major (two buffers)
+  static constexpr int LDST = W + 2;         // interchange staging: 2S rows x W, row-major
   static constexpr int LUT = S + 1;          // panel top block, row-major
-  static constexpr int PL = 4 + 4 * S;       // perm ints per block (count, -, -, -, pairs; 16-byte multiple)
+  static constexpr int PL = 4 + 4 * S;       // pair list (count, -, -, -, dst, src, ...)
+  static constexpr int SLT = B + S;          // slot tables: row -> its pair as source / destination
+  static constexpr int PLW = PL + 2 * SLT;   // per-block workspace ints (16-byte multiple)
   static constexpr int RPW = B / 8;          // GEMM rows per warp
   static constexpr int MT = RPW / 8;         // 8-row m-tiles per warp
-  static constexpr int MAXV = (2 * S * W / 2 + NT - 1) / NT;  // 16-byte interchange moves per thread
   // shared memory (doubles)
-  static constexpr int OFF_Y = 0;
-  static constexpr int OFF_X = OFF_Y + B * LDY;
-  static constexpr int OFF_W = OFF_X + S * LDX;
-  static constexpr int OFF_L = OFF_W + S * LDW;
-  static constexpr int OFF_UT = OFF_L;               // the panel's top block (never live with L_l)
-  static constexpr int OFF_BUF = OFF_L + S * LDL;    // 2 x S (GETRF row interchange)
-  static constexpr int OFF_RED = OFF_BUF + 2 * S;    // 8 warp maxima
+  static constexpr int OFF_ST = 0;                       // staging (2S x LDST); the panel's Ut aliases it
+  static constexpr int OFF_UT = OFF_ST;
+  static constexpr int OFF_L = OFF_ST + 2 * S * LDST;    // 2 x S x LDL
+  static constexpr int OFF_X = OFF_L + 2 * S * LDL;      // 2 x S x LDX
+  static constexpr int OFF_W = OFF_X + 2 * S * LDX;      // 2 x S x LDW
+  static constexpr int OFF_BUF = OFF_W + 2 * S * LDW;    // 2 x S (GETRF row interchange)
+  static constexpr int OFF_RED = OFF_BUF + 2 * S;        // 8 warp maxima
   static constexpr int NDBL = (OFF_RED + 8 + 1) & ~1;
-  static_assert(S * LUT <= S * LDL, "Ut fits the L_l area");
+  static_assert(S * LUT <= 2 * S * LDST, "Ut fits the staging area");
   // ints after the doubles
   static constexpr int IOFF_RIDX = 0;                // 8 warp argmax rows
   static constexpr int IOFF_PIV = 8;                 // S pivots of the current block
   static constexpr int IOFF_CUR = IOFF_PIV + S;      // B (GETRF net-permutation simulation)
   static constexpr int IOFF_CNT = IOFF_CUR + B;      // 1
-  static constexpr int IOFF_PL = (IOFF_CNT + 4 + 3) & ~3;  // the block's interchange list (PL ints)
-  static constexpr int NINT = IOFF_PL + PL;
+  static constexpr int IOFF_BLK = (IOFF_CNT + 4 + 3) & ~3;  // 2 x PLW: the blocks' pair lists + slot tables
+  static constexpr int NINT = IOFF_BLK + 2 * PLW;
   static constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4;
 };
 
@@ -75,212 +73,192 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 
-// 16-row x 4-column I/O tiles of an R x W region: element e of this thread's sweep -> (row pair
-// start r, column c): the thread moves rows r, r + 1 of column c (one 16-byte global access;
-// a warp covers 4 columns x 128 contiguous bytes)
-__device__ __forceinline__ void io_rc2(int e, int& r, int& c) {
-  const int lane = e & 31, t = e >> 5;
-  constexpr int CT = W / 4;
-  const int tc = t % CT, tr = t / CT;
-  r = 16 * tr + 2 * (lane >> 2);
-  c = 4 * tc + (lane & 3);
-}
-
-// ---- one inner block of GESSM (SS = false) / SSSSM (SS = true) on the slice in shared memory ----
-// Ys: rows [0, B) x columns [cl, cl + nc) of the target tile (GESSM: A_kj; SSSSM: A_ij), row-major.
-// L: the tile holding block l's multipliers (GESSM: A_kk, rows >= c0 + S; SSSSM: A_ik, all rows).
-// Wl / pl: block l's W_l (S x S, column-major) and net interchange (count, -, -, -, dst, src,
-// ...: index < B = a Y row, B + r = row r of X_l).  C1 (SSSSM): A_kj, whose rows [c0, c0 + S) are X_l.
+// ---- GESSM (SS = false) / SSSSM (SS = true) on one column slice, inner blocks [l0, l1) ----
+// The slice's accumulators stay in registers for the whole run (warp w owns rows
+// [w RPW, (w + 1) RPW) x W columns as 8x8 DMMA fragments).  A block's interchanges move only the
+// rows its pair list names (<= 2S): each row's owner stores it to a staging row if it is a
+// source and reloads it if it is a destination (the precomputed slot tables give the pair; the
+// register index is static -- every m-tile is visited with a per-lane predicate), so no pass
+// moves the whole slice.  Each block's inputs -- L_l (B x S multipliers; GESSM: rows >= c0 + S),
+// W_l, the pair list and slot tables, SSSSM: X_l = C1's rows [c0, c0 + S) -- are double-buffered
+// and prefetched by cp.async one block ahead, so their L2 latency hides behind the previous
+// block's GEMM.  Y: the target tile (GESSM: A_kj, SSSSM: A_ij); L: the multipliers' tile (A_kk /
+// A_ik); Wsl / wsp: the W slot and workspace slot of those factors; C1 (SSSSM): A_kj.  Rows
+// [r_lo, B) of the slice are stored back (GETRF's trailing update: LU11).
 template <int B, int S, bool SS>
-__device__ __noinline__ void apply_block(double* sm, int l, const double* __restrict__ L,
-                                         const double* __restrict__ Wl, const int* __restrict__ pl, double* C1,
-                                         int cl, int nc) {
+__device__ __forceinline__ void issue_inputs(double* sm, int* ism, int l, const double* __restrict__ L,
+                                             const double* __restrict__ Wsl, const int* __restrict__ wsp,
+                                             const double* C1, int cl, int nc) {
   using C = LCfg<B, S>;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  const int c0 = l * S;
-  double* Ys = sm + C::OFF_Y;
-  double* Xs = sm + C::OFF_X;
-  double* Ws = sm + C::OFF_W;
-  double* Ls = sm + C::OFF_L;
-  int* pls = reinterpret_cast<int*>(sm + C::NDBL) + C::IOFF_PL;
-  // SSSSM: X_l = C1's rows [c0, c0 + S) by 16-byte loads into registers (stored to shared memory
-  // below); cp.async group 1: W_l and the interchange list; group 2: L_l (GESSM: only rows
-  // >= c0 + S are used), waited for only before the GEMM, so its L2 latency hides behind the
-  // interchanges and the W_l product
-  constexpr int XPER = S * W / 2 / NT;
-  double2 xv[SS ? XPER : 1];
-  if (SS) {
-#pragma unroll
-    for (int x = 0; x < XPER; ++x) {
-      int r, cc;
-      io_rc2(tid + x * NT, r, cc);
-      xv[x] = cc < nc ? __ldcg(reinterpret_cast<const double2*>(C1 + (c0 + r) + (size_t)(cl + cc) * B))
-                      : make_double2(0.0, 0.0);
-    }
+  const int tid = threadIdx.x, bf = l & 1, c0 = l * S;
+  double* Ls = sm + C::OFF_L + bf * S * C::LDL;
+  double* Xs = sm + C::OFF_X + bf * S * C::LDX;
+  double* Ws = sm + C::OFF_W + bf * S * C::LDW;
+  int* blk = ism + C::IOFF_BLK + bf * C::PLW;
+  const int r_lo = SS ? 0 : c0 + S;
+  const int nv = (B - r_lo) / 2;  // 16-byte granules per column
+  for (int e = tid; e < nv * S; e += NT) {
+    const int v = e % nv, cc = e / nv;
+    cp_async16(Ls + cc * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + cc) * B);
   }
+  const double* Wl = Wsl + (size_t)l * S * S;
   for (int e = tid; e < S * S / 2; e += NT) {
     const int r2 = e % (S / 2), cc = e / (S / 2);
     cp_async16(Ws + cc * C::LDW + 2 * r2, Wl + cc * S + 2 * r2);
   }
-  for (int e = tid; e < C::PL / 4; e += NT) cp_async16(pls + 4 * e, pl + 4 * e);
-  cp_async_commit();
-  {
-    const int r_lo = SS ? 0 : c0 + S;
-    const int nv = (B - r_lo) / 2;  // 16-byte granules per column
-    for (int e = tid; e < nv * S; e += NT) {
-      const int v = e % nv, cc = e / nv;
-      cp_async16(Ls + cc * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + cc) * B);
-    }
-  }
-  cp_async_commit();
+  const int* pl = wsp + l * C::PLW;
+  for (int e = tid; e < C::PLW / 4; e += NT) cp_async16(blk + 4 * e, pl + 4 * e);
   if (SS) {
-#pragma unroll
-    for (int x = 0; x < XPER; ++x) {
-      int r, cc;
-      io_rc2(tid + x * NT, r, cc);
-      Xs[r * C::LDX + cc] = xv[x].x;
-      Xs[(r + 1) * C::LDX + cc] = xv[x].y;
+    for (int e = tid; e < S * W; e += NT) {
+      const int r = e % S, cc = e / S;
+      if (cc < nc) cp_async8(Xs + r * C::LDX + cc, C1 + (c0 + r) + (size_t)(cl + cc) * B);
     }
   }
-  cp_async_wait<1>();
-  __syncthreads();
-  const int np = pls[0];
-  // the block's interchanges: whole rows, 16 bytes per move, into registers, then to the destinations
-  {
-    double2 v[C::MAXV];
+  cp_async_commit();
+}
+
+template <int B, int S, bool SS>
+__device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const double* __restrict__ L,
+                                        const double* __restrict__ Wsl, const int* __restrict__ wsp, double* C1,
+                                        int cl, int nc, int l0, int l1, int r_lo) {
+  using C = LCfg<B, S>;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int r0 = warp * C::RPW;
+  double* St = sm + C::OFF_ST;
+  // the slice into registers (fragment rows r0 + 8 mt + g, columns 8 nt + 2 t4, + 1)
+  double2 acc[C::MT][W / 8];
 #pragma unroll
-    for (int x = 0; x < C::MAXV; ++x) {
-      const int e = tid + x * NT, pe = e / (W / 2), c2 = e % (W / 2);
-      if (pe < np) {
-        const int src = pls[5 + 2 * pe];
-        v[x] = *reinterpret_cast<const double2*>(src < B ? Ys + src * C::LDY + 2 * c2 : Xs + (src - B) * C::LDX + 2 * c2);
+  for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < W / 8; ++nt) {
+      const int row = r0 + 8 * mt + g, col = 8 * nt + 2 * t4;
+      acc[mt][nt].x = col < nc ? __ldcg(Y + row + (size_t)(cl + col) * B) : 0.0;
+      acc[mt][nt].y = col + 1 < nc ? __ldcg(Y + row + (size_t)(cl + col + 1) * B) : 0.0;
+    }
+  issue_inputs<B, S, SS>(sm, ism, l0, L, Wsl, wsp, C1, cl, nc);
+#pragma unroll 1
+  for (int l = l0; l < l1; ++l) {
+    const int bf = l & 1, c0 = l * S;
+    double* Ls = sm + C::OFF_L + bf * S * C::LDL;
+    double* Xs = sm + C::OFF_X + bf * S * C::LDX;
+    const double* Ws = sm + C::OFF_W + bf * S * C::LDW;
+    const int* blk = ism + C::IOFF_BLK + bf * C::PLW;
+    const int* srcs = blk + C::PL;
+    const int* dsts = srcs + C::SLT;
+    cp_async_wait<0>();
+    __syncthreads();  // block l's inputs landed; every thread is past block l - 1
+    if (l + 1 < l1) issue_inputs<B, S, SS>(sm, ism, l + 1, L, Wsl, wsp, C1, cl, nc);
+    // (1) sources -> staging
+#pragma unroll
+    for (int mt = 0; mt < C::MT; ++mt) {
+      const int sl = srcs[r0 + 8 * mt + g];
+      if (sl >= 0) {
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt)
+          *reinterpret_cast<double2*>(St + sl * C::LDST + 8 * nt + 2 * t4) = acc[mt][nt];
+      }
+    }
+    if (SS) {
+      for (int e = tid; e < S * W / 2; e += NT) {
+        const int r = e / (W / 2), c2 = e % (W / 2);
+        const int sl = srcs[B + r];
+        if (sl >= 0)
+          *reinterpret_cast<double2*>(St + sl * C::LDST + 2 * c2) =
+              *reinterpret_cast<const double2*>(Xs + r * C::LDX + 2 * c2);
       }
     }
     __syncthreads();
+    // (2) destinations <- staging
 #pragma unroll
-    for (int x = 0; x < C::MAXV; ++x) {
-      const int e = tid + x * NT, pe = e / (W / 2), c2 = e % (W / 2);
-      if (pe < np) {
-        const int dst = pls[4 + 2 * pe];
-        *reinterpret_cast<double2*>(dst < B ? Ys + dst * C::LDY + 2 * c2 : Xs + (dst - B) * C::LDX + 2 * c2) = v[x];
+    for (int mt = 0; mt < C::MT; ++mt) {
+      const int sl = dsts[r0 + 8 * mt + g];
+      if (sl >= 0) {
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt)
+          acc[mt][nt] = *reinterpret_cast<const double2*>(St + sl * C::LDST + 8 * nt + 2 * t4);
       }
     }
-  }
-  if (!SS) {  // X_l = Y's rows [c0, c0 + S) after the interchanges
-    __syncthreads();
-    for (int e = tid; e < S * W / 2; e += NT) {
-      const int r = e / (W / 2), c2 = e % (W / 2);
-      *reinterpret_cast<double2*>(Xs + r * C::LDX + 2 * c2) =
-          *reinterpret_cast<const double2*>(Ys + (c0 + r) * C::LDY + 2 * c2);
+    if (SS) {
+      for (int e = tid; e < S * W / 2; e += NT) {
+        const int r = e / (W / 2), c2 = e % (W / 2);
+        const int sl = dsts[B + r];
+        if (sl >= 0)
+          *reinterpret_cast<double2*>(Xs + r * C::LDX + 2 * c2) =
+              *reinterpret_cast<const double2*>(St + sl * C::LDST + 2 * c2);
+      }
+    } else if (r0 >= c0 && r0 < c0 + S) {  // GESSM: X_l = Y's rows [c0, c0 + S) (this warp's band)
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt)
+          *reinterpret_cast<double2*>(Xs + (r0 - c0 + 8 * mt + g) * C::LDX + 8 * nt + 2 * t4) = acc[mt][nt];
     }
-  }
-  __syncthreads();
-  // Xs <- W_l Xs  (M = S, N = W, K = S; results in registers until every warp has read Xs)
-  {
-    constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
-    double d[PER][2];
+    __syncthreads();
+    // (3) X_l <- W_l X_l  (M = S, N = W, K = S; in registers until every warp has read X_l)
+    {
+      constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
+      double d[PER][2];
 #pragma unroll
-    for (int x = 0; x < PER; ++x) d[x][0] = d[x][1] = 0.0;
+      for (int x = 0; x < PER; ++x) d[x][0] = d[x][1] = 0.0;
 #pragma unroll
-    for (int ks = 0; ks < S / 4; ++ks)  // k-step outer: the PER accumulator chains interleave
+      for (int ks = 0; ks < S / 4; ++ks)
+#pragma unroll
+        for (int x = 0; x < PER; ++x) {
+          const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
+          dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], Xs[(4 * ks + t4) * C::LDX + 8 * nt + g]);
+        }
+      __syncthreads();
 #pragma unroll
       for (int x = 0; x < PER; ++x) {
         const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
-        dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], Xs[(4 * ks + t4) * C::LDX + 8 * nt + g]);
+        *reinterpret_cast<double2*>(Xs + (8 * mt + g) * C::LDX + 8 * nt + 2 * t4) = make_double2(d[x][0], d[x][1]);
       }
-    cp_async_wait<0>();  // L_l landed (this thread's part; the barrier publishes everyone's)
-    __syncthreads();
-#pragma unroll
-    for (int x = 0; x < PER; ++x) {
-      const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
-      *reinterpret_cast<double2*>(Xs + (8 * mt + g) * C::LDX + 8 * nt + 2 * t4) = make_double2(d[x][0], d[x][1]);
     }
-  }
-  __syncthreads();
-  // Y -= L_l Xs (a warp owns rows [r0, r0 + RPW); GESSM: rows < c0 + S are not updated, and
-  // with RPW | S a warp is wholly above or below)
-  const int r0 = warp * C::RPW;
-  if (SS || r0 >= c0 + S) {
-    double2 acc[C::MT][W / 8];
-#pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < W / 8; ++nt)
-        acc[mt][nt] = *reinterpret_cast<const double2*>(Ys + (r0 + 8 * mt + g) * C::LDY + 8 * nt + 2 * t4);
+    __syncthreads();
+    // (4) Y -= L_l X_l (GESSM: only rows >= c0 + S; the band rows [c0, c0 + S) take X_l)
+    if (SS || r0 >= c0 + S) {
 #pragma unroll 2
-    for (int ks = 0; ks < S / 4; ++ks) {
-      double a[C::MT];
+      for (int ks = 0; ks < S / 4; ++ks) {
+        double a[C::MT];
 #pragma unroll
-      for (int mt = 0; mt < C::MT; ++mt) a[mt] = -Ls[(4 * ks + t4) * C::LDL + r0 + 8 * mt + g];
+        for (int mt = 0; mt < C::MT; ++mt) a[mt] = -Ls[(4 * ks + t4) * C::LDL + r0 + 8 * mt + g];
 #pragma unroll
-      for (int nt = 0; nt < W / 8; ++nt) {
-        const double bb = Xs[(4 * ks + t4) * C::LDX + 8 * nt + g];
+        for (int nt = 0; nt < W / 8; ++nt) {
+          const double bb = Xs[(4 * ks + t4) * C::LDX + 8 * nt + g];
 #pragma unroll
-        for (int mt = 0; mt < C::MT; ++mt) {
-          double d2[2] = {acc[mt][nt].x, acc[mt][nt].y};
-          dmma(d2, a[mt], bb);
-          acc[mt][nt] = make_double2(d2[0], d2[1]);
+          for (int mt = 0; mt < C::MT; ++mt) {
+            double d2[2] = {acc[mt][nt].x, acc[mt][nt].y};
+            dmma(d2, a[mt], bb);
+            acc[mt][nt] = make_double2(d2[0], d2[1]);
+          }
         }
       }
+    } else if (!SS && r0 >= c0) {
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt)
+          acc[mt][nt] = *reinterpret_cast<const double2*>(Xs + (r0 - c0 + 8 * mt + g) * C::LDX + 8 * nt + 2 * t4);
     }
-#pragma unroll
-    for (int mt = 0; mt < C::MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < W / 8; ++nt)
-        *reinterpret_cast<double2*>(Ys + (r0 + 8 * mt + g) * C::LDY + 8 * nt + 2 * t4) = acc[mt][nt];
-  }
-  if (SS) {  // X_l back to C1 (Xs is final since the previous barrier)
-    for (int e = tid; e < S * W / 2; e += NT) {
-      int r, cc;
-      io_rc2(e, r, cc);
-      if (cc < nc)
-        *reinterpret_cast<double2*>(C1 + (c0 + r) + (size_t)(cl + cc) * B) =
-            make_double2(Xs[r * C::LDX + cc], Xs[(r + 1) * C::LDX + cc]);
+    if (SS) {  // (5) X_l back to C1's rows [c0, c0 + S)
+      for (int e = tid; e < S * W; e += NT) {
+        const int r = e % S, cc = e / S;
+        if (cc < nc) C1[(c0 + r) + (size_t)(cl + cc) * B] = Xs[r * C::LDX + cc];
+      }
     }
-    __syncthreads();
-  } else {
-    __syncthreads();
-    for (int e = tid; e < S * W / 2; e += NT) {
-      const int r = e / (W / 2), c2 = e % (W / 2);
-      *reinterpret_cast<double2*>(Ys + (c0 + r) * C::LDY + 2 * c2) =
-          *reinterpret_cast<const double2*>(Xs + r * C::LDX + 2 * c2);
+  }
+  // the slice back (rows >= r_lo)
+#pragma unroll
+  for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < W / 8; ++nt) {
+      const int row = r0 + 8 * mt + g, col = 8 * nt + 2 * t4;
+      if (row >= r_lo) {
+        if (col < nc) Y[row + (size_t)(cl + col) * B] = acc[mt][nt].x;
+        if (col + 1 < nc) Y[row + (size_t)(cl + col + 1) * B] = acc[mt][nt].y;
+      }
     }
-    __syncthreads();
-  }
-}
-
-template <int B, int S>
-__device__ __noinline__ void load_slice(double* Ys, const double* tile, int cl, int nc) {
-  using C = LCfg<B, S>;
-  constexpr int PER = B * W / 2 / NT;
-  double2 v[PER];
-#pragma unroll
-  for (int x = 0; x < PER; ++x) {
-    int r, c;
-    io_rc2(threadIdx.x + x * NT, r, c);
-    v[x] = c < nc ? __ldcg(reinterpret_cast<const double2*>(tile + r + (size_t)(cl + c) * B)) : make_double2(0.0, 0.0);
-  }
-#pragma unroll
-  for (int x = 0; x < PER; ++x) {
-    int r, c;
-    io_rc2(threadIdx.x + x * NT, r, c);
-    Ys[r * C::LDY + c] = v[x].x;
-    Ys[(r + 1) * C::LDY + c] = v[x].y;
-  }
   __syncthreads();
-}
-// rows [r_lo, B) only (GETRF's trailing update: the rows above block l hold U rows that the
-// concurrent TSTRF tasks of earlier blocks update in these columns, LU11)
-template <int B, int S>
-__device__ __noinline__ void store_slice(const double* Ys, double* tile, int cl, int nc, int r_lo = 0) {
-  using C = LCfg<B, S>;
-  for (int e = threadIdx.x; e < B * W / 2; e += NT) {
-    int r, c;
-    io_rc2(e, r, c);
-    if (c < nc && r >= r_lo)
-      *reinterpret_cast<double2*>(tile + r + (size_t)(cl + c) * B) =
-          make_double2(Ys[r * C::LDY + c], Ys[(r + 1) * C::LDY + c]);
-  }
 }
 
 // block-wide argmax of v (ties: the smaller index); every thread gets (value, index)
@@ -326,6 +304,23 @@ __device__ __forceinline__ void build_w(const double* Ut, double* Wl) {
 #pragma unroll
     for (int r = 0; r < S; ++r) Wl[tid * S + r] = w[r];
   }
+}
+
+// the block's slot tables from its pair list (written by this CTA just before): row -> the
+// index of the pair that has it as source / destination, -1 if none (rows [0, B): Y, [B, B + S): X)
+template <int B, int S>
+__device__ __forceinline__ void build_slots(int* pl) {
+  using C = LCfg<B, S>;
+  int* srcs = pl + C::PL;
+  int* dsts = srcs + C::SLT;
+  for (int e = threadIdx.x; e < C::SLT; e += NT) srcs[e] = dsts[e] = -1;
+  __syncthreads();
+  const int np = __ldcg(pl);
+  for (int e = threadIdx.x; e < np; e += NT) {
+    dsts[__ldcg(pl + 4 + 2 * e)] = e;
+    srcs[__ldcg(pl + 5 + 2 * e)] = e;
+  }
+  __syncthreads();
 }
 
 // GETRF(k) on tile Akk (LU1)
@@ -389,7 +384,7 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
     if (tid == 0) ism[C::IOFF_CNT] = 0;
     __syncthreads();
     double* Wl = Wsl + (size_t)l * S * S;
-    int* pl = perms + l * C::PL;
+    int* pl = perms + l * C::PLW;
     build_w<B, S>(Ut, Wl);
     if (tid < S) pivs[c0 + tid] = spiv[tid];
     if (tid == 0) {  // net permutation of the block's interchanges (at most 2S rows move)
@@ -409,13 +404,9 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
     __syncthreads();
     if (tid == 0) pl[0] = ism[C::IOFF_CNT];
     __syncthreads();
-    for (int cl = c0 + S; cl < B; cl += W) {
-      const int nc = min(W, B - cl);
-      load_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc);
-      apply_block<B, S, false>(sm, l, Akk, Wl, pl, nullptr, cl, nc);
-      store_slice<B, S>(sm + C::OFF_Y, Akk, cl, nc, c0);
-      __syncthreads();
-    }
+    build_slots<B, S>(pl);
+    for (int cl = c0 + S; cl < B; cl += W)
+      update_run<B, S, false>(sm, ism, Akk, Akk, Wsl, perms, nullptr, cl, min(W, B - cl), l, l + 1, c0);
   }
 }
 
@@ -475,7 +466,7 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
       if (c >= r) Ukk[(c0 + r) + (size_t)(c0 + c) * B] = Ut[r * C::LUT + c];
     }
     double* Wl = Wsl + (size_t)l * S * S;
-    int* pl = perms + l * C::PL;
+    int* pl = perms + l * C::PLW;
     build_w<B, S>(Ut, Wl);
     if (tid < S) pivs[c0 + tid] = spiv[tid];
     if (warp == 0) {  // net permutation: X row j <- (previous X row with the same A row) or A row; A row <- last X row
@@ -501,13 +492,9 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
       if (lane == 0) pl[0] = __popc(m1) + __popc(m2);
     }
     __syncthreads();
-    for (int cl = c0 + S; cl < B; cl += W) {
-      const int nc = min(W, B - cl);
-      load_slice<B, S>(sm + C::OFF_Y, Aik, cl, nc);
-      apply_block<B, S, true>(sm, l, Aik, Wl, pl, Ukk, cl, nc);
-      store_slice<B, S>(sm + C::OFF_Y, Aik, cl, nc);
-      __syncthreads();
-    }
+    build_slots<B, S>(pl);
+    for (int cl = c0 + S; cl < B; cl += W)
+      update_run<B, S, true>(sm, ism, Aik, Aik, Wsl, perms, Ukk, cl, min(W, B - cl), l, l + 1, 0);
   }
 }
 
@@ -516,18 +503,15 @@ template <int B, int S, bool SS>
 __device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int i, int j, int sl) {
   using C = LCfg<B, S>;
   const int p = a.p;
-  const int vr = SS ? i : k;  // tile row of the multipliers / W / perm applied
+  const int vr = SS ? i : k;  // tile row of the multipliers / W / interchange lists applied
   double* Y = a.A + ((size_t)(SS ? i : k) + (size_t)j * p) * B * B;
   const double* L = a.A + ((size_t)vr + (size_t)k * p) * B * B;
   const double* Wsl = wslot_ptr(a.W, vr, k, p, B, S);
-  const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PL;
+  const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PLW;
   double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
-  const int cl = sl * W, nc = min(W, B - cl);
-  load_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
-#pragma unroll 1
-  for (int l = 0; l < C::NB; ++l)
-    apply_block<B, S, SS>(sm, l, L, Wsl + (size_t)l * S * S, perms + l * C::PL, SS ? C1 : nullptr, cl, nc);
-  store_slice<B, S>(sm + C::OFF_Y, Y, cl, nc);
+  const int cl = sl * W;
+  update_run<B, S, SS>(sm, reinterpret_cast<int*>(sm + C::NDBL), Y, L, Wsl, perms, SS ? C1 : nullptr, cl,
+                       min(W, B - cl), 0, C::NB, 0);
 }
 
 template <int B, int S>
@@ -573,11 +557,11 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
     const int l0 = sl < 0 ? 0 : sl, l1 = sl < 0 ? C::NB : sl + 1;
     if (kind == LK_G) {
       getrf_task<B, S>(sm, ism, Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
-                       a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PL, l0, l1);
+                       a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_T) {
       double* Aik = a.A + ((size_t)i + (size_t)k * p) * B * B;
       tstrf_task<B, S>(sm, ism, Akk, Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
-                       a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PL, l0, l1);
+                       a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_S) {
       update_task<B, S, true>(sm, a, k, i, j, sl);
     } else {
@@ -629,7 +613,7 @@ bool lu_supported(int b, int s) {
   return false;
 }
 int lu_slice(int b, int s) { return lu_supported(b, s) ? (b < W ? b : W) : 0; }
-int lu_perm_ints(int b, int s) { return (b / s) * (4 + 4 * s); }
+int lu_perm_ints(int b, int s) { return (b / s) * (4 + 4 * s + 2 * (b + s)); }
 int lu_max_ctas(int b, int s, int device) {
 #define MC(BB, SS) if (b == BB && s == SS) return max_ctas_inst<BB, SS>(device);
   LU_INSTANCES(MC)
