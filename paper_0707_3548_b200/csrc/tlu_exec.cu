@@ -85,6 +85,15 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
 // block's GEMM.  Y: the target tile (GESSM: A_kj, SSSSM: A_ij); L: the multipliers' tile (A_kk /
 // A_ik); Wsl / wsp: the W slot and workspace slot of those factors; C1 (SSSSM): A_kj.  Rows
 // [r_lo, B) of the slice are stored back (GETRF's trailing update: LU11).
+// element e of an R x W row-major shared tile <-> column-major global: 8-row x 4-column warp
+// tiles (global: 4 runs of 64 bytes; shared at ld W + 4: the minimum number of wavefronts)
+__device__ __forceinline__ void io_rc(int e, int& r, int& c) {
+  const int lane = e & 31, t = e >> 5;
+  constexpr int CT = W / 4;
+  r = 8 * (t / CT) + (lane >> 2);
+  c = 4 * (t % CT) + (lane & 3);
+}
+
 template <int B, int S, bool SS>
 __device__ __forceinline__ void issue_inputs(double* sm, int* ism, int l, const double* __restrict__ L,
                                              const double* __restrict__ Wsl, const int* __restrict__ wsp,
@@ -110,7 +119,8 @@ __device__ __forceinline__ void issue_inputs(double* sm, int* ism, int l, const 
   for (int e = tid; e < C::PLW / 4; e += NT) cp_async16(blk + 4 * e, pl + 4 * e);
   if (SS) {
     for (int e = tid; e < S * W; e += NT) {
-      const int r = e % S, cc = e / S;
+      int r, cc;
+      io_rc(e, r, cc);
       if (cc < nc) cp_async8(Xs + r * C::LDX + cc, C1 + (c0 + r) + (size_t)(cl + cc) * B);
     }
   }
@@ -125,6 +135,7 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int r0 = warp * C::RPW;
   double* St = sm + C::OFF_ST;
+  issue_inputs<B, S, SS>(sm, ism, l0, L, Wsl, wsp, C1, cl, nc);
   // the slice into registers (fragment rows r0 + 8 mt + g, columns 8 nt + 2 t4, + 1)
   double2 acc[C::MT][W / 8];
 #pragma unroll
@@ -135,7 +146,6 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
       acc[mt][nt].x = col < nc ? __ldcg(Y + row + (size_t)(cl + col) * B) : 0.0;
       acc[mt][nt].y = col + 1 < nc ? __ldcg(Y + row + (size_t)(cl + col + 1) * B) : 0.0;
     }
-  issue_inputs<B, S, SS>(sm, ism, l0, L, Wsl, wsp, C1, cl, nc);
 #pragma unroll 1
   for (int l = l0; l < l1; ++l) {
     const int bf = l & 1, c0 = l * S;
@@ -242,7 +252,8 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
     }
     if (SS) {  // (5) X_l back to C1's rows [c0, c0 + S)
       for (int e = tid; e < S * W; e += NT) {
-        const int r = e % S, cc = e / S;
+        int r, cc;
+        io_rc(e, r, cc);
         if (cc < nc) C1[(c0 + r) + (size_t)(cl + cc) * B] = Xs[r * C::LDX + cc];
       }
     }
