@@ -330,6 +330,10 @@ def run_lu(args, cfg, rank, world, local):
             parity.update(lu_property_parity(At.cpu().numpy(), W.cpu().numpy(), piv_g, U_g, A_host, b, s, threads,
                                              [0, qq - 1]))
     achieved = flops / (kern_ms * 1e-3) / 1e12
+    try:  # one ncu --set full capture of the LU executor on this workload (profiles/traffic.json)
+        lu_traffic = json.load(open(os.path.join(ROOT, "profiles", "traffic.json"))).get("LU_" + args.config)
+    except (OSError, ValueError):
+        lu_traffic = None
     line = {"metric": LU_METRIC, "method": "lu", "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -341,7 +345,9 @@ def run_lu(args, cfg, rank, world, local):
             "pct_of_fp64_peak": 100.0 * value / (FP64_PEAK_TFLOPS * 1e3),
             "executed_gflops": tlu.flops_tiled(m, n, b, s) / (ms * 1e-3) / 1e9,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
-                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "frac": achieved / FP64_PEAK_TFLOPS, "traffic": lu_traffic and lu_traffic["bytes"],
+                         "traffic_source": lu_traffic and (f"dram__bytes_read.sum + dram__bytes_write.sum per "
+                                                           f"launch, {lu_traffic['source']}"),
                          "kernel": f"lu_exec_kernel<{b},{s}> (tlu_getrf)", "kernel_ms": kern_ms,
                          "flops_per_launch": flops,
                          "peak_source": "fp64 DMMA.8x8x4 measured 37.14 TFLOP/s (profiles/r01_m0_fp64_probe.txt)"},

@@ -28,12 +28,25 @@ namespace lu {
 
 constexpr int NT = 256;
 constexpr int W = 64;  // update slice width (columns)
+#ifndef LU_KU
+#define LU_KU 8  // unroll of the update GEMM's k-steps (C3 LU: 2 -> 180.8 ms, 4 -> 180.9, 8 -> 178.0)
+#endif
+#ifndef LU_PF
+#define LU_PF 1  // L2 prefetch of the task this many ticket rounds ahead (0: off; development knob;
+                 // same-box C3 LU: off 178.1-178.4 ms, 1 round 176.1, 2 rounds 178.8, 4 rounds 177.0)
+#endif
+#define LU_STR(x) #x
+#define LU_UNROLL(n) _Pragma(LU_STR(unroll n))
 
 template <int B, int S>
 struct LCfg {
   static_assert(B % 64 == 0 || B == 64, "b: 64, 128, 256");
   static_assert(S % 8 == 0 && B % S == 0 && S <= 32, "s: 8 | s, s | b, s <= 32");
   static constexpr int NB = B / S;
+  // LU12: the update forms Y -= (L_l W_l) X_l next to X_l <- W_l X_l (b = 256: C3 LU 190.9 ->
+  // 180.8 ms); at b <= 128 the panel chain bounds the run and the panels' Ltilde products cost
+  // more than the updates gain (C2 LU 8.74 -> 9.22 ms), so those instances keep L_l
+  static constexpr bool LT = B >= 256;
   static constexpr int LDX = W + 4;          // X_l: S rows x W, row-major (two buffers)
   static constexpr int LDW = S + 4;          // W_l: S x S column-major (two buffers)
   static constexpr int LDL = B + 4;          // L_l: B x S column-major (two buffers)
@@ -53,7 +66,7 @@ struct LCfg {
   static constexpr int OFF_BUF = OFF_W + 2 * S * LDW;    // 2 x S (GETRF row interchange)
   static constexpr int OFF_RED = OFF_BUF + 2 * S;        // 8 warp maxima
   static constexpr int NDBL = (OFF_RED + 8 + 1) & ~1;
-  static_assert(S * LUT <= 2 * S * LDST, "Ut fits the staging area");
+  static_assert(S * LUT + S * S <= 2 * S * LDST, "Ut and the panel's W_l copy fit the staging area");
   // ints after the doubles
   static constexpr int IOFF_RIDX = 0;                // 8 warp argmax rows
   static constexpr int IOFF_PIV = 8;                 // S pivots of the current block
@@ -204,6 +217,88 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
           *reinterpret_cast<double2*>(Xs + (r0 - c0 + 8 * mt + g) * C::LDX + 8 * nt + 2 * t4) = acc[mt][nt];
     }
     __syncthreads();
+    if constexpr (C::LT) {
+    // (3) X_l <- W_l X_l and (4) Y -= Ltilde_l X_l, both from the interchanged X_l (Ltilde_l =
+    // L_l W_l, formed once by the panel: LU12), so neither waits for the other and no barrier
+    // separates them.  SSSSM: warp w forms the X_l fragments f = w + 8x (M = S, N = W, K = S) and
+    // stores them straight to C1's rows [c0, c0 + S); GESSM: the band warps (rows [c0, c0 + S))
+    // form their own rows of W_l X_l, the others update.
+    if (SS) {
+      constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
+      double d[PER][2];
+#pragma unroll
+      for (int x = 0; x < PER; ++x) d[x][0] = d[x][1] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < S / 4; ++ks)
+#pragma unroll
+        for (int x = 0; x < PER; ++x) {
+          const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
+          dmma(d[x], Ws[(4 * ks + t4) * C::LDW + 8 * mt + g], Xs[(4 * ks + t4) * C::LDX + 8 * nt + g]);
+        }
+      LU_UNROLL(LU_KU)
+      for (int ks = 0; ks < S / 4; ++ks) {
+        double a[C::MT];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) a[mt] = -Ls[(4 * ks + t4) * C::LDL + r0 + 8 * mt + g];
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt) {
+          const double bb = Xs[(4 * ks + t4) * C::LDX + 8 * nt + g];
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt) {
+            double d2[2] = {acc[mt][nt].x, acc[mt][nt].y};
+            dmma(d2, a[mt], bb);
+            acc[mt][nt] = make_double2(d2[0], d2[1]);
+          }
+        }
+      }
+      // (5) X_l back to C1's rows [c0, c0 + S), from the fragments' registers
+#pragma unroll
+      for (int x = 0; x < PER; ++x) {
+        const int f = warp + 8 * x, mt = f % SMT, nt = f / SMT;
+        const int row = c0 + 8 * mt + g, col = 8 * nt + 2 * t4;
+        if (col < nc) C1[row + (size_t)(cl + col) * B] = d[x][0];
+        if (col + 1 < nc) C1[row + (size_t)(cl + col + 1) * B] = d[x][1];
+      }
+    } else if (r0 >= c0 + S) {
+      LU_UNROLL(LU_KU)
+      for (int ks = 0; ks < S / 4; ++ks) {
+        double a[C::MT];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) a[mt] = -Ls[(4 * ks + t4) * C::LDL + r0 + 8 * mt + g];
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt) {
+          const double bb = Xs[(4 * ks + t4) * C::LDX + 8 * nt + g];
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt) {
+            double d2[2] = {acc[mt][nt].x, acc[mt][nt].y};
+            dmma(d2, a[mt], bb);
+            acc[mt][nt] = make_double2(d2[0], d2[1]);
+          }
+        }
+      }
+    } else if (r0 >= c0) {  // GESSM band rows: acc <- (W_l X_l)'s rows r0 - c0 + [0, RPW)
+#pragma unroll
+      for (int mt = 0; mt < C::MT; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt) acc[mt][nt] = make_double2(0.0, 0.0);
+#pragma unroll 2
+      for (int ks = 0; ks < S / 4; ++ks) {
+        double a[C::MT];
+#pragma unroll
+        for (int mt = 0; mt < C::MT; ++mt) a[mt] = Ws[(4 * ks + t4) * C::LDW + (r0 - c0) + 8 * mt + g];
+#pragma unroll
+        for (int nt = 0; nt < W / 8; ++nt) {
+          const double bb = Xs[(4 * ks + t4) * C::LDX + 8 * nt + g];
+#pragma unroll
+          for (int mt = 0; mt < C::MT; ++mt) {
+            double d2[2] = {acc[mt][nt].x, acc[mt][nt].y};
+            dmma(d2, a[mt], bb);
+            acc[mt][nt] = make_double2(d2[0], d2[1]);
+          }
+        }
+      }
+    }
+    } else {  // b < 256: W_l X_l first, then Y -= L_l X_l (the panels skip Ltilde, LU12)
     // (3) X_l <- W_l X_l  (M = S, N = W, K = S; in registers until every warp has read X_l)
     {
       constexpr int SMT = S / 8, NNT = W / 8, PER = SMT * NNT / 8;
@@ -257,6 +352,7 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
         if (cc < nc) C1[(c0 + r) + (size_t)(cl + cc) * B] = Xs[r * C::LDX + cc];
       }
     }
+    }
   }
   // the slice back (rows >= r_lo)
 #pragma unroll
@@ -296,7 +392,7 @@ __device__ __forceinline__ void block_argmax(double* sm, int* ism, double v, int
 
 // W_l = (I + strict lower of Ut)^{-1} (unit lower; LU8), column c = thread c, stored column-major
 template <int B, int S>
-__device__ __forceinline__ void build_w(const double* Ut, double* Wl) {
+__device__ __forceinline__ void build_w(const double* Ut, double* Wl, double* Wsm) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x;
   if (tid < S) {
@@ -313,7 +409,31 @@ __device__ __forceinline__ void build_w(const double* Ut, double* Wl) {
       }
     }
 #pragma unroll
-    for (int r = 0; r < S; ++r) Wl[tid * S + r] = w[r];
+    for (int r = 0; r < S; ++r) {
+      Wl[tid * S + r] = w[r];
+      Wsm[tid * S + r] = w[r];
+    }
+  }
+}
+
+// Ltilde_l = L_l W_l for rows [r_lo, B) of the block's multipliers (thread r holds row r in x;
+// W_l unit lower, column-major in Wsm, 16-byte aligned), into the workspace tile Lt: the update tasks then form
+// Y -= Ltilde_l X_l from the interchanged X_l, independent of X_l <- W_l X_l (LU12)
+template <int B, int S>
+__device__ __forceinline__ void store_ltilde(const double (&x)[S], const double* Wsm, double* Lt, int c0, int r_lo) {
+  const int tid = threadIdx.x;
+  if (tid >= r_lo && tid < B) {
+#pragma unroll
+    for (int c = 0; c < S; ++c) {  // column c of W_l is stored whole (zeros above, 1 on the diagonal)
+      double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+      for (int t = c & ~1; t < S; t += 2) {  // 16-byte broadcast loads of W_l
+        const double2 w2 = *reinterpret_cast<const double2*>(Wsm + c * S + t);
+        a0 = fma(x[t], w2.x, a0);
+        a1 = fma(x[t + 1], w2.y, a1);
+      }
+      Lt[tid + (size_t)(c0 + c) * B] = a0 + a1;
+    }
   }
 }
 
@@ -336,8 +456,8 @@ __device__ __forceinline__ void build_slots(int* pl) {
 
 // GETRF(k) on tile Akk (LU1)
 template <int B, int S>
-__device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, double* Wsl, int* pivs, int* perms,
-                                        int l0, int l1) {
+__device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, double* Lkk, double* Wsl, int* pivs,
+                                        int* perms, int l0, int l1) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x;
   double* Ut = sm + C::OFF_UT;
@@ -396,7 +516,8 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
     __syncthreads();
     double* Wl = Wsl + (size_t)l * S * S;
     int* pl = perms + l * C::PLW;
-    build_w<B, S>(Ut, Wl);
+    double* Wsm = Ut + S * C::LUT;
+    build_w<B, S>(Ut, Wl, Wsm);
     if (tid < S) pivs[c0 + tid] = spiv[tid];
     if (tid == 0) {  // net permutation of the block's interchanges (at most 2S rows move)
       for (int jj = 0; jj < S; ++jj) {
@@ -407,6 +528,7 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
       }
     }
     __syncthreads();
+    if constexpr (C::LT) store_ltilde<B, S>(x, Wsm, Lkk, c0, c0 + S);
     if (tid < B && cur[tid] != tid) {
       const int e = atomicAdd(ism + C::IOFF_CNT, 1);
       pl[4 + 2 * e] = tid;
@@ -417,14 +539,14 @@ __device__ __noinline__ void getrf_task(double* sm, int* ism, double* Akk, doubl
     __syncthreads();
     build_slots<B, S>(pl);
     for (int cl = c0 + S; cl < B; cl += W)
-      update_run<B, S, false>(sm, ism, Akk, Akk, Wsl, perms, nullptr, cl, min(W, B - cl), l, l + 1, c0);
+      update_run<B, S, false>(sm, ism, Akk, Lkk, Wsl, perms, nullptr, cl, min(W, B - cl), l, l + 1, c0);
   }
 }
 
 // TSTRF(k,i) on [U_kk; A_ik] (LU3)
 template <int B, int S>
-__device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Wsl, int* pivs, int* perms,
-                                        int l0, int l1) {
+__device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, double* Aik, double* Lik, double* Wsl, int* pivs,
+                                        int* perms, int l0, int l1) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   double* Ut = sm + C::OFF_UT;
@@ -478,7 +600,8 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
     }
     double* Wl = Wsl + (size_t)l * S * S;
     int* pl = perms + l * C::PLW;
-    build_w<B, S>(Ut, Wl);
+    double* Wsm = Ut + S * C::LUT;
+    build_w<B, S>(Ut, Wl, Wsm);
     if (tid < S) pivs[c0 + tid] = spiv[tid];
     if (warp == 0) {  // net permutation: X row j <- (previous X row with the same A row) or A row; A row <- last X row
       const int r = lane < S ? spiv[lane] : -1;
@@ -503,9 +626,10 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
       if (lane == 0) pl[0] = __popc(m1) + __popc(m2);
     }
     __syncthreads();
+    if constexpr (C::LT) store_ltilde<B, S>(x, Wsm, Lik, c0, 0);
     build_slots<B, S>(pl);
     for (int cl = c0 + S; cl < B; cl += W)
-      update_run<B, S, true>(sm, ism, Aik, Aik, Wsl, perms, Ukk, cl, min(W, B - cl), l, l + 1, 0);
+      update_run<B, S, true>(sm, ism, Aik, Lik, Wsl, perms, Ukk, cl, min(W, B - cl), l, l + 1, 0);
   }
 }
 
@@ -516,13 +640,32 @@ __device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int
   const int p = a.p;
   const int vr = SS ? i : k;  // tile row of the multipliers / W / interchange lists applied
   double* Y = a.A + ((size_t)(SS ? i : k) + (size_t)j * p) * B * B;
-  const double* L = a.A + ((size_t)vr + (size_t)k * p) * B * B;
+  const double* L = (C::LT ? a.Lw : a.A) + ((size_t)vr + (size_t)k * p) * B * B;  // Ltilde (LU12) / L
   const double* Wsl = wslot_ptr(a.W, vr, k, p, B, S);
   const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PLW;
   double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
   const int cl = sl * W;
   update_run<B, S, SS>(sm, reinterpret_cast<int*>(sm + C::NDBL), Y, L, Wsl, perms, SS ? C1 : nullptr, cl,
                        min(W, B - cl), 0, C::NB, 0);
+}
+
+// L2 prefetch of the target of task record q (update: its tile-column slice, 128 KiB contiguous;
+// panel: its block's columns), issued LU_PF ticket rounds ahead (148 tickets per round).  A hint only: L2 is coherent,
+// so prefetching before the task's dependencies hold is safe; the slice loads at the start of
+// an update task then hit L2 instead of HBM.
+template <int B, int S>
+__device__ __forceinline__ void lu_prefetch(const LuArgs& a, const int* q) {
+  const int kind = q[0], k = q[1], i = q[2], j = q[3], sl = q[4];
+  const int p = a.p;
+  if (kind == LK_S || kind == LK_L) {
+    const double* Y = a.A + ((size_t)(kind == LK_S ? i : k) + (size_t)j * p) * B * B;
+    const int cl = sl * W, nc = min(W, B - cl);
+    prefetch_l2(Y + (size_t)cl * B, (unsigned)(nc * B * 8));
+  } else {
+    const double* T = a.A + ((size_t)(kind == LK_T ? i : k) + (size_t)k * p) * B * B;
+    const int l0 = sl < 0 ? 0 : sl, nb = sl < 0 ? B / S : 1;
+    prefetch_l2(T + (size_t)l0 * S * B, (unsigned)(nb * S * B * 8));
+  }
 }
 
 template <int B, int S>
@@ -567,11 +710,11 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
     // panel tasks: inner block sl (record [4]; -1: the whole tile)
     const int l0 = sl < 0 ? 0 : sl, l1 = sl < 0 ? C::NB : sl + 1;
     if (kind == LK_G) {
-      getrf_task<B, S>(sm, ism, Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
+      getrf_task<B, S>(sm, ism, Akk, C::LT ? a.Lw + ((size_t)k + (size_t)k * p) * B * B : Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
                        a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_T) {
       double* Aik = a.A + ((size_t)i + (size_t)k * p) * B * B;
-      tstrf_task<B, S>(sm, ism, Akk, Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
+      tstrf_task<B, S>(sm, ism, Akk, Aik, C::LT ? a.Lw + ((size_t)i + (size_t)k * p) * B * B : Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
                        a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_S) {
       update_task<B, S, true>(sm, a, k, i, j, sl);
@@ -579,6 +722,11 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
       update_task<B, S, false>(sm, a, k, i, j, sl);
     }
     __syncthreads();
+    if (LU_PF > 0 && C::LT && tid == 32) {  // overlaps thread 0's release and next ticket round trip
+      // (b = 256 only: at b = 128 the panel chain bounds the run; C2 LU 8.83 -> 8.90 ms with it)
+      const int nx = tk + LU_PF * (int)gridDim.x;
+      if (nx < a.ntasks) lu_prefetch<B, S>(a, a.tasks + (size_t)nx * TASK_INTS);
+    }
     if (tid == 0) {
       __threadfence();
       st_release(a.ctr + s_task[5], s_task[6]);
@@ -624,6 +772,12 @@ bool lu_supported(int b, int s) {
   return false;
 }
 int lu_slice(int b, int s) { return lu_supported(b, s) ? (b < W ? b : W) : 0; }
+bool lu_uses_ltilde(int b, int s) {
+#define LT_(BB, SS) if (b == BB && s == SS) return LCfg<BB, SS>::LT;
+  LU_INSTANCES(LT_)
+#undef LT_
+  return false;
+}
 int lu_perm_ints(int b, int s) { return (b / s) * (4 + 4 * s + 2 * (b + s)); }
 int lu_max_ctas(int b, int s, int device) {
 #define MC(BB, SS) if (b == BB && s == SS) return max_ctas_inst<BB, SS>(device);

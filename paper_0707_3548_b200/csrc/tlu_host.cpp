@@ -255,10 +255,18 @@ tqr_status tlu_sizes(const tlu_plan* P, size_t* a_doubles, size_t* w_doubles, si
   return TQR_OK;
 }
 
+// workspace = the blocks' interchange lists, then (16-byte aligned) the Ltilde tiles (LU12)
+static size_t perm_bytes(const tlu_plan* P) {
+  const size_t n = sizeof(int) * (size_t)P->p * (size_t)P->K * (size_t)lu_perm_ints(P->prm.b, P->prm.s);
+  return (n + 15) & ~(size_t)15;
+}
+
 tqr_status tlu_workspace_size(const tlu_plan* P, size_t* bytes) {
   if (!P) return bad(1, "plan is NULL");
   if (!bytes) return bad(2, "bytes is NULL");
-  *bytes = sizeof(int) * (size_t)P->p * (size_t)P->K * (size_t)lu_perm_ints(P->prm.b, P->prm.s);
+  *bytes = perm_bytes(P);
+  if (lu_uses_ltilde(P->prm.b, P->prm.s))
+    *bytes += sizeof(double) * (size_t)P->p * (size_t)P->K * (size_t)P->prm.b * (size_t)P->prm.b;
   return TQR_OK;
 }
 
@@ -309,6 +317,7 @@ tqr_status tlu_getrf(tlu_plan* P, double* At, double* Wt, int32_t* piv, void* wo
   a.W = Wt;
   a.piv = piv;
   a.perm = (int*)work;
+  a.Lw = lu_uses_ltilde(P->prm.b, P->prm.s) ? (double*)((char*)work + perm_bytes(P)) : nullptr;
   a.p = (int)P->p;
   a.q = (int)P->q;
   a.nctr = P->nctr;
