@@ -53,7 +53,7 @@ tqr_status tlu_plan_destroy(tlu_plan* plan);
 /* Element counts of At (doubles), W (doubles), piv (int32). */
 tqr_status tlu_sizes(const tlu_plan* plan, size_t* a_doubles, size_t* w_doubles, size_t* piv_ints);
 /* Bytes of the caller-allocated workspace of tlu_getrf: each block's net interchange lists, then
- * (b = 256) p x min(p, q) tiles of b x b doubles holding each block's L_l W_l (the multipliers
+ * (b = 256) p x min(p, q) tiles of b x (b + 4) doubles holding each block's L_l W_l (the multipliers
  * times W_l, LU12; scratch, not an output).  Device memory, 16-byte aligned. */
 tqr_status tlu_workspace_size(const tlu_plan* plan, size_t* bytes);
 /* Column-major A (m x n, lda >= m) -> tiles (zero padding); tiles -> column-major. */

@@ -47,6 +47,9 @@ struct LCfg {
   // 180.8 ms); at b <= 128 the panel chain bounds the run and the panels' Ltilde products cost
   // more than the updates gain (C2 LU 8.74 -> 9.22 ms), so those instances keep L_l
   static constexpr bool LT = B >= 256;
+  // LT: the workspace holds each block's L_l W_l in the shared-memory layout (S columns at ld
+  // LDL), so one bulk copy per block brings it in (one thread, completion on an mbarrier)
+  static constexpr int LTT = LT ? B * (B + 4) : 0;  // doubles per workspace tile
   static constexpr int LDX = W + 4;          // X_l: S rows x W, row-major (two buffers)
   static constexpr int LDW = S + 4;          // W_l: S x S column-major (two buffers)
   static constexpr int LDL = B + 4;          // L_l: B x S column-major (two buffers)
@@ -73,7 +76,9 @@ struct LCfg {
   static constexpr int IOFF_CUR = IOFF_PIV + S;      // B (GETRF net-permutation simulation)
   static constexpr int IOFF_CNT = IOFF_CUR + B;      // 1
   static constexpr int IOFF_BLK = (IOFF_CNT + 4 + 3) & ~3;  // 2 x PLW: the blocks' pair lists + slot tables
-  static constexpr int NINT = IOFF_BLK + 2 * PLW;
+  static constexpr int IOFF_MB = (IOFF_BLK + 2 * PLW + 1) & ~1;  // LT: 2 mbarriers (L_l W_l bulk copies) ...
+  static constexpr int IOFF_USE = IOFF_MB + 4;                    // ... and their completed-phase counts
+  static constexpr int NINT = IOFF_USE + 2;
   static constexpr size_t SMEM = (size_t)NDBL * 8 + (size_t)NINT * 4;
 };
 
@@ -117,11 +122,21 @@ __device__ __forceinline__ void issue_inputs(double* sm, int* ism, int l, const 
   double* Xs = sm + C::OFF_X + bf * S * C::LDX;
   double* Ws = sm + C::OFF_W + bf * S * C::LDW;
   int* blk = ism + C::IOFF_BLK + bf * C::PLW;
-  const int r_lo = SS ? 0 : c0 + S;
-  const int nv = (B - r_lo) / 2;  // 16-byte granules per column
-  for (int e = tid; e < nv * S; e += NT) {
-    const int v = e % nv, cc = e / nv;
-    cp_async16(Ls + cc * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + cc) * B);
+  if constexpr (C::LT) {  // L_l W_l: one bulk copy of the block (rows < r_lo unused by GESSM)
+    if (tid == 0) {
+      unsigned long long* bar = reinterpret_cast<unsigned long long*>(ism + C::IOFF_MB) + bf;
+      constexpr unsigned bytes = S * C::LDL * 8;
+      fence_proxy_async();  // the panel's generic stores (acquired / barrier-ordered) before the async read
+      mbar_expect_tx(bar, bytes);
+      bulk_g2s(Ls, L + (size_t)c0 * C::LDL, bytes, bar);
+    }
+  } else {
+    const int r_lo = SS ? 0 : c0 + S;
+    const int nv = (B - r_lo) / 2;  // 16-byte granules per column
+    for (int e = tid; e < nv * S; e += NT) {
+      const int v = e % nv, cc = e / nv;
+      cp_async16(Ls + cc * C::LDL + r_lo + 2 * v, L + r_lo + 2 * v + (size_t)(c0 + cc) * B);
+    }
   }
   const double* Wl = Wsl + (size_t)l * S * S;
   for (int e = tid; e < S * S / 2; e += NT) {
@@ -169,7 +184,10 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
     const int* srcs = blk + C::PL;
     const int* dsts = srcs + C::SLT;
     cp_async_wait<0>();
+    if constexpr (C::LT)
+      mbar_wait(reinterpret_cast<unsigned long long*>(ism + C::IOFF_MB) + bf, ism[C::IOFF_USE + bf] & 1);
     __syncthreads();  // block l's inputs landed; every thread is past block l - 1
+    if (C::LT && tid == 0) ++ism[C::IOFF_USE + bf];  // read again only after the next barrier
     if (l + 1 < l1) issue_inputs<B, S, SS>(sm, ism, l + 1, L, Wsl, wsp, C1, cl, nc);
     // (1) sources -> staging
 #pragma unroll
@@ -432,7 +450,7 @@ __device__ __forceinline__ void store_ltilde(const double (&x)[S], const double*
         a0 = fma(x[t], w2.x, a0);
         a1 = fma(x[t + 1], w2.y, a1);
       }
-      Lt[tid + (size_t)(c0 + c) * B] = a0 + a1;
+      Lt[tid + (size_t)(c0 + c) * (B + 4)] = a0 + a1;  // the update's shared layout (LDL = B + 4)
     }
   }
 }
@@ -640,7 +658,7 @@ __device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int
   const int p = a.p;
   const int vr = SS ? i : k;  // tile row of the multipliers / W / interchange lists applied
   double* Y = a.A + ((size_t)(SS ? i : k) + (size_t)j * p) * B * B;
-  const double* L = (C::LT ? a.Lw : a.A) + ((size_t)vr + (size_t)k * p) * B * B;  // Ltilde (LU12) / L
+  const double* L = C::LT ? a.Lw + ((size_t)vr + (size_t)k * p) * C::LTT : a.A + ((size_t)vr + (size_t)k * p) * B * B;
   const double* Wsl = wslot_ptr(a.W, vr, k, p, B, S);
   const int* perms = a.perm + ((size_t)vr + (size_t)k * p) * C::NB * C::PLW;
   double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
@@ -677,6 +695,12 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
   __shared__ int s_ticket;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = a.p;
+  if (C::LT && tid < 2) {
+    mbar_init(reinterpret_cast<unsigned long long*>(ism + C::IOFF_MB) + tid, 1);
+    ism[C::IOFF_USE + tid] = 0;
+  }
+  fence_mbar_init();
+  __syncthreads();
   for (;;) {
     if (tid == 0) s_ticket = atomicAdd(a.ticket, 1);
     __syncthreads();
@@ -710,11 +734,11 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
     // panel tasks: inner block sl (record [4]; -1: the whole tile)
     const int l0 = sl < 0 ? 0 : sl, l1 = sl < 0 ? C::NB : sl + 1;
     if (kind == LK_G) {
-      getrf_task<B, S>(sm, ism, Akk, C::LT ? a.Lw + ((size_t)k + (size_t)k * p) * B * B : Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
+      getrf_task<B, S>(sm, ism, Akk, C::LT ? a.Lw + ((size_t)k + (size_t)k * p) * C::LTT : Akk, wslot_ptr(a.W, k, k, p, B, S), a.piv + ((size_t)k + (size_t)k * p) * B,
                        a.perm + ((size_t)k + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_T) {
       double* Aik = a.A + ((size_t)i + (size_t)k * p) * B * B;
-      tstrf_task<B, S>(sm, ism, Akk, Aik, C::LT ? a.Lw + ((size_t)i + (size_t)k * p) * B * B : Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
+      tstrf_task<B, S>(sm, ism, Akk, Aik, C::LT ? a.Lw + ((size_t)i + (size_t)k * p) * C::LTT : Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
                        a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_S) {
       update_task<B, S, true>(sm, a, k, i, j, sl);
@@ -777,6 +801,12 @@ bool lu_uses_ltilde(int b, int s) {
   LU_INSTANCES(LT_)
 #undef LT_
   return false;
+}
+int lu_ltilde_doubles(int b, int s) {
+#define LTD(BB, SS) if (b == BB && s == SS) return LCfg<BB, SS>::LTT;
+  LU_INSTANCES(LTD)
+#undef LTD
+  return 0;
 }
 int lu_perm_ints(int b, int s) { return (b / s) * (4 + 4 * s + 2 * (b + s)); }
 int lu_max_ctas(int b, int s, int device) {

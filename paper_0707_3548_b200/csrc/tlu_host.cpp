@@ -266,7 +266,7 @@ tqr_status tlu_workspace_size(const tlu_plan* P, size_t* bytes) {
   if (!bytes) return bad(2, "bytes is NULL");
   *bytes = perm_bytes(P);
   if (lu_uses_ltilde(P->prm.b, P->prm.s))
-    *bytes += sizeof(double) * (size_t)P->p * (size_t)P->K * (size_t)P->prm.b * (size_t)P->prm.b;
+    *bytes += sizeof(double) * (size_t)P->p * (size_t)P->K * (size_t)lu_ltilde_doubles(P->prm.b, P->prm.s);
   return TQR_OK;
 }
 

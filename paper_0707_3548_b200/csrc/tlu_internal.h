@@ -24,7 +24,7 @@ struct LuArgs {
   int* perm;    // workspace: p x K slots of (b / s) x (2 + 4 s) ints -- each block's net interchange
                 //   as (count, -, dst0, src0, dst1, src1, ...; 4 + 4s ints per block) over rows [0, b) of the updated tile
                 //   and [b, b + s) of the s pivot-block rows (the GESSM / SSSSM "X" rows)
-  double* Lw;   // workspace: p x K tiles of b x b -- each block's Ltilde_l = L_l W_l (LU12),
+  double* Lw;   // workspace: p x K tiles of b x (b + 4) -- each block's Ltilde_l = L_l W_l (LU12),
                 //   written by the panels, read by the update tasks instead of L_l (b = 256 only)
   int p, q;
   int nctr;
@@ -35,6 +35,7 @@ bool lu_supported(int b, int s);
 int lu_slice(int b, int s);          // columns per update task slice
 int lu_perm_ints(int b, int s);      // perm ints per slot
 bool lu_uses_ltilde(int b, int s);   // the instance's update reads Ltilde tiles from the workspace (LU12)
+int lu_ltilde_doubles(int b, int s); // doubles per workspace Ltilde tile (b (b + 4): the shared layout)
 int lu_max_ctas(int b, int s, int device);
 cudaError_t launch_lu_exec(int b, int s, const LuArgs& a, int grid, cudaStream_t st);
 
