@@ -35,6 +35,13 @@ constexpr int W = 64;  // update slice width (columns)
 #define LU_PF 1  // L2 prefetch of the task this many ticket rounds ahead (0: off; development knob;
                  // same-box C3 LU: off 178.1-178.4 ms, 1 round 176.1, 2 rounds 178.8, 4 rounds 177.0)
 #endif
+#ifndef LU_NEXT
+#define LU_NEXT 0  // cross-task pipelining of the dispatch (as the QR executor): half-way through an
+                   // update task thread 0 takes the next ticket, one block later fetches its record
+                   // (cp.async), so both round trips overlap the GEMMs (0: off; 2: also the L2
+                   // prefetch of that task's slice one more block later)
+#endif
+constexpr int NX_TK = TASK_INTS, NX_REC = TASK_INTS + 1;  // s_next: the held ticket / its record's ticket
 #define LU_STR(x) #x
 #define LU_UNROLL(n) _Pragma(LU_STR(unroll n))
 
@@ -155,15 +162,23 @@ __device__ __forceinline__ void issue_inputs(double* sm, int* ism, int l, const 
   cp_async_commit();
 }
 
+template <int B, int S>
+__device__ __forceinline__ void lu_prefetch(const LuArgs& a, const int* q);
+
+// pa / s_next (update tasks over all NB blocks only): the dispatch pipelining of LU_NEXT.  Holding
+// one ticket ahead cannot deadlock: every wait is on a smaller ticket, and the smallest
+// unfinished ticket is some CTA's current task.
 template <int B, int S, bool SS>
 __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const double* __restrict__ L,
                                         const double* __restrict__ Wsl, const int* __restrict__ wsp, double* C1,
-                                        int cl, int nc, int l0, int l1, int r_lo) {
+                                        int cl, int nc, int l0, int l1, int r_lo, const LuArgs* pa = nullptr,
+                                        int* s_next = nullptr) {
   using C = LCfg<B, S>;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
   const int r0 = warp * C::RPW;
   double* St = sm + C::OFF_ST;
   issue_inputs<B, S, SS>(sm, ism, l0, L, Wsl, wsp, C1, cl, nc);
+  int ntk = -1;  // thread 0: the next ticket (LU_NEXT)
   // the slice into registers (fragment rows r0 + 8 mt + g, columns 8 nt + 2 t4, + 1)
   double2 acc[C::MT][W / 8];
 #pragma unroll
@@ -189,6 +204,20 @@ __device__ __noinline__ void update_run(double* sm, int* ism, double* Y, const d
     __syncthreads();  // block l's inputs landed; every thread is past block l - 1
     if (C::LT && tid == 0) ++ism[C::IOFF_USE + bf];  // read again only after the next barrier
     if (l + 1 < l1) issue_inputs<B, S, SS>(sm, ism, l + 1, L, Wsl, wsp, C1, cl, nc);
+    if (LU_NEXT > 0 && pa && tid == 0) {  // (pa: l1 - l0 = NB >= 4, so all three blocks below exist)
+      const int lm = l0 + (l1 - l0) / 2 - 1;
+      if (l == lm) ntk = atomicAdd(pa->ticket, 1);
+      if (l == lm + 1) {
+        s_next[NX_TK] = ntk;
+        if (ntk < pa->ntasks) {
+#pragma unroll
+          for (int x = 0; x < TASK_INTS; x += 4) cp_async16(s_next + x, pa->tasks + (size_t)ntk * TASK_INTS + x);
+          cp_async_commit();
+          s_next[NX_REC] = ntk;
+        }
+      }
+      if (LU_NEXT > 1 && l == lm + 2 && ntk < pa->ntasks) lu_prefetch<B, S>(*pa, s_next);  // (landed: wait above)
+    }
     // (1) sources -> staging
 #pragma unroll
     for (int mt = 0; mt < C::MT; ++mt) {
@@ -653,7 +682,7 @@ __device__ __noinline__ void tstrf_task(double* sm, int* ism, double* Ukk, doubl
 
 // GESSM(k,j,sl) (SS = false) / SSSSM(k,i,j,sl) (SS = true): one 64-column slice, every block
 template <int B, int S, bool SS>
-__device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int i, int j, int sl) {
+__device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int i, int j, int sl, int* s_next) {
   using C = LCfg<B, S>;
   const int p = a.p;
   const int vr = SS ? i : k;  // tile row of the multipliers / W / interchange lists applied
@@ -664,7 +693,7 @@ __device__ __noinline__ void update_task(double* sm, const LuArgs& a, int k, int
   double* C1 = a.A + ((size_t)k + (size_t)j * p) * B * B;
   const int cl = sl * W;
   update_run<B, S, SS>(sm, reinterpret_cast<int*>(sm + C::NDBL), Y, L, Wsl, perms, SS ? C1 : nullptr, cl,
-                       min(W, B - cl), 0, C::NB, 0);
+                       min(W, B - cl), 0, C::NB, 0, LU_NEXT > 0 && C::NB >= 4 ? &a : nullptr, s_next);
 }
 
 // L2 prefetch of the target of task record q (update: its tile-column slice, 128 KiB contiguous;
@@ -693,8 +722,11 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
   int* ism = reinterpret_cast<int*>(sm + C::NDBL);
   __shared__ int s_task[TASK_INTS];
   __shared__ int s_ticket;
+  __shared__ __align__(16) int s_next[TASK_INTS + 4];  // a prefetched record, [NX_TK], [NX_REC] (LU_NEXT)
+  __shared__ int s_have;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = a.p;
+  if (tid == 0) s_next[NX_TK] = s_next[NX_REC] = -1;
   if (C::LT && tid < 2) {
     mbar_init(reinterpret_cast<unsigned long long*>(ism + C::IOFF_MB) + tid, 1);
     ism[C::IOFF_USE + tid] = 0;
@@ -702,11 +734,18 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
   fence_mbar_init();
   __syncthreads();
   for (;;) {
-    if (tid == 0) s_ticket = atomicAdd(a.ticket, 1);
+    if (tid == 0) {
+      int nt = LU_NEXT > 0 ? s_next[NX_TK] : -1;
+      if (nt < 0) nt = atomicAdd(a.ticket, 1);
+      if (LU_NEXT > 0) cp_async_wait<0>();  // a prefetched record has landed
+      s_ticket = nt;
+      s_have = LU_NEXT > 0 && s_next[NX_REC] == nt;
+      s_next[NX_TK] = -1;
+    }
     __syncthreads();
     const int tk = s_ticket;
     if (tk >= a.ntasks) return;
-    if (tid < TASK_INTS) s_task[tid] = a.tasks[(size_t)tk * TASK_INTS + tid];
+    if (tid < TASK_INTS) s_task[tid] = s_have ? s_next[tid] : a.tasks[(size_t)tk * TASK_INTS + tid];
     __syncthreads();
     unsigned long long t_grab = 0, t_start = 0;
     if (a.trace && tid == 0) t_grab = globaltimer();
@@ -741,9 +780,9 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
       tstrf_task<B, S>(sm, ism, Akk, Aik, C::LT ? a.Lw + ((size_t)i + (size_t)k * p) * C::LTT : Aik, wslot_ptr(a.W, i, k, p, B, S), a.piv + ((size_t)i + (size_t)k * p) * B,
                        a.perm + ((size_t)i + (size_t)k * p) * C::NB * C::PLW, l0, l1);
     } else if (kind == LK_S) {
-      update_task<B, S, true>(sm, a, k, i, j, sl);
+      update_task<B, S, true>(sm, a, k, i, j, sl, s_next);
     } else {
-      update_task<B, S, false>(sm, a, k, i, j, sl);
+      update_task<B, S, false>(sm, a, k, i, j, sl, s_next);
     }
     __syncthreads();
     if (LU_PF > 0 && C::LT && tid == 32) {  // overlaps thread 0's release and next ticket round trip
