@@ -35,6 +35,10 @@ constexpr int W = 64;  // update slice width (columns)
 #define LU_PF 1  // L2 prefetch of the task this many ticket rounds ahead (0: off; development knob;
                  // same-box C3 LU: off 178.1-178.4 ms, 1 round 176.1, 2 rounds 178.8, 4 rounds 177.0)
 #endif
+#ifndef LU_DISP
+#define LU_DISP 0  // 1: warp 2 dispatches (ticket, record, dependency poll) while thread 0 of the
+                   // previous task is still in its fence + release; one barrier per dispatch
+#endif
 #ifndef LU_NEXT
 #define LU_NEXT 0  // cross-task pipelining of the dispatch (as the QR executor): half-way through an
                    // update task thread 0 takes the next ticket, one block later fetches its record
@@ -724,6 +728,7 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
   __shared__ int s_ticket;
   __shared__ __align__(16) int s_next[TASK_INTS + 4];  // a prefetched record, [NX_TK], [NX_REC] (LU_NEXT)
   __shared__ int s_have;
+  __shared__ unsigned long long s_tgrab;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int p = a.p;
   if (tid == 0) s_next[NX_TK] = s_next[NX_REC] = -1;
@@ -734,6 +739,46 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
   fence_mbar_init();
   __syncthreads();
   for (;;) {
+#if LU_DISP
+    // Dispatch by warp 2 (thread 0 of the previous task is still in its fence + release): the
+    // ticket, its record and the dependency poll follow one another in one warp, one barrier.
+    if (warp == 2) {
+      int nt = 0;
+      if (lane == 0) nt = atomicAdd(a.ticket, 1);
+      nt = __shfl_sync(0xffffffffu, nt, 0);
+      if (lane == 0) {
+        s_ticket = nt;
+        if (a.trace) s_tgrab = globaltimer();
+      }
+      if (nt < a.ntasks) {
+        int rv = lane < TASK_INTS ? a.tasks[(size_t)nt * TASK_INTS + lane] : 0;
+        if (lane < TASK_INTS) s_task[lane] = rv;
+#pragma unroll
+        for (int d = 0; d < TASK_NDEP; ++d) {
+          const int code = __shfl_sync(0xffffffffu, rv, 8 + 2 * d), val = __shfl_sync(0xffffffffu, rv, 9 + 2 * d);
+          const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+          for (int x = lane; x < cnt; x += 32) {
+            const int* c = a.ctr + idx + x;
+            if (ld_acquire(c) >= val) continue;
+            const unsigned long long t0w = globaltimer();
+            while (ld_acquire(c) < val) {
+              __nanosleep(64);
+              if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();  // schedule bug: fail loudly
+            }
+          }
+        }
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    const int tk = s_ticket;
+    if (tk >= a.ntasks) return;
+    unsigned long long t_grab = 0, t_start = 0;
+    if (a.trace && tid == 0) {
+      t_grab = s_tgrab;
+      t_start = globaltimer();
+    }
+#else
     if (tid == 0) {
       int nt = LU_NEXT > 0 ? s_next[NX_TK] : -1;
       if (nt < 0) nt = atomicAdd(a.ticket, 1);
@@ -768,7 +813,9 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
     }
     __syncthreads();
     if (a.trace && tid == 0) t_start = globaltimer();
+#endif
     const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
+    const int out_c = s_task[5], out_v = s_task[6];  // (s_task is rewritten while thread 0 releases)
     double* Akk = a.A + ((size_t)k + (size_t)k * p) * B * B;
     // panel tasks: inner block sl (record [4]; -1: the whole tile)
     const int l0 = sl < 0 ? 0 : sl, l1 = sl < 0 ? C::NB : sl + 1;
@@ -792,7 +839,7 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
     }
     if (tid == 0) {
       __threadfence();
-      st_release(a.ctr + s_task[5], s_task[6]);
+      st_release(a.ctr + out_c, out_v);
       if (a.trace) {
         unsigned long long* tr = a.trace + (size_t)tk * 4;
         tr[0] = smid();

@@ -101,10 +101,12 @@ def _conflicts(a, b, nb):
     return hit(wa, rb | wb) or hit(wb, ra)
 
 
-def _replay(rec, nctr, p, q, nsl, nb, workers, seed):
+def _replay(rec, nctr, p, q, nsl, nb, workers, seed, hold=False):
     """Replay the tickets on `workers` simulated CTAs that finish in random order; a task starts
     only when its counter dependencies hold.  Returns the first (task, earlier conflicting task
-    not yet done) violation, or None; raises on deadlock."""
+    not yet done) violation, or None; raises on deadlock.  hold: a CTA running an update task may
+    take its next ticket early (the executor's dispatch pipelining, LU_NEXT); that ticket is
+    then out of the pool but starts only after the CTA's current task."""
     seq = _sequential_order(p, q, nsl, nb)
     pos = {t: x for x, t in enumerate(seq)}
     by_region = {}
@@ -115,10 +117,16 @@ def _replay(rec, nctr, p, q, nsl, nb, workers, seed):
     rng = random.Random(seed)
     ctr = [0] * nctr
     done, running, nxt = set(), [], 0
+    held = {}  # running ticket -> the ticket its CTA holds ahead
     while nxt < len(rec) or running:
         while nxt < len(rec) and len(running) < workers:
             running.append(nxt)
             nxt += 1
+        if hold:
+            for t in running:
+                if t not in held and nxt < len(rec) and rec[t][0] >= 2 and rng.random() < 0.7:
+                    held[t] = nxt
+                    nxt += 1
         ready = [t for t in running
                  if all(ctr[(rec[t][8 + 2 * d] & 0xFFFFFF) + x] >= rec[t][9 + 2 * d]
                         for d in range(3) for x in range(int(rec[t][8 + 2 * d]) >> 24))]
@@ -131,6 +139,8 @@ def _replay(rec, nctr, p, q, nsl, nb, workers, seed):
                 if pos[other] < pos[key] and _conflicts(other, key, nb) and other not in done:
                     return key, other
         running.remove(t)
+        if t in held:
+            running.append(held.pop(t))  # the same CTA goes on with the ticket it holds
         done.add(key)
         ctr[rec[t][5]] = max(ctr[rec[t][5]], int(rec[t][6]))
     return None
@@ -149,6 +159,18 @@ def test_dispatch_order_respects_every_data_dependence(L, m, n, b, s, workers):
     assert len(rec) == len(seq) and sorted(tuple(int(v) for v in r[:5]) for r in rec) == sorted(seq)
     for seed in range(3):
         assert _replay(rec, nctr, p, q, nsl, nb, workers, seed) is None
+
+
+@pytest.mark.parametrize("m,n,b,s,workers", [(320, 192, 64, 16, 2), (1024, 1024, 256, 32, 7), (2048, 512, 256, 32, 3)])
+def test_holding_one_ticket_ahead_neither_deadlocks_nor_races(L, m, n, b, s, workers):
+    """The executor's dispatch pipelining (LU_NEXT): a CTA takes its next ticket half-way through
+    an update task.  Every wait is on a smaller ticket and the smallest unfinished ticket is some
+    CTA's current task, so the replay never stalls and the data dependences still hold."""
+    rec, nctr = L.schedule_records(m, n, b, s, workers)
+    p, q = -(-m // b), -(-n // b)
+    nsl, nb = b // min(64, b), b // s
+    for seed in range(4):
+        assert _replay(rec, nctr, p, q, nsl, nb, workers, seed, hold=True) is None
 
 
 def test_replay_detects_a_dropped_dependency(L):
