@@ -36,8 +36,9 @@ constexpr int W = 64;  // update slice width (columns)
                  // same-box C3 LU: off 178.1-178.4 ms, 1 round 176.1, 2 rounds 178.8, 4 rounds 177.0)
 #endif
 #ifndef LU_DISP
-#define LU_DISP 0  // 1: warp 2 dispatches (ticket, record, dependency poll) while thread 0 of the
-                   // previous task is still in its fence + release; one barrier per dispatch
+#define LU_DISP 0  // (unused) LuArgs::disp selects the kernel instance whose warp 2 takes the ticket, its
+                   // record and polls the dependencies while thread 0 of the previous task is still in
+                   // its fence + release (one barrier per dispatch)
 #endif
 #ifndef LU_NEXT
 #define LU_NEXT 0  // cross-task pipelining of the dispatch (as the QR executor): half-way through an
@@ -719,7 +720,7 @@ __device__ __forceinline__ void lu_prefetch(const LuArgs& a, const int* q) {
   }
 }
 
-template <int B, int S>
+template <int B, int S, bool DISP>
 __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ LuArgs a) {
   using C = LCfg<B, S>;
   extern __shared__ __align__(16) double sm[];
@@ -739,23 +740,65 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
   fence_mbar_init();
   __syncthreads();
   for (;;) {
-#if LU_DISP
-    // Dispatch by warp 2 (thread 0 of the previous task is still in its fence + release): the
-    // ticket, its record and the dependency poll follow one another in one warp, one barrier.
-    if (warp == 2) {
-      int nt = 0;
-      if (lane == 0) nt = atomicAdd(a.ticket, 1);
-      nt = __shfl_sync(0xffffffffu, nt, 0);
-      if (lane == 0) {
-        s_ticket = nt;
-        if (a.trace) s_tgrab = globaltimer();
+    int tk;
+    unsigned long long t_grab = 0, t_start = 0;
+    if constexpr (DISP) {
+      // Dispatch by warp 2 (thread 0 of the previous task is still in its fence + release): the
+      // ticket, its record and the dependency poll follow one another in one warp, one barrier.
+      if (warp == 2) {
+        int nt = 0;
+        if (lane == 0) nt = atomicAdd(a.ticket, 1);
+        nt = __shfl_sync(0xffffffffu, nt, 0);
+        if (lane == 0) {
+          s_ticket = nt;
+          if (a.trace) s_tgrab = globaltimer();
+        }
+        if (nt < a.ntasks) {
+          int rv = lane < TASK_INTS ? a.tasks[(size_t)nt * TASK_INTS + lane] : 0;
+          if (lane < TASK_INTS) s_task[lane] = rv;
+#pragma unroll
+          for (int d = 0; d < TASK_NDEP; ++d) {
+            const int code = __shfl_sync(0xffffffffu, rv, 8 + 2 * d), val = __shfl_sync(0xffffffffu, rv, 9 + 2 * d);
+            const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
+            for (int x = lane; x < cnt; x += 32) {
+              const int* c = a.ctr + idx + x;
+              if (ld_acquire(c) >= val) continue;
+              const unsigned long long t0w = globaltimer();
+              while (ld_acquire(c) < val) {
+                __nanosleep(64);
+                if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();  // schedule bug: fail loudly
+              }
+            }
+          }
+          __syncwarp();
+        }
       }
-      if (nt < a.ntasks) {
-        int rv = lane < TASK_INTS ? a.tasks[(size_t)nt * TASK_INTS + lane] : 0;
-        if (lane < TASK_INTS) s_task[lane] = rv;
+      __syncthreads();
+      tk = s_ticket;
+      if (tk >= a.ntasks) return;
+      if (a.trace && tid == 0) {
+        t_grab = s_tgrab;
+        t_start = globaltimer();
+      }
+    } else {
+      if (tid == 0) {
+        int nt = LU_NEXT > 0 ? s_next[NX_TK] : -1;
+        if (nt < 0) nt = atomicAdd(a.ticket, 1);
+        if (LU_NEXT > 0) cp_async_wait<0>();  // a prefetched record has landed
+        s_ticket = nt;
+        s_have = LU_NEXT > 0 && s_next[NX_REC] == nt;
+        s_next[NX_TK] = -1;
+      }
+      __syncthreads();
+      tk = s_ticket;
+      if (tk >= a.ntasks) return;
+      if (tid < TASK_INTS) s_task[tid] = s_have ? s_next[tid] : a.tasks[(size_t)tk * TASK_INTS + tid];
+      __syncthreads();
+      if (a.trace && tid == 0) t_grab = globaltimer();
+      if (warp == 0) {
 #pragma unroll
         for (int d = 0; d < TASK_NDEP; ++d) {
-          const int code = __shfl_sync(0xffffffffu, rv, 8 + 2 * d), val = __shfl_sync(0xffffffffu, rv, 9 + 2 * d);
+          const int code = s_task[8 + 2 * d], val = s_task[9 + 2 * d];
           const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
           for (int x = lane; x < cnt; x += 32) {
             const int* c = a.ctr + idx + x;
@@ -769,51 +812,9 @@ __global__ void __launch_bounds__(NT, 1) lu_exec_kernel(const __grid_constant__ 
         }
         __syncwarp();
       }
+      __syncthreads();
+      if (a.trace && tid == 0) t_start = globaltimer();
     }
-    __syncthreads();
-    const int tk = s_ticket;
-    if (tk >= a.ntasks) return;
-    unsigned long long t_grab = 0, t_start = 0;
-    if (a.trace && tid == 0) {
-      t_grab = s_tgrab;
-      t_start = globaltimer();
-    }
-#else
-    if (tid == 0) {
-      int nt = LU_NEXT > 0 ? s_next[NX_TK] : -1;
-      if (nt < 0) nt = atomicAdd(a.ticket, 1);
-      if (LU_NEXT > 0) cp_async_wait<0>();  // a prefetched record has landed
-      s_ticket = nt;
-      s_have = LU_NEXT > 0 && s_next[NX_REC] == nt;
-      s_next[NX_TK] = -1;
-    }
-    __syncthreads();
-    const int tk = s_ticket;
-    if (tk >= a.ntasks) return;
-    if (tid < TASK_INTS) s_task[tid] = s_have ? s_next[tid] : a.tasks[(size_t)tk * TASK_INTS + tid];
-    __syncthreads();
-    unsigned long long t_grab = 0, t_start = 0;
-    if (a.trace && tid == 0) t_grab = globaltimer();
-    if (warp == 0) {
-#pragma unroll
-      for (int d = 0; d < TASK_NDEP; ++d) {
-        const int code = s_task[8 + 2 * d], val = s_task[9 + 2 * d];
-        const int cnt = (int)((unsigned)code >> 24), idx = code & 0xFFFFFF;
-        for (int x = lane; x < cnt; x += 32) {
-          const int* c = a.ctr + idx + x;
-          if (ld_acquire(c) >= val) continue;
-          const unsigned long long t0w = globaltimer();
-          while (ld_acquire(c) < val) {
-            __nanosleep(64);
-            if (globaltimer() - t0w > 20ull * 1000000000ull) __trap();  // schedule bug: fail loudly
-          }
-        }
-      }
-      __syncwarp();
-    }
-    __syncthreads();
-    if (a.trace && tid == 0) t_start = globaltimer();
-#endif
     const int kind = s_task[0], k = s_task[1], i = s_task[2], j = s_task[3], sl = s_task[4];
     const int out_c = s_task[5], out_v = s_task[6];  // (s_task is rewritten while thread 0 releases)
     double* Akk = a.A + ((size_t)k + (size_t)k * p) * B * B;
@@ -855,10 +856,13 @@ template <int B, int S>
 static cudaError_t launch_inst(const LuArgs& a, int grid, cudaStream_t st) {
   using C = LCfg<B, S>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
-  cudaError_t e = cudaFuncSetAttribute(lu_exec_kernel<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+  // two instances per (b, s): LuArgs::disp picks the dispatch (one kernel holding both paths
+  // cost each of them ~1%: C3 LU 166.9 -> 168.2 ms with disp, 168.9 -> 170.3 without)
+  const void* fn = a.disp ? (const void*)lu_exec_kernel<B, S, true> : (const void*)lu_exec_kernel<B, S, false>;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
   if (e != cudaSuccess) return e;
   void* args[] = {(void*)&a};
-  return cudaLaunchCooperativeKernel((void*)lu_exec_kernel<B, S>, dim3(grid), dim3(NT), args, C::SMEM, st);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(NT), args, C::SMEM, st);
 }
 
 template <int B, int S>
@@ -866,11 +870,13 @@ static int max_ctas_inst(int device) {
   using C = LCfg<B, S>;
   int nsm = 0, per = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device);
-  if (cudaFuncSetAttribute(lu_exec_kernel<B, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) !=
-      cudaSuccess)
+  int per2 = 0;
+  if (cudaFuncSetAttribute(lu_exec_kernel<B, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess ||
+      cudaFuncSetAttribute(lu_exec_kernel<B, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM) != cudaSuccess)
     return 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lu_exec_kernel<B, S>, NT, C::SMEM) != cudaSuccess) return 0;
-  return nsm * per;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, lu_exec_kernel<B, S, false>, NT, C::SMEM) != cudaSuccess) return 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, lu_exec_kernel<B, S, true>, NT, C::SMEM) != cudaSuccess) return 0;
+  return nsm * (per < per2 ? per : per2);
 }
 
 #define LU_INSTANCES(X) X(256, 32) X(128, 32) X(64, 16)

@@ -28,6 +28,7 @@ struct LuArgs {
                 //   written by the panels, read by the update tasks instead of L_l (b = 256 only)
   int p, q;
   int nctr;
+  int disp;  // 1: the next task is dispatched by warp 2 during the previous task's release (throughput-bound grids)
   unsigned long long* trace;  // 4 per task or nullptr
 };
 
