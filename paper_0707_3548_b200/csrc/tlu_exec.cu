@@ -35,11 +35,6 @@ constexpr int W = 64;  // update slice width (columns)
 #define LU_PF 1  // L2 prefetch of the task this many ticket rounds ahead (0: off; development knob;
                  // same-box C3 LU: off 178.1-178.4 ms, 1 round 176.1, 2 rounds 178.8, 4 rounds 177.0)
 #endif
-#ifndef LU_DISP
-#define LU_DISP 0  // (unused) LuArgs::disp selects the kernel instance whose warp 2 takes the ticket, its
-                   // record and polls the dependencies while thread 0 of the previous task is still in
-                   // its fence + release (one barrier per dispatch)
-#endif
 #ifndef LU_NEXT
 #define LU_NEXT 0  // cross-task pipelining of the dispatch (as the QR executor): half-way through an
                    // update task thread 0 takes the next ticket, one block later fetches its record

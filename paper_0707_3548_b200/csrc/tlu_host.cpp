@@ -321,7 +321,7 @@ tqr_status tlu_getrf(tlu_plan* P, double* At, double* Wt, int32_t* piv, void* wo
   a.p = (int)P->p;
   a.q = (int)P->q;
   a.nctr = P->nctr;
-  // dispatch by warp 2 during the release (tlu_exec.cu LU_DISP): throughput-bound grids only --
+  // dispatch by warp 2 during the release (tlu_exec.cu, the DISP kernel instance): throughput-bound grids only --
   // same-box C3 LU 169.0 -> 166.9 ms; the chain-bound C2 (8.80 -> 8.99 ms) and C4 (52.9 -> 53.7)
   // keep the dispatch after the release
   a.disp = P->prm.b >= 256 && std::min(P->p, P->q) >= 32;
